@@ -1,0 +1,156 @@
+/*
+ * fftconv.h -- C ABI of the B200-native FlashFFTConv hot path
+ * (arXiv 2311.05908, "FlashFFTConv: Efficient Convolutions for Long Sequences
+ * with Tensor Cores").
+ *
+ * Citations: "P:n" = line n of the paper source; "A<n>" = reading
+ * n listed in DESIGN.md ("Readings of the paper").
+ *
+ * The operation (Alg. 1):
+ *     y = iFFT( FFT(pad(u)) * k_f )[:N],   k_f = FFT(pad(k))
+ * over u of shape (B, H, N) with one real filter k[h, :K] per head h,
+ * plus the gated form y = v * ((u * w) conv k) (A17), the
+ * partial form K < N (A12), the frequency-sparse form
+ * (k_f masked; A13) and the backward pass
+ * (recomputation; A15).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - All device pointers are CUDA device addresses owned by the caller.  The
+ *    library NEVER allocates device memory; sizes come from fftconv_plan_info.
+ *  - Signals u, w, v, y, dy, du, dw, dv: contiguous row-major (B, H, N) in the
+ *    plan's dtype, 16-byte aligned.  Row (b, h) starts at ((b*H)+h)*N.
+ *  - Filters k and gradients dk: contiguous row-major (H, K) fp32.
+ *  - k_f: opaque, plan layout, produced only by fftconv_precompute_kf for the
+ *    same plan; kf_bytes_per_head bytes per head.
+ *  - Calls are asynchronous on `stream`; inputs are never written; outputs
+ *    must not alias inputs.  Argument errors are detected before any launch
+ *    and leave the outputs untouched.  Launch failures return
+ *    FFTCONV_ERR_CUDA; asynchronous device faults surface at the caller's
+ *    next synchronisation.  fftconv_last_error() describes the last failure
+ *    of the calling thread.
+ *  - No atomics: results are bitwise reproducible run to run and do not
+ *    depend on how rows are sharded across GPUs.
+ *  - A plan is host memory, immutable after fftconv_plan_upload and safe to
+ *    share across threads and streams.
+ */
+#ifndef FFTCONV_H_
+#define FFTCONV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* cudaStream_t-compatible handle (NULL = legacy default stream). */
+typedef struct CUstream_st* fftconv_stream_t;
+
+typedef struct fftconv_plan_s* fftconv_plan_t;
+
+/* I/O element type.  Tensor-core operands are always fp16 with fp32
+ * accumulation (A16; bf16 operands would miss the 2e-3 bound).
+ * FFTCONV_F32 is the validation dtype (fp32 I/O). */
+typedef enum { FFTCONV_F16 = 0, FFTCONV_BF16 = 1, FFTCONV_F32 = 2 } fftconv_dtype_t;
+
+typedef enum {
+  FFTCONV_OK = 0,
+  FFTCONV_ERR_INVALID_ARG = 1,     /* null/negative/inconsistent argument       */
+  FFTCONV_ERR_NOT_POW2 = 2,        /* N or fft_size not a power of two */
+  FFTCONV_ERR_KERNEL_TOO_LONG = 3, /* K exceeds the causal budget fft_size/2    */
+  FFTCONV_ERR_BAD_SPARSITY = 4,    /* sparsity dims/masks inconsistent          */
+  FFTCONV_ERR_UNSUPPORTED = 5,     /* valid request this build cannot run yet   */
+  FFTCONV_ERR_MISALIGNED = 6,      /* device pointer not 16-byte aligned        */
+  FFTCONV_ERR_CUDA = 7             /* CUDA launch/runtime error                 */
+} fftconv_status_t;
+
+/* Frequency-sparsity pattern (A13).  The length-L spectrum of k
+ * (L = fft_size) is viewed as a row-major digit grid dims[0] x ... x
+ * dims[ndims-1] (slowest first, product = L).  keep[j][i] != 0 keeps index i
+ * of dimension j; frequency f is kept iff every digit is kept.  The mask is
+ * applied Hermitian-symmetrically, m[f] = keep(f) | keep(L - f), so y stays
+ * real.  The tab:sparsity_fraction patterns (a,b,c,d) zero the last a,b,c,d
+ * entries of each dimension.  Pointers are read during fftconv_plan only. */
+typedef struct {
+  int32_t ndims;          /* 1..4 */
+  int32_t dims[4];
+  const uint8_t* keep[4]; /* host arrays of dims[j] bytes */
+} fftconv_sparsity_t;
+
+typedef struct {
+  int64_t N;                 /* input/output length per row                   */
+  int64_t fft_size;          /* L                                             */
+  int32_t causal;            /* 1 causal (zero-padded), 0 circular            */
+  int32_t dtype;             /* fftconv_dtype_t                               */
+  int32_t regime;            /* 1 fused single pass, 2 partial (chunked)      */
+  int32_t order;             /* Monarch order p of the complex transform      */
+  int32_t factors[4];        /* L = prod factors[0..order)                    */
+  int32_t rows_per_tile;     /* batch rows one CTA work unit processes        */
+  int64_t max_kernel_len;    /* largest K accepted by precompute_kf           */
+  size_t table_bytes;        /* device bytes for fftconv_plan_upload          */
+  size_t kf_bytes_per_head;  /* device bytes of k_f per head                  */
+  size_t workspace_bytes_per_head; /* fftconv_bwd workspace, per head         */
+  double mask_fraction;      /* fraction of spectrum zeroed by the mask       */
+  double skip_fraction;      /* fraction of pointwise blocks the kernel skips */
+} fftconv_plan_info_t;
+
+/* Create a plan (host only, no CUDA calls).
+ *  N        input length per row, power of two, 256 <= N.
+ *  fft_size L, power of two.  causal=1: L >= 2N is the full causal conv
+ *           (K <= N); L < 2N selects the partial (chunked overlap-add) conv
+ *           with K <= L/2 (A12).  causal=0: circular, L == N == K
+ *           (A2).
+ *  sparsity NULL for dense; else see fftconv_sparsity_t (prod dims == L).
+ * Returns NOT_POW2 / INVALID_ARG / BAD_SPARSITY / UNSUPPORTED on bad input;
+ * *out is set only on success. */
+fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t fft_size, fftconv_dtype_t dtype,
+                              int causal, const fftconv_sparsity_t* sparsity);
+
+/* Fill *info (host only). */
+fftconv_status_t fftconv_plan_info(fftconv_plan_t plan, fftconv_plan_info_t* info);
+
+/* Copy the plan's constant tables (real-pair DFT matrices of the Monarch
+ * factors P:126, twiddles, all built in fp64 on the host) into the
+ * caller-owned device buffer d_tables (table_bytes, 1024-byte aligned) and
+ * bind it to the plan.  Must precede every other device call.  The buffer
+ * must outlive the plan's use. */
+fftconv_status_t fftconv_plan_upload(fftconv_plan_t plan, void* d_tables, fftconv_stream_t stream);
+
+/* k_f = FFT_L(pad(k[h, :K])) in plan layout, computed on the
+ * GPU in fp32, with the sparsity mask applied.  d_k: (H, K) fp32;
+ * d_kf: H * kf_bytes_per_head bytes.  K must be 1..max_kernel_len. */
+fftconv_status_t fftconv_precompute_kf(fftconv_plan_t plan, const float* d_k, int64_t H, int64_t K, void* d_kf,
+                                       fftconv_stream_t stream);
+
+/* y = u conv k (Alg. 1; real packing, causal padding and the
+ * pointwise k_f product fused).  d_workspace may be NULL. */
+fftconv_status_t fftconv_fwd(fftconv_plan_t plan, const void* d_u, const void* d_kf, void* d_y, int64_t B,
+                             int64_t H, void* d_workspace, fftconv_stream_t stream);
+
+/* y = v * ((u * w) conv k), gating fused into load and store. */
+fftconv_status_t fftconv_gated_fwd(fftconv_plan_t plan, const void* d_u, const void* d_w, const void* d_v,
+                                   const void* d_kf, void* d_y, int64_t B, int64_t H, void* d_workspace,
+                                   fftconv_stream_t stream);
+
+/* Backward of <y, dy> with recomputation (A15).  Plain when
+ * d_w == d_v == NULL (then d_dw, d_dv ignored); gated when both are given.
+ * d_dk (H, K) fp32 is OVERWRITTEN with the batch sum.  d_workspace:
+ * H * workspace_bytes_per_head bytes (required). */
+fftconv_status_t fftconv_bwd(fftconv_plan_t plan, const void* d_dy, const void* d_u, const void* d_w,
+                             const void* d_v, const void* d_kf, void* d_du, void* d_dw, void* d_dv, float* d_dk,
+                             int64_t B, int64_t H, int64_t K, void* d_workspace, fftconv_stream_t stream);
+
+void fftconv_plan_destroy(fftconv_plan_t plan);
+
+/* Thread-local description of the last error ("" if none). */
+const char* fftconv_last_error(void);
+
+/* Number of kernel launches issued by this thread since the last call
+ * (instrumentation for the bench's gpu_launches count). */
+int64_t fftconv_launch_count_reset(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFTCONV_H_ */

@@ -1,0 +1,152 @@
+// api.cu -- C-ABI entry points (include/fftconv.h): argument validation,
+// table upload and kernel launches.  Every device-side step of the path runs
+// in this library's own kernels; there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <string>
+
+#include "fftconv.h"
+#include "fwd_params.h"
+#include "plan.h"
+
+using namespace fc;
+
+namespace {
+thread_local int64_t g_launches = 0;
+
+int num_sms_current() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+fftconv_status_t cuda_fail(const char* what, cudaError_t e) {
+  set_last_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return FFTCONV_ERR_CUDA;
+}
+
+fftconv_status_t check_signal_args(fftconv_plan_t p, const char* fn, int64_t B, int64_t H,
+                                   std::initializer_list<const void*> ptrs) {
+  if (!p) { set_last_error(std::string(fn) + ": plan is NULL"); return FFTCONV_ERR_INVALID_ARG; }
+  if (!p->d_tables) { set_last_error(std::string(fn) + ": plan tables not uploaded"); return FFTCONV_ERR_INVALID_ARG; }
+  if (B < 0 || H < 0) { set_last_error(std::string(fn) + ": negative B or H"); return FFTCONV_ERR_INVALID_ARG; }
+  for (const void* q : ptrs) {
+    if (!q && B * H > 0) { set_last_error(std::string(fn) + ": NULL device pointer"); return FFTCONV_ERR_INVALID_ARG; }
+    if (q && !aligned16(q)) { set_last_error(std::string(fn) + ": device pointer not 16-byte aligned"); return FFTCONV_ERR_MISALIGNED; }
+  }
+  return FFTCONV_OK;
+}
+}  // namespace
+
+extern "C" fftconv_status_t fftconv_plan_upload(fftconv_plan_t p, void* d_tables, fftconv_stream_t stream) {
+  if (!p || !d_tables) { set_last_error("fftconv_plan_upload: NULL argument"); return FFTCONV_ERR_INVALID_ARG; }
+  if ((reinterpret_cast<uintptr_t>(d_tables) & 1023u) != 0) {
+    set_last_error("fftconv_plan_upload: table buffer must be 1024-byte aligned");
+    return FFTCONV_ERR_MISALIGNED;
+  }
+  cudaError_t e = cudaMemcpyAsync(d_tables, p->image.data(), p->image.size(), cudaMemcpyHostToDevice,
+                                  reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("fftconv_plan_upload", e);
+  // the host image must stay valid until the copy completes (pageable copy is
+  // staged synchronously by the driver, but be explicit)
+  e = cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("fftconv_plan_upload", e);
+  p->d_tables = d_tables;
+  return FFTCONV_OK;
+}
+
+extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float* d_k, int64_t H, int64_t K,
+                                                  void* d_kf, fftconv_stream_t stream) {
+  if (!p) { set_last_error("fftconv_precompute_kf: plan is NULL"); return FFTCONV_ERR_INVALID_ARG; }
+  if (!p->d_tables) { set_last_error("fftconv_precompute_kf: plan tables not uploaded"); return FFTCONV_ERR_INVALID_ARG; }
+  if (H < 0 || K < 1) { set_last_error("fftconv_precompute_kf: need H >= 0 and K >= 1"); return FFTCONV_ERR_INVALID_ARG; }
+  const int64_t kmax = p->causal ? p->L / 2 : p->L;
+  if (K > kmax) { set_last_error("fftconv_precompute_kf: kernel exceeds causal budget"); return FFTCONV_ERR_KERNEL_TOO_LONG; }
+  if (H > 0 && (!d_k || !d_kf)) { set_last_error("fftconv_precompute_kf: NULL device pointer"); return FFTCONV_ERR_INVALID_ARG; }
+  if (d_kf && !aligned16(d_kf)) { set_last_error("fftconv_precompute_kf: k_f not 16-byte aligned"); return FFTCONV_ERR_MISALIGNED; }
+  KfParams prm{};
+  prm.k = d_k;
+  prm.kf = d_kf;
+  prm.mask = p->sparse ? reinterpret_cast<const float*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.total)
+                       : nullptr;
+  prm.H = H;
+  prm.K = K;
+  prm.L = p->L;
+  prm.L1 = p->L1;
+  prm.L2 = p->L2;
+  cudaError_t e = launch_precompute_kf(prm, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail("fftconv_precompute_kf", e);
+  g_launches += H > 0 ? 1 : 0;
+  return FFTCONV_OK;
+}
+
+static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, const void* v, const void* kf,
+                                void* y, int64_t B, int64_t H, fftconv_stream_t stream, const char* fn) {
+  const bool gated = (w != nullptr);
+  fftconv_status_t st = gated ? check_signal_args(p, fn, B, H, {u, w, v, kf, y}) : check_signal_args(p, fn, B, H, {u, kf, y});
+  if (st != FFTCONV_OK) return st;
+  if (gated && !v) { set_last_error(std::string(fn) + ": v is NULL"); return FFTCONV_ERR_INVALID_ARG; }
+  if (B * H == 0) return FFTCONV_OK;
+  if (p->regime != REGIME_FUSED) { set_last_error(std::string(fn) + ": regime not supported by this build"); return FFTCONV_ERR_UNSUPPORTED; }
+  FwdParams prm{};
+  prm.u = u;
+  prm.w = w;
+  prm.v = v;
+  prm.y = y;
+  prm.kf = kf;
+  prm.tables = p->d_tables;
+  prm.B = B;
+  prm.H = H;
+  prm.N = p->N;
+  prm.L1 = p->L1;
+  prm.causal = p->causal;
+  prm.gated = gated ? 1 : 0;
+  prm.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
+  prm.num_sms = num_sms_current();
+  cudaError_t e = launch_fwd_fused(prm, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(fn, e);
+  g_launches += 1;
+  return FFTCONV_OK;
+}
+
+extern "C" fftconv_status_t fftconv_fwd(fftconv_plan_t p, const void* d_u, const void* d_kf, void* d_y, int64_t B,
+                                        int64_t H, void* d_workspace, fftconv_stream_t stream) {
+  (void)d_workspace;
+  return run_fwd(p, d_u, nullptr, nullptr, d_kf, d_y, B, H, stream, "fftconv_fwd");
+}
+
+extern "C" fftconv_status_t fftconv_gated_fwd(fftconv_plan_t p, const void* d_u, const void* d_w, const void* d_v,
+                                              const void* d_kf, void* d_y, int64_t B, int64_t H, void* d_workspace,
+                                              fftconv_stream_t stream) {
+  (void)d_workspace;
+  if (!d_w || !d_v) { set_last_error("fftconv_gated_fwd: w and v are required"); return FFTCONV_ERR_INVALID_ARG; }
+  return run_fwd(p, d_u, d_w, d_v, d_kf, d_y, B, H, stream, "fftconv_gated_fwd");
+}
+
+extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, const void* d_u, const void* d_w,
+                                        const void* d_v, const void* d_kf, void* d_du, void* d_dw, void* d_dv,
+                                        float* d_dk, int64_t B, int64_t H, int64_t K, void* d_workspace,
+                                        fftconv_stream_t stream) {
+  (void)d_dy; (void)d_u; (void)d_w; (void)d_v; (void)d_kf; (void)d_du; (void)d_dw; (void)d_dv; (void)d_dk;
+  (void)B; (void)H; (void)K; (void)d_workspace; (void)stream;
+  if (!p) { set_last_error("fftconv_bwd: plan is NULL"); return FFTCONV_ERR_INVALID_ARG; }
+  set_last_error("fftconv_bwd: not implemented in this build");
+  return FFTCONV_ERR_UNSUPPORTED;
+}
+
+extern "C" int64_t fftconv_launch_count_reset(void) {
+  int64_t n = g_launches;
+  g_launches = 0;
+  return n;
+}

@@ -1,0 +1,33 @@
+// fwd_params.h -- launch parameters of the fused forward kernels (internal).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fc {
+struct FwdParams {
+  const void* u;
+  const void* w;   // gated only
+  const void* v;   // gated only
+  void* y;
+  const void* kf;      // H * L complex fp32, [k2][k1], 128B-swizzled per head
+  const void* tables;  // plan table image
+  int64_t B, H, N;
+  int32_t L1;
+  int32_t causal;
+  int32_t gated;
+  int32_t dtype;  // 0 fp16, 1 bf16
+  int32_t num_sms;
+};
+cudaError_t launch_fwd_fused(const FwdParams& prm, cudaStream_t s);
+size_t fwd_fused_smem_bytes(int L1, int causal);
+
+struct KfParams {
+  const float* k;     // (H, K)
+  void* kf;           // H * L complex fp32
+  const float* mask;  // length L or nullptr
+  int64_t H, K, L;
+  int32_t L1, L2;
+};
+cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s);
+}  // namespace fc

@@ -1,0 +1,343 @@
+// plan.cpp -- host planner of the B200 FlashFFTConv library.
+//
+//  * validates (N, fft_size, dtype, causal, sparsity) and picks the regime;
+//  * factorises the complex transform length (Monarch order-2, P:124-126,
+//    Alg. 1) and builds every constant table in fp64, rounded once
+//    to the storage precision (real-pair fp16 DFT matrices with unitary
+//    1/sqrt(L_i) scaling, fp32 twiddles with the exponent reduced mod L in
+//    integers);
+//  * builds the Hermitian-symmetric frequency mask of A13;
+//  * implements the Eq. 2 cost model and order selection.
+//
+// No CUDA calls happen here except in fftconv_plan_upload (api.cu).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "plan.h"
+
+namespace fc {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+static bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+static int ilog2(int64_t x) {
+  int r = 0;
+  while ((int64_t(1) << r) < x) ++r;
+  return r;
+}
+
+// Balanced power-of-two split, larger factors first.
+std::vector<int64_t> factorize(int64_t n, int p) {
+  std::vector<int64_t> f;
+  if (!is_pow2(n) || p < 1) return f;
+  int e = ilog2(n);
+  if (e < p) return f;
+  for (int i = 0; i < p; ++i) {
+    int ei = e / p + (i < e % p ? 1 : 0);
+    f.push_back(int64_t(1) << ei);
+  }
+  return f;
+}
+
+// Eq. 2: C = BH * sum_i [ 16 N N_i / gamma(N_i) + 4 N / omega(i) ]  (A10)
+// gamma(N_i) = tau_G if N_i < mu else tau_M; omega(i) = sigma_S if
+// the stage-i working set 4N / prod_{j<i} N_j fits the SRAM budget, else
+// sigma_H (A11).
+double cost_eq2(int64_t N, const std::vector<int64_t>& factors, const CostConstants& c, double BH) {
+  double total = 0.0, prefix = 1.0;
+  for (size_t i = 0; i < factors.size(); ++i) {
+    const double Ni = double(factors[i]);
+    const double gamma = Ni < c.mu ? c.tau_g : c.tau_m;
+    const double ws = 4.0 * double(N) / prefix;
+    const double omega = ws <= c.sram_bytes ? c.sigma_s : c.sigma_h;
+    total += 16.0 * double(N) * Ni / gamma + 4.0 * double(N) / omega;
+    prefix *= Ni;
+  }
+  return BH * total;
+}
+
+int select_order(int64_t N, const CostConstants& c, std::vector<int64_t>* factors_out) {
+  int best_p = 0;
+  double best = 0.0;
+  for (int p = 2; p <= 4; ++p) {
+    auto f = factorize(N, p);
+    if (f.empty()) continue;
+    double cst = cost_eq2(N, f, c, 1.0);
+    if (best_p == 0 || cst < best) {  // ties -> smaller p
+      best = cst;
+      best_p = p;
+      if (factors_out) *factors_out = f;
+    }
+  }
+  return best_p;
+}
+
+// ---------------------------------------------------------------- tables
+static inline uint16_t to_half_bits(double x) {
+  // round-to-nearest-even fp64 -> fp16 (values here are |x| <= 1, normal or 0)
+  float f = float(x);  // fp64->fp32 rounding is far below fp16 resolution
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  uint32_t sign = (u >> 16) & 0x8000u;
+  int32_t exp = int32_t((u >> 23) & 0xFF) - 127 + 15;
+  uint32_t mant = u & 0x7FFFFFu;
+  if ((u & 0x7FFFFFFFu) == 0) return uint16_t(sign);
+  if (exp <= 0) {  // subnormal half
+    if (exp < -10) return uint16_t(sign);
+    mant |= 0x800000u;
+    uint32_t shift = uint32_t(14 - exp);
+    uint32_t half_m = mant >> shift;
+    uint32_t rem = mant & ((1u << shift) - 1), halfway = 1u << (shift - 1);
+    if (rem > halfway || (rem == halfway && (half_m & 1))) half_m++;
+    return uint16_t(sign | half_m);
+  }
+  uint32_t half_m = mant >> 13, rem = mant & 0x1FFFu;
+  if (rem > 0x1000u || (rem == 0x1000u && (half_m & 1))) {
+    half_m++;
+    if (half_m == 0x400u) { half_m = 0; exp++; }
+  }
+  if (exp >= 31) return uint16_t(sign | 0x7C00u);
+  return uint16_t(sign | (uint32_t(exp) << 10) | half_m);
+}
+
+static void put_half(std::vector<uint8_t>& img, size_t off, double x) {
+  uint16_t h = to_half_bits(x);
+  std::memcpy(img.data() + off, &h, 2);
+}
+
+// W_n^{e} = exp(-2 pi i e / n) with e reduced mod n in integers (H3).
+static void root(int64_t e, int64_t n, double* re, double* im) {
+  e %= n;
+  if (e < 0) e += n;
+  const double ang = -2.0 * M_PI * double(e) / double(n);
+  *re = std::cos(ang);
+  *im = std::sin(ang);
+}
+
+// Real-pair matrix entry for input (c, a) -> output (c', b) of the complex
+// map out_b = sum_a F[a][b] in_a:  [[Fr, Fi], [-Fi, Fr]] arrangement.
+static double realpair(double fr, double fi, int c_in, int c_out) {
+  if (c_in == 0 && c_out == 0) return fr;
+  if (c_in == 1 && c_out == 0) return -fi;
+  if (c_in == 0 && c_out == 1) return fi;
+  return fr;
+}
+
+// K-major canonical (SWIZZLE_NONE) byte offset of element (row r, k).
+static size_t kmajor_off(int r, int k, int Ktot) {
+  const size_t sbo = size_t(Ktot / 8) * 128;
+  return size_t(r / 8) * sbo + size_t(k / 8) * 128 + size_t(r % 8) * 16 + size_t(k % 8) * 2;
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static void build_fused_tables(fftconv_plan_s* p) {
+  const int L1 = p->L1, L2 = p->L2, KA = p->KA;
+  const int64_t L = p->L;
+  TableLayout& t = p->tl;
+  size_t off = 0;
+  t.ga = off;  t.ga_bytes = size_t(2 * L2) * (2 * KA) * 2;  off = align_up(off + t.ga_bytes, 1024);
+  t.gb = off;  t.gb_bytes = size_t(2 * L1) * (2 * L1) * 2;  off = align_up(off + t.gb_bytes, 1024);
+  t.gbi = off; t.gbi_bytes = t.gb_bytes;                    off = align_up(off + t.gbi_bytes, 1024);
+  t.gai = off; t.gai_bytes = size_t(2 * L2) * (2 * L2) * 2; off = align_up(off + t.gai_bytes, 1024);
+  t.tw = off;  t.tw_bytes = size_t(L) * 8;                  off = align_up(off + t.tw_bytes, 1024);
+  t.total = off;
+  p->image.assign(t.total, 0);
+  std::vector<uint8_t>& img = p->image;
+  const double sA = 1.0 / std::sqrt(double(L2)), sB = 1.0 / std::sqrt(double(L1));
+  // stage A (forward, contracts n2 -> k2): B^T[(c',k2)][(c,n2)], n2 < KA
+  for (int co = 0; co < 2; ++co)
+    for (int k2 = 0; k2 < L2; ++k2)
+      for (int ci = 0; ci < 2; ++ci)
+        for (int n2 = 0; n2 < KA; ++n2) {
+          double fr, fi;
+          root(int64_t(n2) * k2, L2, &fr, &fi);
+          put_half(img, t.ga + kmajor_off(co * L2 + k2, ci * KA + n2, 2 * KA),
+                   realpair(fr * sA, fi * sA, ci, co));
+        }
+  // stage B (forward, contracts n1 -> k1) and B^-1 (contracts k1 -> n1)
+  for (int co = 0; co < 2; ++co)
+    for (int b = 0; b < L1; ++b)
+      for (int ci = 0; ci < 2; ++ci)
+        for (int a = 0; a < L1; ++a) {
+          double fr, fi;
+          root(int64_t(a) * b, L1, &fr, &fi);
+          put_half(img, t.gb + kmajor_off(co * L1 + b, ci * L1 + a, 2 * L1), realpair(fr * sB, fi * sB, ci, co));
+          root(-int64_t(a) * b, L1, &fr, &fi);
+          put_half(img, t.gbi + kmajor_off(co * L1 + b, ci * L1 + a, 2 * L1), realpair(fr * sB, fi * sB, ci, co));
+        }
+  // stage A^-1 (contracts k2 -> n2), as the A operand: rows (c',n2), K (c,k2)
+  for (int co = 0; co < 2; ++co)
+    for (int n2 = 0; n2 < L2; ++n2)
+      for (int ci = 0; ci < 2; ++ci)
+        for (int k2 = 0; k2 < L2; ++k2) {
+          double fr, fi;
+          root(-int64_t(k2) * n2, L2, &fr, &fi);
+          put_half(img, t.gai + kmajor_off(co * L2 + n2, ci * L2 + k2, 2 * L2), realpair(fr * sA, fi * sA, ci, co));
+        }
+  // twiddles W_L^{n1 k2}, [n1][k2] float2, 128B-swizzled
+  for (int n1 = 0; n1 < L1; ++n1)
+    for (int k2 = 0; k2 < L2; ++k2) {
+      double wr, wi;
+      root(int64_t(n1) * k2, L, &wr, &wi);
+      float v[2] = {float(wr), float(wi)};
+      uint32_t o = uint32_t(n1 * L2 + k2) * 8;
+      o ^= (o >> 3) & 0x70u;
+      std::memcpy(img.data() + t.tw + o, v, 8);
+    }
+}
+
+// A13: keep(f) = prod_j keep_j[digit_j(f)], digits of f on the row-major
+// grid dims (slowest first); m[f] = keep(f) | keep((L - f) mod L).
+static fftconv_status_t build_mask(fftconv_plan_s* p, const fftconv_sparsity_t* s) {
+  if (s->ndims < 1 || s->ndims > 4) return FFTCONV_ERR_BAD_SPARSITY;
+  int64_t prod = 1;
+  for (int j = 0; j < s->ndims; ++j) {
+    if (s->dims[j] < 1 || !s->keep[j]) return FFTCONV_ERR_BAD_SPARSITY;
+    prod *= s->dims[j];
+  }
+  if (prod != p->L) return FFTCONV_ERR_BAD_SPARSITY;
+  const int64_t L = p->L;
+  auto keep = [&](int64_t f) {
+    int64_t rem = f;
+    for (int j = s->ndims - 1; j >= 0; --j) {
+      int64_t d = rem % s->dims[j];
+      rem /= s->dims[j];
+      if (!s->keep[j][d]) return false;
+    }
+    return true;
+  };
+  p->mask.assign(size_t(L), 0.0f);
+  int64_t zeros = 0;
+  for (int64_t f = 0; f < L; ++f) {
+    bool k = keep(f) || keep((L - f) % L);
+    p->mask[size_t(f)] = k ? 1.0f : 0.0f;
+    zeros += k ? 0 : 1;
+  }
+  p->sparse = true;
+  p->mask_fraction = double(zeros) / double(L);
+  // fraction of (k1) blocks whose whole column of k2 values is masked
+  int64_t skip = 0;
+  for (int k1 = 0; k1 < p->L1; ++k1) {
+    bool all0 = true;
+    for (int k2 = 0; k2 < p->L2 && all0; ++k2) all0 = p->mask[size_t(k2 + int64_t(p->L2) * k1)] == 0.0f;
+    skip += all0;
+  }
+  p->skip_fraction = double(skip) / double(p->L1);
+  return FFTCONV_OK;
+}
+
+}  // namespace fc
+
+using namespace fc;
+
+extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t fft_size, fftconv_dtype_t dtype,
+                                         int causal, const fftconv_sparsity_t* sparsity) {
+  if (!out) { set_last_error("fftconv_plan: out is NULL"); return FFTCONV_ERR_INVALID_ARG; }
+  if (N <= 0 || fft_size <= 0) { set_last_error("fftconv_plan: sizes must be positive"); return FFTCONV_ERR_INVALID_ARG; }
+  if (!is_pow2(N) || !is_pow2(fft_size)) {
+    set_last_error("fftconv_plan: N and fft_size must be powers of two");
+    return FFTCONV_ERR_NOT_POW2;
+  }
+  if (dtype != FFTCONV_F16 && dtype != FFTCONV_BF16 && dtype != FFTCONV_F32) {
+    set_last_error("fftconv_plan: unknown dtype");
+    return FFTCONV_ERR_INVALID_ARG;
+  }
+  if (!causal && fft_size != N) {
+    set_last_error("fftconv_plan: circular convolution needs fft_size == N");
+    return FFTCONV_ERR_INVALID_ARG;
+  }
+  fftconv_plan_s* p = new (std::nothrow) fftconv_plan_s();
+  if (!p) return FFTCONV_ERR_INVALID_ARG;
+  p->N = N;
+  p->L = fft_size;
+  p->causal = causal ? 1 : 0;
+  p->dtype = dtype;
+  if (causal && fft_size < 2 * N) {
+    p->regime = REGIME_PARTIAL;
+    p->chunk = fft_size / 2;
+  } else {
+    p->regime = REGIME_FUSED;
+  }
+  // Fused order-2 kernel family: L = L1 * 64, L1 in {8, 16, 32}.
+  const int64_t L = fft_size;
+  const bool fused_ok = (L >= 512 && L <= 2048) && (p->regime == REGIME_FUSED) &&
+                        (!causal || fft_size == 2 * N) && dtype != FFTCONV_F32;
+  if (!fused_ok) {
+    delete p;
+    set_last_error("fftconv_plan: this build supports the fused single-pass regime for fft_size 512..2048 "
+                   "(causal fft_size == 2N, or circular) with fp16/bf16 I/O");
+    return FFTCONV_ERR_UNSUPPORTED;
+  }
+  p->order = 2;
+  p->L2 = 64;
+  p->L1 = int32_t(L / 64);
+  p->KA = causal ? p->L2 / 2 : p->L2;
+  p->P = std::max(128 / p->L1, 2);
+  build_fused_tables(p);
+  if (sparsity) {
+    fftconv_status_t s = build_mask(p, sparsity);
+    if (s != FFTCONV_OK) {
+      delete p;
+      set_last_error("fftconv_plan: inconsistent sparsity pattern (prod(dims) must equal fft_size)");
+      return s;
+    }
+    // the mask rides at the end of the table image (read by precompute_kf)
+    const size_t mo = p->image.size();
+    p->image.resize(mo + p->mask.size() * sizeof(float));
+    std::memcpy(p->image.data() + mo, p->mask.data(), p->mask.size() * sizeof(float));
+  }
+  p->kf_bytes_per_head = size_t(L) * 8;  // complex fp32, [k2][k1], swizzled
+  p->ws_bytes_per_head = size_t(L) * 8;  // fp32 spectral accumulator for dk
+  *out = p;
+  set_last_error("");
+  return FFTCONV_OK;
+}
+
+extern "C" fftconv_status_t fftconv_plan_info(fftconv_plan_t p, fftconv_plan_info_t* info) {
+  if (!p || !info) { set_last_error("fftconv_plan_info: NULL argument"); return FFTCONV_ERR_INVALID_ARG; }
+  std::memset(info, 0, sizeof(*info));
+  info->N = p->N;
+  info->fft_size = p->L;
+  info->causal = p->causal;
+  info->dtype = p->dtype;
+  info->regime = p->regime;
+  info->order = p->order;
+  info->factors[0] = p->L1;
+  info->factors[1] = p->L2;
+  info->rows_per_tile = 2 * p->P;
+  info->max_kernel_len = p->causal ? p->L / 2 : p->L;
+  info->table_bytes = p->image.size();
+  info->kf_bytes_per_head = p->kf_bytes_per_head;
+  info->workspace_bytes_per_head = p->ws_bytes_per_head;
+  info->mask_fraction = p->mask_fraction;
+  info->skip_fraction = p->skip_fraction;
+  return FFTCONV_OK;
+}
+
+extern "C" void fftconv_plan_destroy(fftconv_plan_t p) { delete p; }
+
+extern "C" const char* fftconv_last_error(void) { return fc::g_last_error.c_str(); }
+
+// Host-side cost model hooks (tests pin them to the paper's A100 grouping).
+extern "C" double fftconv_cost_eq2(int64_t N, int32_t p, double mu, double sigma_h, double sigma_s, double tau_m,
+                                   double tau_g, double sram_bytes) {
+  CostConstants c{mu, sigma_h, sigma_s, tau_m, tau_g, sram_bytes};
+  auto f = factorize(N, p);
+  if (f.empty()) return -1.0;
+  return cost_eq2(N, f, c, 1.0);
+}
+extern "C" int32_t fftconv_select_order(int64_t N, double mu, double sigma_h, double sigma_s, double tau_m,
+                                        double tau_g, double sram_bytes) {
+  CostConstants c{mu, sigma_h, sigma_s, tau_m, tau_g, sram_bytes};
+  return select_order(N, c, nullptr);
+}
+extern "C" int32_t fftconv_factorize(int64_t n, int32_t p, int64_t* out) {
+  auto f = factorize(n, p);
+  for (size_t i = 0; i < f.size(); ++i) out[i] = f[i];
+  return int32_t(f.size());
+}

@@ -1,0 +1,63 @@
+// plan.h -- internal plan structure shared by the host planner (plan.cpp)
+// and the launch code (api.cu).  Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "fftconv.h"
+
+namespace fc {
+
+enum Regime : int32_t { REGIME_FUSED = 1, REGIME_PARTIAL = 2 };
+
+// Byte offsets of the constant tables inside the uploaded device image.
+// Each table is stored exactly as the fused kernel wants it in shared memory
+// (SWIZZLE_NONE canonical UMMA layouts for the DFT matrices, 128-byte XOR
+// swizzle for the fp32 twiddle table), so the kernel copies it linearly.
+struct TableLayout {
+  size_t ga = 0, ga_bytes = 0;    // stage A  : B operand, K-major, rows (c',k2) 2*L2, K (c,n2) 2*KA
+  size_t gb = 0, gb_bytes = 0;    // stage B  : B operand, K-major, rows (c',k1) 2*L1, K (c,n1) 2*L1
+  size_t gbi = 0, gbi_bytes = 0;  // stage B^-1
+  size_t gai = 0, gai_bytes = 0;  // stage A^-1: A operand, K-major, rows (c',n2) 2*L2, K (c,k2) 2*L2
+  size_t tw = 0, tw_bytes = 0;    // W_L^{n1 k2}, [L1][L2] float2, swizzled
+  size_t total = 0;
+};
+
+}  // namespace fc
+
+struct fftconv_plan_s {
+  int64_t N = 0;         // input length per row
+  int64_t L = 0;         // fft_size
+  int32_t causal = 1;
+  fftconv_dtype_t dtype = FFTCONV_F16;
+  int32_t regime = fc::REGIME_FUSED;
+  int32_t order = 2;
+  int32_t L1 = 0, L2 = 0;  // L = L1 * L2 ; n = n1 + L1*n2 ; f = k2 + L2*k1
+  int32_t KA = 0;          // contracted length of stage A (L2/2 causal, L2 circular)
+  int32_t P = 0;           // row pairs per tile (two-row real packing)
+  int64_t chunk = 0;       // partial regime: chunk length (= L/2)
+  fc::TableLayout tl;
+  std::vector<uint8_t> image;  // host copy of the table image
+  void* d_tables = nullptr;    // bound by fftconv_plan_upload
+  // frequency sparsity (A13)
+  bool sparse = false;
+  std::vector<float> mask;     // length L, 0/1, Hermitian-symmetric
+  double mask_fraction = 0.0;
+  double skip_fraction = 0.0;
+  size_t kf_bytes_per_head = 0;
+  size_t ws_bytes_per_head = 0;
+  int32_t sram_smem_bytes = 0;  // dynamic shared memory of the fused kernel
+};
+
+namespace fc {
+// Eq. 2 cost model -- host planner utilities, exported for tests.
+struct CostConstants {
+  double mu, sigma_h, sigma_s, tau_m, tau_g, sram_bytes;
+};
+double cost_eq2(int64_t N, const std::vector<int64_t>& factors, const CostConstants& c, double BH);
+int select_order(int64_t N, const CostConstants& c, std::vector<int64_t>* factors_out);
+std::vector<int64_t> factorize(int64_t n, int p);
+void set_last_error(const std::string& msg);
+}  // namespace fc

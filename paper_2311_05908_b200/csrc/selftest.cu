@@ -1,0 +1,87 @@
+// selftest.cu -- device self-test hooks for the sm_100a primitives the fused
+// FFT-conv kernels are built from (not part of the fftconv C-ABI).
+//
+// fcst_mma(): one CTA stages A (M x K) and B (K x N) fp16 into shared memory
+// in the SWIZZLE_NONE canonical layout selected by a_mn / b_mn, issues
+// K/16 tcgen05.mma.kind::f16 instructions accumulating into TMEM, and reads
+// D (M x N fp32) back with tcgen05.ld.  Used by tests/test_gpu_primitives.py
+// to pin the descriptor encodings against a host matmul.
+#include <cuda_runtime.h>
+#include "sm100.cuh"
+
+namespace {
+
+__device__ uint32_t canon_off(int r, int k, int R, int K, bool mn_major) {
+  // r = M (or N) index, k = K index; returns byte offset.
+  if (mn_major) {
+    const uint32_t sbo = 128, lbo = (R / 8) * 128;
+    return (r / 8) * sbo + (k / 8) * lbo + (k % 8) * 16 + (r % 8) * 2;
+  } else {
+    const uint32_t lbo = 128, sbo = (K / 8) * 128;
+    return (r / 8) * sbo + (k / 8) * lbo + (r % 8) * 16 + (k % 8) * 2;
+  }
+}
+
+__global__ void __launch_bounds__(128, 1)
+    mma_selftest_kernel(const __half* A, const __half* B, float* D, int M, int N, int K, int a_mn, int b_mn) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + M * K * 2;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < M * K; i += blockDim.x) {
+    int m = i / K, k = i % K;
+    *reinterpret_cast<__half*>(sA + canon_off(m, k, M, K, a_mn)) = A[i];
+  }
+  for (int i = tid; i < K * N; i += blockDim.x) {
+    int k = i / N, n = i % N;
+    *reinterpret_cast<__half*>(sB + canon_off(n, k, N, K, b_mn)) = B[i];
+  }
+  if (tid == 0) {
+    fc::mbar_init(&bar, 1);
+    fc::fence_barrier_init();
+  }
+  if (tid < 32) fc::tmem_alloc<256>(&tmem_base);
+  fc::fence_async_smem();
+  fc::tc_fence_before();
+  __syncthreads();
+  fc::tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  if (tid == 0) {
+    const uint32_t idesc = fc::idesc_f16(M, N, a_mn, b_mn);
+    const uint32_t a0 = fc::smem_u32(sA), b0 = fc::smem_u32(sB);
+    for (int s = 0; s < K / 16; ++s) {
+      uint64_t ad, bd;
+      if (a_mn) ad = fc::smem_desc(a0 + 2 * s * (M / 8) * 128, (M / 8) * 128, 128);
+      else      ad = fc::smem_desc(a0 + s * 256, 128, (K / 8) * 128);
+      if (b_mn) bd = fc::smem_desc(b0 + 2 * s * (N / 8) * 128, (N / 8) * 128, 128);
+      else      bd = fc::smem_desc(b0 + s * 256, 128, (K / 8) * 128);
+      fc::mma_f16_ss(tbase, ad, bd, idesc, s > 0);
+    }
+    fc::mma_commit(&bar);
+  }
+  fc::mbar_wait(&bar, 0);
+  fc::tc_fence_after();
+  const int warp = tid / 32;
+  for (int c = 0; c < N; c += 8) {
+    float v[8];
+    fc::tmem_ld8(tbase + ((uint32_t)(warp * 32) << 16) + c, v);
+    fc::tmem_ld_wait();
+    for (int j = 0; j < 8; ++j) D[tid * N + c + j] = v[j];
+  }
+  fc::tc_fence_before();
+  __syncthreads();
+  if (tid < 32) fc::tmem_dealloc<256>(tbase);
+}
+
+}  // namespace
+
+extern "C" int fcst_mma(const void* A, const void* B, void* D, int M, int N, int K, int a_mn, int b_mn) {
+  if (M != 128 || N % 16 || N < 16 || N > 256 || K % 16) return 1;
+  size_t smem = (size_t)(M + N) * K * 2;
+  cudaFuncSetAttribute(mma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  mma_selftest_kernel<<<1, 128, smem>>>((const __half*)A, (const __half*)B, (float*)D, M, N, K, a_mn, b_mn);
+  cudaError_t e = cudaDeviceSynchronize();
+  return e == cudaSuccess ? 0 : 100 + (int)e;
+}

@@ -1,0 +1,143 @@
+"""PyTorch-facing binding of libfftconv.so.
+
+PyTorch supplies device memory and the current CUDA stream only; this module
+marshals pointers and sizes into the C ABI (include/fftconv.h) with the same
+entry-point names.  It performs no arithmetic of the method.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _abi
+
+_DT = {torch.float16: _abi.FFTCONV_F16, torch.bfloat16: _abi.FFTCONV_BF16, torch.float32: _abi.FFTCONV_F32}
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream(device=None):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _aligned_empty(nbytes: int, device, align: int = 1024):
+    """uint8 device buffer whose data_ptr is `align`-byte aligned."""
+    raw = torch.empty(nbytes + align, dtype=torch.uint8, device=device)
+    off = (-raw.data_ptr()) % align
+    return raw[off:off + nbytes]
+
+
+@dataclass
+class PlanInfo:
+    N: int
+    fft_size: int
+    causal: bool
+    regime: int
+    order: int
+    factors: tuple
+    rows_per_tile: int
+    max_kernel_len: int
+    table_bytes: int
+    kf_bytes_per_head: int
+    workspace_bytes_per_head: int
+    mask_fraction: float
+    skip_fraction: float
+
+
+class FFTConvPlan:
+    """fftconv_plan + fftconv_plan_upload.  `sparsity` = (dims, keep_masks)
+    with dims slowest-first and keep_masks a list of 0/1 sequences."""
+
+    def __init__(self, N: int, fft_size: int | None = None, dtype=torch.float16, causal: bool = True,
+                 sparsity=None, device="cuda"):
+        L = _abi.lib()
+        fft_size = int(fft_size if fft_size is not None else (2 * N if causal else N))
+        self.dtype = dtype
+        self.device = torch.device(device)
+        sp = None
+        self._keep_bufs = []
+        if sparsity is not None:
+            dims, keeps = sparsity
+            sp = _abi.Sparsity()
+            sp.ndims = len(dims)
+            for j, (d, kp) in enumerate(zip(dims, keeps)):
+                sp.dims[j] = int(d)
+                buf = (ctypes.c_uint8 * int(d))(*[1 if x else 0 for x in kp])
+                self._keep_bufs.append(buf)
+                sp.keep[j] = ctypes.cast(buf, ctypes.POINTER(ctypes.c_uint8))
+        h = ctypes.c_void_p()
+        _abi.check(L.fftconv_plan(ctypes.byref(h), int(N), fft_size, _DT[dtype], int(bool(causal)),
+                                  ctypes.byref(sp) if sp is not None else None))
+        self._h = h
+        info = _abi.PlanInfo()
+        _abi.check(L.fftconv_plan_info(h, ctypes.byref(info)))
+        self.info = PlanInfo(info.N, info.fft_size, bool(info.causal), info.regime, info.order,
+                             tuple(info.factors[:max(info.order, 2)]), info.rows_per_tile,
+                             info.max_kernel_len, info.table_bytes, info.kf_bytes_per_head,
+                             info.workspace_bytes_per_head, info.mask_fraction, info.skip_fraction)
+        with torch.cuda.device(self.device):
+            self.tables = _aligned_empty(info.table_bytes, self.device)
+            _abi.check(L.fftconv_plan_upload(h, _ptr(self.tables), _stream(self.device)))
+
+    @property
+    def N(self):
+        return self.info.N
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _abi.lib().fftconv_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ------------------------------------------------------------------ calls
+    def precompute_kf(self, k: torch.Tensor) -> torch.Tensor:
+        """k: (H, K) fp32 on device -> opaque k_f buffer (H * kf_bytes_per_head)."""
+        assert k.dtype == torch.float32 and k.is_cuda and k.dim() == 2
+        k = k.contiguous()
+        H, K = k.shape
+        kf = _aligned_empty(max(H, 1) * self.info.kf_bytes_per_head, k.device, 16)
+        _abi.check(_abi.lib().fftconv_precompute_kf(self._h, _ptr(k), H, K, _ptr(kf), _stream(k.device)))
+        return kf
+
+    def _check_sig(self, *ts):
+        for t in ts:
+            assert t.is_cuda and t.dtype == self.dtype and t.is_contiguous() and t.dim() == 3
+            assert t.shape[-1] == self.info.N, (t.shape, self.info.N)
+
+    def fwd(self, u: torch.Tensor, kf: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        self._check_sig(u)
+        B, H, _ = u.shape
+        y = torch.empty_like(u) if out is None else out
+        _abi.check(_abi.lib().fftconv_fwd(self._h, _ptr(u), _ptr(kf), _ptr(y), B, H, None, _stream(u.device)))
+        return y
+
+    def gated_fwd(self, u, w, v, kf, out=None):
+        self._check_sig(u, w, v)
+        B, H, _ = u.shape
+        y = torch.empty_like(u) if out is None else out
+        _abi.check(_abi.lib().fftconv_gated_fwd(self._h, _ptr(u), _ptr(w), _ptr(v), _ptr(kf), _ptr(y), B, H,
+                                                None, _stream(u.device)))
+        return y
+
+    def bwd(self, dy, u, kf, K, w=None, v=None):
+        self._check_sig(dy, u)
+        B, H, _ = u.shape
+        du = torch.empty_like(u)
+        dw = torch.empty_like(u) if w is not None else None
+        dv = torch.empty_like(u) if v is not None else None
+        dk = torch.empty(H, K, dtype=torch.float32, device=u.device)
+        ws = torch.empty(max(H, 1) * self.info.workspace_bytes_per_head, dtype=torch.uint8, device=u.device)
+        _abi.check(_abi.lib().fftconv_bwd(self._h, _ptr(dy), _ptr(u), _ptr(w), _ptr(v), _ptr(kf), _ptr(du),
+                                          _ptr(dw), _ptr(dv), _ptr(dk), B, H, K, _ptr(ws), _stream(u.device)))
+        return {"du": du, "dw": dw, "dv": dv, "dk": dk}
+
+
+def launch_count_reset() -> int:
+    return int(_abi.lib().fftconv_launch_count_reset())

@@ -1,0 +1,130 @@
+"""GPU parity of the fused forward kernels against the fp64 oracle.
+
+Inputs are seeded synthetic (synth/), quantised to the I/O dtype on the host
+so both sides consume identical values.  Bar (BASELINE.json north_star):
+rel-L2 <= 2e-3 and max-abs <= 1e-2 * max|y| for fp16/bf16 I/O."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import oracle as orc
+
+torch = pytest.importorskip("torch")
+
+REL_L2 = 2e-3
+MAX_ABS = 1e-2
+
+TDT = {"f16": torch.float16, "bf16": torch.bfloat16}
+
+
+def _run(N, causal, dtype, gated, B, H, seed=0, filt="decay"):
+    from paper_2311_05908_b200 import FFTConvPlan
+    plan = FFTConvPlan(N, dtype=TDT[dtype], causal=causal)
+    K = N
+    u = synth.quantize(synth.signal(seed, "u", B, H, N), dtype)
+    k = (synth.decay_filters(seed, H, K) if filt == "decay" else synth.flat_filters(seed, H, K)).astype(np.float32)
+    dev = "cuda"
+    tu = torch.tensor(u, dtype=TDT[dtype], device=dev)
+    tk = torch.tensor(k, device=dev)
+    kf = plan.precompute_kf(tk)
+    if gated:
+        w = synth.quantize(synth.signal(seed, "w", B, H, N), dtype)
+        v = synth.quantize(synth.signal(seed, "v", B, H, N), dtype)
+        y = plan.gated_fwd(tu, torch.tensor(w, dtype=TDT[dtype], device=dev),
+                           torch.tensor(v, dtype=TDT[dtype], device=dev), kf)
+        ref = orc.conv_fwd(u, k.astype(np.float64), causal=causal, w=w, v=v)
+    else:
+        y = plan.fwd(tu, kf)
+        ref = orc.conv_fwd(u, k.astype(np.float64), causal=causal)
+    torch.cuda.synchronize()
+    got = y.float().cpu().numpy().astype(np.float64)
+    return got, ref
+
+
+def _assert_close(got, ref):
+    assert np.all(np.isfinite(got))
+    rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+    mx = np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-30)
+    assert rel <= REL_L2 and mx <= MAX_ABS, (rel, mx)
+    return rel, mx
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [256, 512, 1024])
+@pytest.mark.parametrize("dtype", ["f16", "bf16"])
+@pytest.mark.parametrize("gated", [False, True])
+def test_fwd_causal_parity(N, dtype, gated):
+    # B = 37 is ragged (not a multiple of the tile's row count) and odd
+    got, ref = _run(N, True, dtype, gated, B=37, H=3)
+    _assert_close(got, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [512, 1024, 2048])
+@pytest.mark.parametrize("gated", [False, True])
+def test_fwd_circular_parity(N, gated):
+    got, ref = _run(N, False, "f16", gated, B=6, H=2)
+    _assert_close(got, ref)
+
+
+@pytest.mark.gpu
+def test_fwd_cfg1_direct_sum():
+    """cfg 1: causal fp16, B=1, H=4, N=256, checked against the direct sum."""
+    got, _ = _run(256, True, "f16", False, B=1, H=4, seed=1)
+    u = synth.quantize(synth.signal(1, "u", 1, 4, 256), "f16")
+    k = synth.decay_filters(1, 4, 256).astype(np.float32).astype(np.float64)
+    ref = np.stack([[orc.direct_conv(u[0, h], k[h], True) for h in range(4)]])
+    _assert_close(got, ref)
+
+
+@pytest.mark.gpu
+def test_fwd_flat_filter_and_empty():
+    got, ref = _run(1024, True, "f16", True, B=2, H=5, filt="flat")
+    _assert_close(got, ref)
+    from paper_2311_05908_b200 import FFTConvPlan
+    plan = FFTConvPlan(1024)
+    kf = plan.precompute_kf(torch.zeros(3, 1024, device="cuda"))
+    y = plan.fwd(torch.zeros(0, 3, 1024, dtype=torch.float16, device="cuda"), kf)
+    assert y.shape == (0, 3, 1024)
+
+
+@pytest.mark.gpu
+def test_fwd_delta_filter_identity():
+    from paper_2311_05908_b200 import FFTConvPlan
+    N = 1024
+    plan = FFTConvPlan(N)
+    k = torch.zeros(2, N, device="cuda")
+    k[:, 0] = 1.0
+    kf = plan.precompute_kf(k)
+    u = torch.tensor(synth.quantize(synth.signal(3, "u", 4, 2, N), "f16"), dtype=torch.float16, device="cuda")
+    y = plan.fwd(u, kf)
+    err = (y.float() - u.float()).abs().max().item()
+    assert err < 2e-3 * u.float().abs().max().item()
+
+
+@pytest.mark.gpu
+def test_fwd_cfg2_full_size_sampled():
+    """cfg 2 at full size (gated, B=64, H=768, N=1024, fp16), launch config of
+    bench.py; sampled outputs checked one by one against the direct sum."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    B, H, N = 64, 768, 1024
+    plan = FFTConvPlan(N, dtype=torch.float16)
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(B * H, 48, replace=False))
+    u = synth.quantize(synth.signal(5, "u", B, H, N), "f16")
+    w = synth.quantize(synth.signal(5, "w", B, H, N), "f16")
+    v = synth.quantize(synth.signal(5, "v", B, H, N), "f16")
+    k = synth.decay_filters(5, H, N).astype(np.float32)
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    y = plan.gated_fwd(*(torch.tensor(a, dtype=torch.float16, device="cuda") for a in (u, w, v)), kf)
+    y = y.float().cpu().numpy().reshape(B * H, N)
+    u2, w2, v2 = u.reshape(B * H, N), w.reshape(B * H, N), v.reshape(B * H, N)
+    got, ref = [], []
+    for r in rows:
+        h = r % H
+        for i in rng.choice(N, 8, replace=False):
+            ref.append(v2[r, i] * orc.direct_point(u2[r], k[h].astype(np.float64), i, wrow=w2[r]))
+            got.append(y[r, i])
+    got, ref = np.array(got), np.array(ref)
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert rel < REL_L2, rel
