@@ -22,12 +22,19 @@
 //               when causal]
 // Every stage is one or more tcgen05.mma.kind::f16 (fp16 operands, fp32
 // accumulators in TMEM); complex arithmetic is a real-pair GEMM with the
-// real/imag planes stacked in K.  The elementwise steps between stages run
-// on TMEM -> registers -> shared memory, where the write layout performs the
-// "permutation as transpose" of P:226-234 for free: each stage's operand is
-// written directly in the canonical UMMA layout (MN-major or K-major) the next
-// MMA reads.  Gating (u*w on load, *v on store) is fused.
+// real/imag planes stacked in K.  Stages followed by a complex multiply also
+// emit a negated copy of one plane (an extra block of N columns -- tensor
+// cores are idle in this HBM-bound regime) so the multiply is two FMUL2 and
+// two FFMA2 per element pair with no sign fix-ups.
+// The elementwise steps between stages run TMEM -> registers -> shared
+// memory, where the write layout performs the "permutation as transpose" of
+// P:226-234 for free: each stage's operand is written directly in the
+// canonical UMMA layout (MN-major or K-major) the next MMA reads.  Gating
+// (u*w on load, *v on store) is fused.  16 warps split every
+// elementwise phase by TMEM column slices.
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include "fwd_params.h"
 #include "sm100.cuh"
@@ -69,6 +76,8 @@ struct IO<__nv_bfloat16> {
   }
 };
 
+constexpr int kWGThreads = 256;        // 8 warps: 4 TMEM lane quadrants x 2 column slices
+
 template <int L1, bool CAUSAL>
 struct O2Cfg {
   static constexpr int L2 = 64;
@@ -78,9 +87,11 @@ struct O2Cfg {
   static constexpr int KA = CAUSAL ? L2 / 2 : L2;
   static constexpr int NOUT = CAUSAL ? L / 2 : L;  // row length N
   static constexpr int CH = NOUT / 8;           // 16-byte chunks per row (16-bit I/O)
+  static constexpr int NA = 3 * L2;             // stage A N: re | im | -im
+  static constexpr int NB = (3 * L1 + 15) / 16 * 16;  // stage B/B^-1 N: re | im | -im (-re) | pad
   // tables (same offsets as the host image, see plan.cpp)
-  static constexpr uint32_t GA_BYTES = 2 * L2 * 2 * KA * 2;
-  static constexpr uint32_t GB_BYTES = 2 * L1 * 2 * L1 * 2;
+  static constexpr uint32_t GA_BYTES = NA * 2 * KA * 2;
+  static constexpr uint32_t GB_BYTES = NB * 2 * L1 * 2;
   static constexpr uint32_t GAI_BYTES = 2 * L2 * 2 * L2 * 2;
   static constexpr uint32_t TW_BYTES = L * 8;
   static constexpr uint32_t al(uint32_t x) { return (x + 1023u) / 1024u * 1024u; }
@@ -88,61 +99,94 @@ struct O2Cfg {
   static constexpr uint32_t OFF_GB = al(OFF_GA + GA_BYTES);
   static constexpr uint32_t OFF_GBI = al(OFF_GB + GB_BYTES);
   static constexpr uint32_t OFF_GAI = al(OFF_GBI + GB_BYTES);
-  static constexpr uint32_t OFF_TW = al(OFF_GAI + GAI_BYTES);
-  static constexpr uint32_t TABLES = al(OFF_TW + TW_BYTES);
-  // working buffers
-  static constexpr uint32_t KF_BYTES = L * 8;
-  static constexpr uint32_t BUFA_BYTES = 128 * 2 * KA * 2;     // stage A operand
-  static constexpr uint32_t BUFX_BYTES = P * L * 4;            // complex fp16 per tile
-  static constexpr bool STAGE = CAUSAL;                        // cp.async prefetch staging
-  static constexpr uint32_t ST_BYTES = STAGE ? R * NOUT * 2 : 0;
-  static constexpr uint32_t OFF_KF = TABLES;
-  static constexpr uint32_t OFF_BUFA = al(OFF_KF + KF_BYTES);
-  static constexpr uint32_t OFF_BUFX = al(OFF_BUFA + BUFA_BYTES);
-  static constexpr uint32_t OFF_STU = al(OFF_BUFX + BUFX_BYTES);
-  static constexpr uint32_t OFF_STW = al(OFF_STU + ST_BYTES);
-  static constexpr uint32_t SMEM = al(OFF_STW + ST_BYTES) + 1024;  // + alignment slack
+  static constexpr uint32_t OFF_TW = al(OFF_GAI + GAI_BYTES);   // [n1][k2/2] {wr,wr',wi,wi'}
+  static constexpr uint32_t OFF_TWT = al(OFF_TW + TW_BYTES);    // [k2][n1/2] {wr,wr',wi,wi'}
+  static constexpr uint32_t TABLES = al(OFF_TWT + TW_BYTES);
+  // per-warpgroup working buffers
+  static constexpr uint32_t KF_BYTES = L * 8;                  // [k2][k1/2] {kr,kr',ki,ki'}
+  static constexpr uint32_t BUFX_BYTES = P * L * 4;            // complex fp16 per tile (stage A operand aliases it)
+  static constexpr uint32_t WG_BYTES = al(KF_BYTES) + al(BUFX_BYTES);
+  static constexpr uint32_t OFF_WG = TABLES;
+  // two independent tile pipelines when both fit in shared memory, else one
+  static constexpr int WG = (OFF_WG + 2 * WG_BYTES + 1024 <= 227 * 1024) ? 2 : 1;
+  static constexpr int THREADS = WG * kWGThreads;
+  static constexpr uint32_t SMEM = OFF_WG + WG * WG_BYTES + 1024;  // + alignment slack
   // operand strides
-  static constexpr uint32_t SBO_A = (2 * KA / 8) * 128;   // bufA: MN-group stride (K groups contiguous)
+  static constexpr uint32_t SBO_A = (2 * KA / 8) * 128;   // stage A operand: MN-group stride (K groups contiguous)
   static constexpr uint32_t LBO_B = (P * L2 / 8) * 128;   // epi1 -> stage B (MN-major, K-group stride)
   static constexpr uint32_t SBO_BP = (2 * L1 / 8) * 128;  // epi2 -> stage B^-1 (K-major, row-group stride)
   static constexpr uint32_t SBO_GB = (2 * L1 / 8) * 128;  // G_B / G_B^-1 row-group stride
   static constexpr uint32_t SBO_GA = (2 * KA / 8) * 128;
   static constexpr uint32_t SBO_GAI = (2 * L2 / 8) * 128;
   static constexpr uint32_t SBO_XA = (2 * L2 / 8) * 128;  // epi3 -> stage A^-1 (MN-major B, N-group stride)
+  static constexpr uint32_t TMEM_COLS = 256;              // per warpgroup
   static_assert(P * L1 == 128, "stage A covers one 128-row MMA group");
-  static_assert(P % 2 == 0, "stage B groups hold two pairs");
+  static_assert(P % 4 == 0, "stage B halves hold whole groups of two pairs");
+  static_assert((P / 2) * NB <= 256 && NA <= 256, "TMEM budget");
+  static_assert(128 * 2 * KA * 2 <= BUFX_BYTES, "stage A operand fits in bufX");
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
-// Complex multiply helpers (fp32).
-FC_DEVICE void cmul(float& xr, float& xi, float wr, float wi) {
-  float r = xr * wr - xi * wi;
-  float i = xr * wi + xi * wr;
-  xr = r;
-  xi = i;
-}
-FC_DEVICE void cmulc(float& xr, float& xi, float wr, float wi) {  // x * conj(w)
-  float r = xr * wr + xi * wi;
-  float i = xi * wr - xr * wi;
-  xr = r;
-  xi = i;
+FC_DEVICE void st_half8(uint32_t addr, const float* v) {
+  st_shared_v4(addr, pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
+               pack_half2(v[6], v[7]));
 }
 
+// x <- x * w for 8 consecutive elements held as planes (xr, xi, -xi);
+// w given as 4 float4 {wr_j, wr_j+1, wi_j, wi_j+1}.
+FC_DEVICE void cmul8(float* xr, float* xi, const float* nxi, const float4* w) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 r = make_float2(xr[2 * j], xr[2 * j + 1]);
+    const float2 i = make_float2(xi[2 * j], xi[2 * j + 1]);
+    const float2 ni = make_float2(nxi[2 * j], nxi[2 * j + 1]);
+    const float2 wr = make_float2(w[j].x, w[j].y), wi = make_float2(w[j].z, w[j].w);
+    const float2 orr = fma2(r, wr, mul2(ni, wi));
+    const float2 oi = fma2(i, wr, mul2(r, wi));
+    xr[2 * j] = orr.x; xr[2 * j + 1] = orr.y;
+    xi[2 * j] = oi.x;  xi[2 * j + 1] = oi.y;
+  }
+}
+// x <- x * conj(w); planes (xr, xi, -xr).
+FC_DEVICE void cmulc8(float* xr, float* xi, const float* nxr, const float4* w) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 r = make_float2(xr[2 * j], xr[2 * j + 1]);
+    const float2 i = make_float2(xi[2 * j], xi[2 * j + 1]);
+    const float2 nr = make_float2(nxr[2 * j], nxr[2 * j + 1]);
+    const float2 wr = make_float2(w[j].x, w[j].y), wi = make_float2(w[j].z, w[j].w);
+    const float2 orr = fma2(r, wr, mul2(i, wi));
+    const float2 oi = fma2(i, wr, mul2(nr, wi));
+    xr[2 * j] = orr.x; xr[2 * j + 1] = orr.y;
+    xi[2 * j] = oi.x;  xi[2 * j + 1] = oi.y;
+  }
+}
+
+// Each CTA runs kWG independent warpgroups; warpgroup g processes tiles
+// t0 + g, t0 + g + kWG, ... of the CTA's contiguous tile range, with its own
+// TMEM columns, mbarriers, named barrier, k_f copy and operand buffer, so one
+// warpgroup's MMAs, memory waits and barriers overlap the other's math.
 template <int L1, bool CAUSAL, bool GATED, typename T>
-__global__ void __launch_bounds__(128, 1) fftconv_fwd_o2_kernel(const FwdParams prm) {
+__global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_kernel(const FwdParams prm) {
   using C = O2Cfg<L1, CAUSAL>;
+  constexpr int kWG = C::WG;
+  constexpr int kThreads = C::THREADS;
   constexpr int L2 = C::L2;
   extern __shared__ uint8_t smem_raw[];
-  __shared__ uint64_t mma_bar;
+  __shared__ uint64_t mma_bar[kWG][2];  // completion of the first / second half of a stage
   __shared__ uint32_t tmem_slot;
-  // 1024-aligned base
-  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;  // 1024-aligned
   const uint32_t sGA = base + C::OFF_GA, sGB = base + C::OFF_GB, sGBI = base + C::OFF_GBI,
-                 sGAI = base + C::OFF_GAI, sTW = base + C::OFF_TW, sKF = base + C::OFF_KF,
-                 bufA = base + C::OFF_BUFA, bufX = base + C::OFF_BUFX, stU = base + C::OFF_STU,
-                 stW = base + C::OFF_STW;
+                 sGAI = base + C::OFF_GAI, sTW = base + C::OFF_TW, sTWT = base + C::OFF_TWT;
 
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wg = warp >> 3;              // warpgroup
+  const int wtid = tid & (kWGThreads - 1);
+  const int quad = warp & 3;             // TMEM lane quadrant this warp may access
+  const int slice = (warp >> 2) & 1;     // column slice 0..1
+  const int m = quad * 32 + lane;        // TMEM lane / MMA row owned by this thread
+  const uint32_t sKF = base + C::OFF_WG + wg * C::WG_BYTES;
+  const uint32_t bufX = sKF + C::al(C::KF_BYTES);
   const int64_t B = prm.B, H = prm.H, N = prm.N;
   const int64_t nbt = (B + C::R - 1) / C::R;
   const int64_t tiles = H * nbt;
@@ -155,284 +199,305 @@ __global__ void __launch_bounds__(128, 1) fftconv_fwd_o2_kernel(const FwdParams 
   T* __restrict__ gy = reinterpret_cast<T*>(prm.y);
   const uint8_t* __restrict__ gkf = reinterpret_cast<const uint8_t*>(prm.kf);
 
-  // ---- one-time setup: tables -> smem, barrier, TMEM
+  // ---- one-time setup: tables -> smem, barriers, TMEM (both warpgroups)
   {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.tables);
-    for (uint32_t o = tid * 16; o < C::TABLES; o += 128 * 16) cp_async16(base + o, src + o, true);
+    for (uint32_t o = tid * 16; o < C::TABLES; o += kThreads * 16) cp_async16(base + o, src + o, true);
     cp_async_commit();
   }
   if (tid == 0) {
-    mbar_init(&mma_bar, 1);
+    for (int g = 0; g < kWG; ++g) {
+      mbar_init(&mma_bar[g][0], 1);
+      mbar_init(&mma_bar[g][1], 1);
+    }
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc<128>(&tmem_slot);
-
-  // ---- input staging (cp.async prefetch) of tile t
-  auto issue_input = [&](int64_t t) {
-    const int64_t h = t / nbt, bt = t % nbt;
-    for (int q = tid; q < C::R * C::CH; q += 128) {
-      const int r = q / C::CH, pos = q % C::CH;
-      const int64_t b = bt * C::R + r;
-      const bool ok = b < B;
-      const int64_t goff = ((ok ? b : 0) * H + h) * N + int64_t(pos) * 8;
-      const uint32_t so = swz128(uint32_t(q) * 16);
-      cp_async16(stU + so, gu + goff, ok);
-      if (GATED) cp_async16(stW + so, gw + goff, ok);
-    }
-    cp_async_commit();
-  };
-
-  // ---- staging (or global) -> bufA, gating u*w, fp16 operand
-  auto convert_input = [&](int64_t t) {
-    const int64_t h = t / nbt, bt = t % nbt;
-    constexpr int KROWS = C::KA;                 // n2 rows per row
-    constexpr int JC = L1 / 8;                   // 8-element n1 chunks
-    for (int q = tid; q < C::R * C::CH; q += 128) {
-      // n2 fastest so 8 consecutive threads fill one 128 B core matrix
-      const int n2 = q % KROWS;
-      const int j = (q / KROWS) % JC;
-      const int r = q / (KROWS * JC);
-      const int pos = n2 * JC + j;  // chunk index in the row (n = 8*pos)
-      float g[8];
-      if (C::STAGE) {
-        const uint32_t so = swz128(uint32_t(r * C::CH + pos) * 16);
-        uint4 uv = ld_shared_u4(stU + so);
-        IO<T>::to_f32x8(uv, g);
-        if (GATED) {
-          float wv[8];
-          IO<T>::to_f32x8(ld_shared_u4(stW + so), wv);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) g[e] *= wv[e];
-        }
-      } else {
-        const int64_t b = bt * C::R + r;
-        if (b < B) {
-          const int64_t goff = (b * H + h) * N + int64_t(pos) * 8;
-          uint4 uv = *reinterpret_cast<const uint4*>(gu + goff);
-          IO<T>::to_f32x8(uv, g);
-          if (GATED) {
-            float wv[8];
-            IO<T>::to_f32x8(*reinterpret_cast<const uint4*>(gw + goff), wv);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) g[e] *= wv[e];
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) g[e] = 0.f;
-        }
-      }
-      const int p = r >> 1, c = r & 1;
-      const int mg = p * JC + j;
-      const int k = c * C::KA + n2;
-      const uint32_t off = mg * C::SBO_A + (k >> 3) * 128 + (k & 7) * 16;
-      st_shared_v4(bufA + off, pack_half2(g[0], g[1]), pack_half2(g[2], g[3]), pack_half2(g[4], g[5]),
-                   pack_half2(g[6], g[7]));
-    }
-  };
-
+  if (warp == 0) tmem_alloc<(kWG * C::TMEM_COLS > 512 ? 512 : kWG * C::TMEM_COLS)>(&tmem_slot);
   cp_async_wait_all();
-  if (C::STAGE) issue_input(t0);
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_slot;
-  const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  const uint32_t tmem = tmem_slot + wg * C::TMEM_COLS;
+  const uint32_t tq = tmem + (uint32_t(quad * 32) << 16);  // this warp's lane quadrant
+  uint64_t* bars = mma_bar[wg];
+  const uint32_t bar_id = 1 + wg;  // named barrier of this warpgroup
   uint32_t phase = 0;
   int64_t cur_h = -1;
 
-  auto sync_and_issue = [&](auto&& issue) {
+  auto wg_sync = [&] { named_sync(bar_id, kWGThreads); };
+  // Operands written -> warpgroup barrier -> one thread issues the stage as
+  // two halves, each committed to its own mbarrier so the epilogue of the
+  // first half overlaps the MMAs of the second.
+  auto sync_and_issue = [&](auto&& issue_half) {
     fence_async_smem();
     tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
+    wg_sync();
+    if (wtid == 0) {
       tc_fence_after();
-      issue();
-      mma_commit(&mma_bar);
+      issue_half(0);
+      mma_commit(&bars[0]);
+      issue_half(1);
+      mma_commit(&bars[1]);
     }
-    mbar_wait(&mma_bar, phase);
-    phase ^= 1;
+    phase ^= 1;  // both barriers complete once per stage
+  };
+  auto wait_half = [&](int hh) {  // parity of the stage issued last
+    mbar_wait_warp(&bars[hh], phase ^ 1);
     tc_fence_after();
   };
 
-  for (int64_t t = t0; t < t1; ++t) {
+  for (int64_t t = t0 + wg; t < t1; t += kWG) {
     const int64_t h = t / nbt, bt = t % nbt;
-    if (h != cur_h) {
+    const bool new_h = h != cur_h;
+    if (new_h) {  // refresh this warpgroup's k_f copy (previous tile's epi2 is long done)
       const uint8_t* src = gkf + h * int64_t(C::KF_BYTES);
-      for (uint32_t o = tid * 16; o < C::KF_BYTES; o += 128 * 16) cp_async16(sKF + o, src + o, true);
+      for (uint32_t o = wtid * 16; o < C::KF_BYTES; o += kWGThreads * 16) cp_async16(sKF + o, src + o, true);
       cp_async_commit();
       cur_h = h;
     }
-    cp_async_wait_all();
-    __syncthreads();
-    convert_input(t);
-    if (C::STAGE && t + 1 < t1) {
-      __syncthreads();  // everyone finished reading the staging buffers
-      issue_input(t + 1);
-    }
 
-    // ---------------- stage A: D[(p,n1)][(c',k2)] = X[(p,n1)][(c,n2)] * G_A
-    sync_and_issue([&] {
-      constexpr uint32_t idesc = idesc_f16(128, 2 * L2, true, false);
+    // ---------------- load (+ gate) the tile's rows straight into the stage A operand
+    {
+      constexpr int KROWS = C::KA;  // n2 rows per row
+      constexpr int JC = L1 / 8;    // 8-element n1 chunks
+      constexpr int NCH = C::R * C::CH;
+      constexpr int PER_ALL = NCH / kWGThreads;
+      constexpr int PER = PER_ALL < 4 ? PER_ALL : 4;  // loads in flight per batch (register budget)
+#pragma unroll 1
+      for (int i0 = 0; i0 < PER_ALL; i0 += PER) {
+      uint4 uv[PER], wv[PER];
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int q = wtid + (i0 + i) * kWGThreads;
+        const int n2 = q % KROWS, j = (q / KROWS) % JC, r = q / (KROWS * JC);
+        const int64_t b = bt * C::R + r;
+        if (b < B) {
+          const int64_t goff = (b * H + h) * N + int64_t(n2 * JC + j) * 8;
+          uv[i] = *reinterpret_cast<const uint4*>(gu + goff);
+          if (GATED) wv[i] = *reinterpret_cast<const uint4*>(gw + goff);
+        } else {
+          uv[i] = make_uint4(0, 0, 0, 0);
+          wv[i] = make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        // n2 fastest so 8 consecutive threads fill one 128 B core matrix
+        const int q = wtid + (i0 + i) * kWGThreads;
+        const int n2 = q % KROWS, j = (q / KROWS) % JC, r = q / (KROWS * JC);
+        const int p = r >> 1, c = r & 1;
+        const int k = c * C::KA + n2;
+        const uint32_t dst = bufX + (p * JC + j) * C::SBO_A + (k >> 3) * 128 + (k & 7) * 16;
+        if constexpr (std::is_same<T, __half>::value) {
+          // the fp16 product of two fp16 values equals the fp32 product rounded
+          // to fp16, so gate with HMUL2 and skip conversions
+          uint4 g = uv[i];
+          if (GATED) {
+            __half2* a = reinterpret_cast<__half2*>(&g);
+            const __half2* bb = reinterpret_cast<const __half2*>(&wv[i]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) a[e] = __hmul2(a[e], bb[e]);
+          }
+          st_shared_v4(dst, g.x, g.y, g.z, g.w);
+        } else {
+          float g[8];
+          IO<T>::to_f32x8(uv[i], g);
+          if (GATED) {
+            float w8[8];
+            IO<T>::to_f32x8(wv[i], w8);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) g[e] *= w8[e];
+          }
+          st_half8(dst, g);
+        }
+      }
+    }
+    }
+    if (new_h) cp_async_wait_all();
+
+    // ---------------- stage A: D[(p,n1)][(re|im|-im, k2)] = X[(p,n1)][(c,n2)] * G_A
+    sync_and_issue([&](int hh) {  // half hh: k2 in [32 hh, 32 hh + 32) of each block
+      constexpr uint32_t idesc = idesc_f16(128, L2 / 2, true, false);
 #pragma unroll
       for (int s = 0; s < 2 * C::KA / 16; ++s) {
-        uint64_t ad = smem_desc(bufA + 256 * s, 128, C::SBO_A);
-        uint64_t bd = smem_desc(sGA + 256 * s, 128, C::SBO_GA);
-        mma_f16_ss(tmem, ad, bd, idesc, s > 0);
+        const uint64_t ad = smem_desc(bufX + 256 * s, 128, C::SBO_A);
+#pragma unroll
+        for (int blk = 0; blk < 3; ++blk) {
+          const uint32_t row0 = blk * L2 + hh * (L2 / 2);
+          const uint64_t bd = smem_desc(sGA + (row0 / 8) * C::SBO_GA + 256 * s, 128, C::SBO_GA);
+          mma_f16_ss(tmem + row0, ad, bd, idesc, s > 0);
+        }
       }
     });
 
-    // ---------------- epilogue 1: twiddle, transpose -> stage B operand (MN-major)
+    // ---------------- epilogue 1: twiddle W^{n1 k2}, transpose -> stage B operand (MN-major)
+    // Every stage's operand aliases bufX, so stores wait for BOTH halves of
+    // the stage (the other half's MMAs may still read bufX); math on the
+    // first item only needs this warp's half.
     {
-      const int m = tid, p = m / L1, n1 = m % L1;
+      const int p = m / L1, n1 = m % L1;
+      wait_half(slice);
 #pragma unroll 1
-      for (int k2c = 0; k2c < L2 / 8; ++k2c) {
-        float re[8], im[8];
-        tmem_ld8(tmem + lane_base + k2c * 8, re);
-        tmem_ld8(tmem + lane_base + L2 + k2c * 8, im);
-        tmem_ld_wait();
+      for (int sub = 0; sub < 2; ++sub) {
+        const int k20 = slice * 32 + sub * 16;  // 16 k2 per item
+        float re[16], im[16], ni[16];
+        tmem_ld16(tq + k20, re);
+        tmem_ld16(tq + L2 + k20, im);
+        tmem_ld16(tq + 2 * L2 + k20, ni);
+        float4 w[8];
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          float4 w = ld_shared_f4(sTW + swz128(uint32_t(n1 * L2 + k2c * 8 + 2 * jj) * 8));
-          cmul(re[2 * jj], im[2 * jj], w.x, w.y);
-          cmul(re[2 * jj + 1], im[2 * jj + 1], w.z, w.w);
+        for (int jj = 0; jj < 8; ++jj) w[jj] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1, k20 / 2 + jj));
+        tmem_ld_wait();
+        cmul8(re, im, ni, w);
+        cmul8(re + 8, im + 8, ni + 8, w + 4);
+        if (sub == 0) wait_half(slice ^ 1);
+#pragma unroll
+        for (int hh2 = 0; hh2 < 2; ++hh2) {
+          const int mg = p * (L2 / 8) + k20 / 8 + hh2;
+          st_half8(bufX + mg * 128 + (n1 >> 3) * C::LBO_B + (n1 & 7) * 16, re + 8 * hh2);
+          st_half8(bufX + mg * 128 + ((L1 + n1) >> 3) * C::LBO_B + (n1 & 7) * 16, im + 8 * hh2);
         }
-        const int mg = p * (L2 / 8) + k2c;
-        const uint32_t o_re = mg * 128 + (n1 >> 3) * C::LBO_B + (n1 & 7) * 16;
-        const uint32_t o_im = mg * 128 + ((L1 + n1) >> 3) * C::LBO_B + (n1 & 7) * 16;
-        st_shared_v4(bufX + o_re, pack_half2(re[0], re[1]), pack_half2(re[2], re[3]), pack_half2(re[4], re[5]),
-                     pack_half2(re[6], re[7]));
-        st_shared_v4(bufX + o_im, pack_half2(im[0], im[1]), pack_half2(im[2], im[3]), pack_half2(im[4], im[5]),
-                     pack_half2(im[6], im[7]));
       }
     }
 
     // ---------------- stage B: per group of 128 rows (p,k2), contract n1 -> k1
-    sync_and_issue([&] {
-      constexpr uint32_t idesc = idesc_f16(128, 2 * L1, true, false);
+    sync_and_issue([&](int hh) {
+      constexpr uint32_t idesc = idesc_f16(128, C::NB, true, false);
 #pragma unroll 1
-      for (int gi = 0; gi < C::P / 2; ++gi) {
+      for (int gi = hh * (C::P / 4); gi < (hh + 1) * (C::P / 4); ++gi) {
 #pragma unroll
         for (int s = 0; s < 2 * L1 / 16; ++s) {
           uint64_t ad = smem_desc(bufX + gi * 2048 + 2 * s * C::LBO_B, C::LBO_B, 128);
           uint64_t bd = smem_desc(sGB + 256 * s, 128, C::SBO_GB);
-          mma_f16_ss(tmem + gi * 2 * L1, ad, bd, idesc, s > 0);
+          mma_f16_ss(tmem + gi * C::NB, ad, bd, idesc, s > 0);
         }
       }
     });
 
-    // ---------------- epilogue 2: pointwise * k_f -> stage B^-1 operand (K-major)
-#pragma unroll 1
-    for (int gi = 0; gi < C::P / 2; ++gi) {
-      const int m = tid, k2 = m & 63;
-      const int row = gi * 128 + m;  // (p, k2) with p = 2 gi + m / 64
-#pragma unroll 1
-      for (int k1c = 0; k1c < L1 / 8; ++k1c) {
-        float re[8], im[8];
-        tmem_ld8(tmem + lane_base + gi * 2 * L1 + k1c * 8, re);
-        tmem_ld8(tmem + lane_base + gi * 2 * L1 + L1 + k1c * 8, im);
-        tmem_ld_wait();
+    // ---------------- epilogue 2: pointwise * k_f -> stage B^-1 operand (K-major, own row)
+    {
+      const int k2 = m & 63;
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          float4 kf = ld_shared_f4(sKF + swz128(uint32_t(k2 * L1 + k1c * 8 + 2 * jj) * 8));
-          cmul(re[2 * jj], im[2 * jj], kf.x, kf.y);
-          cmul(re[2 * jj + 1], im[2 * jj + 1], kf.z, kf.w);
-        }
-        const uint32_t o_re = (row >> 3) * C::SBO_BP + k1c * 128 + (row & 7) * 16;
-        const uint32_t o_im = (row >> 3) * C::SBO_BP + (L1 / 8 + k1c) * 128 + (row & 7) * 16;
-        st_shared_v4(bufX + o_re, pack_half2(re[0], re[1]), pack_half2(re[2], re[3]), pack_half2(re[4], re[5]),
-                     pack_half2(re[6], re[7]));
-        st_shared_v4(bufX + o_im, pack_half2(im[0], im[1]), pack_half2(im[2], im[3]), pack_half2(im[4], im[5]),
-                     pack_half2(im[6], im[7]));
+      for (int i = 0; i < 4; ++i) {
+        const int it = slice + 2 * i;  // items 0..3 in half 0, 4..7 in half 1
+        const int gi = it / (L1 / 8), k1c = it % (L1 / 8);
+        const int row = gi * 128 + m;  // (p, k2) with p = 2 gi + m / 64
+        if (i == 0) wait_half(0);
+        const uint32_t col = gi * C::NB + k1c * 8;
+        float re[8], im[8], ni[8];
+        tmem_ld8(tq + col, re);
+        tmem_ld8(tq + col + L1, im);
+        tmem_ld8(tq + col + 2 * L1, ni);
+        float4 kf[4];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) kf[jj] = ld_shared_f4(sKF + tab_off<L1 / 2>(k2, k1c * 4 + jj));
+        tmem_ld_wait();
+        cmul8(re, im, ni, kf);
+        if (i == 0) wait_half(1);  // stores may overwrite operands of the second half
+        st_half8(bufX + (row >> 3) * C::SBO_BP + k1c * 128 + (row & 7) * 16, re);
+        st_half8(bufX + (row >> 3) * C::SBO_BP + (L1 / 8 + k1c) * 128 + (row & 7) * 16, im);
       }
     }
 
     // ---------------- stage B^-1: contract k1 -> n1
-    sync_and_issue([&] {
-      constexpr uint32_t idesc = idesc_f16(128, 2 * L1, false, false);
+    sync_and_issue([&](int hh) {
+      constexpr uint32_t idesc = idesc_f16(128, C::NB, false, false);
 #pragma unroll 1
-      for (int gi = 0; gi < C::P / 2; ++gi) {
+      for (int gi = hh * (C::P / 4); gi < (hh + 1) * (C::P / 4); ++gi) {
 #pragma unroll
         for (int s = 0; s < 2 * L1 / 16; ++s) {
           uint64_t ad = smem_desc(bufX + gi * 16 * C::SBO_BP + 256 * s, 128, C::SBO_BP);
           uint64_t bd = smem_desc(sGBI + 256 * s, 128, C::SBO_GB);
-          mma_f16_ss(tmem + gi * 2 * L1, ad, bd, idesc, s > 0);
+          mma_f16_ss(tmem + gi * C::NB, ad, bd, idesc, s > 0);
         }
       }
     });
 
     // ---------------- epilogue 3: conj twiddle, transpose -> stage A^-1 operand (MN-major B)
-#pragma unroll 1
-    for (int gi = 0; gi < C::P / 2; ++gi) {
-      const int m = tid, k2 = m & 63;
-      const int p = gi * 2 + (m >> 6);
-#pragma unroll 1
-      for (int n1c = 0; n1c < L1 / 8; ++n1c) {
-        float re[8], im[8];
-        tmem_ld8(tmem + lane_base + gi * 2 * L1 + n1c * 8, re);
-        tmem_ld8(tmem + lane_base + gi * 2 * L1 + L1 + n1c * 8, im);
-        tmem_ld_wait();
+    {
+      const int k2 = m & 63;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int n1 = n1c * 8 + e;
-          float2 w = ld_shared_f2(sTW + swz128(uint32_t(n1 * L2 + k2) * 8));
-          cmulc(re[e], im[e], w.x, w.y);
-        }
+      for (int i = 0; i < 4; ++i) {
+        const int it = slice + 2 * i;
+        const int gi = it / (L1 / 8), n1c = it % (L1 / 8);
+        const int p = gi * 2 + (m >> 6);
+        if (i == 0) wait_half(0);
+        const uint32_t col = gi * C::NB + n1c * 8;
+        float re[8], im[8], nr[8];
+        tmem_ld8(tq + col, re);
+        tmem_ld8(tq + col + L1, im);
+        tmem_ld8(tq + col + 2 * L1, nr);
+        float4 w[4];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) w[jj] = ld_shared_f4(sTWT + tab_off<L1 / 2>(k2, n1c * 4 + jj));
+        tmem_ld_wait();
+        cmulc8(re, im, nr, w);
+        if (i == 0) wait_half(1);  // stores may overwrite operands of the second half
         const int ng = (p * L1) / 8 + n1c;
-        const uint32_t o_re = ng * C::SBO_XA + (k2 >> 3) * 128 + (k2 & 7) * 16;
-        const uint32_t o_im = ng * C::SBO_XA + ((L2 + k2) >> 3) * 128 + (k2 & 7) * 16;
-        st_shared_v4(bufX + o_re, pack_half2(re[0], re[1]), pack_half2(re[2], re[3]), pack_half2(re[4], re[5]),
-                     pack_half2(re[6], re[7]));
-        st_shared_v4(bufX + o_im, pack_half2(im[0], im[1]), pack_half2(im[2], im[3]), pack_half2(im[4], im[5]),
-                     pack_half2(im[6], im[7]));
+        st_half8(bufX + ng * C::SBO_XA + (k2 >> 3) * 128 + (k2 & 7) * 16, re);
+        st_half8(bufX + ng * C::SBO_XA + ((L2 + k2) >> 3) * 128 + (k2 & 7) * 16, im);
       }
     }
 
     // ---------------- stage A^-1: D[(c',n2)][(p,n1)] = G_A^-1 * X[(c,k2)][(p,n1)]
-    sync_and_issue([&] {
-      constexpr uint32_t idesc = idesc_f16(128, 128, false, true);
+    sync_and_issue([&](int hh) {  // half hh: output columns (p, n1) in [64 hh, 64 hh + 64)
+      constexpr uint32_t idesc = idesc_f16(128, 64, false, true);
 #pragma unroll
       for (int s = 0; s < 2 * L2 / 16; ++s) {
         uint64_t ad = smem_desc(sGAI + 256 * s, 128, C::SBO_GAI);
-        uint64_t bd = smem_desc(bufX + 256 * s, 128, C::SBO_XA);
-        mma_f16_ss(tmem, ad, bd, idesc, s > 0);
+        uint64_t bd = smem_desc(bufX + hh * 8 * C::SBO_XA + 256 * s, 128, C::SBO_XA);
+        mma_f16_ss(tmem + hh * 64, ad, bd, idesc, s > 0);
       }
     });
 
     // ---------------- epilogue 4: (gate), convert, store y
     {
-      const int m = tid, cp = m >> 6, n2 = m & 63;
+      const int cp = m >> 6, n2 = m & 63;
       if (!CAUSAL || n2 < L2 / 2) {  // warp-uniform
-#pragma unroll 1
-        for (int p = 0; p < C::P; ++p) {
+        // this warp's items cover output columns [64 slice, 64 slice + 64)
+        constexpr int NIT = C::P * (L1 / 8);  // (pair, 8-wide n1 chunk) items
+        constexpr int PER = NIT / 2;
+        int64_t goff[PER];
+        bool ok[PER];
+        uint4 vv[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          const int it = slice * PER + i;
+          const int p = it / (L1 / 8), n1c = it % (L1 / 8);
           const int64_t b = bt * C::R + 2 * p + cp;
-          if (b >= B) continue;  // warp-uniform
-          const int64_t goff = (b * H + h) * N + int64_t(L1) * n2;
+          ok[i] = b < B;
+          goff[i] = ((ok[i] ? b : 0) * H + h) * N + int64_t(L1) * n2 + n1c * 8;
+          if (GATED && ok[i]) vv[i] = *reinterpret_cast<const uint4*>(gv + goff[i]);
+        }
+        wait_half(slice);
 #pragma unroll
-          for (int n1c = 0; n1c < L1 / 8; ++n1c) {
-            float o[8];
-            tmem_ld8(tmem + lane_base + p * L1 + n1c * 8, o);
-            tmem_ld_wait();
-            if (GATED) {
-              float vv[8];
-              IO<T>::to_f32x8(*reinterpret_cast<const uint4*>(gv + goff + n1c * 8), vv);
+        for (int i = 0; i < PER; ++i) {
+          const int it = slice * PER + i;
+          const int p = it / (L1 / 8), n1c = it % (L1 / 8);
+          float o[8];
+          tmem_ld8(tq + p * L1 + n1c * 8, o);
+          tmem_ld_wait();
+          if (GATED) {
+            float v8[8];
+            IO<T>::to_f32x8(vv[i], v8);
 #pragma unroll
-              for (int e = 0; e < 8; ++e) o[e] *= vv[e];
-            }
-            uint4 st;
-            st.x = IO<T>::pack2(o[0], o[1]);
-            st.y = IO<T>::pack2(o[2], o[3]);
-            st.z = IO<T>::pack2(o[4], o[5]);
-            st.w = IO<T>::pack2(o[6], o[7]);
-            *reinterpret_cast<uint4*>(gy + goff + n1c * 8) = st;
+            for (int e = 0; e < 8; ++e) o[e] *= v8[e];
           }
+          uint4 st;
+          st.x = IO<T>::pack2(o[0], o[1]);
+          st.y = IO<T>::pack2(o[2], o[3]);
+          st.z = IO<T>::pack2(o[4], o[5]);
+          st.w = IO<T>::pack2(o[6], o[7]);
+          if (ok[i]) *reinterpret_cast<uint4*>(gy + goff[i]) = st;
         }
       }
     }
     tc_fence_before();
+    wg_sync();  // TMEM columns and bufX are reused by the next tile
   }
   __syncthreads();
-  if (warp == 0) tmem_dealloc<128>(tmem);
+  if (warp == 0) tmem_dealloc<(kWG * C::TMEM_COLS > 512 ? 512 : kWG * C::TMEM_COLS)>(tmem_slot);
 }
 
 // ------------------------------------------------------------------ launch
@@ -450,7 +515,7 @@ static cudaError_t launch_o2(const FwdParams& prm, cudaStream_t stream) {
   const int64_t tiles = prm.H * nbt;
   int grid = int(tiles < prm.num_sms ? tiles : prm.num_sms);
   if (grid < 1) return cudaSuccess;
-  kern<<<grid, 128, C::SMEM, stream>>>(prm);
+  kern<<<grid, C::THREADS, C::SMEM, stream>>>(prm);
   return cudaGetLastError();
 }
 
@@ -473,18 +538,6 @@ static cudaError_t dispatch_t(const FwdParams& prm, cudaStream_t s) {
 cudaError_t launch_fwd_fused(const FwdParams& prm, cudaStream_t s) {
   if (prm.causal) return prm.gated ? dispatch_t<true, true>(prm, s) : dispatch_t<true, false>(prm, s);
   return prm.gated ? dispatch_t<false, true>(prm, s) : dispatch_t<false, false>(prm, s);
-}
-
-size_t fwd_fused_smem_bytes(int L1, int causal) {
-  switch (L1 * 2 + (causal ? 1 : 0)) {
-    case 17: return O2Cfg<8, true>::SMEM;
-    case 16: return O2Cfg<8, false>::SMEM;
-    case 33: return O2Cfg<16, true>::SMEM;
-    case 32: return O2Cfg<16, false>::SMEM;
-    case 65: return O2Cfg<32, true>::SMEM;
-    case 64: return O2Cfg<32, false>::SMEM;
-  }
-  return 0;
 }
 
 }  // namespace fc

@@ -17,6 +17,7 @@
 #include <string>
 
 #include "plan.h"
+#include "layout.h"
 
 namespace fc {
 
@@ -135,40 +136,65 @@ static size_t kmajor_off(int r, int k, int Ktot) {
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+static void put_float(std::vector<uint8_t>& img, size_t off, double x) {
+  float f = float(x);
+  std::memcpy(img.data() + off, &f, 4);
+}
+
+// Table image of the fused order-2 kernel (kernels_fwd.cu, O2Cfg):
+//  GA  : stage A B-operand, K-major rows (re|im|-im, k2) = 3*L2, K (c,n2) = 2*KA
+//  GB  : stage B B-operand, rows (re|im|-im|pad, k1) = NB, K (c,n1) = 2*L1
+//  GBI : stage B^-1, rows (re|im|-re|pad, n1) = NB, K (c,k1) = 2*L1
+//  GAI : stage A^-1 A-operand, rows (c',n2) = 2*L2, K (c,k2) = 2*L2
+//  TW  : [n1][k2/2] {wr(k2), wr(k2+1), wi(k2), wi(k2+1)} fp32, W = W_L^{n1 k2}
+//  TWT : [k2][n1/2] {wr(n1), wr(n1+1), wi(n1), wi(n1+1)} fp32
+// DFT matrices carry the unitary 1/sqrt(L_i) scale, so the whole forward +
+// inverse pair scales by 1/L and k_f is used unscaled.
 static void build_fused_tables(fftconv_plan_s* p) {
   const int L1 = p->L1, L2 = p->L2, KA = p->KA;
+  const int NA = 3 * L2, NB = (3 * L1 + 15) / 16 * 16;
   const int64_t L = p->L;
   TableLayout& t = p->tl;
   size_t off = 0;
-  t.ga = off;  t.ga_bytes = size_t(2 * L2) * (2 * KA) * 2;  off = align_up(off + t.ga_bytes, 1024);
-  t.gb = off;  t.gb_bytes = size_t(2 * L1) * (2 * L1) * 2;  off = align_up(off + t.gb_bytes, 1024);
+  t.ga = off;  t.ga_bytes = size_t(NA) * (2 * KA) * 2;      off = align_up(off + t.ga_bytes, 1024);
+  t.gb = off;  t.gb_bytes = size_t(NB) * (2 * L1) * 2;      off = align_up(off + t.gb_bytes, 1024);
   t.gbi = off; t.gbi_bytes = t.gb_bytes;                    off = align_up(off + t.gbi_bytes, 1024);
   t.gai = off; t.gai_bytes = size_t(2 * L2) * (2 * L2) * 2; off = align_up(off + t.gai_bytes, 1024);
   t.tw = off;  t.tw_bytes = size_t(L) * 8;                  off = align_up(off + t.tw_bytes, 1024);
+  t.twt = off; t.twt_bytes = size_t(L) * 8;                 off = align_up(off + t.twt_bytes, 1024);
   t.total = off;
   p->image.assign(t.total, 0);
   std::vector<uint8_t>& img = p->image;
   const double sA = 1.0 / std::sqrt(double(L2)), sB = 1.0 / std::sqrt(double(L1));
-  // stage A (forward, contracts n2 -> k2): B^T[(c',k2)][(c,n2)], n2 < KA
-  for (int co = 0; co < 2; ++co)
+  // stage A (forward, contracts n2 -> k2): B^T[(blk,k2)][(c,n2)], n2 < KA
+  for (int blk = 0; blk < 3; ++blk)
     for (int k2 = 0; k2 < L2; ++k2)
       for (int ci = 0; ci < 2; ++ci)
         for (int n2 = 0; n2 < KA; ++n2) {
           double fr, fi;
           root(int64_t(n2) * k2, L2, &fr, &fi);
-          put_half(img, t.ga + kmajor_off(co * L2 + k2, ci * KA + n2, 2 * KA),
-                   realpair(fr * sA, fi * sA, ci, co));
+          const int co = blk == 0 ? 0 : 1;
+          const double sgn = blk == 2 ? -1.0 : 1.0;
+          put_half(img, t.ga + kmajor_off(blk * L2 + k2, ci * KA + n2, 2 * KA),
+                   sgn * realpair(fr * sA, fi * sA, ci, co));
         }
-  // stage B (forward, contracts n1 -> k1) and B^-1 (contracts k1 -> n1)
-  for (int co = 0; co < 2; ++co)
+  // stage B (forward, contracts n1 -> k1; blocks re | im | -im) and
+  // B^-1 (contracts k1 -> n1; blocks re | im | -re)
+  for (int blk = 0; blk < 3; ++blk)
     for (int b = 0; b < L1; ++b)
       for (int ci = 0; ci < 2; ++ci)
         for (int a = 0; a < L1; ++a) {
           double fr, fi;
           root(int64_t(a) * b, L1, &fr, &fi);
-          put_half(img, t.gb + kmajor_off(co * L1 + b, ci * L1 + a, 2 * L1), realpair(fr * sB, fi * sB, ci, co));
+          const int co_f = blk == 0 ? 0 : 1;
+          const double sg_f = blk == 2 ? -1.0 : 1.0;
+          put_half(img, t.gb + kmajor_off(blk * L1 + b, ci * L1 + a, 2 * L1),
+                   sg_f * realpair(fr * sB, fi * sB, ci, co_f));
           root(-int64_t(a) * b, L1, &fr, &fi);
-          put_half(img, t.gbi + kmajor_off(co * L1 + b, ci * L1 + a, 2 * L1), realpair(fr * sB, fi * sB, ci, co));
+          const int co_i = blk == 1 ? 1 : 0;
+          const double sg_i = blk == 2 ? -1.0 : 1.0;
+          put_half(img, t.gbi + kmajor_off(blk * L1 + b, ci * L1 + a, 2 * L1),
+                   sg_i * realpair(fr * sB, fi * sB, ci, co_i));
         }
   // stage A^-1 (contracts k2 -> n2), as the A operand: rows (c',n2), K (c,k2)
   for (int co = 0; co < 2; ++co)
@@ -179,15 +205,17 @@ static void build_fused_tables(fftconv_plan_s* p) {
           root(-int64_t(k2) * n2, L2, &fr, &fi);
           put_half(img, t.gai + kmajor_off(co * L2 + n2, ci * L2 + k2, 2 * L2), realpair(fr * sA, fi * sA, ci, co));
         }
-  // twiddles W_L^{n1 k2}, [n1][k2] float2, 128B-swizzled
+  // twiddles W_L^{n1 k2} as element pairs, row-XOR swizzled (tab_off_rt)
   for (int n1 = 0; n1 < L1; ++n1)
     for (int k2 = 0; k2 < L2; ++k2) {
       double wr, wi;
       root(int64_t(n1) * k2, L, &wr, &wi);
-      float v[2] = {float(wr), float(wi)};
-      uint32_t o = uint32_t(n1 * L2 + k2) * 8;
-      o ^= (o >> 3) & 0x70u;
-      std::memcpy(img.data() + t.tw + o, v, 8);
+      const uint32_t q = tab_off_rt(uint32_t(L2 / 2), uint32_t(n1), uint32_t(k2 / 2));
+      put_float(img, t.tw + q + (k2 & 1) * 4, wr);
+      put_float(img, t.tw + q + 8 + (k2 & 1) * 4, wi);
+      const uint32_t r = tab_off_rt(uint32_t(L1 / 2), uint32_t(k2), uint32_t(n1 / 2));
+      put_float(img, t.twt + r + (n1 & 1) * 4, wr);
+      put_float(img, t.twt + r + 8 + (n1 & 1) * 4, wi);
     }
 }
 

@@ -21,7 +21,8 @@ struct TableLayout {
   size_t gb = 0, gb_bytes = 0;    // stage B  : B operand, K-major, rows (c',k1) 2*L1, K (c,n1) 2*L1
   size_t gbi = 0, gbi_bytes = 0;  // stage B^-1
   size_t gai = 0, gai_bytes = 0;  // stage A^-1: A operand, K-major, rows (c',n2) 2*L2, K (c,k2) 2*L2
-  size_t tw = 0, tw_bytes = 0;    // W_L^{n1 k2}, [L1][L2] float2, swizzled
+  size_t tw = 0, tw_bytes = 0;    // W_L^{n1 k2}, [n1][k2/2] float4 pairs, swizzled
+  size_t twt = 0, twt_bytes = 0;  // same values, [k2][n1/2]
   size_t total = 0;
 };
 

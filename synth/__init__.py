@@ -120,3 +120,52 @@ def quantize(x: np.ndarray, dtype: str) -> np.ndarray:
         b = (b + np.uint64(0x7FFF) + lsb) & np.uint64(0xFFFF0000)
         return b.astype(np.uint32).view(np.float32).astype(np.float64)
     raise ValueError(dtype)
+
+
+# --------------------------------------------------------------------------
+# same generator on a torch device (for large bench inputs)
+# --------------------------------------------------------------------------
+def _to_i64(c: int) -> int:
+    return c - (1 << 64) if c >= (1 << 63) else c
+
+
+def _mix_t(x):
+    import torch
+    m30 = (1 << 34) - 1
+    m27 = (1 << 37) - 1
+    m31 = (1 << 33) - 1
+    x = x ^ ((x >> 30) & m30)
+    x = x * _to_i64(0xBF58476D1CE4E5B9)
+    x = x ^ ((x >> 27) & m27)
+    x = x * _to_i64(0x94D049BB133111EB)
+    x = x ^ ((x >> 31) & m31)
+    return x
+
+
+def normal_torch(seed: int, tensor: int, row0: int, nrows: int, n: int, device, chunk_rows: int = 4096):
+    """Same counter-based N(0,1) stream as normal(), generated with int64
+    torch ops on `device` (values agree with numpy up to the last bits of
+    log/cos); returns float32 (nrows, n)."""
+    import torch
+    out = torch.empty(nrows, n, dtype=torch.float32, device=device)
+    base = _to_i64((seed * 0x9E3779B97F4A7C15 + tensor * 0xD1B54A32D192ED03) % (1 << 64))
+    cr = _to_i64(0x8CB92BA72F3D8DD7)
+    alt = _to_i64(0xA0761D6478BD642F)
+    cols = torch.arange(n, dtype=torch.int64, device=device)
+    for r0 in range(0, nrows, chunk_rows):
+        r1 = min(nrows, r0 + chunk_rows)
+        rows = torch.arange(row0 + r0, row0 + r1, dtype=torch.int64, device=device)
+        k = base + rows[:, None] * cr + cols[None, :]
+        h1 = _mix_t(k)
+        h2 = _mix_t(k ^ alt)
+        u1 = (((h1 >> 11) & ((1 << 53) - 1)).double() + 1.0) * (1.0 / 9007199254740992.0)
+        u2 = ((h2 >> 11) & ((1 << 53) - 1)).double() * (1.0 / 9007199254740992.0)
+        out[r0:r1] = (torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(2.0 * np.pi * u2)).float()
+    return out
+
+
+def signal_torch(seed: int, name: str, B: int, H: int, N: int, device, dtype, row0: int = 0):
+    """(B, H, N) tensor of the given torch dtype on device; rows row0.. of the
+    global (b*H + h) numbering (row0 lets ranks generate their own shard)."""
+    x = normal_torch(seed, TENSOR_IDS[name], row0, B * H, N, device)
+    return x.reshape(B, H, N).to(dtype)
