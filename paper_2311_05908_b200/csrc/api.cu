@@ -80,6 +80,7 @@ extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float*
   prm.kf = d_kf;
   prm.mask = p->sparse ? reinterpret_cast<const float*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.total)
                        : nullptr;
+  prm.twiddle = reinterpret_cast<const float2*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.wl);
   prm.H = H;
   prm.K = K;
   prm.L = p->L;

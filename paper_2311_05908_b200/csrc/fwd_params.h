@@ -20,12 +20,12 @@ struct FwdParams {
   int32_t num_sms;
 };
 cudaError_t launch_fwd_fused(const FwdParams& prm, cudaStream_t s);
-size_t fwd_fused_smem_bytes(int L1, int causal);
 
 struct KfParams {
   const float* k;     // (H, K)
   void* kf;           // H * L complex fp32
   const float* mask;  // length L or nullptr
+  const float2* twiddle;  // W_L^e, e < L (plan table)
   int64_t H, K, L;
   int32_t L1, L2;
 };

@@ -93,7 +93,8 @@ struct O2Cfg {
   static constexpr uint32_t GA_BYTES = NA * 2 * KA * 2;
   static constexpr uint32_t GB_BYTES = NB * 2 * L1 * 2;
   static constexpr uint32_t GAI_BYTES = 2 * L2 * 2 * L2 * 2;
-  static constexpr uint32_t TW_BYTES = L * 8;
+  static constexpr uint32_t TW_BYTES = L1 * (L2 / 2 * 16 + 16);    // padded rows, see layout.h
+  static constexpr uint32_t TWT_BYTES = L2 * (L1 / 2 * 16 + 16);
   static constexpr uint32_t al(uint32_t x) { return (x + 1023u) / 1024u * 1024u; }
   static constexpr uint32_t OFF_GA = 0;
   static constexpr uint32_t OFF_GB = al(OFF_GA + GA_BYTES);
@@ -101,9 +102,9 @@ struct O2Cfg {
   static constexpr uint32_t OFF_GAI = al(OFF_GBI + GB_BYTES);
   static constexpr uint32_t OFF_TW = al(OFF_GAI + GAI_BYTES);   // [n1][k2/2] {wr,wr',wi,wi'}
   static constexpr uint32_t OFF_TWT = al(OFF_TW + TW_BYTES);    // [k2][n1/2] {wr,wr',wi,wi'}
-  static constexpr uint32_t TABLES = al(OFF_TWT + TW_BYTES);
+  static constexpr uint32_t TABLES = al(OFF_TWT + TWT_BYTES);
   // per-warpgroup working buffers
-  static constexpr uint32_t KF_BYTES = L * 8;                  // [k2][k1/2] {kr,kr',ki,ki'}
+  static constexpr uint32_t KF_BYTES = L2 * (L1 / 2 * 16 + 16); // [k2][k1/2] {kr,kr',ki,ki'}, padded rows
   static constexpr uint32_t BUFX_BYTES = P * L * 4;            // complex fp16 per tile (stage A operand aliases it)
   static constexpr uint32_t WG_BYTES = al(KF_BYTES) + al(BUFX_BYTES);
   static constexpr uint32_t OFF_WG = TABLES;
@@ -225,6 +226,17 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
   uint32_t phase = 0;
   int64_t cur_h = -1;
 
+  // UMMA shared-memory descriptors: built once, offsets added as (bytes >> 4)
+  const uint64_t dXA = smem_desc(bufX, 128, C::SBO_A);          // stage A operand (MN-major)
+  const uint64_t dGA = smem_desc(sGA, 128, C::SBO_GA);
+  const uint64_t dXB = smem_desc(bufX, C::LBO_B, 128);          // stage B operand (MN-major)
+  const uint64_t dGB = smem_desc(sGB, 128, C::SBO_GB);
+  const uint64_t dXBP = smem_desc(bufX, 128, C::SBO_BP);        // stage B^-1 operand (K-major)
+  const uint64_t dGBI = smem_desc(sGBI, 128, C::SBO_GB);
+  const uint64_t dGAI = smem_desc(sGAI, 128, C::SBO_GAI);
+  const uint64_t dXAI = smem_desc(bufX, 128, C::SBO_XA);        // stage A^-1 operand (MN-major B)
+  auto dadd = [](uint64_t d, uint32_t off) { return d + uint64_t(off >> 4); };
+
   auto wg_sync = [&] { named_sync(bar_id, kWGThreads); };
   // Operands written -> warpgroup barrier -> one thread issues the stage as
   // two halves, each committed to its own mbarrier so the epilogue of the
@@ -247,8 +259,23 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
     tc_fence_after();
   };
 
-  for (int64_t t = t0 + wg; t < t1; t += kWG) {
-    const int64_t h = t / nbt, bt = t % nbt;
+  // Per-thread invariants of the input loader: chunk q = wtid + i * 256 maps
+  // to (n2, j, r) with n2, j fixed and r = r0 + i * RSTEP.
+  constexpr int KROWS = C::KA;  // n2 rows per row
+  constexpr int JC = L1 / 8;    // 8-element n1 chunks
+  constexpr int RSTEP = kWGThreads / (KROWS * JC);
+  static_assert(kWGThreads % (KROWS * JC) == 0, "loader mapping");
+  const int64_t HN = H * N;
+  const int ld_n2 = wtid % KROWS, ld_j = (wtid / KROWS) % JC, ld_r0 = wtid / (KROWS * JC);
+  const int64_t ld_off0 = int64_t(ld_r0) * HN + int64_t(ld_n2 * JC + ld_j) * 8;
+  // epilogue-4 invariants: row (2p + cp) of the tile, positions L1*n2 + 8*n1c
+  const int64_t st_off0 = int64_t(m >> 6) * HN + int64_t(L1) * (m & 63);
+
+  int64_t h = (t0 + wg) / nbt, bt = (t0 + wg) % nbt;
+  for (int64_t t = t0 + wg; t < t1; t += kWG, bt += kWG) {
+    while (bt >= nbt) { bt -= nbt; ++h; }
+    const int64_t tile_base = (bt * C::R * H + h) * N;  // element offset of row (bt*R, h)
+    const int rows_left = int(B - bt * C::R < C::R ? B - bt * C::R : C::R);
     const bool new_h = h != cur_h;
     if (new_h) {  // refresh this warpgroup's k_f copy (previous tile's epi2 is long done)
       const uint8_t* src = gkf + h * int64_t(C::KF_BYTES);
@@ -259,8 +286,6 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
 
     // ---------------- load (+ gate) the tile's rows straight into the stage A operand
     {
-      constexpr int KROWS = C::KA;  // n2 rows per row
-      constexpr int JC = L1 / 8;    // 8-element n1 chunks
       constexpr int NCH = C::R * C::CH;
       constexpr int PER_ALL = NCH / kWGThreads;
       constexpr int PER = PER_ALL < 4 ? PER_ALL : 4;  // loads in flight per batch (register budget)
@@ -269,11 +294,9 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
       uint4 uv[PER], wv[PER];
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
-        const int q = wtid + (i0 + i) * kWGThreads;
-        const int n2 = q % KROWS, j = (q / KROWS) % JC, r = q / (KROWS * JC);
-        const int64_t b = bt * C::R + r;
-        if (b < B) {
-          const int64_t goff = (b * H + h) * N + int64_t(n2 * JC + j) * 8;
+        const int r = ld_r0 + (i0 + i) * RSTEP;
+        if (r < rows_left) {
+          const int64_t goff = tile_base + ld_off0 + int64_t((i0 + i) * RSTEP) * HN;
           uv[i] = *reinterpret_cast<const uint4*>(gu + goff);
           if (GATED) wv[i] = *reinterpret_cast<const uint4*>(gw + goff);
         } else {
@@ -284,11 +307,10 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         // n2 fastest so 8 consecutive threads fill one 128 B core matrix
-        const int q = wtid + (i0 + i) * kWGThreads;
-        const int n2 = q % KROWS, j = (q / KROWS) % JC, r = q / (KROWS * JC);
+        const int r = ld_r0 + (i0 + i) * RSTEP;
         const int p = r >> 1, c = r & 1;
-        const int k = c * C::KA + n2;
-        const uint32_t dst = bufX + (p * JC + j) * C::SBO_A + (k >> 3) * 128 + (k & 7) * 16;
+        const int k = c * C::KA + ld_n2;
+        const uint32_t dst = bufX + (p * JC + ld_j) * C::SBO_A + (k >> 3) * 128 + (k & 7) * 16;
         if constexpr (std::is_same<T, __half>::value) {
           // the fp16 product of two fp16 values equals the fp32 product rounded
           // to fp16, so gate with HMUL2 and skip conversions
@@ -321,11 +343,11 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
       constexpr uint32_t idesc = idesc_f16(128, L2 / 2, true, false);
 #pragma unroll
       for (int s = 0; s < 2 * C::KA / 16; ++s) {
-        const uint64_t ad = smem_desc(bufX + 256 * s, 128, C::SBO_A);
+        const uint64_t ad = dadd(dXA, 256 * s);
 #pragma unroll
         for (int blk = 0; blk < 3; ++blk) {
           const uint32_t row0 = blk * L2 + hh * (L2 / 2);
-          const uint64_t bd = smem_desc(sGA + (row0 / 8) * C::SBO_GA + 256 * s, 128, C::SBO_GA);
+          const uint64_t bd = dadd(dGA, (row0 / 8) * C::SBO_GA + 256 * s);
           mma_f16_ss(tmem + row0, ad, bd, idesc, s > 0);
         }
       }
@@ -364,12 +386,12 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
     // ---------------- stage B: per group of 128 rows (p,k2), contract n1 -> k1
     sync_and_issue([&](int hh) {
       constexpr uint32_t idesc = idesc_f16(128, C::NB, true, false);
-#pragma unroll 1
+#pragma unroll
       for (int gi = hh * (C::P / 4); gi < (hh + 1) * (C::P / 4); ++gi) {
 #pragma unroll
         for (int s = 0; s < 2 * L1 / 16; ++s) {
-          uint64_t ad = smem_desc(bufX + gi * 2048 + 2 * s * C::LBO_B, C::LBO_B, 128);
-          uint64_t bd = smem_desc(sGB + 256 * s, 128, C::SBO_GB);
+          uint64_t ad = dadd(dXB, gi * 2048 + 2 * s * C::LBO_B);
+          uint64_t bd = dadd(dGB, 256 * s);
           mma_f16_ss(tmem + gi * C::NB, ad, bd, idesc, s > 0);
         }
       }
@@ -403,12 +425,12 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
     // ---------------- stage B^-1: contract k1 -> n1
     sync_and_issue([&](int hh) {
       constexpr uint32_t idesc = idesc_f16(128, C::NB, false, false);
-#pragma unroll 1
+#pragma unroll
       for (int gi = hh * (C::P / 4); gi < (hh + 1) * (C::P / 4); ++gi) {
 #pragma unroll
         for (int s = 0; s < 2 * L1 / 16; ++s) {
-          uint64_t ad = smem_desc(bufX + gi * 16 * C::SBO_BP + 256 * s, 128, C::SBO_BP);
-          uint64_t bd = smem_desc(sGBI + 256 * s, 128, C::SBO_GB);
+          uint64_t ad = dadd(dXBP, gi * 16 * C::SBO_BP + 256 * s);
+          uint64_t bd = dadd(dGBI, 256 * s);
           mma_f16_ss(tmem + gi * C::NB, ad, bd, idesc, s > 0);
         }
       }
@@ -445,16 +467,16 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
       constexpr uint32_t idesc = idesc_f16(128, 64, false, true);
 #pragma unroll
       for (int s = 0; s < 2 * L2 / 16; ++s) {
-        uint64_t ad = smem_desc(sGAI + 256 * s, 128, C::SBO_GAI);
-        uint64_t bd = smem_desc(bufX + hh * 8 * C::SBO_XA + 256 * s, 128, C::SBO_XA);
+        uint64_t ad = dadd(dGAI, 256 * s);
+        uint64_t bd = dadd(dXAI, hh * 8 * C::SBO_XA + 256 * s);
         mma_f16_ss(tmem + hh * 64, ad, bd, idesc, s > 0);
       }
     });
 
     // ---------------- epilogue 4: (gate), convert, store y
     {
-      const int cp = m >> 6, n2 = m & 63;
-      if (!CAUSAL || n2 < L2 / 2) {  // warp-uniform
+      const int cp = m >> 6;
+      if (!CAUSAL || (m & 63) < L2 / 2) {  // warp-uniform
         // this warp's items cover output columns [64 slice, 64 slice + 64)
         constexpr int NIT = C::P * (L1 / 8);  // (pair, 8-wide n1 chunk) items
         constexpr int PER = NIT / 2;
@@ -465,9 +487,8 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
         for (int i = 0; i < PER; ++i) {
           const int it = slice * PER + i;
           const int p = it / (L1 / 8), n1c = it % (L1 / 8);
-          const int64_t b = bt * C::R + 2 * p + cp;
-          ok[i] = b < B;
-          goff[i] = ((ok[i] ? b : 0) * H + h) * N + int64_t(L1) * n2 + n1c * 8;
+          ok[i] = 2 * p + cp < rows_left;
+          goff[i] = tile_base + st_off0 + int64_t(2 * p) * HN + n1c * 8;
           if (GATED && ok[i]) vv[i] = *reinterpret_cast<const uint4*>(gv + goff[i]);
         }
         wait_half(slice);

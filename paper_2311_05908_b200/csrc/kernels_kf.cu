@@ -1,11 +1,14 @@
 // kernels_kf.cu -- k_f = FFT_L(pad(k)) on the GPU in fp32.
 //
-// One CTA per head: the zero-padded filter row is transformed by an
-// iterative radix-2 FFT in shared memory (fp32, twiddles from sincospif of an
-// exactly representable dyadic argument), multiplied by the frequency mask
+// One CTA per head.  The zero-padded filter row is transformed by a
+// Stockham autosort FFT (radix-8 passes, one radix-2/4 pass when log2 L is
+// not a multiple of 3) ping-ponging between two shared-memory buffers; each
+// thread transforms 8 (or 4, 2) elements in registers per pass.  Twiddles
+// W_L^e come from the plan's fp32 table (built in fp64 on the host, exponent
+// reduced mod L in integers).  The result is multiplied by the frequency mask
 // (A13) and written in the fused kernel's plan layout: complex fp32 at
-// f = k2 + L2 k1 stored as [k2][k1/2] element pairs {re, re', im, im'}, 128-byte XOR-swizzled so the pointwise
-// epilogue reads it bank-conflict free.  No cuFFT.
+// f = k2 + L2 k1 stored as [k2][k1/2] element pairs {re, re', im, im'} with
+// padded rows (layout.h).  No cuFFT.
 #include <cuda_runtime.h>
 
 #include "fwd_params.h"
@@ -13,63 +16,126 @@
 
 namespace fc {
 
-__global__ void __launch_bounds__(512) precompute_kf_kernel(const KfParams prm) {
-  extern __shared__ float2 xs[];  // L data + L/2 twiddles
-  const int64_t h = blockIdx.x;
-  const int64_t L = prm.L, K = prm.K;
-  float2* tw = xs + L;
-  const int lg = __ffsll(L) - 1;
-  const float* krow = prm.k + h * K;
-  // twiddle table W_L^j, j < L/2 (dyadic argument, exact in fp32)
-  for (int64_t j = threadIdx.x; j < L / 2; j += blockDim.x) {
-    float sn, cs;
-    sincospif(-2.0f * float(j) / float(L), &sn, &cs);
-    tw[j] = make_float2(cs, sn);
+namespace {
+
+FC_DEVICE float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+FC_DEVICE float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+FC_DEVICE float2 cmulf(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+FC_DEVICE float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }  // a * (-i)
+
+// in-register forward DFTs, natural order in and out
+FC_DEVICE void dft2(float2* v) {
+  const float2 a = v[0], b = v[1];
+  v[0] = cadd(a, b);
+  v[1] = csub(a, b);
+}
+FC_DEVICE void dft4(float2* v) {
+  const float2 e0 = cadd(v[0], v[2]), e1 = csub(v[0], v[2]);
+  const float2 o0 = cadd(v[1], v[3]), o1 = mul_mi(csub(v[1], v[3]));
+  v[0] = cadd(e0, o0);
+  v[2] = csub(e0, o0);
+  v[1] = cadd(e1, o1);
+  v[3] = csub(e1, o1);
+}
+FC_DEVICE void dft8(float2* v) {
+  float2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+  dft4(e);
+  dft4(o);
+  const float r = 0.70710678118654752f;
+  o[1] = make_float2(r * (o[1].x + o[1].y), r * (o[1].y - o[1].x));    // * W8^1
+  o[2] = mul_mi(o[2]);                                                 // * W8^2
+  o[3] = make_float2(r * (o[3].y - o[3].x), -r * (o[3].x + o[3].y));   // * W8^3
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    v[k] = cadd(e[k], o[k]);
+    v[k + 4] = csub(e[k], o[k]);
   }
-  // bit-reversed load of the zero-padded row
-  for (int64_t n = threadIdx.x; n < L; n += blockDim.x) {
-    const int64_t r = __brevll(uint64_t(n)) >> (64 - lg);
-    xs[r] = make_float2(n < K ? krow[n] : 0.f, 0.f);
-  }
-  __syncthreads();
-  for (int64_t len = 2, stride = L / 2; len <= L; len <<= 1, stride >>= 1) {
-    const int64_t half = len >> 1;
-    for (int64_t i = threadIdx.x; i < L / 2; i += blockDim.x) {
-      const int64_t j = i & (half - 1), s = (i - j) * 2;
-      const float2 w = tw[j * stride];
-      const float2 a = xs[s + j], b = xs[s + j + half];
-      const float2 t = make_float2(b.x * w.x - b.y * w.y, b.x * w.y + b.y * w.x);
-      xs[s + j] = make_float2(a.x + t.x, a.y + t.y);
-      xs[s + j + half] = make_float2(a.x - t.x, a.y - t.y);
+}
+
+template <int R>
+FC_DEVICE void stockham_pass(const float2* __restrict__ x, float2* __restrict__ y, const float2* __restrict__ tw,
+                             int L, int Ns) {
+  const int G = L / R;  // butterfly groups per pass
+  for (int j = threadIdx.x; j < G; j += blockDim.x) {
+    float2 v[R];
+    const int jm = j % Ns;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = x[j + r * G];
+    if (Ns > 1) {
+      const int step = L / (Ns * R);  // W_{Ns R}^{jm r} = W_L^{jm r step}
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = cmulf(v[r], tw[(jm * r * step) & (L - 1)]);
     }
+    if constexpr (R == 8) dft8(v);
+    else if constexpr (R == 4) dft4(v);
+    else dft2(v);
+    const int base = (j / Ns) * Ns * R + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) y[base + r * Ns] = v[r];
+  }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) {
+  extern __shared__ float2 sm[];  // two L-element ping-pong buffers + L twiddles
+  const int h = blockIdx.x;
+  const int L = int(prm.L), K = int(prm.K);
+  float2* bufs[2] = {sm, sm + L};
+  float2* tws = sm + 2 * L;
+  {
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.twiddle);
+    const uint32_t dst = smem_u32(tws);
+    for (int o = threadIdx.x * 16; o < L * 8; o += blockDim.x * 16) cp_async16(dst + o, src + o, true);
+    cp_async_commit();
+  }
+  const float* krow = prm.k + int64_t(h) * K;
+  for (int n = threadIdx.x; n < L; n += blockDim.x) sm[n] = make_float2(n < K ? krow[n] : 0.f, 0.f);
+  cp_async_wait_all();
+  __syncthreads();
+  int cur = 0, Ns = 1;
+  const int lg = __ffs(L) - 1;
+  const int rem = lg % 3;
+  if (rem) {  // leading radix-2/4 pass
+    if (rem == 1) stockham_pass<2>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
+    else stockham_pass<4>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
+    Ns <<= rem;
+    cur ^= 1;
     __syncthreads();
   }
-  uint8_t* out = reinterpret_cast<uint8_t*>(prm.kf) + h * L * 8;
-  for (int64_t f = threadIdx.x; f < L; f += blockDim.x) {
-    const int k2 = int(f % prm.L2), k1 = int(f / prm.L2);
-    float2 v = xs[f];
+  for (; Ns < L; Ns <<= 3) {
+    stockham_pass<8>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
+    cur ^= 1;
+    __syncthreads();
+  }
+  const float2* xs = bufs[cur];
+  // plan layout: row k2 holds pairs (k1, k1 + 1) as {kr, kr', ki, ki'}
+  const int L1 = prm.L1, L2 = prm.L2, cpr = L1 / 2;
+  uint8_t* out = reinterpret_cast<uint8_t*>(prm.kf) + int64_t(h) * L2 * tab_stride(uint32_t(cpr));
+  for (int q = threadIdx.x; q < L2 * cpr; q += blockDim.x) {
+    const int k2 = q / cpr, k1 = 2 * (q % cpr);
+    const int f0 = k2 + L2 * k1, f1 = f0 + L2;
+    float2 v0 = xs[f0], v1 = xs[f1];
     if (prm.mask) {
-      const float m = prm.mask[f];
-      v.x *= m;
-      v.y *= m;
+      const float m0 = prm.mask[f0], m1 = prm.mask[f1];
+      v0.x *= m0; v0.y *= m0;
+      v1.x *= m1; v1.y *= m1;
     }
-    // [k2][k1/2] float4 {kr(k1), kr(k1+1), ki(k1), ki(k1+1)}, row-XOR swizzled (tab_off_rt)
-    const uint32_t o = tab_off_rt(uint32_t(prm.L1 / 2), uint32_t(k2), uint32_t(k1 / 2)) + (k1 & 1) * 4;
-    *reinterpret_cast<float*>(out + o) = v.x;
-    *reinterpret_cast<float*>(out + o + 8) = v.y;
+    *reinterpret_cast<float4*>(out + tab_off_rt(uint32_t(cpr), uint32_t(k2), uint32_t(k1 / 2))) =
+        make_float4(v0.x, v1.x, v0.y, v1.y);
   }
 }
 
 cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s) {
   if (prm.H <= 0) return cudaSuccess;
-  const size_t smem = size_t(prm.L) * sizeof(float2) * 3 / 2;
+  const size_t smem = size_t(prm.L) * sizeof(float2) * 3;
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(precompute_kf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  precompute_kf_kernel<<<unsigned(prm.H), 512, smem, s>>>(prm);
+  precompute_kf_kernel<<<unsigned(prm.H), 256, smem, s>>>(prm);
   return cudaGetLastError();
 }
 

@@ -12,20 +12,12 @@
 namespace fc {
 
 // Bank-conflict-free layout of a row-major table of 16-byte chunks read
-// "one row per lane": chunk j of row r lives at chunk (j ^ (r & 7)) when a row
-// has >= 8 chunks, and at the 128B-swizzled position for 4-chunk rows.
+// "one row per lane": rows are padded by one chunk, so consecutive rows start
+// 4 banks apart and 8 lanes reading chunk j of 8 consecutive rows hit 8
+// distinct 4-bank groups.  Chunk addresses stay base + j*16 (immediates).
+FC_HD uint32_t tab_stride(uint32_t cpr) { return cpr * 16u + 16u; }
+FC_HD uint32_t tab_off_rt(uint32_t cpr, uint32_t row, uint32_t j) { return row * tab_stride(cpr) + j * 16u; }
 template <int CPR>
-FC_HD uint32_t tab_off(uint32_t row, uint32_t j) {
-  if constexpr (CPR >= 8) {
-    return (row * CPR + (j ^ (row & 7u))) * 16u;
-  } else {
-    static_assert(CPR == 4, "rows of 4 or >= 8 chunks");
-    return (row * 4u + (j ^ ((row >> 1) & 3u))) * 16u;
-  }
-}
-
-FC_HD uint32_t tab_off_rt(uint32_t cpr, uint32_t row, uint32_t j) {
-  return cpr >= 8 ? (row * cpr + (j ^ (row & 7u))) * 16u : (row * cpr + (j ^ ((row >> 1) & 3u))) * 16u;
-}
+FC_HD uint32_t tab_off(uint32_t row, uint32_t j) { return row * (CPR * 16u + 16u) + j * 16u; }
 
 }  // namespace fc

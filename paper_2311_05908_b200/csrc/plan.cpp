@@ -160,8 +160,9 @@ static void build_fused_tables(fftconv_plan_s* p) {
   t.gb = off;  t.gb_bytes = size_t(NB) * (2 * L1) * 2;      off = align_up(off + t.gb_bytes, 1024);
   t.gbi = off; t.gbi_bytes = t.gb_bytes;                    off = align_up(off + t.gbi_bytes, 1024);
   t.gai = off; t.gai_bytes = size_t(2 * L2) * (2 * L2) * 2; off = align_up(off + t.gai_bytes, 1024);
-  t.tw = off;  t.tw_bytes = size_t(L) * 8;                  off = align_up(off + t.tw_bytes, 1024);
-  t.twt = off; t.twt_bytes = size_t(L) * 8;                 off = align_up(off + t.twt_bytes, 1024);
+  t.tw = off;  t.tw_bytes = size_t(L1) * tab_stride(L2 / 2); off = align_up(off + t.tw_bytes, 1024);
+  t.twt = off; t.twt_bytes = size_t(L2) * tab_stride(L1 / 2); off = align_up(off + t.twt_bytes, 1024);
+  t.wl = off;  t.wl_bytes = size_t(L) * 8;                  off = align_up(off + t.wl_bytes, 1024);
   t.total = off;
   p->image.assign(t.total, 0);
   std::vector<uint8_t>& img = p->image;
@@ -205,7 +206,7 @@ static void build_fused_tables(fftconv_plan_s* p) {
           root(-int64_t(k2) * n2, L2, &fr, &fi);
           put_half(img, t.gai + kmajor_off(co * L2 + n2, ci * L2 + k2, 2 * L2), realpair(fr * sA, fi * sA, ci, co));
         }
-  // twiddles W_L^{n1 k2} as element pairs, row-XOR swizzled (tab_off_rt)
+  // twiddles W_L^{n1 k2} as element pairs, padded rows (tab_off_rt)
   for (int n1 = 0; n1 < L1; ++n1)
     for (int k2 = 0; k2 < L2; ++k2) {
       double wr, wi;
@@ -217,6 +218,13 @@ static void build_fused_tables(fftconv_plan_s* p) {
       put_float(img, t.twt + r + (n1 & 1) * 4, wr);
       put_float(img, t.twt + r + 8 + (n1 & 1) * 4, wi);
     }
+  // full-length twiddles for the k_f precompute
+  for (int64_t e = 0; e < L; ++e) {
+    double wr, wi;
+    root(e, L, &wr, &wi);
+    put_float(img, t.wl + size_t(e) * 8, wr);
+    put_float(img, t.wl + size_t(e) * 8 + 4, wi);
+  }
 }
 
 // A13: keep(f) = prod_j keep_j[digit_j(f)], digits of f on the row-major
@@ -319,7 +327,7 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
     p->image.resize(mo + p->mask.size() * sizeof(float));
     std::memcpy(p->image.data() + mo, p->mask.data(), p->mask.size() * sizeof(float));
   }
-  p->kf_bytes_per_head = size_t(L) * 8;  // complex fp32, [k2][k1], swizzled
+  p->kf_bytes_per_head = size_t(p->L2) * tab_stride(uint32_t(p->L1 / 2));  // complex fp32 [k2][k1/2] pairs, padded rows
   p->ws_bytes_per_head = size_t(L) * 8;  // fp32 spectral accumulator for dk
   *out = p;
   set_last_error("");

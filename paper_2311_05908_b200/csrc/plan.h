@@ -23,6 +23,7 @@ struct TableLayout {
   size_t gai = 0, gai_bytes = 0;  // stage A^-1: A operand, K-major, rows (c',n2) 2*L2, K (c,k2) 2*L2
   size_t tw = 0, tw_bytes = 0;    // W_L^{n1 k2}, [n1][k2/2] float4 pairs, swizzled
   size_t twt = 0, twt_bytes = 0;  // same values, [k2][n1/2]
+  size_t wl = 0, wl_bytes = 0;    // W_L^e, e < L, float2 (k_f precompute)
   size_t total = 0;
 };
 

@@ -1,0 +1,132 @@
+"""CPU tests of the C-ABI library: it loads without a GPU, exports every
+symbol include/fftconv.h declares, validates arguments before any launch, and
+its host planner (Eq. 2 cost model, factorisation, sparsity mask) matches the
+paper's printed values."""
+import ctypes
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2311_05908_b200 import _abi, build
+    build.build()  # in-tree nvcc build (cross-compiles without a GPU)
+    return _abi.lib()
+
+
+def test_header_symbols_exported(lib):
+    hdr = open(os.path.join(ROOT, "include", "fftconv.h")).read()
+    declared = set(re.findall(r"^(?:fftconv_status_t|void|const char\*|int64_t)\s+(fftconv_[a-z_]+)\s*\(", hdr, re.M))
+    assert {"fftconv_plan", "fftconv_precompute_kf", "fftconv_fwd", "fftconv_gated_fwd", "fftconv_bwd"} <= declared
+    for name in declared:
+        assert hasattr(lib, name), name
+    from paper_2311_05908_b200 import _abi
+    assert set(_abi.ABI_SYMBOLS) == declared
+
+
+def _plan(lib, N, L, dtype=0, causal=1, sp=None):
+    h = ctypes.c_void_p()
+    rc = lib.fftconv_plan(ctypes.byref(h), N, L, dtype, causal, sp)
+    return rc, h
+
+
+def test_plan_validation(lib):
+    assert _plan(lib, 1000, 2000)[0] == 2                 # not a power of two
+    assert _plan(lib, 1024, 3000)[0] == 2
+    assert _plan(lib, 0, 2048)[0] == 1                    # invalid
+    assert _plan(lib, 1024, 2048, dtype=9)[0] == 1
+    assert _plan(lib, 1024, 2048, causal=0)[0] == 1       # circular needs fft_size == N
+    rc, h = _plan(lib, 1024, 2048)
+    assert rc == 0
+    lib.fftconv_plan_destroy(h)
+    rc, h = _plan(lib, 1024, 1024, causal=0)
+    assert rc == 0
+    lib.fftconv_plan_destroy(h)
+    assert lib.fftconv_last_error() is not None
+
+
+def test_plan_info_and_calls_without_upload(lib):
+    from paper_2311_05908_b200 import _abi
+    rc, h = _plan(lib, 1024, 2048)
+    info = _abi.PlanInfo()
+    assert lib.fftconv_plan_info(h, ctypes.byref(info)) == 0
+    assert (info.N, info.fft_size, info.causal, info.regime, info.order) == (1024, 2048, 1, 1, 2)
+    assert info.factors[0] * info.factors[1] == 2048
+    assert info.max_kernel_len == 1024
+    assert info.table_bytes > 0 and info.kf_bytes_per_head >= 2048 * 8
+    # argument errors are caught before any CUDA call (no GPU here)
+    assert lib.fftconv_fwd(h, None, None, None, 1, 1, None, None) == 1
+    assert lib.fftconv_precompute_kf(h, None, 1, 1, None, None) == 1
+    assert lib.fftconv_plan_upload(None, None, None) == 1
+    lib.fftconv_plan_destroy(h)
+
+
+def test_factorize_examples(lib):
+    # SPEC S:210-212 examples of the balanced split
+    out = (ctypes.c_int64 * 4)()
+    for n, p, exp in [(4096, 3, [16, 16, 16]), (1024, 2, [32, 32]), (2 ** 22, 4, [64, 64, 32, 32])]:
+        k = lib.fftconv_factorize(n, p, out)
+        assert list(out[:k]) == exp
+
+
+def test_cost_model_reproduces_paper_order_grouping(lib, golden_dir):
+    g = json.load(open(os.path.join(golden_dir, "order_selection_a100.json")))
+    c = g["constants"]
+    args = [c["mu"], c["sigma_H"], c["sigma_S"], c["tau_M"], c["tau_G"], c["sram_bytes"]]
+    for n, p in g["expected_p"].items():
+        assert lib.fftconv_select_order(int(n), *args) == p, n
+    # Eq. 2 compute term example: n=4096, p=2 -> 2*16*4096*64/234e12 s
+    cost = lib.fftconv_cost_eq2(4096, 2, *args)
+    flop = 2 * 16 * 4096 * 64 / 234e12
+    io = 2 * 4 * 4096 / 9.5e12
+    assert abs(cost - (flop + io)) < 1e-15
+    # linear growth O(N^{(p+1)/p}) of the flop term for equal factors
+    c1 = lib.fftconv_cost_eq2(2 ** 12, 2, 1, 1e30, 1e30, 1.0, 1.0, 1e30)
+    c2 = lib.fftconv_cost_eq2(2 ** 16, 2, 1, 1e30, 1e30, 1.0, 1.0, 1e30)
+    assert abs(c2 / c1 - (2 ** 16 / 2 ** 12) ** 1.5) < 1e-9
+
+
+def test_sparsity_mask_matches_oracle_reading(lib):
+    """The planner's Hermitian-symmetric mask (A13) has the same zero
+    fraction as the oracle's independently written mask."""
+    from paper_2311_05908_b200 import _abi
+    L = 2048
+    dims = [32, 64]
+    zeroed = [16, 32]
+    keeps = orc.keep_masks_from_zero_counts(dims, zeroed)
+    sp = _abi.Sparsity()
+    sp.ndims = 2
+    bufs = []
+    for j, (d, kp) in enumerate(zip(dims, keeps)):
+        sp.dims[j] = d
+        b = (ctypes.c_uint8 * d)(*[int(x) for x in kp])
+        bufs.append(b)
+        sp.keep[j] = ctypes.cast(b, ctypes.POINTER(ctypes.c_uint8))
+    h = ctypes.c_void_p()
+    assert lib.fftconv_plan(ctypes.byref(h), 1024, L, 0, 1, ctypes.byref(sp)) == 0
+    info = _abi.PlanInfo()
+    lib.fftconv_plan_info(h, ctypes.byref(info))
+    m = orc.frequency_mask(dims, keeps)
+    assert abs(info.mask_fraction - (1.0 - m.mean())) < 1e-12
+    lib.fftconv_plan_destroy(h)
+    sp.dims[0] = 31
+    assert lib.fftconv_plan(ctypes.byref(h), 1024, L, 0, 1, ctypes.byref(sp)) == 4
+
+
+def test_no_cpu_fallback_in_product():
+    """The product package never imports the oracle."""
+    pkg = os.path.join(ROOT, "paper_2311_05908_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "liboracle" not in txt, f
