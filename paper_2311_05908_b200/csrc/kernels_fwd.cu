@@ -271,6 +271,54 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
   // epilogue-4 invariants: row (2p + cp) of the tile, positions L1*n2 + 8*n1c
   const int64_t st_off0 = int64_t(m >> 6) * HN + int64_t(L1) * (m & 63);
 
+  // u (*w) -> fp16 operand chunk of 8 elements
+  auto gate8 = [&](uint4 uv, uint4 wv) -> uint4 {
+    if constexpr (std::is_same<T, __half>::value) {
+      // the fp16 product of two fp16 values equals the fp32 product rounded
+      // to fp16, so gate with HMUL2 and skip conversions
+      if (GATED) {
+        __half2* a = reinterpret_cast<__half2*>(&uv);
+        const __half2* bb = reinterpret_cast<const __half2*>(&wv);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) a[e] = __hmul2(a[e], bb[e]);
+      }
+      return uv;
+    } else {
+      float g[8];
+      IO<T>::to_f32x8(uv, g);
+      if (GATED) {
+        float w8[8];
+        IO<T>::to_f32x8(wv, w8);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) g[e] *= w8[e];
+      }
+      return make_uint4(pack_half2(g[0], g[1]), pack_half2(g[2], g[3]), pack_half2(g[4], g[5]),
+                        pack_half2(g[6], g[7]));
+    }
+  };
+  // stage A operand address of (row r of the tile, n2, n1 chunk j)
+  auto chunk_dst = [&](int r, int n2, int j) -> uint32_t {
+    const int k = (r & 1) * C::KA + n2;
+    return bufX + ((r >> 1) * JC + j) * C::SBO_A + (k >> 3) * 128 + (k & 7) * 16;
+  };
+  // Causal tiles leave TMEM lane quadrants 1 and 3 idle in epilogue 4 (their
+  // rows are the discarded n2 >= L2/2 half): those 4 warps prefetch the next
+  // tile's (gated) input into spare TMEM columns [192, 256) of their own
+  // lanes (the two column slices of a quadrant share lanes: 32 columns each).
+  constexpr bool PF = CAUSAL;
+  const uint32_t PF_COL = 192 + 32 * slice;
+  // live from epilogue 4 of tile t to the start of tile t+1: only stage A^-1
+  // (columns < 128) and the next stage A (< NA) write TMEM in between
+  static_assert(C::NA <= 192, "prefetch columns are free");
+  constexpr int PF_CH = (C::R * C::CH) / 128;  // chunks per idle thread
+  const bool idle4 = CAUSAL && (quad & 1);
+  const int pf_ii = ((quad >> 1) * 2 + slice) * 32 + lane;  // 0..127 among idle threads
+  const int pf_n2 = pf_ii % KROWS, pf_j = (pf_ii / KROWS) % JC, pf_r0 = pf_ii / (KROWS * JC);
+  constexpr int PF_RSTEP = 128 / (KROWS * JC);
+  static_assert(!PF || (128 % (KROWS * JC) == 0 && PF_CH == 8), "prefetch mapping");
+  const int64_t pf_off0 = int64_t(pf_r0) * HN + int64_t(pf_n2 * JC + pf_j) * 8;
+  bool prefetched = false;
+
   int64_t h = (t0 + wg) / nbt, bt = (t0 + wg) % nbt;
   for (int64_t t = t0 + wg; t < t1; t += kWG, bt += kWG) {
     while (bt >= nbt) { bt -= nbt; ++h; }
@@ -285,7 +333,18 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
     }
 
     // ---------------- load (+ gate) the tile's rows straight into the stage A operand
-    {
+    if (prefetched) {
+      if (idle4) {
+        uint32_t v[32];
+        tmem_ld16(tq + PF_COL, reinterpret_cast<float*>(v));
+        tmem_ld16(tq + PF_COL + 16, reinterpret_cast<float*>(v + 16));
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < PF_CH; ++i)
+          st_shared_v4(chunk_dst(pf_r0 + i * PF_RSTEP, pf_n2, pf_j), v[4 * i], v[4 * i + 1], v[4 * i + 2],
+                       v[4 * i + 3]);
+      }
+    } else {
       constexpr int NCH = C::R * C::CH;
       constexpr int PER_ALL = NCH / kWGThreads;
       constexpr int PER = PER_ALL < 4 ? PER_ALL : 4;  // loads in flight per batch (register budget)
@@ -307,32 +366,8 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         // n2 fastest so 8 consecutive threads fill one 128 B core matrix
-        const int r = ld_r0 + (i0 + i) * RSTEP;
-        const int p = r >> 1, c = r & 1;
-        const int k = c * C::KA + ld_n2;
-        const uint32_t dst = bufX + (p * JC + ld_j) * C::SBO_A + (k >> 3) * 128 + (k & 7) * 16;
-        if constexpr (std::is_same<T, __half>::value) {
-          // the fp16 product of two fp16 values equals the fp32 product rounded
-          // to fp16, so gate with HMUL2 and skip conversions
-          uint4 g = uv[i];
-          if (GATED) {
-            __half2* a = reinterpret_cast<__half2*>(&g);
-            const __half2* bb = reinterpret_cast<const __half2*>(&wv[i]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) a[e] = __hmul2(a[e], bb[e]);
-          }
-          st_shared_v4(dst, g.x, g.y, g.z, g.w);
-        } else {
-          float g[8];
-          IO<T>::to_f32x8(uv[i], g);
-          if (GATED) {
-            float w8[8];
-            IO<T>::to_f32x8(wv[i], w8);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) g[e] *= w8[e];
-          }
-          st_half8(dst, g);
-        }
+        const uint4 g = gate8(uv[i], wv[i]);
+        st_shared_v4(chunk_dst(ld_r0 + (i0 + i) * RSTEP, ld_n2, ld_j), g.x, g.y, g.z, g.w);
       }
     }
     }
@@ -476,7 +511,36 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
     // ---------------- epilogue 4: (gate), convert, store y
     {
       const int cp = m >> 6;
-      if (!CAUSAL || (m & 63) < L2 / 2) {  // warp-uniform
+      const bool has_next = t + kWG < t1;
+      if (idle4) {  // warp-uniform: prefetch the next tile's input into TMEM
+        if (has_next) {
+          int64_t h2 = h, bt2 = bt + kWG;
+          while (bt2 >= nbt) { bt2 -= nbt; ++h2; }
+          const int64_t base2 = (bt2 * C::R * H + h2) * N;
+          const int left2 = int(B - bt2 * C::R < C::R ? B - bt2 * C::R : C::R);
+          uint4 uv[PF_CH], wv[PF_CH];
+#pragma unroll
+          for (int i = 0; i < PF_CH; ++i) {
+            const int r = pf_r0 + i * PF_RSTEP;
+            if (r < left2) {
+              const int64_t goff = base2 + pf_off0 + int64_t(i * PF_RSTEP) * HN;
+              uv[i] = *reinterpret_cast<const uint4*>(gu + goff);
+              if (GATED) wv[i] = *reinterpret_cast<const uint4*>(gw + goff);
+            } else {
+              uv[i] = make_uint4(0, 0, 0, 0);
+              wv[i] = make_uint4(0, 0, 0, 0);
+            }
+          }
+          uint32_t v[32];
+#pragma unroll
+          for (int i = 0; i < PF_CH; ++i) {
+            const uint4 g = gate8(uv[i], wv[i]);
+            v[4 * i] = g.x; v[4 * i + 1] = g.y; v[4 * i + 2] = g.z; v[4 * i + 3] = g.w;
+          }
+          tmem_st32(tq + PF_COL, v);
+          tmem_st_wait();
+        }
+      } else if (!CAUSAL || (m & 63) < L2 / 2) {  // warp-uniform
         // this warp's items cover output columns [64 slice, 64 slice + 64)
         constexpr int NIT = C::P * (L1 / 8);  // (pair, 8-wide n1 chunk) items
         constexpr int PER = NIT / 2;
@@ -516,6 +580,7 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
     }
     tc_fence_before();
     wg_sync();  // TMEM columns and bufX are reused by the next tile
+    prefetched = PF && (t + kWG < t1);
   }
   __syncthreads();
   if (warp == 0) tmem_dealloc<(kWG * C::TMEM_COLS > 512 ? 512 : kWG * C::TMEM_COLS)>(tmem_slot);
