@@ -83,7 +83,9 @@ typedef struct {
   int64_t fft_size;          /* L                                             */
   int32_t causal;            /* 1 causal (zero-padded), 0 circular            */
   int32_t dtype;             /* fftconv_dtype_t                               */
-  int32_t regime;            /* 1 fused single pass, 2 partial (chunked)      */
+  int32_t regime;            /* 1 fused single pass, 2 partial (chunked),
+                                3 multipass (outer L0-point passes + fused
+                                inner transform, Alg. 4)                     */
   int32_t order;             /* Monarch order p of the complex transform      */
   int32_t factors[4];        /* L = prod factors[0..order)                    */
   int32_t rows_per_tile;     /* batch rows one CTA work unit processes        */
@@ -123,8 +125,16 @@ fftconv_status_t fftconv_plan_upload(fftconv_plan_t plan, void* d_tables, fftcon
 fftconv_status_t fftconv_precompute_kf(fftconv_plan_t plan, const float* d_k, int64_t H, int64_t K, void* d_kf,
                                        fftconv_stream_t stream);
 
+/* Device workspace the forward (for_bwd = 0) or backward (for_bwd = 1) call
+ * needs for a (B, H) problem.  The fused regime's forward needs none; the
+ * multipass regime (regime 3, Alg. 4) keeps its fp16 intermediate
+ * there (2 * ceil(B/2) * H * fft_size * 2 bytes). */
+fftconv_status_t fftconv_workspace_size(fftconv_plan_t plan, int64_t B, int64_t H, int for_bwd, size_t* bytes);
+
 /* y = u conv k (Alg. 1; real packing, causal padding and the
- * pointwise k_f product fused).  d_workspace may be NULL. */
+ * pointwise k_f product fused).  d_workspace: at least
+ * fftconv_workspace_size(plan, B, H, 0) bytes, 16-byte aligned (NULL allowed
+ * when that size is 0). */
 fftconv_status_t fftconv_fwd(fftconv_plan_t plan, const void* d_u, const void* d_kf, void* d_y, int64_t B,
                              int64_t H, void* d_workspace, fftconv_stream_t stream);
 

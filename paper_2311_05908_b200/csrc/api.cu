@@ -10,6 +10,7 @@
 #include "fftconv.h"
 #include "fwd_params.h"
 #include "plan.h"
+#include "layout.h"
 
 using namespace fc;
 
@@ -86,19 +87,53 @@ extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float*
   prm.L = p->L;
   prm.L1 = p->L1;
   prm.L2 = p->L2;
-  cudaError_t e = launch_precompute_kf(prm, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e;
+  if (p->regime == REGIME_MULTIPASS) {
+    const size_t block = size_t(p->L2) * tab_stride(uint32_t(p->L1 / 2));
+    prm.L = p->Lp;
+    e = launch_mp_precompute_kf(prm, reinterpret_cast<const float2*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.wbase),
+                                p->L0, p->Lp, block, reinterpret_cast<cudaStream_t>(stream));
+    g_launches += H > 0 ? 2 : 0;
+  } else {
+    e = launch_precompute_kf(prm, reinterpret_cast<cudaStream_t>(stream));
+    g_launches += H > 0 ? 1 : 0;
+  }
   if (e != cudaSuccess) return cuda_fail("fftconv_precompute_kf", e);
-  g_launches += H > 0 ? 1 : 0;
   return FFTCONV_OK;
 }
 
 static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, const void* v, const void* kf,
-                                void* y, int64_t B, int64_t H, fftconv_stream_t stream, const char* fn) {
+                                void* y, int64_t B, int64_t H, void* ws, fftconv_stream_t stream, const char* fn) {
   const bool gated = (w != nullptr);
-  fftconv_status_t st = gated ? check_signal_args(p, fn, B, H, {u, w, v, kf, y}) : check_signal_args(p, fn, B, H, {u, kf, y});
-  if (st != FFTCONV_OK) return st;
+  fftconv_status_t chk = gated ? check_signal_args(p, fn, B, H, {u, w, v, kf, y}) : check_signal_args(p, fn, B, H, {u, kf, y});
+  if (chk != FFTCONV_OK) return chk;
   if (gated && !v) { set_last_error(std::string(fn) + ": v is NULL"); return FFTCONV_ERR_INVALID_ARG; }
   if (B * H == 0) return FFTCONV_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (p->regime == REGIME_MULTIPASS) {
+    if (!ws) { set_last_error(std::string(fn) + ": multipass regime needs a workspace"); return FFTCONV_ERR_INVALID_ARG; }
+    if (!aligned16(ws)) { set_last_error(std::string(fn) + ": workspace not 16-byte aligned"); return FFTCONV_ERR_MISALIGNED; }
+    MpParams mp{};
+    mp.u = u; mp.w = w; mp.v = v; mp.y = y; mp.ws = ws;
+    mp.wbase = reinterpret_cast<const float2*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.wbase);
+    mp.B = B; mp.H = H; mp.N = p->N; mp.L0 = p->L0; mp.Lp = p->Lp;
+    mp.gated = gated ? 1 : 0;
+    mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
+    cudaError_t e = launch_mp_pass(mp, 1, st);
+    if (e != cudaSuccess) return cuda_fail(fn, e);
+    // pass 2: the fused circular kernel over the complex rows of T, in place
+    FwdParams in{};
+    in.u = ws; in.y = ws; in.kf = kf; in.tables = p->d_tables;
+    in.B = 2 * ((B + 1) / 2); in.H = H * p->L0; in.N = p->Lp;
+    in.L1 = p->L1; in.causal = 0; in.gated = 0; in.dtype = 0;
+    in.num_sms = num_sms_current();
+    e = launch_fwd_fused(in, st);
+    if (e != cudaSuccess) return cuda_fail(fn, e);
+    e = launch_mp_pass(mp, 3, st);
+    if (e != cudaSuccess) return cuda_fail(fn, e);
+    g_launches += 3;
+    return FFTCONV_OK;
+  }
   if (p->regime != REGIME_FUSED) { set_last_error(std::string(fn) + ": regime not supported by this build"); return FFTCONV_ERR_UNSUPPORTED; }
   FwdParams prm{};
   prm.u = u;
@@ -115,7 +150,7 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
   prm.gated = gated ? 1 : 0;
   prm.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
   prm.num_sms = num_sms_current();
-  cudaError_t e = launch_fwd_fused(prm, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_fwd_fused(prm, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
   g_launches += 1;
   return FFTCONV_OK;
@@ -123,16 +158,14 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
 
 extern "C" fftconv_status_t fftconv_fwd(fftconv_plan_t p, const void* d_u, const void* d_kf, void* d_y, int64_t B,
                                         int64_t H, void* d_workspace, fftconv_stream_t stream) {
-  (void)d_workspace;
-  return run_fwd(p, d_u, nullptr, nullptr, d_kf, d_y, B, H, stream, "fftconv_fwd");
+  return run_fwd(p, d_u, nullptr, nullptr, d_kf, d_y, B, H, d_workspace, stream, "fftconv_fwd");
 }
 
 extern "C" fftconv_status_t fftconv_gated_fwd(fftconv_plan_t p, const void* d_u, const void* d_w, const void* d_v,
                                               const void* d_kf, void* d_y, int64_t B, int64_t H, void* d_workspace,
                                               fftconv_stream_t stream) {
-  (void)d_workspace;
   if (!d_w || !d_v) { set_last_error("fftconv_gated_fwd: w and v are required"); return FFTCONV_ERR_INVALID_ARG; }
-  return run_fwd(p, d_u, d_w, d_v, d_kf, d_y, B, H, stream, "fftconv_gated_fwd");
+  return run_fwd(p, d_u, d_w, d_v, d_kf, d_y, B, H, d_workspace, stream, "fftconv_gated_fwd");
 }
 
 extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, const void* d_u, const void* d_w,
@@ -144,6 +177,15 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   if (!p) { set_last_error("fftconv_bwd: plan is NULL"); return FFTCONV_ERR_INVALID_ARG; }
   set_last_error("fftconv_bwd: not implemented in this build");
   return FFTCONV_ERR_UNSUPPORTED;
+}
+
+extern "C" fftconv_status_t fftconv_workspace_size(fftconv_plan_t p, int64_t B, int64_t H, int for_bwd, size_t* bytes) {
+  if (!p || !bytes || B < 0 || H < 0) { set_last_error("fftconv_workspace_size: bad argument"); return FFTCONV_ERR_INVALID_ARG; }
+  size_t n = 0;
+  if (p->regime == REGIME_MULTIPASS) n = size_t(2 * ((B + 1) / 2)) * size_t(H) * size_t(p->L) * 2;
+  if (for_bwd) n += size_t(H) * p->ws_bytes_per_head;
+  *bytes = n;
+  return FFTCONV_OK;
 }
 
 extern "C" int64_t fftconv_launch_count_reset(void) {

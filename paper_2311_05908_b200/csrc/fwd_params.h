@@ -30,4 +30,21 @@ struct KfParams {
   int32_t L1, L2;
 };
 cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s);
+
+// multipass regime (kernels_mp.cu)
+struct MpParams {
+  const void* u;
+  const void* w;
+  const void* v;
+  void* y;
+  void* ws;             // T: fp16 rows (2 * pairs, H * L0, Lp)
+  const float2* wbase;  // W_L^{n'}, n' < Lp
+  int64_t B, H, N;
+  int32_t L0, Lp;
+  int32_t gated;
+  int32_t dtype;
+};
+cudaError_t launch_mp_pass(const MpParams& prm, int pass, cudaStream_t s);
+cudaError_t launch_mp_precompute_kf(const KfParams& prm, const float2* wbase, int L0, int Lp, size_t block_bytes,
+                                    cudaStream_t s);
 }  // namespace fc

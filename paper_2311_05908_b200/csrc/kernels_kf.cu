@@ -126,6 +126,70 @@ __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) 
   }
 }
 
+// Multipass regime, k_f step 2: one CTA per (head, k0) transforms the L'
+// complex values left by step 1 at the start of block (h, k0) and writes the
+// inner plan layout of K_f[k0 + L0 f'] over the same block (in place).
+__global__ void __launch_bounds__(256) mp_kf_rows_kernel(const KfParams prm, int L0, int Lp, size_t block_bytes) {
+  extern __shared__ float2 sm[];
+  const int L = Lp;
+  float2* bufs[2] = {sm, sm + L};
+  float2* tws = sm + 2 * L;
+  const int64_t blk = blockIdx.x;  // h * L0 + k0
+  const int k0 = int(blk % L0);
+  uint8_t* block = reinterpret_cast<uint8_t*>(prm.kf) + blk * block_bytes;
+  {
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.twiddle);
+    const uint32_t dst = smem_u32(tws);
+    for (int o = threadIdx.x * 16; o < L * 8; o += blockDim.x * 16) cp_async16(dst + o, src + o, true);
+    const uint32_t dd = smem_u32(sm);
+    for (int o = threadIdx.x * 16; o < L * 8; o += blockDim.x * 16) cp_async16(dd + o, block + o, true);
+    cp_async_commit();
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  int cur = 0, Ns = 1;
+  const int lg = __ffs(L) - 1;
+  const int rem = lg % 3;
+  if (rem) {
+    if (rem == 1) stockham_pass<2>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
+    else stockham_pass<4>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
+    Ns <<= rem;
+    cur ^= 1;
+    __syncthreads();
+  }
+  for (; Ns < L; Ns <<= 3) {
+    stockham_pass<8>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
+    cur ^= 1;
+    __syncthreads();
+  }
+  const float2* xs = bufs[cur];
+  const int L1 = prm.L1, L2 = prm.L2, cpr = L1 / 2;
+  for (int q = threadIdx.x; q < L2 * cpr; q += blockDim.x) {
+    const int k2 = q / cpr, k1 = 2 * (q % cpr);
+    const int f0 = k2 + L2 * k1, f1 = f0 + L2;
+    float2 v0 = xs[f0], v1 = xs[f1];
+    if (prm.mask) {
+      const float m0 = prm.mask[k0 + int64_t(L0) * f0], m1 = prm.mask[k0 + int64_t(L0) * f1];
+      v0.x *= m0; v0.y *= m0;
+      v1.x *= m1; v1.y *= m1;
+    }
+    *reinterpret_cast<float4*>(block + tab_off_rt(uint32_t(cpr), uint32_t(k2), uint32_t(k1 / 2))) =
+        make_float4(v0.x, v1.x, v0.y, v1.y);
+  }
+}
+
+cudaError_t launch_mp_kf_rows(const KfParams& prm, int L0, int Lp, size_t block_bytes, cudaStream_t s) {
+  const size_t smem = size_t(Lp) * sizeof(float2) * 3;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(mp_kf_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  mp_kf_rows_kernel<<<unsigned(prm.H * L0), 256, smem, s>>>(prm, L0, Lp, block_bytes);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s) {
   if (prm.H <= 0) return cudaSuccess;
   const size_t smem = size_t(prm.L) * sizeof(float2) * 3;

@@ -1,0 +1,240 @@
+// kernels_mp.cu -- multipass regime for long sequences (Alg. 4).
+//
+// L = L0 * L' with L' = 2048 (the fused order-2 kernel's circular size) and
+// L0 = L / L' in {2, 4, 8, 16}; n = n' + L' n0, f = k0 + L0 f'.
+//   pass 1 (outer forward, this file): for each row pair z = g_b + i g_{b+1}
+//     and column n', DFT_L0 over n0 (only n0 < L0/2 are non-zero: causal
+//     padding), twiddle W_L^{n' k0}, scale 1/sqrt(L0)  ->  T,
+//     stored as fp16 rows (2p + re/im, h L0 + k0, n').
+//   pass 2 (inner, kernels_fwd.cu): the fused circular kernel on T with
+//     H' = H L0 "heads" (h, k0); head (h, k0) uses the k_f block
+//     K_f[k0 + L0 f'] ("fold N1 into H").
+//   pass 3 (outer inverse, this file): conj twiddle, IDFT_L0 over k0, keep
+//     n0 < L0/2 (causal output), scale 1/sqrt(L0), split re/im into rows b,
+//     b+1, gate by v, store.
+// The outer DFTs are small (L0 <= 16) and run in fp32 registers; the
+// tensor-core work is in pass 2.  T is written in place by pass 2.
+#include <cuda_runtime.h>
+
+#include "dft_small.cuh"
+#include "fwd_params.h"
+#include "sm100.cuh"
+
+namespace fc {
+
+namespace {
+
+template <typename T>
+FC_DEVICE float2 ld2(const T* p);
+template <>
+FC_DEVICE float2 ld2<__half>(const __half* p) {
+  return __half22float2(*reinterpret_cast<const __half2*>(p));
+}
+template <>
+FC_DEVICE float2 ld2<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+}
+template <typename T>
+FC_DEVICE void st2(T* p, float a, float b);
+template <>
+FC_DEVICE void st2<__half>(__half* p, float a, float b) {
+  *reinterpret_cast<__half2*>(p) = __floats2half2_rn(a, b);
+}
+template <>
+FC_DEVICE void st2<__nv_bfloat16>(__nv_bfloat16* p, float a, float b) {
+  *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(a, b);
+}
+
+// Each thread owns two adjacent columns (n', n'+1) of one (pair, head).
+template <int L0, bool GATED, typename T>
+__global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
+  const int64_t NP = int64_t(prm.Lp) / 2;  // column pairs per (pair, head)
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t pairs = (prm.B + 1) / 2;
+  if (idx >= pairs * prm.H * NP) return;
+  const int cp = int(idx % NP);
+  const int64_t ph = idx / NP;
+  const int64_t h = ph % prm.H, p = ph / prm.H;
+  const int n = 2 * cp;  // first column n'
+  const int64_t b0 = 2 * p, b1 = 2 * p + 1;
+  const bool has1 = b1 < prm.B;
+  const T* __restrict__ u = reinterpret_cast<const T*>(prm.u);
+  const T* __restrict__ w = reinterpret_cast<const T*>(prm.w);
+  const int64_t r0 = (b0 * prm.H + h) * prm.N + n, r1 = (b1 * prm.H + h) * prm.N + n;
+  float2 z0[L0], z1[L0];  // column n and n+1, complex z = g_b + i g_{b+1}
+#pragma unroll
+  for (int n0 = 0; n0 < L0; ++n0) {
+    z0[n0] = make_float2(0.f, 0.f);
+    z1[n0] = make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int n0 = 0; n0 < L0 / 2; ++n0) {
+    const int64_t o = int64_t(n0) * prm.Lp;
+    float2 a = ld2<T>(u + r0 + o);  // row b, columns n, n+1
+    float2 c = has1 ? ld2<T>(u + r1 + o) : make_float2(0.f, 0.f);
+    if (GATED) {
+      const float2 wa = ld2<T>(w + r0 + o);
+      const float2 wc = has1 ? ld2<T>(w + r1 + o) : make_float2(0.f, 0.f);
+      a.x *= wa.x; a.y *= wa.y;
+      c.x *= wc.x; c.y *= wc.y;
+    }
+    z0[n0] = make_float2(a.x, c.x);
+    z1[n0] = make_float2(a.y, c.y);
+  }
+  DftReg<L0, false>::run(z0);
+  DftReg<L0, false>::run(z1);
+  // twiddle W_L^{n' k0} by recurrence from W_L^{n'} (error ~ L0 ulp, fp32)
+  const float2 b0w = prm.wbase[n], b1w = prm.wbase[n + 1];
+  float2 t0 = make_float2(1.f, 0.f), t1 = make_float2(1.f, 0.f);
+  const float s = rsqrtf(float(L0));
+  __half* __restrict__ Tw = reinterpret_cast<__half*>(prm.ws);
+  const int64_t HL0 = prm.H * L0;
+#pragma unroll
+  for (int k0 = 0; k0 < L0; ++k0) {
+    const float2 a = c_mul(z0[k0], t0), c = c_mul(z1[k0], t1);
+    const int64_t row_re = ((2 * p) * HL0 + h * L0 + k0) * prm.Lp + n;
+    const int64_t row_im = ((2 * p + 1) * HL0 + h * L0 + k0) * prm.Lp + n;
+    *reinterpret_cast<__half2*>(Tw + row_re) = __floats2half2_rn(a.x * s, c.x * s);
+    *reinterpret_cast<__half2*>(Tw + row_im) = __floats2half2_rn(a.y * s, c.y * s);
+    t0 = c_mul(t0, b0w);
+    t1 = c_mul(t1, b1w);
+  }
+}
+
+template <int L0, bool GATED, typename T>
+__global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
+  const int64_t NP = int64_t(prm.Lp) / 2;
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t pairs = (prm.B + 1) / 2;
+  if (idx >= pairs * prm.H * NP) return;
+  const int cp = int(idx % NP);
+  const int64_t ph = idx / NP;
+  const int64_t h = ph % prm.H, p = ph / prm.H;
+  const int n = 2 * cp;
+  const __half* __restrict__ Tw = reinterpret_cast<const __half*>(prm.ws);
+  const int64_t HL0 = prm.H * L0;
+  float2 x0[L0], x1[L0];
+  const float2 b0w = prm.wbase[n], b1w = prm.wbase[n + 1];
+  float2 t0 = make_float2(1.f, 0.f), t1 = make_float2(1.f, 0.f);
+#pragma unroll
+  for (int k0 = 0; k0 < L0; ++k0) {
+    const int64_t row_re = ((2 * p) * HL0 + h * L0 + k0) * prm.Lp + n;
+    const int64_t row_im = ((2 * p + 1) * HL0 + h * L0 + k0) * prm.Lp + n;
+    const float2 re = __half22float2(*reinterpret_cast<const __half2*>(Tw + row_re));
+    const float2 im = __half22float2(*reinterpret_cast<const __half2*>(Tw + row_im));
+    x0[k0] = c_mulc(make_float2(re.x, im.x), t0);
+    x1[k0] = c_mulc(make_float2(re.y, im.y), t1);
+    t0 = c_mul(t0, b0w);
+    t1 = c_mul(t1, b1w);
+  }
+  DftReg<L0, true>::run(x0);
+  DftReg<L0, true>::run(x1);
+  const float s = rsqrtf(float(L0));
+  const int64_t b0 = 2 * p, b1 = 2 * p + 1;
+  const bool has1 = b1 < prm.B;
+  T* __restrict__ y = reinterpret_cast<T*>(prm.y);
+  const T* __restrict__ v = reinterpret_cast<const T*>(prm.v);
+  const int64_t r0 = (b0 * prm.H + h) * prm.N + n, r1 = (b1 * prm.H + h) * prm.N + n;
+#pragma unroll
+  for (int n0 = 0; n0 < L0 / 2; ++n0) {  // causal: first half of the output only
+    const int64_t o = int64_t(n0) * prm.Lp;
+    float a0 = x0[n0].x * s, a1 = x1[n0].x * s;  // row b
+    float c0 = x0[n0].y * s, c1 = x1[n0].y * s;  // row b+1
+    if (GATED) {
+      const float2 va = ld2<T>(v + r0 + o);
+      a0 *= va.x; a1 *= va.y;
+      if (has1) {
+        const float2 vc = ld2<T>(v + r1 + o);
+        c0 *= vc.x; c1 *= vc.y;
+      }
+    }
+    st2<T>(y + r0 + o, a0, a1);
+    if (has1) st2<T>(y + r1 + o, c0, c1);
+  }
+}
+
+// k_f, step 1: per (head, column n'): DFT_L0 of k[n' + L' n0] (n0 < L0/2,
+// K <= L/2), twiddle W_L^{n' k0}; fp32 scratch written into the head's k_f
+// blocks (block k0 holds the L' complex values of row k0, unpadded).
+template <int L0>
+__global__ void __launch_bounds__(256) mp_kf_cols_kernel(const KfParams prm, const float2* __restrict__ wbase,
+                                                         int Lp, size_t block_bytes) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= prm.H * Lp) return;
+  const int n = int(idx % Lp);
+  const int64_t h = idx / Lp;
+  float2 z[L0];
+#pragma unroll
+  for (int n0 = 0; n0 < L0; ++n0) {
+    const int64_t t = int64_t(n) + int64_t(n0) * Lp;
+    z[n0] = make_float2(t < prm.K ? prm.k[h * prm.K + t] : 0.f, 0.f);
+  }
+  DftReg<L0, false>::run(z);
+  const float2 bw = wbase[n];
+  float2 tw = make_float2(1.f, 0.f);
+  uint8_t* base = reinterpret_cast<uint8_t*>(prm.kf) + h * L0 * block_bytes;
+#pragma unroll
+  for (int k0 = 0; k0 < L0; ++k0) {
+    reinterpret_cast<float2*>(base + k0 * block_bytes)[n] = c_mul(z[k0], tw);
+    tw = c_mul(tw, bw);
+  }
+}
+
+}  // namespace
+
+// k_f, step 2 lives in kernels_kf.cu (row FFTs into the inner plan layout).
+cudaError_t launch_mp_kf_rows(const KfParams& prm, int L0, int Lp, size_t block_bytes, cudaStream_t s);
+
+template <int L0>
+static cudaError_t launch_mp_l0(const MpParams& prm, int pass, cudaStream_t s) {
+  const int64_t total = ((prm.B + 1) / 2) * prm.H * (prm.Lp / 2);
+  const unsigned grid = unsigned((total + 255) / 256);
+  if (total == 0) return cudaSuccess;
+  const bool g = prm.gated != 0;
+  if (pass == 1) {
+    if (prm.dtype == 0) {
+      if (g) mp_pass1_kernel<L0, true, __half><<<grid, 256, 0, s>>>(prm);
+      else mp_pass1_kernel<L0, false, __half><<<grid, 256, 0, s>>>(prm);
+    } else {
+      if (g) mp_pass1_kernel<L0, true, __nv_bfloat16><<<grid, 256, 0, s>>>(prm);
+      else mp_pass1_kernel<L0, false, __nv_bfloat16><<<grid, 256, 0, s>>>(prm);
+    }
+  } else {
+    if (prm.dtype == 0) {
+      if (g) mp_pass3_kernel<L0, true, __half><<<grid, 256, 0, s>>>(prm);
+      else mp_pass3_kernel<L0, false, __half><<<grid, 256, 0, s>>>(prm);
+    } else {
+      if (g) mp_pass3_kernel<L0, true, __nv_bfloat16><<<grid, 256, 0, s>>>(prm);
+      else mp_pass3_kernel<L0, false, __nv_bfloat16><<<grid, 256, 0, s>>>(prm);
+    }
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mp_pass(const MpParams& prm, int pass, cudaStream_t s) {
+  switch (prm.L0) {
+    case 2: return launch_mp_l0<2>(prm, pass, s);
+    case 4: return launch_mp_l0<4>(prm, pass, s);
+    case 8: return launch_mp_l0<8>(prm, pass, s);
+    case 16: return launch_mp_l0<16>(prm, pass, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_mp_precompute_kf(const KfParams& prm, const float2* wbase, int L0, int Lp, size_t block_bytes,
+                                    cudaStream_t s) {
+  if (prm.H <= 0) return cudaSuccess;
+  const unsigned grid = unsigned((prm.H * Lp + 255) / 256);
+  switch (L0) {
+    case 2: mp_kf_cols_kernel<2><<<grid, 256, 0, s>>>(prm, wbase, Lp, block_bytes); break;
+    case 4: mp_kf_cols_kernel<4><<<grid, 256, 0, s>>>(prm, wbase, Lp, block_bytes); break;
+    case 8: mp_kf_cols_kernel<8><<<grid, 256, 0, s>>>(prm, wbase, Lp, block_bytes); break;
+    case 16: mp_kf_cols_kernel<16><<<grid, 256, 0, s>>>(prm, wbase, Lp, block_bytes); break;
+    default: return cudaErrorInvalidValue;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_mp_kf_rows(prm, L0, Lp, block_bytes, s);
+}
+
+}  // namespace fc

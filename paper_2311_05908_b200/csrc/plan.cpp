@@ -150,10 +150,9 @@ static void put_float(std::vector<uint8_t>& img, size_t off, double x) {
 //  TWT : [k2][n1/2] {wr(n1), wr(n1+1), wi(n1), wi(n1+1)} fp32
 // DFT matrices carry the unitary 1/sqrt(L_i) scale, so the whole forward +
 // inverse pair scales by 1/L and k_f is used unscaled.
-static void build_fused_tables(fftconv_plan_s* p) {
+static void build_fused_tables(fftconv_plan_s* p, int64_t L) {
   const int L1 = p->L1, L2 = p->L2, KA = p->KA;
   const int NA = 3 * L2, NB = (3 * L1 + 15) / 16 * 16;
-  const int64_t L = p->L;
   TableLayout& t = p->tl;
   size_t off = 0;
   t.ga = off;  t.ga_bytes = size_t(NA) * (2 * KA) * 2;      off = align_up(off + t.ga_bytes, 1024);
@@ -163,6 +162,8 @@ static void build_fused_tables(fftconv_plan_s* p) {
   t.tw = off;  t.tw_bytes = size_t(L1) * tab_stride(L2 / 2); off = align_up(off + t.tw_bytes, 1024);
   t.twt = off; t.twt_bytes = size_t(L2) * tab_stride(L1 / 2); off = align_up(off + t.twt_bytes, 1024);
   t.wl = off;  t.wl_bytes = size_t(L) * 8;                  off = align_up(off + t.wl_bytes, 1024);
+  const int64_t Lfull = p->L;  // the whole transform (== L unless multipass)
+  t.wbase = off; t.wbase_bytes = Lfull != L ? size_t(L) * 8 : 0; off = align_up(off + t.wbase_bytes, 1024);
   t.total = off;
   p->image.assign(t.total, 0);
   std::vector<uint8_t>& img = p->image;
@@ -218,13 +219,21 @@ static void build_fused_tables(fftconv_plan_s* p) {
       put_float(img, t.twt + r + (n1 & 1) * 4, wr);
       put_float(img, t.twt + r + 8 + (n1 & 1) * 4, wi);
     }
-  // full-length twiddles for the k_f precompute
+  // full-length twiddles of the (inner) transform for the k_f precompute
   for (int64_t e = 0; e < L; ++e) {
     double wr, wi;
     root(e, L, &wr, &wi);
     put_float(img, t.wl + size_t(e) * 8, wr);
     put_float(img, t.wl + size_t(e) * 8 + 4, wi);
   }
+  // multipass outer twiddle bases W_Lfull^{n'} ("Twiddle factors")
+  if (t.wbase_bytes)
+    for (int64_t e = 0; e < L; ++e) {
+      double wr, wi;
+      root(e, Lfull, &wr, &wi);
+      put_float(img, t.wbase + size_t(e) * 8, wr);
+      put_float(img, t.wbase + size_t(e) * 8 + 4, wi);
+    }
 }
 
 // A13: keep(f) = prod_j keep_j[digit_j(f)], digits of f on the row-major
@@ -299,22 +308,35 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
   } else {
     p->regime = REGIME_FUSED;
   }
-  // Fused order-2 kernel family: L = L1 * 64, L1 in {8, 16, 32}.
+  // Regimes:
+  //  fused     : L = L1 * 64, L1 in {8, 16, 32}; causal L = 2N or circular L = N
+  //  multipass : causal, L = L0 * 2048 with L0 in {2, 4, 8, 16} (N = 2048..16384)
   const int64_t L = fft_size;
-  const bool fused_ok = (L >= 512 && L <= 2048) && (p->regime == REGIME_FUSED) &&
-                        (!causal || fft_size == 2 * N) && dtype != FFTCONV_F32;
-  if (!fused_ok) {
+  const bool io_ok = dtype != FFTCONV_F32;
+  if (io_ok && p->regime == REGIME_FUSED && L >= 512 && L <= 2048 && (!causal || fft_size == 2 * N)) {
+    p->order = 2;
+    p->L2 = 64;
+    p->L1 = int32_t(L / 64);
+    p->KA = causal ? p->L2 / 2 : p->L2;
+    p->P = std::max(128 / p->L1, 2);
+    build_fused_tables(p, L);
+    p->Lp = int32_t(L);
+  } else if (io_ok && p->regime == REGIME_FUSED && causal && fft_size == 2 * N && L >= 4096 && L <= 32768) {
+    p->regime = REGIME_MULTIPASS;
+    p->order = 3;
+    p->Lp = 2048;
+    p->L0 = int32_t(L / 2048);
+    p->L2 = 64;
+    p->L1 = 32;
+    p->KA = 64;  // the inner transform is circular over complex rows
+    p->P = 4;
+    build_fused_tables(p, p->Lp);
+  } else {
     delete p;
-    set_last_error("fftconv_plan: this build supports the fused single-pass regime for fft_size 512..2048 "
-                   "(causal fft_size == 2N, or circular) with fp16/bf16 I/O");
+    set_last_error("fftconv_plan: this build supports fp16/bf16 I/O with fft_size 512..2048 (fused; causal "
+                   "fft_size == 2N or circular) and causal fft_size 4096..32768 == 2N (multipass)");
     return FFTCONV_ERR_UNSUPPORTED;
   }
-  p->order = 2;
-  p->L2 = 64;
-  p->L1 = int32_t(L / 64);
-  p->KA = causal ? p->L2 / 2 : p->L2;
-  p->P = std::max(128 / p->L1, 2);
-  build_fused_tables(p);
   if (sparsity) {
     fftconv_status_t s = build_mask(p, sparsity);
     if (s != FFTCONV_OK) {
@@ -327,7 +349,8 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
     p->image.resize(mo + p->mask.size() * sizeof(float));
     std::memcpy(p->image.data() + mo, p->mask.data(), p->mask.size() * sizeof(float));
   }
-  p->kf_bytes_per_head = size_t(p->L2) * tab_stride(uint32_t(p->L1 / 2));  // complex fp32 [k2][k1/2] pairs, padded rows
+  // complex fp32 [k2][k1/2] pairs with padded rows, one block per outer index k0
+  p->kf_bytes_per_head = size_t(p->L0) * size_t(p->L2) * tab_stride(uint32_t(p->L1 / 2));
   p->ws_bytes_per_head = size_t(L) * 8;  // fp32 spectral accumulator for dk
   *out = p;
   set_last_error("");
@@ -343,8 +366,14 @@ extern "C" fftconv_status_t fftconv_plan_info(fftconv_plan_t p, fftconv_plan_inf
   info->dtype = p->dtype;
   info->regime = p->regime;
   info->order = p->order;
-  info->factors[0] = p->L1;
-  info->factors[1] = p->L2;
+  if (p->regime == REGIME_MULTIPASS) {
+    info->factors[0] = p->L0;
+    info->factors[1] = p->L1;
+    info->factors[2] = p->L2;
+  } else {
+    info->factors[0] = p->L1;
+    info->factors[1] = p->L2;
+  }
   info->rows_per_tile = 2 * p->P;
   info->max_kernel_len = p->causal ? p->L / 2 : p->L;
   info->table_bytes = p->image.size();

@@ -10,7 +10,7 @@
 
 namespace fc {
 
-enum Regime : int32_t { REGIME_FUSED = 1, REGIME_PARTIAL = 2 };
+enum Regime : int32_t { REGIME_FUSED = 1, REGIME_PARTIAL = 2, REGIME_MULTIPASS = 3 };
 
 // Byte offsets of the constant tables inside the uploaded device image.
 // Each table is stored exactly as the fused kernel wants it in shared memory
@@ -24,6 +24,7 @@ struct TableLayout {
   size_t tw = 0, tw_bytes = 0;    // W_L^{n1 k2}, [n1][k2/2] float4 pairs, swizzled
   size_t twt = 0, twt_bytes = 0;  // same values, [k2][n1/2]
   size_t wl = 0, wl_bytes = 0;    // W_L^e, e < L, float2 (k_f precompute)
+  size_t wbase = 0, wbase_bytes = 0;  // multipass: W_L^{n'}, n' < L', float2
   size_t total = 0;
 };
 
@@ -40,6 +41,8 @@ struct fftconv_plan_s {
   int32_t KA = 0;          // contracted length of stage A (L2/2 causal, L2 circular)
   int32_t P = 0;           // row pairs per tile (two-row real packing)
   int64_t chunk = 0;       // partial regime: chunk length (= L/2)
+  int32_t L0 = 1;          // multipass: outer factor, L = L0 * Lp
+  int32_t Lp = 0;          // multipass: inner (fused) transform length
   fc::TableLayout tl;
   std::vector<uint8_t> image;  // host copy of the table image
   void* d_tables = nullptr;    // bound by fftconv_plan_upload

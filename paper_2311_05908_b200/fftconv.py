@@ -111,19 +111,32 @@ class FFTConvPlan:
             assert t.is_cuda and t.dtype == self.dtype and t.is_contiguous() and t.dim() == 3
             assert t.shape[-1] == self.info.N, (t.shape, self.info.N)
 
-    def fwd(self, u: torch.Tensor, kf: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    def workspace_bytes(self, B: int, H: int, for_bwd: bool = False) -> int:
+        n = ctypes.c_size_t()
+        _abi.check(_abi.lib().fftconv_workspace_size(self._h, B, H, int(for_bwd), ctypes.byref(n)))
+        return int(n.value)
+
+    def workspace(self, B: int, H: int, for_bwd: bool = False, device=None):
+        n = self.workspace_bytes(B, H, for_bwd)
+        if n == 0:
+            return None
+        return _aligned_empty(n, device or self.device, 16)
+
+    def fwd(self, u: torch.Tensor, kf: torch.Tensor, out: torch.Tensor | None = None, workspace=None) -> torch.Tensor:
         self._check_sig(u)
         B, H, _ = u.shape
         y = torch.empty_like(u) if out is None else out
-        _abi.check(_abi.lib().fftconv_fwd(self._h, _ptr(u), _ptr(kf), _ptr(y), B, H, None, _stream(u.device)))
+        ws = workspace if workspace is not None else self.workspace(B, H, device=u.device)
+        _abi.check(_abi.lib().fftconv_fwd(self._h, _ptr(u), _ptr(kf), _ptr(y), B, H, _ptr(ws), _stream(u.device)))
         return y
 
-    def gated_fwd(self, u, w, v, kf, out=None):
+    def gated_fwd(self, u, w, v, kf, out=None, workspace=None):
         self._check_sig(u, w, v)
         B, H, _ = u.shape
         y = torch.empty_like(u) if out is None else out
+        ws = workspace if workspace is not None else self.workspace(B, H, device=u.device)
         _abi.check(_abi.lib().fftconv_gated_fwd(self._h, _ptr(u), _ptr(w), _ptr(v), _ptr(kf), _ptr(y), B, H,
-                                                None, _stream(u.device)))
+                                                _ptr(ws), _stream(u.device)))
         return y
 
     def bwd(self, dy, u, kf, K, w=None, v=None):

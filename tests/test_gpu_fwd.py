@@ -128,3 +128,39 @@ def test_fwd_cfg2_full_size_sampled():
     got, ref = np.array(got), np.array(ref)
     rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     assert rel < REL_L2, rel
+
+
+# ---------------------------------------------------------------- multipass regime (N >= 2048)
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [2048, 4096, 8192, 16384])
+@pytest.mark.parametrize("dtype,gated", [("f16", False), ("f16", True), ("bf16", True)])
+def test_fwd_multipass_parity(N, dtype, gated):
+    # odd B exercises the zero-filled partner row of the last pair
+    got, ref = _run(N, True, dtype, gated, B=3, H=2)
+    _assert_close(got, ref)
+
+
+@pytest.mark.gpu
+def test_fwd_multipass_cfg3_shape_sampled():
+    """cfg 3 shape (gated causal bf16, B=16, H=768, N=8192), sampled outputs
+    against the direct sum."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    B, H, N = 16, 768, 8192
+    plan = FFTConvPlan(N, dtype=torch.bfloat16)
+    assert plan.info.regime == 3
+    rng = np.random.default_rng(3)
+    u = synth.quantize(synth.signal(7, "u", B, H, N), "bf16")
+    w = synth.quantize(synth.signal(7, "w", B, H, N), "bf16")
+    v = synth.quantize(synth.signal(7, "v", B, H, N), "bf16")
+    k = synth.decay_filters(7, H, N).astype(np.float32)
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    y = plan.gated_fwd(*(torch.tensor(a, dtype=torch.bfloat16, device="cuda") for a in (u, w, v)), kf)
+    y = y.float().cpu().numpy().reshape(B * H, N)
+    u2, w2, v2 = u.reshape(B * H, N), w.reshape(B * H, N), v.reshape(B * H, N)
+    got, ref = [], []
+    for r in rng.choice(B * H, 24, replace=False):
+        for i in rng.choice(N, 6, replace=False):
+            ref.append(v2[r, i] * orc.direct_point(u2[r], k[r % H].astype(np.float64), i, wrow=w2[r]))
+            got.append(y[r, i])
+    got, ref = np.array(got), np.array(ref)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < REL_L2
