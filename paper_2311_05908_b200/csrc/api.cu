@@ -168,22 +168,126 @@ extern "C" fftconv_status_t fftconv_gated_fwd(fftconv_plan_t p, const void* d_u,
   return run_fwd(p, d_u, d_w, d_v, d_kf, d_y, B, H, d_workspace, stream, "fftconv_gated_fwd");
 }
 
+// Workspace layout of the backward pass (bytes):
+//  fused     : [partials: H * nbt * L complex fp32]
+//  multipass : [T_g][T_dc] (fp16 rows, 2 * ceil(B/2) * H * L each)
+//              [partials: H * L0 * nbt' * Lp complex fp32][scratch: H * L complex fp32]
+static size_t bwd_ws_bytes(const fftconv_plan_s* p, int64_t B, int64_t H) {
+  if (p->regime == REGIME_MULTIPASS) {
+    const int64_t rows = 2 * ((B + 1) / 2);
+    const size_t t = size_t(rows) * size_t(H) * size_t(p->L) * 2;
+    const size_t part = size_t(H) * p->L0 * size_t(bwd_tiles_per_head(rows, p->L1)) * size_t(p->Lp) * 8;
+    return 2 * t + part + size_t(H) * size_t(p->L) * 8;
+  }
+  return size_t(H) * size_t(bwd_tiles_per_head(B, p->L1)) * size_t(p->L) * 8;
+}
+
 extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, const void* d_u, const void* d_w,
                                         const void* d_v, const void* d_kf, void* d_du, void* d_dw, void* d_dv,
                                         float* d_dk, int64_t B, int64_t H, int64_t K, void* d_workspace,
                                         fftconv_stream_t stream) {
-  (void)d_dy; (void)d_u; (void)d_w; (void)d_v; (void)d_kf; (void)d_du; (void)d_dw; (void)d_dv; (void)d_dk;
-  (void)B; (void)H; (void)K; (void)d_workspace; (void)stream;
-  if (!p) { set_last_error("fftconv_bwd: plan is NULL"); return FFTCONV_ERR_INVALID_ARG; }
-  set_last_error("fftconv_bwd: not implemented in this build");
-  return FFTCONV_ERR_UNSUPPORTED;
+  const char* fn = "fftconv_bwd";
+  const bool gated = d_w != nullptr || d_v != nullptr;
+  if (gated && !(d_w && d_v && d_dw && d_dv)) {
+    set_last_error("fftconv_bwd: gated backward needs w, v, dw and dv");
+    return FFTCONV_ERR_INVALID_ARG;
+  }
+  fftconv_status_t chk = gated ? check_signal_args(p, fn, B, H, {d_dy, d_u, d_w, d_v, d_kf, d_du, d_dw, d_dv, d_workspace})
+                               : check_signal_args(p, fn, B, H, {d_dy, d_u, d_kf, d_du, d_workspace});
+  if (chk != FFTCONV_OK) return chk;
+  const int64_t kmax = p->causal ? p->L / 2 : p->L;
+  if (K < 1 || K > kmax) { set_last_error("fftconv_bwd: K out of range"); return FFTCONV_ERR_KERNEL_TOO_LONG; }
+  if (!d_dk && H > 0) { set_last_error("fftconv_bwd: dk is NULL"); return FFTCONV_ERR_INVALID_ARG; }
+  if (H == 0) return FFTCONV_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (B == 0) {
+    cudaError_t e = cudaMemsetAsync(d_dk, 0, size_t(H) * size_t(K) * sizeof(float), st);
+    return e == cudaSuccess ? FFTCONV_OK : cuda_fail(fn, e);
+  }
+  const uint8_t* tab = static_cast<const uint8_t*>(p->d_tables);
+  DkParams dk{};
+  dk.dk = d_dk;
+  dk.mask = p->sparse ? reinterpret_cast<const float*>(tab + p->tl.total) : nullptr;
+  dk.twiddle = reinterpret_cast<const float2*>(tab + p->tl.wl);
+  dk.H = H;
+  dk.K = K;
+  cudaError_t e;
+  if (p->regime == REGIME_FUSED) {
+    BwdParams b{};
+    b.u = d_u; b.w = d_w; b.v = d_v; b.dy = d_dy; b.du = d_du; b.dw = d_dw; b.dv = d_dv;
+    b.kf = d_kf; b.tables = p->d_tables; b.acc = d_workspace;
+    b.B = B; b.H = H; b.N = p->N; b.L1 = p->L1; b.causal = p->causal;
+    b.gate_io = gated ? 1 : 0; b.need_c = gated ? 1 : 0;
+    b.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
+    b.num_sms = num_sms_current();
+    e = launch_bwd_fused(b, st);
+    if (e != cudaSuccess) return cuda_fail(fn, e);
+    dk.part = static_cast<const float2*>(d_workspace);
+    dk.nbt = bwd_tiles_per_head(B, p->L1);
+    dk.L0 = 1;
+    dk.Lp = int32_t(p->L);
+    e = launch_dk_finalize(dk, st);
+    if (e != cudaSuccess) return cuda_fail(fn, e);
+    g_launches += 2;
+    return FFTCONV_OK;
+  }
+  if (p->regime != REGIME_MULTIPASS) { set_last_error("fftconv_bwd: regime not supported by this build"); return FFTCONV_ERR_UNSUPPORTED; }
+  const int64_t rows = 2 * ((B + 1) / 2);
+  uint8_t* ws = static_cast<uint8_t*>(d_workspace);
+  const size_t tbytes = size_t(rows) * size_t(H) * size_t(p->L) * 2;
+  void* Tg = ws;
+  void* Tdc = ws + tbytes;
+  void* part = ws + 2 * tbytes;
+  const int64_t nbt_in = bwd_tiles_per_head(rows, p->L1);
+  void* scratch = static_cast<uint8_t*>(part) + size_t(H) * p->L0 * size_t(nbt_in) * size_t(p->Lp) * 8;
+  MpParams mp{};
+  mp.wbase = reinterpret_cast<const float2*>(tab + p->tl.wbase);
+  mp.B = B; mp.H = H; mp.N = p->N; mp.L0 = p->L0; mp.Lp = p->Lp;
+  mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
+  // pass 1 on g = u (* w) and on dc = dy (* v)
+  mp.u = d_u; mp.w = d_w; mp.gated = gated ? 1 : 0; mp.ws = Tg;
+  e = launch_mp_pass(mp, 1, st);
+  if (e != cudaSuccess) return cuda_fail(fn, e);
+  mp.u = d_dy; mp.w = d_v; mp.ws = Tdc;
+  e = launch_mp_pass(mp, 1, st);
+  if (e != cudaSuccess) return cuda_fail(fn, e);
+  // inner backward on the complex rows (circular), in place
+  BwdParams b{};
+  b.u = Tg; b.dy = Tdc; b.dv = Tg; b.du = Tdc;
+  b.kf = d_kf; b.tables = p->d_tables; b.acc = part;
+  b.B = rows; b.H = H * p->L0; b.N = p->Lp; b.L1 = p->L1; b.causal = 0;
+  b.gate_io = 0; b.need_c = gated ? 1 : 0; b.dtype = 0;
+  b.num_sms = num_sms_current();
+  e = launch_bwd_fused(b, st);
+  if (e != cudaSuccess) return cuda_fail(fn, e);
+  // pass 3: dv = dy * c ; du = dg * w (or dg), dw = dg * u
+  if (gated) {
+    mp.ws = Tg; mp.gated = 1; mp.v = d_dy; mp.y = d_dv; mp.v2 = nullptr; mp.y2 = nullptr;
+    e = launch_mp_pass(mp, 3, st);
+    if (e != cudaSuccess) return cuda_fail(fn, e);
+    mp.ws = Tdc; mp.v = d_w; mp.y = d_du; mp.v2 = d_u; mp.y2 = d_dw;
+  } else {
+    mp.ws = Tdc; mp.gated = 0; mp.v = nullptr; mp.y = d_du; mp.v2 = nullptr; mp.y2 = nullptr;
+  }
+  e = launch_mp_pass(mp, 3, st);
+  if (e != cudaSuccess) return cuda_fail(fn, e);
+  dk.part = static_cast<const float2*>(part);
+  dk.scratch = static_cast<float2*>(scratch);
+  dk.wbase = mp.wbase;
+  dk.nbt = nbt_in;
+  dk.L0 = p->L0;
+  dk.Lp = p->Lp;
+  e = launch_dk_finalize(dk, st);
+  if (e != cudaSuccess) return cuda_fail(fn, e);
+  g_launches += gated ? 7 : 6;
+  return FFTCONV_OK;
 }
 
 extern "C" fftconv_status_t fftconv_workspace_size(fftconv_plan_t p, int64_t B, int64_t H, int for_bwd, size_t* bytes) {
   if (!p || !bytes || B < 0 || H < 0) { set_last_error("fftconv_workspace_size: bad argument"); return FFTCONV_ERR_INVALID_ARG; }
   size_t n = 0;
-  if (p->regime == REGIME_MULTIPASS) n = size_t(2 * ((B + 1) / 2)) * size_t(H) * size_t(p->L) * 2;
-  if (for_bwd) n += size_t(H) * p->ws_bytes_per_head;
+  if (for_bwd) n = bwd_ws_bytes(p, B, H);
+  else if (p->regime == REGIME_MULTIPASS) n = size_t(2 * ((B + 1) / 2)) * size_t(H) * size_t(p->L) * 2;
   *bytes = n;
   return FFTCONV_OK;
 }

@@ -1,0 +1,136 @@
+// fused_common.cuh -- pieces shared by the fused forward and backward
+// order-2 kernels: I/O conversions, the tile configuration (shared-memory
+// table offsets must match the host image built in plan.cpp), operand store
+// helpers and the f32x2 complex multiplies.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "sm100.cuh"
+
+namespace fc {
+
+template <typename T>
+struct IO;
+template <>
+struct IO<__half> {
+  static FC_DEVICE void to_f32x8(const uint4& v, float* f) {
+    const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 t = __half22float2(h[i]);
+      f[2 * i] = t.x;
+      f[2 * i + 1] = t.y;
+    }
+  }
+  static FC_DEVICE uint32_t pack2(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+};
+template <>
+struct IO<__nv_bfloat16> {
+  static FC_DEVICE void to_f32x8(const uint4& v, float* f) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 t = __bfloat1622float2(h[i]);
+      f[2 * i] = t.x;
+      f[2 * i + 1] = t.y;
+    }
+  }
+  static FC_DEVICE uint32_t pack2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+};
+
+constexpr int kWGThreads = 256;        // 8 warps: 4 TMEM lane quadrants x 2 column slices
+
+template <int L1, bool CAUSAL>
+struct O2Cfg {
+  static constexpr int L2 = 64;
+  static constexpr int L = L1 * L2;
+  static constexpr int P = 128 / L1;            // row pairs per tile
+  static constexpr int R = 2 * P;               // batch rows per tile
+  static constexpr int KA = CAUSAL ? L2 / 2 : L2;
+  static constexpr int NOUT = CAUSAL ? L / 2 : L;  // row length N
+  static constexpr int CH = NOUT / 8;           // 16-byte chunks per row (16-bit I/O)
+  static constexpr int NA = 3 * L2;             // stage A N: re | im | -im
+  static constexpr int NB = (3 * L1 + 15) / 16 * 16;  // stage B/B^-1 N: re | im | -im (-re) | pad
+  // tables (same offsets as the host image, see plan.cpp)
+  static constexpr uint32_t GA_BYTES = NA * 2 * KA * 2;
+  static constexpr uint32_t GB_BYTES = NB * 2 * L1 * 2;
+  static constexpr uint32_t GAI_BYTES = 2 * L2 * 2 * L2 * 2;
+  static constexpr uint32_t TW_BYTES = L1 * (L2 / 2 * 16 + 16);    // padded rows, see layout.h
+  static constexpr uint32_t TWT_BYTES = L2 * (L1 / 2 * 16 + 16);
+  static constexpr uint32_t al(uint32_t x) { return (x + 1023u) / 1024u * 1024u; }
+  static constexpr uint32_t OFF_GA = 0;
+  static constexpr uint32_t OFF_GB = al(OFF_GA + GA_BYTES);
+  static constexpr uint32_t OFF_GBI = al(OFF_GB + GB_BYTES);
+  static constexpr uint32_t OFF_GAI = al(OFF_GBI + GB_BYTES);
+  static constexpr uint32_t OFF_TW = al(OFF_GAI + GAI_BYTES);   // [n1][k2/2] {wr,wr',wi,wi'}
+  static constexpr uint32_t OFF_TWT = al(OFF_TW + TW_BYTES);    // [k2][n1/2] {wr,wr',wi,wi'}
+  static constexpr uint32_t TABLES = al(OFF_TWT + TWT_BYTES);
+  // per-warpgroup working buffers
+  static constexpr uint32_t KF_BYTES = L2 * (L1 / 2 * 16 + 16); // [k2][k1/2] {kr,kr',ki,ki'}, padded rows
+  static constexpr uint32_t BUFX_BYTES = P * L * 4;            // complex fp16 per tile (stage A operand aliases it)
+  static constexpr uint32_t WG_BYTES = al(KF_BYTES) + al(BUFX_BYTES);
+  static constexpr uint32_t OFF_WG = TABLES;
+  // two independent tile pipelines when both fit in shared memory, else one
+  static constexpr int WG = (OFF_WG + 2 * WG_BYTES + 1024 <= 227 * 1024) ? 2 : 1;
+  static constexpr int THREADS = WG * kWGThreads;
+  static constexpr uint32_t SMEM = OFF_WG + WG * WG_BYTES + 1024;  // + alignment slack
+  // operand strides
+  static constexpr uint32_t SBO_A = (2 * KA / 8) * 128;   // stage A operand: MN-group stride (K groups contiguous)
+  static constexpr uint32_t LBO_B = (P * L2 / 8) * 128;   // epi1 -> stage B (MN-major, K-group stride)
+  static constexpr uint32_t SBO_BP = (2 * L1 / 8) * 128;  // epi2 -> stage B^-1 (K-major, row-group stride)
+  static constexpr uint32_t SBO_GB = (2 * L1 / 8) * 128;  // G_B / G_B^-1 row-group stride
+  static constexpr uint32_t SBO_GA = (2 * KA / 8) * 128;
+  static constexpr uint32_t SBO_GAI = (2 * L2 / 8) * 128;
+  static constexpr uint32_t SBO_XA = (2 * L2 / 8) * 128;  // epi3 -> stage A^-1 (MN-major B, N-group stride)
+  static constexpr uint32_t TMEM_COLS = 256;              // per warpgroup
+  static_assert(P * L1 == 128, "stage A covers one 128-row MMA group");
+  static_assert(P % 4 == 0, "stage B halves hold whole groups of two pairs");
+  static_assert((P / 2) * NB <= 256 && NA <= 256, "TMEM budget");
+  static_assert(128 * 2 * KA * 2 <= BUFX_BYTES, "stage A operand fits in bufX");
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
+
+FC_DEVICE void st_half8(uint32_t addr, const float* v) {
+  st_shared_v4(addr, pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
+               pack_half2(v[6], v[7]));
+}
+
+// x <- x * w for 8 consecutive elements held as planes (xr, xi, -xi);
+// w given as 4 float4 {wr_j, wr_j+1, wi_j, wi_j+1}.
+FC_DEVICE void cmul8(float* xr, float* xi, const float* nxi, const float4* w) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 r = make_float2(xr[2 * j], xr[2 * j + 1]);
+    const float2 i = make_float2(xi[2 * j], xi[2 * j + 1]);
+    const float2 ni = make_float2(nxi[2 * j], nxi[2 * j + 1]);
+    const float2 wr = make_float2(w[j].x, w[j].y), wi = make_float2(w[j].z, w[j].w);
+    const float2 orr = fma2(r, wr, mul2(ni, wi));
+    const float2 oi = fma2(i, wr, mul2(r, wi));
+    xr[2 * j] = orr.x; xr[2 * j + 1] = orr.y;
+    xi[2 * j] = oi.x;  xi[2 * j + 1] = oi.y;
+  }
+}
+// x <- x * conj(w); planes (xr, xi, -xr).
+FC_DEVICE void cmulc8(float* xr, float* xi, const float* nxr, const float4* w) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 r = make_float2(xr[2 * j], xr[2 * j + 1]);
+    const float2 i = make_float2(xi[2 * j], xi[2 * j + 1]);
+    const float2 nr = make_float2(nxr[2 * j], nxr[2 * j + 1]);
+    const float2 wr = make_float2(w[j].x, w[j].y), wi = make_float2(w[j].z, w[j].w);
+    const float2 orr = fma2(r, wr, mul2(i, wi));
+    const float2 oi = fma2(i, wr, mul2(nr, wi));
+    xr[2 * j] = orr.x; xr[2 * j + 1] = orr.y;
+    xi[2 * j] = oi.x;  xi[2 * j + 1] = oi.y;
+  }
+}
+
+}  // namespace fc

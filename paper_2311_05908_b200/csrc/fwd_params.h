@@ -39,12 +39,50 @@ struct MpParams {
   void* y;
   void* ws;             // T: fp16 rows (2 * pairs, H * L0, Lp)
   const float2* wbase;  // W_L^{n'}, n' < Lp
+  const void* v2;       // pass 3 only: optional second gate (y2 = x * v2)
+  void* y2;
   int64_t B, H, N;
   int32_t L0, Lp;
   int32_t gated;
   int32_t dtype;
 };
 cudaError_t launch_mp_pass(const MpParams& prm, int pass, cudaStream_t s);
+
+// backward (kernels_bwd.cu)
+struct BwdParams {
+  const void* u;   // g source (or T_g rows)
+  const void* w;   // gate of u (gated)
+  const void* v;   // gate of dy (gated)
+  const void* dy;  // dc source (or T_dc rows)
+  void* du;        // dg * w (gated), dg (plain / inner)
+  void* dw;        // dg * u (gated)
+  void* dv;        // dy * c (gated), c (inner)
+  const void* kf;
+  const void* tables;
+  void* acc;       // per-tile partial spectra [tile][L] complex fp32
+  int64_t B, H, N;
+  int32_t L1;
+  int32_t causal;
+  int32_t gate_io;
+  int32_t need_c;
+  int32_t dtype;
+  int32_t num_sms;
+};
+cudaError_t launch_bwd_fused(const BwdParams& prm, cudaStream_t s);
+int64_t bwd_tiles_per_head(int64_t B, int L1);
+
+// dk = Re IFFT(mask * sum of partial spectra)[:K] (kernels_kf.cu)
+struct DkParams {
+  const float2* part;   // [H * L0][nbt][Lp] partial spectra
+  float2* scratch;      // multipass: H * L0 * Lp complex fp32 (may alias part)
+  float* dk;            // (H, K)
+  const float* mask;    // length L or nullptr
+  const float2* twiddle;  // W_Lp^e, e < Lp
+  const float2* wbase;    // multipass: W_L^{n'}, n' < Lp
+  int64_t H, K, nbt;
+  int32_t L0, Lp;
+};
+cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s);
 cudaError_t launch_mp_precompute_kf(const KfParams& prm, const float2* wbase, int L0, int Lp, size_t block_bytes,
                                     cudaStream_t s);
 }  // namespace fc

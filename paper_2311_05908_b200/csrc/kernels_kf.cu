@@ -190,6 +190,113 @@ cudaError_t launch_mp_kf_rows(const KfParams& prm, int L0, int Lp, size_t block_
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- dk
+// Fused regime: one CTA per head sums the head's per-tile partial spectra in
+// tile order (deterministic), applies the mask, and takes
+// dk[t] = Re sum_f acc[f] W_L^{-f t} = Re FFT(conj(acc))[t].
+// Multipass regime, step 1: the same per (head, k0) over the inner length Lp,
+// leaving a[k0][n'] = sum_f' acc[k0 + L0 f'] W_Lp^{-n' f'} (complex) in scratch.
+__global__ void __launch_bounds__(256) dk_rows_kernel(const DkParams prm) {
+  extern __shared__ float2 sm[];
+  const int L = prm.Lp;
+  float2* bufs[2] = {sm, sm + L};
+  float2* tws = sm + 2 * L;
+  const int64_t row = blockIdx.x;  // h * L0 + k0
+  const int k0 = int(row % prm.L0);
+  {
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.twiddle);
+    const uint32_t dst = smem_u32(tws);
+    for (int o = threadIdx.x * 16; o < L * 8; o += blockDim.x * 16) cp_async16(dst + o, src + o, true);
+    cp_async_commit();
+  }
+  const float2* part = prm.part + row * prm.nbt * L;
+  for (int f = threadIdx.x; f < L; f += blockDim.x) {
+    float2 a = make_float2(0.f, 0.f);
+    for (int64_t j = 0; j < prm.nbt; ++j) {
+      const float2 v = part[j * L + f];
+      a.x += v.x;
+      a.y += v.y;
+    }
+    if (prm.mask) {
+      const float mk = prm.mask[k0 + int64_t(prm.L0) * f];
+      a.x *= mk;
+      a.y *= mk;
+    }
+    sm[f] = make_float2(a.x, -a.y);  // conj: inverse transform via the forward one
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  int cur = 0, Ns = 1;
+  const int lg = __ffs(L) - 1;
+  const int rem = lg % 3;
+  if (rem) {
+    if (rem == 1) stockham_pass<2>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
+    else stockham_pass<4>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
+    Ns <<= rem;
+    cur ^= 1;
+    __syncthreads();
+  }
+  for (; Ns < L; Ns <<= 3) {
+    stockham_pass<8>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
+    cur ^= 1;
+    __syncthreads();
+  }
+  const float2* xs = bufs[cur];
+  if (prm.L0 == 1) {
+    float* dk = prm.dk + row * prm.K;
+    for (int t = threadIdx.x; t < prm.K; t += blockDim.x) dk[t] = xs[t].x;
+  } else {
+    float2* a = prm.scratch + row * L;
+    for (int t = threadIdx.x; t < L; t += blockDim.x) a[t] = make_float2(xs[t].x, -xs[t].y);  // undo conj
+  }
+}
+
+// Multipass regime, step 2: per (head, n'):
+// dk[n' + Lp n0] = Re sum_k0 W_L^{-n' k0} W_L0^{-n0 k0} a[k0][n'].
+__global__ void __launch_bounds__(256) dk_cols_kernel(const DkParams prm) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= prm.H * prm.Lp) return;
+  const int n = int(idx % prm.Lp);
+  const int64_t h = idx / prm.Lp;
+  const int L0 = prm.L0;
+  const float2 bw = prm.wbase[n];
+  float2 tw = make_float2(1.f, 0.f);
+  float2 x[16];
+  for (int k0 = 0; k0 < L0; ++k0) {
+    const float2 a = prm.scratch[(h * L0 + k0) * prm.Lp + n];
+    x[k0] = make_float2(a.x * tw.x + a.y * tw.y, a.y * tw.x - a.x * tw.y);  // a * conj(tw)
+    const float2 t2 = make_float2(tw.x * bw.x - tw.y * bw.y, tw.x * bw.y + tw.y * bw.x);
+    tw = t2;
+  }
+  for (int n0 = 0; n0 < L0; ++n0) {
+    const int64_t t = int64_t(n) + int64_t(n0) * prm.Lp;
+    if (t >= prm.K) break;
+    float s = 0.f;
+    for (int k0 = 0; k0 < L0; ++k0) {
+      float sn, cs;
+      sincospif(2.0f * float((n0 * k0) % L0) / float(L0), &sn, &cs);  // W_L0^{-n0 k0}
+      s += x[k0].x * cs - x[k0].y * sn;
+    }
+    prm.dk[h * prm.K + t] = s;
+  }
+}
+
+cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
+  if (prm.H <= 0) return cudaSuccess;
+  const size_t smem = size_t(prm.Lp) * sizeof(float2) * 3;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(dk_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  dk_rows_kernel<<<unsigned(prm.H * prm.L0), 256, smem, s>>>(prm);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || prm.L0 == 1) return e;
+  dk_cols_kernel<<<unsigned((prm.H * prm.Lp + 255) / 256), 256, 0, s>>>(prm);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s) {
   if (prm.H <= 0) return cudaSuccess;
   const size_t smem = size_t(prm.L) * sizeof(float2) * 3;

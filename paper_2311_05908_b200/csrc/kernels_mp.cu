@@ -148,6 +148,16 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
         c0 *= vc.x; c1 *= vc.y;
       }
     }
+    if (prm.y2) {  // second gated output (backward: dw = dg * u)
+      const T* v2 = reinterpret_cast<const T*>(prm.v2);
+      T* y2 = reinterpret_cast<T*>(prm.y2);
+      const float2 vb = ld2<T>(v2 + r0 + o);
+      st2<T>(y2 + r0 + o, x0[n0].x * s * vb.x, x1[n0].x * s * vb.y);
+      if (has1) {
+        const float2 vd = ld2<T>(v2 + r1 + o);
+        st2<T>(y2 + r1 + o, x0[n0].y * s * vd.x, x1[n0].y * s * vd.y);
+      }
+    }
     st2<T>(y + r0 + o, a0, a1);
     if (has1) st2<T>(y + r1 + o, c0, c1);
   }

@@ -140,13 +140,14 @@ class FFTConvPlan:
         return y
 
     def bwd(self, dy, u, kf, K, w=None, v=None):
+        """Gradients of <y, dy>: returns du, dw, dv (None when ungated) and dk (H, K)."""
         self._check_sig(dy, u)
         B, H, _ = u.shape
         du = torch.empty_like(u)
         dw = torch.empty_like(u) if w is not None else None
         dv = torch.empty_like(u) if v is not None else None
         dk = torch.empty(H, K, dtype=torch.float32, device=u.device)
-        ws = torch.empty(max(H, 1) * self.info.workspace_bytes_per_head, dtype=torch.uint8, device=u.device)
+        ws = self.workspace(B, H, for_bwd=True, device=u.device)
         _abi.check(_abi.lib().fftconv_bwd(self._h, _ptr(dy), _ptr(u), _ptr(w), _ptr(v), _ptr(kf), _ptr(du),
                                           _ptr(dw), _ptr(dv), _ptr(dk), B, H, K, _ptr(ws), _stream(u.device)))
         return {"du": du, "dw": dw, "dv": dv, "dk": dk}

@@ -1,0 +1,56 @@
+"""GPU parity of the backward pass (fused and multipass regimes) against the
+fp64 oracle's gradients (A15): du, dw, dv per element and dk (batch sum)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import oracle as orc
+
+torch = pytest.importorskip("torch")
+
+REL_L2 = 2e-3
+TDT = {"f16": torch.float16, "bf16": torch.bfloat16}
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _run(N, dtype, gated, B, H, seed=0):
+    from paper_2311_05908_b200 import FFTConvPlan
+    plan = FFTConvPlan(N, dtype=TDT[dtype], causal=True)
+    K = N
+    q = lambda name: synth.quantize(synth.signal(seed, name, B, H, N), dtype)
+    u, dy = q("u"), q("dy")
+    w = q("w") if gated else None
+    v = q("v") if gated else None
+    k = synth.decay_filters(seed, H, K).astype(np.float32)
+    t = lambda a: torch.tensor(a, dtype=TDT[dtype], device="cuda") if a is not None else None
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    g = plan.bwd(t(dy), t(u), kf, K, w=t(w), v=t(v))
+    torch.cuda.synchronize()
+    ref = orc.conv_bwd(dy, u, k.astype(np.float64), w=w, v=v)
+    out = {key: (g[key].float().cpu().numpy().astype(np.float64) if g[key] is not None else None) for key in g}
+    return out, ref
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [256, 1024, 2048, 8192])
+@pytest.mark.parametrize("dtype,gated", [("f16", False), ("f16", True), ("bf16", True)])
+def test_bwd_parity(N, dtype, gated):
+    got, ref = _run(N, dtype, gated, B=5, H=3)
+    for key in ("du", "dw", "dv", "dk"):
+        if ref[key] is None:
+            assert got[key] is None
+            continue
+        assert np.all(np.isfinite(got[key])), key
+        assert _rel(got[key], ref[key]) < REL_L2, (key, _rel(got[key], ref[key]))
+
+
+@pytest.mark.gpu
+def test_bwd_deterministic():
+    a, _ = _run(1024, "f16", True, B=9, H=2, seed=3)
+    b, _ = _run(1024, "f16", True, B=9, H=2, seed=3)
+    for key in a:
+        if a[key] is not None:
+            assert np.array_equal(a[key], b[key]), key
