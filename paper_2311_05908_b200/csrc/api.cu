@@ -88,7 +88,7 @@ extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float*
   prm.L1 = p->L1;
   prm.L2 = p->L2;
   cudaError_t e;
-  if (p->regime == REGIME_MULTIPASS) {
+  if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
     const size_t block = size_t(p->L2) * tab_stride(uint32_t(p->L1 / 2));
     prm.L = p->Lp;
     e = launch_mp_precompute_kf(prm, reinterpret_cast<const float2*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.wbase),
@@ -110,7 +110,7 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
   if (gated && !v) { set_last_error(std::string(fn) + ": v is NULL"); return FFTCONV_ERR_INVALID_ARG; }
   if (B * H == 0) return FFTCONV_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (p->regime == REGIME_MULTIPASS) {
+  if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
     if (!ws) { set_last_error(std::string(fn) + ": multipass regime needs a workspace"); return FFTCONV_ERR_INVALID_ARG; }
     if (!aligned16(ws)) { set_last_error(std::string(fn) + ": workspace not 16-byte aligned"); return FFTCONV_ERR_MISALIGNED; }
     MpParams mp{};
@@ -119,12 +119,18 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     mp.B = B; mp.H = H; mp.N = p->N; mp.L0 = p->L0; mp.Lp = p->Lp;
     mp.gated = gated ? 1 : 0;
     mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
+    if (p->regime == REGIME_PARTIAL) {  // overlap-save windows as virtual rows
+      mp.partial = 1;
+      mp.C = p->L / 2;
+      mp.NC = p->N / mp.C;
+      mp.B = B * mp.NC;
+    }
     cudaError_t e = launch_mp_pass(mp, 1, st);
     if (e != cudaSuccess) return cuda_fail(fn, e);
     // pass 2: the fused circular kernel over the complex rows of T, in place
     FwdParams in{};
     in.u = ws; in.y = ws; in.kf = kf; in.tables = p->d_tables;
-    in.B = 2 * ((B + 1) / 2); in.H = H * p->L0; in.N = p->Lp;
+    in.B = 2 * ((mp.B + 1) / 2); in.H = H * p->L0; in.N = p->Lp;
     in.L1 = p->L1; in.causal = 0; in.gated = 0; in.dtype = 0;
     in.num_sms = num_sms_current();
     e = launch_fwd_fused(in, st);
@@ -288,6 +294,10 @@ extern "C" fftconv_status_t fftconv_workspace_size(fftconv_plan_t p, int64_t B, 
   size_t n = 0;
   if (for_bwd) n = bwd_ws_bytes(p, B, H);
   else if (p->regime == REGIME_MULTIPASS) n = size_t(2 * ((B + 1) / 2)) * size_t(H) * size_t(p->L) * 2;
+  else if (p->regime == REGIME_PARTIAL) {
+    const int64_t Bv = B * (p->N / (p->L / 2));
+    n = size_t(2 * ((Bv + 1) / 2)) * size_t(H) * size_t(p->L) * 2;
+  }
   *bytes = n;
   return FFTCONV_OK;
 }

@@ -45,6 +45,11 @@ struct MpParams {
   int32_t L0, Lp;
   int32_t gated;
   int32_t dtype;
+  // partial (overlap-save) mode: virtual row b_v = b * NC + j is the window
+  // u[b, h, (j-1) C : (j+1) C] (zero before 0); its output is the second half
+  // of the circular result, y[b, h, j C : (j+1) C].  B above is then B * NC.
+  int32_t partial;
+  int64_t NC, C;
 };
 cudaError_t launch_mp_pass(const MpParams& prm, int pass, cudaStream_t s);
 

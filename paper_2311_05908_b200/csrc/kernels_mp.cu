@@ -16,6 +16,8 @@
 // tensor-core work is in pass 2.  T is written in place by pass 2.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "dft_small.cuh"
 #include "fwd_params.h"
 #include "sm100.cuh"
@@ -60,21 +62,36 @@ __global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
   const bool has1 = b1 < prm.B;
   const T* __restrict__ u = reinterpret_cast<const T*>(prm.u);
   const T* __restrict__ w = reinterpret_cast<const T*>(prm.w);
-  const int64_t r0 = (b0 * prm.H + h) * prm.N + n, r1 = (b1 * prm.H + h) * prm.N + n;
+  // element offset of sample n0 = 0 of each row; window start (may be < 0)
+  int64_t r0, r1, s0 = 0, s1 = 0;
+  if (prm.partial) {
+    const int64_t j0 = b0 % prm.NC, j1 = b1 % prm.NC;
+    s0 = (j0 - 1) * prm.C;
+    s1 = (j1 - 1) * prm.C;
+    r0 = ((b0 / prm.NC) * prm.H + h) * prm.N + s0 + n;
+    r1 = ((b1 / prm.NC) * prm.H + h) * prm.N + s1 + n;
+  } else {
+    r0 = (b0 * prm.H + h) * prm.N + n;
+    r1 = (b1 * prm.H + h) * prm.N + n;
+  }
   float2 z0[L0], z1[L0];  // column n and n+1, complex z = g_b + i g_{b+1}
 #pragma unroll
   for (int n0 = 0; n0 < L0; ++n0) {
     z0[n0] = make_float2(0.f, 0.f);
     z1[n0] = make_float2(0.f, 0.f);
   }
+  // causal: the zero-padded upper half is never loaded; partial: full window
+  constexpr int NL = L0;
 #pragma unroll
-  for (int n0 = 0; n0 < L0 / 2; ++n0) {
+  for (int n0 = 0; n0 < NL; ++n0) {
+    if (!prm.partial && n0 >= L0 / 2) break;
     const int64_t o = int64_t(n0) * prm.Lp;
-    float2 a = ld2<T>(u + r0 + o);  // row b, columns n, n+1
-    float2 c = has1 ? ld2<T>(u + r1 + o) : make_float2(0.f, 0.f);
+    const bool ok0 = s0 + o >= 0, ok1 = has1 && s1 + o >= 0;
+    float2 a = ok0 ? ld2<T>(u + r0 + o) : make_float2(0.f, 0.f);  // row b, columns n, n+1
+    float2 c = ok1 ? ld2<T>(u + r1 + o) : make_float2(0.f, 0.f);
     if (GATED) {
-      const float2 wa = ld2<T>(w + r0 + o);
-      const float2 wc = has1 ? ld2<T>(w + r1 + o) : make_float2(0.f, 0.f);
+      const float2 wa = ok0 ? ld2<T>(w + r0 + o) : make_float2(0.f, 0.f);
+      const float2 wc = ok1 ? ld2<T>(w + r1 + o) : make_float2(0.f, 0.f);
       a.x *= wa.x; a.y *= wa.y;
       c.x *= wc.x; c.y *= wc.y;
     }
@@ -134,33 +151,48 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
   const bool has1 = b1 < prm.B;
   T* __restrict__ y = reinterpret_cast<T*>(prm.y);
   const T* __restrict__ v = reinterpret_cast<const T*>(prm.v);
-  const int64_t r0 = (b0 * prm.H + h) * prm.N + n, r1 = (b1 * prm.H + h) * prm.N + n;
-#pragma unroll
-  for (int n0 = 0; n0 < L0 / 2; ++n0) {  // causal: first half of the output only
-    const int64_t o = int64_t(n0) * prm.Lp;
-    float a0 = x0[n0].x * s, a1 = x1[n0].x * s;  // row b
-    float c0 = x0[n0].y * s, c1 = x1[n0].y * s;  // row b+1
-    if (GATED) {
-      const float2 va = ld2<T>(v + r0 + o);
-      a0 *= va.x; a1 *= va.y;
-      if (has1) {
-        const float2 vc = ld2<T>(v + r1 + o);
-        c0 *= vc.x; c1 *= vc.y;
-      }
-    }
-    if (prm.y2) {  // second gated output (backward: dw = dg * u)
-      const T* v2 = reinterpret_cast<const T*>(prm.v2);
-      T* y2 = reinterpret_cast<T*>(prm.y2);
-      const float2 vb = ld2<T>(v2 + r0 + o);
-      st2<T>(y2 + r0 + o, x0[n0].x * s * vb.x, x1[n0].x * s * vb.y);
-      if (has1) {
-        const float2 vd = ld2<T>(v2 + r1 + o);
-        st2<T>(y2 + r1 + o, x0[n0].y * s * vd.x, x1[n0].y * s * vd.y);
-      }
-    }
-    st2<T>(y + r0 + o, a0, a1);
-    if (has1) st2<T>(y + r1 + o, c0, c1);
+  int64_t r0, r1;
+  int q0 = 0;  // first output block: causal keeps n0 < L0/2, partial keeps n0 >= L0/2
+  if (prm.partial) {
+    r0 = ((b0 / prm.NC) * prm.H + h) * prm.N + (b0 % prm.NC) * prm.C + n;
+    r1 = ((b1 / prm.NC) * prm.H + h) * prm.N + (b1 % prm.NC) * prm.C + n;
+    q0 = L0 / 2;
+  } else {
+    r0 = (b0 * prm.H + h) * prm.N + n;
+    r1 = (b1 * prm.H + h) * prm.N + n;
   }
+  auto emit = [&](auto q0c) {
+    constexpr int Q0 = decltype(q0c)::value;
+  #pragma unroll
+      for (int i0 = 0; i0 < L0 / 2; ++i0) {
+        const int n0 = i0 + Q0;
+      const int64_t o = int64_t(i0) * prm.Lp;
+      float a0 = x0[n0].x * s, a1 = x1[n0].x * s;  // row b
+      float c0 = x0[n0].y * s, c1 = x1[n0].y * s;  // row b+1
+      if (GATED) {
+        const float2 va = ld2<T>(v + r0 + o);
+        a0 *= va.x; a1 *= va.y;
+        if (has1) {
+          const float2 vc = ld2<T>(v + r1 + o);
+          c0 *= vc.x; c1 *= vc.y;
+        }
+      }
+      if (prm.y2) {  // second gated output (backward: dw = dg * u)
+        const T* v2 = reinterpret_cast<const T*>(prm.v2);
+        T* y2 = reinterpret_cast<T*>(prm.y2);
+        const float2 vb = ld2<T>(v2 + r0 + o);
+        st2<T>(y2 + r0 + o, x0[n0].x * s * vb.x, x1[n0].x * s * vb.y);
+        if (has1) {
+          const float2 vd = ld2<T>(v2 + r1 + o);
+          st2<T>(y2 + r1 + o, x0[n0].y * s * vd.x, x1[n0].y * s * vd.y);
+        }
+      }
+      st2<T>(y + r0 + o, a0, a1);
+      if (has1) st2<T>(y + r1 + o, c0, c1);
+    }
+  };
+  if (q0) emit(std::integral_constant<int, L0 / 2>{});
+  else emit(std::integral_constant<int, 0>{});
 }
 
 // k_f, step 1: per (head, column n'): DFT_L0 of k[n' + L' n0] (n0 < L0/2,

@@ -321,8 +321,11 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
     p->P = std::max(128 / p->L1, 2);
     build_fused_tables(p, L);
     p->Lp = int32_t(L);
-  } else if (io_ok && p->regime == REGIME_FUSED && causal && fft_size == 2 * N && L >= 4096 && L <= 32768) {
-    p->regime = REGIME_MULTIPASS;
+  } else if (io_ok && causal && L >= 4096 && L <= 32768 &&
+             (fft_size == 2 * N || (p->regime == REGIME_PARTIAL && N % (L / 2) == 0))) {
+    // multipass; the partial regime (K <= L/2 < N) runs the same passes on
+    // overlap-save windows of length L (A12)
+    if (p->regime != REGIME_PARTIAL) p->regime = REGIME_MULTIPASS;
     p->order = 3;
     p->Lp = 2048;
     p->L0 = int32_t(L / 2048);
@@ -334,7 +337,8 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
   } else {
     delete p;
     set_last_error("fftconv_plan: this build supports fp16/bf16 I/O with fft_size 512..2048 (fused; causal "
-                   "fft_size == 2N or circular) and causal fft_size 4096..32768 == 2N (multipass)");
+                   "fft_size == 2N or circular), causal fft_size 4096..32768 == 2N (multipass) and partial "
+                   "convolutions with fft_size 4096..32768 < 2N dividing 2N (overlap-save)");
     return FFTCONV_ERR_UNSUPPORTED;
   }
   if (sparsity) {
@@ -366,7 +370,7 @@ extern "C" fftconv_status_t fftconv_plan_info(fftconv_plan_t p, fftconv_plan_inf
   info->dtype = p->dtype;
   info->regime = p->regime;
   info->order = p->order;
-  if (p->regime == REGIME_MULTIPASS) {
+  if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
     info->factors[0] = p->L0;
     info->factors[1] = p->L1;
     info->factors[2] = p->L2;

@@ -1,0 +1,54 @@
+"""GPU parity of the partial convolution (filter truncated to K < N,
+P:300-303, A12) computed as overlap-save windows of length fft_size = 2C,
+C >= K, against the fp64 oracle (causal conv with the truncated filter)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import oracle as orc
+
+torch = pytest.importorskip("torch")
+REL_L2 = 2e-3
+TDT = {"f16": torch.float16, "bf16": torch.bfloat16}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,L,K", [(16384, 4096, 2048), (16384, 4096, 700), (32768, 16384, 8192)])
+@pytest.mark.parametrize("dtype,gated", [("f16", False), ("bf16", True)])
+def test_partial_parity(N, L, K, dtype, gated):
+    from paper_2311_05908_b200 import FFTConvPlan
+    B, H = 2, 3
+    plan = FFTConvPlan(N, fft_size=L, dtype=TDT[dtype], causal=True)
+    assert plan.info.regime == 2
+    q = lambda name: synth.quantize(synth.signal(11, name, B, H, N), dtype)
+    u = q("u")
+    w, v = (q("w"), q("v")) if gated else (None, None)
+    k = synth.decay_filters(11, H, K).astype(np.float32)
+    t = lambda a: torch.tensor(a, dtype=TDT[dtype], device="cuda")
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    y = plan.gated_fwd(t(u), t(w), t(v), kf) if gated else plan.fwd(t(u), kf)
+    got = y.float().cpu().numpy().astype(np.float64)
+    ref = orc.conv_fwd(u, k.astype(np.float64), causal=True, w=w, v=v)
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert rel < REL_L2, rel
+
+
+@pytest.mark.gpu
+def test_partial_cfg4_shape_sampled():
+    """cfg 4: HyenaDNA partial conv B=1, H=256, N=2^20, K=8192 (fft 16384),
+    fp16, DNA-like piecewise-constant input; sampled outputs vs direct sums."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    B, H, N, K, L = 1, 256, 1 << 20, 8192, 16384
+    plan = FFTConvPlan(N, fft_size=L, dtype=torch.float16, causal=True)
+    u = synth.quantize(synth.dna_like(4, B, H, N), "f16")
+    k = synth.decay_filters(4, H, K).astype(np.float32)
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    y = plan.fwd(torch.tensor(u, dtype=torch.float16, device="cuda"), kf).float().cpu().numpy()
+    rng = np.random.default_rng(4)
+    got, ref = [], []
+    for h in rng.choice(H, 12, replace=False):
+        for i in list(rng.choice(N, 6, replace=False)) + [0, K - 1, K, N - 1]:
+            ref.append(orc.direct_point(u[0, h], k[h].astype(np.float64), int(i)))
+            got.append(y[0, h, i])
+    got, ref = np.array(got), np.array(ref)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < REL_L2
