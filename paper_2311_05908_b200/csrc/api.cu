@@ -119,6 +119,8 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     mp.B = B; mp.H = H; mp.N = p->N; mp.L0 = p->L0; mp.Lp = p->Lp;
     mp.gated = gated ? 1 : 0;
     mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
+    const bool skip = p->sparse && p->row_map.size() < size_t(p->L0);
+    if (skip) mp.row_keep = static_cast<const uint8_t*>(p->d_tables) + p->row_keep_off;
     if (p->regime == REGIME_PARTIAL) {  // overlap-save windows as virtual rows
       mp.partial = 1;
       mp.C = p->L / 2;
@@ -133,6 +135,11 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     in.B = 2 * ((mp.B + 1) / 2); in.H = H * p->L0; in.N = p->Lp;
     in.L1 = p->L1; in.causal = 0; in.gated = 0; in.dtype = 0;
     in.num_sms = num_sms_current();
+    if (skip) {  // frequency-sparse: only rows k0 with a non-zero mask are transformed
+      in.row_map = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(p->d_tables) + p->row_map_off);
+      in.nrow = int32_t(p->row_map.size());
+      in.row_L0 = p->L0;
+    }
     e = launch_fwd_fused(in, st);
     if (e != cudaSuccess) return cuda_fail(fn, e);
     e = launch_mp_pass(mp, 3, st);

@@ -18,6 +18,10 @@ struct FwdParams {
   int32_t gated;
   int32_t dtype;  // 0 fp16, 1 bf16
   int32_t num_sms;
+  // sparse multipass: iterate over Hi = (H / row_L0) * nrow heads only; head
+  // hh maps to tensor head (hh / nrow) * row_L0 + row_map[hh % nrow]
+  const int32_t* row_map;
+  int32_t nrow, row_L0;
 };
 cudaError_t launch_fwd_fused(const FwdParams& prm, cudaStream_t s);
 
@@ -50,6 +54,7 @@ struct MpParams {
   // of the circular result, y[b, h, j C : (j+1) C].  B above is then B * NC.
   int32_t partial;
   int64_t NC, C;
+  const uint8_t* row_keep;  // sparse: L0 flags, rows with 0 are never written/read
 };
 cudaError_t launch_mp_pass(const MpParams& prm, int pass, cudaStream_t s);
 

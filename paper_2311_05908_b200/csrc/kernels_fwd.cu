@@ -69,7 +69,11 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
   const uint32_t bufX = sKF + C::al(C::KF_BYTES);
   const int64_t B = prm.B, H = prm.H, N = prm.N;
   const int64_t nbt = (B + C::R - 1) / C::R;
-  const int64_t tiles = H * nbt;
+  const int64_t Hi = prm.row_map ? (H / prm.row_L0) * prm.nrow : H;  // heads iterated
+  auto phys_head = [&](int64_t hh) -> int64_t {
+    return prm.row_map ? (hh / prm.nrow) * prm.row_L0 + prm.row_map[hh % prm.nrow] : hh;
+  };
+  const int64_t tiles = Hi * nbt;
   const int64_t t0 = tiles * blockIdx.x / gridDim.x, t1 = tiles * (blockIdx.x + 1) / gridDim.x;
   if (t0 >= t1) return;
 
@@ -198,9 +202,10 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
   const int64_t pf_off0 = int64_t(pf_r0) * HN + int64_t(pf_n2 * JC + pf_j) * 8;
   bool prefetched = false;
 
-  int64_t h = (t0 + wg) / nbt, bt = (t0 + wg) % nbt;
+  int64_t hh = (t0 + wg) / nbt, bt = (t0 + wg) % nbt;
   for (int64_t t = t0 + wg; t < t1; t += kWG, bt += kWG) {
-    while (bt >= nbt) { bt -= nbt; ++h; }
+    while (bt >= nbt) { bt -= nbt; ++hh; }
+    const int64_t h = phys_head(hh);
     const int64_t tile_base = (bt * C::R * H + h) * N;  // element offset of row (bt*R, h)
     const int rows_left = int(B - bt * C::R < C::R ? B - bt * C::R : C::R);
     const bool new_h = h != cur_h;
@@ -393,8 +398,9 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
       const bool has_next = t + kWG < t1;
       if (idle4) {  // warp-uniform: prefetch the next tile's input into TMEM
         if (has_next) {
-          int64_t h2 = h, bt2 = bt + kWG;
-          while (bt2 >= nbt) { bt2 -= nbt; ++h2; }
+          int64_t hh2 = hh, bt2 = bt + kWG;
+          while (bt2 >= nbt) { bt2 -= nbt; ++hh2; }
+          const int64_t h2 = phys_head(hh2);
           const int64_t base2 = (bt2 * C::R * H + h2) * N;
           const int left2 = int(B - bt2 * C::R < C::R ? B - bt2 * C::R : C::R);
           uint4 uv[PF_CH], wv[PF_CH];
@@ -477,7 +483,7 @@ static cudaError_t launch_o2(const FwdParams& prm, cudaStream_t stream) {
     attr_set = true;
   }
   const int64_t nbt = (prm.B + C::R - 1) / C::R;
-  const int64_t tiles = prm.H * nbt;
+  const int64_t tiles = (prm.row_map ? (prm.H / prm.row_L0) * prm.nrow : prm.H) * nbt;
   int grid = int(tiles < prm.num_sms ? tiles : prm.num_sms);
   if (grid < 1) return cudaSuccess;
   kern<<<grid, C::THREADS, C::SMEM, stream>>>(prm);

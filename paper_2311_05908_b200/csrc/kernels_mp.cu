@@ -111,8 +111,10 @@ __global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
     const float2 a = c_mul(z0[k0], t0), c = c_mul(z1[k0], t1);
     const int64_t row_re = ((2 * p) * HL0 + h * L0 + k0) * prm.Lp + n;
     const int64_t row_im = ((2 * p + 1) * HL0 + h * L0 + k0) * prm.Lp + n;
-    *reinterpret_cast<__half2*>(Tw + row_re) = __floats2half2_rn(a.x * s, c.x * s);
-    *reinterpret_cast<__half2*>(Tw + row_im) = __floats2half2_rn(a.y * s, c.y * s);
+    if (!prm.row_keep || prm.row_keep[k0]) {  // masked rows are skipped downstream
+      *reinterpret_cast<__half2*>(Tw + row_re) = __floats2half2_rn(a.x * s, c.x * s);
+      *reinterpret_cast<__half2*>(Tw + row_im) = __floats2half2_rn(a.y * s, c.y * s);
+    }
     t0 = c_mul(t0, b0w);
     t1 = c_mul(t1, b1w);
   }
@@ -137,8 +139,9 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
   for (int k0 = 0; k0 < L0; ++k0) {
     const int64_t row_re = ((2 * p) * HL0 + h * L0 + k0) * prm.Lp + n;
     const int64_t row_im = ((2 * p + 1) * HL0 + h * L0 + k0) * prm.Lp + n;
-    const float2 re = __half22float2(*reinterpret_cast<const __half2*>(Tw + row_re));
-    const float2 im = __half22float2(*reinterpret_cast<const __half2*>(Tw + row_im));
+    const bool kept = !prm.row_keep || prm.row_keep[k0];
+    const float2 re = kept ? __half22float2(*reinterpret_cast<const __half2*>(Tw + row_re)) : make_float2(0.f, 0.f);
+    const float2 im = kept ? __half22float2(*reinterpret_cast<const __half2*>(Tw + row_im)) : make_float2(0.f, 0.f);
     x0[k0] = c_mulc(make_float2(re.x, im.x), t0);
     x1[k0] = c_mulc(make_float2(re.y, im.y), t1);
     t0 = c_mul(t0, b0w);

@@ -265,14 +265,21 @@ static fftconv_status_t build_mask(fftconv_plan_s* p, const fftconv_sparsity_t* 
   }
   p->sparse = true;
   p->mask_fraction = double(zeros) / double(L);
-  // fraction of (k1) blocks whose whole column of k2 values is masked
-  int64_t skip = 0;
-  for (int k1 = 0; k1 < p->L1; ++k1) {
-    bool all0 = true;
-    for (int k2 = 0; k2 < p->L2 && all0; ++k2) all0 = p->mask[size_t(k2 + int64_t(p->L2) * k1)] == 0.0f;
-    skip += all0;
+  // Skippable work: in the multipass / partial regimes the inner pass runs
+  // one row per outer frequency k0 (f = k0 + L0 f'); a row whose whole
+  // spectrum is masked contributes nothing and is skipped ("skip one
+  // iteration of the outer loop").  The fused regime skips nothing yet.
+  p->row_map.clear();
+  if (p->L0 > 1) {
+    for (int k0 = 0; k0 < p->L0; ++k0) {
+      bool any = false;
+      for (int64_t fp = 0; fp < p->Lp && !any; ++fp) any = p->mask[size_t(k0 + int64_t(p->L0) * fp)] != 0.0f;
+      if (any) p->row_map.push_back(k0);
+    }
+    p->skip_fraction = 1.0 - double(p->row_map.size()) / double(p->L0);
+  } else {
+    p->skip_fraction = 0.0;
   }
-  p->skip_fraction = double(skip) / double(p->L1);
   return FFTCONV_OK;
 }
 
@@ -348,10 +355,22 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
       set_last_error("fftconv_plan: inconsistent sparsity pattern (prod(dims) must equal fft_size)");
       return s;
     }
-    // the mask rides at the end of the table image (read by precompute_kf)
+    // the mask rides at the end of the table image (read by precompute_kf),
+    // followed by the row keep flags and the list of kept rows
     const size_t mo = p->image.size();
     p->image.resize(mo + p->mask.size() * sizeof(float));
     std::memcpy(p->image.data() + mo, p->mask.data(), p->mask.size() * sizeof(float));
+    if (p->L0 > 1) {
+      p->row_keep_off = p->image.size();
+      std::vector<uint8_t> keep(size_t(p->L0), 0);
+      for (int32_t k0 : p->row_map) keep[size_t(k0)] = 1;
+      p->image.insert(p->image.end(), keep.begin(), keep.end());
+      p->image.resize(align_up(p->image.size(), 16), 0);
+      p->row_map_off = p->image.size();
+      const size_t bytes = p->row_map.size() * sizeof(int32_t);
+      p->image.resize(p->image.size() + align_up(bytes, 16), 0);
+      std::memcpy(p->image.data() + p->row_map_off, p->row_map.data(), bytes);
+    }
   }
   // complex fp32 [k2][k1/2] pairs with padded rows, one block per outer index k0
   p->kf_bytes_per_head = size_t(p->L0) * size_t(p->L2) * tab_stride(uint32_t(p->L1 / 2));

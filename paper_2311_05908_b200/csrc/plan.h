@@ -49,6 +49,8 @@ struct fftconv_plan_s {
   // frequency sparsity (A13)
   bool sparse = false;
   std::vector<float> mask;     // length L, 0/1, Hermitian-symmetric
+  std::vector<int32_t> row_map;  // multipass: kept outer rows k0 (empty = all)
+  size_t row_keep_off = 0, row_map_off = 0;  // image offsets (sparse multipass)
   double mask_fraction = 0.0;
   double skip_fraction = 0.0;
   size_t kf_bytes_per_head = 0;

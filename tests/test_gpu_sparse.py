@@ -1,0 +1,66 @@
+"""GPU parity of frequency-sparse convolutions (k_f masked, P:310-314,
+P:1006-1060; mask semantics A13) against the fp64 oracle with the same mask,
+and checks that masked rows of the multipass inner pass are skipped."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import oracle as orc
+
+torch = pytest.importorskip("torch")
+REL_L2 = 2e-3
+
+
+def _run(N, dims, keeps, B=4, H=3, gated=False, seed=21):
+    from paper_2311_05908_b200 import FFTConvPlan
+    plan = FFTConvPlan(N, dtype=torch.float16, causal=True, sparsity=(dims, keeps))
+    q = lambda name: synth.quantize(synth.signal(seed, name, B, H, N), "f16")
+    u = q("u")
+    w, v = (q("w"), q("v")) if gated else (None, None)
+    k = synth.decay_filters(seed, H, N).astype(np.float32)
+    t = lambda a: torch.tensor(a, dtype=torch.float16, device="cuda")
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    y = plan.gated_fwd(t(u), t(w), t(v), kf) if gated else plan.fwd(t(u), kf)
+    m = orc.frequency_mask(dims, keeps)
+    ref = orc.conv_fwd(u, k.astype(np.float64), w=w, v=v, mask=m)
+    got = y.float().cpu().numpy().astype(np.float64)
+    return plan, got, ref, m
+
+
+@pytest.mark.gpu
+def test_sparse_rows_skipped_cfg5_pattern():
+    """cfg 5 shape of the mask: N=16384 (fft 32768 = 16 outer rows x 2048);
+    keeping outer rows {0, 1, 8, 15} (closed under f -> L - f) skips 75% of the
+    inner Monarch rows."""
+    N = 16384
+    keep_k0 = np.zeros(16, bool)
+    keep_k0[[0, 1, 8, 15]] = True
+    dims, keeps = [2048, 16], [np.ones(2048, bool), keep_k0]
+    plan, got, ref, m = _run(N, dims, keeps)
+    assert abs(plan.info.skip_fraction - 0.75) < 1e-12
+    assert abs(plan.info.mask_fraction - 0.75) < 1e-12
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert rel < REL_L2, rel
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,dims,zeroed", [
+    (16384, [8, 8, 8, 64], [4, 4, 0, 0]),      # tab:sparsity_fraction-style trailing zeros
+    (4096, [32, 256], [16, 0]),                # low-pass half of the slow digit
+    (1024, [32, 64], [16, 32]),                # fused regime (no skipping, mask only)
+])
+@pytest.mark.parametrize("gated", [False, True])
+def test_sparse_patterns(N, dims, zeroed, gated):
+    keeps = orc.keep_masks_from_zero_counts(dims, zeroed)
+    plan, got, ref, m = _run(N, dims, keeps, gated=gated)
+    assert abs(plan.info.mask_fraction - (1 - m.mean())) < 1e-12
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert rel < REL_L2, rel
+
+
+@pytest.mark.gpu
+def test_sparse_all_masked_is_zero():
+    N = 8192
+    dims, keeps = [16384], [np.zeros(16384, bool)]
+    plan, got, ref, m = _run(N, dims, keeps, B=2, H=2)
+    assert np.all(got == 0) and np.all(ref == 0)
