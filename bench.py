@@ -3,12 +3,14 @@
 
 One step = one pass of the whole hot path over one batch of synthetic input:
 fftconv_precompute_kf (k -> k_f; filters change every
-training step) + the fused gated causal convolution (a3-a7).
+training step) + the convolution call(s) of the workload (a3-a11).
 
-Workload (BASELINE.json configs[1], the metric's configuration at N=1):
-cfg2 "M2-BERT-base gated conv B=64 H=768 N=1024 fp16", causal (fft_size 2048).
-Multi-GPU (torchrun): every rank processes its own B x H rows (weak scaling,
-rows are independent; no collective on the data path).
+Default workload (BASELINE.json configs[1], the metric's configuration at
+N=1): cfg2 "M2-BERT-base gated conv B=64 H=768 N=1024 fp16", causal
+(fft_size 2048).  Other configs: --workload cfg1|cfg3|cfg4|cfg5|cfg5dense|
+sweep<N>.  Multi-GPU (torchrun): every rank processes its own B x H rows of
+the workload (weak scaling; rows are independent, no collective on the data
+path).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fftconv|reference]
 """
@@ -27,22 +29,42 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+
+def _wl(name, B, H, N, gated=False, dtype="f16", bwd=False, fft=None, K=None, sparse=None):
+    return dict(name=name, B=B, H=H, N=N, gated=gated, causal=True, dtype=dtype, bwd=bwd,
+                fft=fft or 2 * N, K=K or N, sparse=sparse)
+
+
 WORKLOADS = {
-    "cfg2": dict(name="cfg2: M2-BERT-base gated causal conv B=64 H=768 N=1024 fp16 (fft_size 2048)",
-                 B=64, H=768, N=1024, gated=True, causal=True, dtype="f16"),
-    "cfg1": dict(name="cfg1: causal fp16 conv B=1 H=4 N=256 (fft_size 512)",
-                 B=1, H=4, N=256, gated=False, causal=True, dtype="f16"),
-    "sweep256": dict(name="sweep: causal fp16 conv B=64 H=768 N=256", B=64, H=768, N=256, gated=False,
-                     causal=True, dtype="f16"),
-    "sweep512": dict(name="sweep: causal fp16 conv B=64 H=768 N=512", B=64, H=768, N=512, gated=False,
-                     causal=True, dtype="f16"),
-    "sweep1024": dict(name="sweep: causal fp16 conv B=64 H=768 N=1024", B=64, H=768, N=1024, gated=False,
-                      causal=True, dtype="f16"),
+    "cfg1": _wl("cfg1: causal fp16 conv B=1 H=4 N=256 (fft_size 512)", 1, 4, 256),
+    "cfg2": _wl("cfg2: M2-BERT-base gated causal conv B=64 H=768 N=1024 fp16 (fft_size 2048)", 64, 768, 1024,
+                gated=True),
+    "cfg3": _wl("cfg3: Hyena-GPT-s gated causal conv B=16 H=768 N=8192 bf16, fwd+bwd", 16, 768, 8192, gated=True,
+                dtype="bf16", bwd=True),
+    "cfg4": _wl("cfg4: HyenaDNA partial conv B=1 H=256 N=1048576 K=8192 fp16 (fft_size 16384, overlap-save)",
+                1, 256, 1 << 20, fft=16384, K=8192),
+    "cfg5": _wl("cfg5: frequency-sparse causal conv B=8 H=768 N=16384 fp16, 75% of inner Monarch rows skipped",
+                8, 768, 16384, sparse="rows75"),
+    "cfg5dense": _wl("cfg5 dense reference: causal conv B=8 H=768 N=16384 fp16", 8, 768, 16384),
 }
+for _n in (256, 512, 1024, 2048, 4096, 8192, 16384):
+    WORKLOADS[f"sweep{_n}"] = _wl(f"sweep: causal fp16 conv B*H=49152 N={_n}", 64, 768, _n)
+
 METRIC = "fused FFT-conv sequences/s & % HBM/tensor roofline, N=256–4M, at 1/2/4/8 B200"
-# paper's padded (causal) gated H100 row at FFT 2K (input 1K), 0.59 ms for
-# B=64 H=768 -> 8.33e7 seq/s -- another machine: context only.
+# paper's padded (causal) H100 rows for the same workload, another
+# machine: context only.  cfg2 = gated FFT-2K row 0.59 ms.
 PAPER_SEQ_S = {"cfg2": 49152 / 0.59e-3}
+
+
+def sparsity_spec(kind, fft):
+    if kind is None:
+        return None
+    if kind == "rows75":  # keep outer rows {0, 1, L0/2, L0-1} of the multipass layout
+        L0 = fft // 2048
+        keep = np.zeros(L0, bool)
+        keep[[0, 1, L0 // 2, L0 - 1]] = True
+        return ([2048, L0], [np.ones(2048, bool), keep])
+    raise ValueError(kind)
 
 
 def load_peaks():
@@ -105,83 +127,95 @@ class ClockSampler:
                 "reasons": rs, "samples": len(self.samples)}
 
 
-def oracle_rows_per_s(wl, target_s=8.0):
-    """The fp64 oracle as it stands, on a bounded sample of the workload's
-    rows, on this host's cores.  Returns (rows/s, cores, sample text)."""
+# ----------------------------------------------------------------- CPU oracle
+def _oracle_sample(wl, Bs, rows=None):
+    """Run the fp64 oracle on Bs x (rows or H) rows of the workload; seconds."""
     import synth
     from oracle import oracle as orc
+    H, N, K = wl["H"], wl["N"], wl["K"]
+    Hs = H if rows is None else rows
+    k = synth.decay_filters(0, H, K)[:Hs].astype(np.float32).astype(np.float64)
+    rows = np.array([b * H + h for b in range(Bs) for h in range(Hs)])
+    q = lambda name: synth.quantize(synth.normal(0, synth.TENSOR_IDS[name], rows, N).reshape(Bs, Hs, N),
+                                    wl["dtype"])
+    u = q("u")
+    kw = {}
+    if wl["gated"]:
+        kw = dict(w=q("w"), v=q("v"))
+    mask = None
+    if wl["sparse"]:
+        dims, keeps = sparsity_spec(wl["sparse"], wl["fft"])
+        mask = orc.frequency_mask(dims, keeps)
+    t = time.perf_counter()
+    orc.conv_fwd(u, k, causal=True, mask=mask, **kw)
+    if wl["bwd"]:
+        dy = q("dy")
+        orc.conv_bwd(dy, u, k, causal=True, mask=mask, **kw)
+    return time.perf_counter() - t
+
+
+def oracle_rows_per_s(wl, target_s=8.0):
+    """The fp64 oracle as it stands, on a bounded sample of the workload's
+    rows, on this host's cores.  Returns (rows/s, cores, sample text, seconds, Bs, Hs)."""
+    from oracle import oracle as orc
     H, N = wl["H"], wl["N"]
-    k = synth.decay_filters(0, H, N).astype(np.float32).astype(np.float64)
-
-    def run(Bs):
-        u = synth.quantize(synth.signal(0, "u", Bs, H, N), wl["dtype"])
-        kw = {}
-        if wl["gated"]:
-            kw = dict(w=synth.quantize(synth.signal(0, "w", Bs, H, N), wl["dtype"]),
-                      v=synth.quantize(synth.signal(0, "v", Bs, H, N), wl["dtype"]))
-        t = time.perf_counter()
-        orc.conv_fwd(u, k, causal=wl["causal"], **kw)
-        return time.perf_counter() - t
-
-    Bs = 1
-    dt = run(Bs)
+    Hs = H if N <= 16384 else 2  # long rows: a couple of heads only
+    dt = _oracle_sample(wl, 1, Hs)
     Bs = max(1, min(wl["B"], int(target_s / max(dt, 1e-3))))
-    dt = run(Bs)
-    sample = f"{Bs}x{H} rows of N={N} ({'gated ' if wl['gated'] else ''}causal conv + k_f per head), fp64 oracle"
-    return Bs * H / dt, orc.num_threads(), sample, dt
+    if Bs > 1:
+        dt = _oracle_sample(wl, Bs, Hs)
+    what = ("gated " if wl["gated"] else "") + ("fwd+bwd" if wl["bwd"] else "fwd")
+    sample = f"{Bs}x{Hs} rows of N={N} ({what} causal conv + k_f per head), fp64 oracle, {orc.num_threads()} threads"
+    return Bs * Hs / dt, orc.num_threads(), sample, dt, Bs, Hs
 
 
 def run_reference(args, wl, rank, world):
     if rank != 0:
         return
-    import synth  # noqa: F401
-    from oracle import oracle as orc
-    H, N = wl["H"], wl["N"]
-    rate0, cores, sample, dt = oracle_rows_per_s(wl, target_s=min(20.0, 2.0 + 0.5 * args.steps))
-    # each step: a bounded sample (Bs rows x H heads) of the workload
-    Bs = max(1, int(round(rate0 * dt / H)))
-    import synth as sy
-    k = sy.decay_filters(0, H, N).astype(np.float32).astype(np.float64)
-    u = sy.quantize(sy.signal(0, "u", Bs, H, N), wl["dtype"])
-    kw = {}
-    if wl["gated"]:
-        kw = dict(w=sy.quantize(sy.signal(0, "w", Bs, H, N), wl["dtype"]),
-                  v=sy.quantize(sy.signal(0, "v", Bs, H, N), wl["dtype"]))
-    for _ in range(args.warmup):
-        orc.conv_fwd(u[:1], k, causal=wl["causal"], **{a: b[:1] for a, b in kw.items()})
-    ts = []
-    for _ in range(args.steps):
-        t = time.perf_counter()
-        orc.conv_fwd(u, k, causal=wl["causal"], **kw)
-        ts.append(time.perf_counter() - t)
+    rate, cores, sample, dt, Bs, Hs = oracle_rows_per_s(wl, target_s=min(20.0, 2.0 + 0.5 * args.steps))
+    for _ in range(min(args.warmup, 1)):
+        _oracle_sample(wl, 1, Hs)
+    ts = [_oracle_sample(wl, Bs, Hs) for _ in range(args.steps)]
     step = statistics.mean(ts)
-    value = Bs * H / step
+    value = Bs * Hs / step
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "sequences/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["name"] + f" -- bounded sample of {Bs}x{H} rows per step",
-                   "B": Bs, "H": H, "N": N, "fft_size": 2 * N if wl["causal"] else N},
-        "cpu_baseline": {"value": value, "unit": "sequences/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{Bs}x{H} rows of the workload per step, fp64 oracle (oracle/oracle.c)"},
+        "config": {"workload": wl["name"] + f" -- bounded sample of {Bs}x{Hs} rows per step",
+                   "B": Bs, "H": Hs, "N": wl["N"], "fft_size": wl["fft"]},
+        "cpu_baseline": {"value": value, "unit": "sequences/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "sequences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(out), flush=True)
 
 
+# ----------------------------------------------------------------- GPU arm
+def algorithmic_bytes(wl, H_L8):
+    B, H, N = wl["B"], wl["H"], wl["N"]
+    el = B * H * N * 2  # one (B, H, N) tensor of 16-bit I/O
+    fwd = el * (4 if wl["gated"] else 2) + H_L8
+    if not wl["bwd"]:
+        return fwd
+    bwd = el * (7 if wl["gated"] else 3) + H_L8 + H * wl["K"] * 4
+    return fwd + bwd
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="fftconv", choices=["fftconv", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = WORKLOADS[args.workload]
+    if args.steps is None:
+        args.steps = 500 if wl["B"] * wl["H"] * wl["N"] <= (1 << 26) else 40
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -202,44 +236,55 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    B, H, N = wl["B"], wl["H"], wl["N"]
+    B, H, N, K, L = wl["B"], wl["H"], wl["N"], wl["K"], wl["fft"]
     tdt = {"f16": torch.float16, "bf16": torch.bfloat16}[wl["dtype"]]
-    plan = FFTConvPlan(N, dtype=tdt, causal=wl["causal"], device=dev)
+    plan = FFTConvPlan(N, fft_size=L, dtype=tdt, causal=True, device=dev,
+                       sparsity=sparsity_spec(wl["sparse"], L))
     row0 = rank * B * H  # this rank's rows of the global problem (weak scaling)
     u = synth.signal_torch(0, "u", B, H, N, dev, tdt, row0=row0)
     w = synth.signal_torch(0, "w", B, H, N, dev, tdt, row0=row0) if wl["gated"] else None
     v = synth.signal_torch(0, "v", B, H, N, dev, tdt, row0=row0) if wl["gated"] else None
-    k = torch.tensor(synth.decay_filters(rank, H, N), dtype=torch.float32, device=dev)
+    dy = synth.signal_torch(0, "dy", B, H, N, dev, tdt, row0=row0) if wl["bwd"] else None
+    k = torch.tensor(synth.decay_filters(rank, H, K), dtype=torch.float32, device=dev)
     y = torch.empty_like(u)
+    ws_f = plan.workspace(B, H, device=dev)
+    ws_b = plan.workspace(B, H, for_bwd=True, device=dev) if wl["bwd"] else None
+    grads = None
+    if wl["bwd"]:
+        grads = dict(du=torch.empty_like(u), dw=torch.empty_like(u) if w is not None else None,
+                     dv=torch.empty_like(u) if v is not None else None,
+                     dk=torch.empty(H, K, dtype=torch.float32, device=dev))
 
-    def step():
-        kf = plan.precompute_kf(k)
+    from paper_2311_05908_b200 import _abi
+    from paper_2311_05908_b200.fftconv import _ptr, _stream
+
+    def conv(kf, uu, ww, vv, out):
         if wl["gated"]:
-            plan.gated_fwd(u, w, v, kf, out=y)
+            plan.gated_fwd(uu, ww, vv, kf, out=out, workspace=ws_f)
         else:
-            plan.fwd(u, kf, out=y)
-        return kf
+            plan.fwd(uu, kf, out=out, workspace=ws_f)
+        if wl["bwd"]:
+            _abi.check(_abi.lib().fftconv_bwd(
+                plan._h, _ptr(dy), _ptr(uu), _ptr(ww), _ptr(vv), _ptr(kf), _ptr(grads["du"]), _ptr(grads["dw"]),
+                _ptr(grads["dv"]), _ptr(grads["dk"]), B, H, K, _ptr(ws_b), _stream(dev)))
 
     for _ in range(args.warmup):
-        step()
+        conv(plan.precompute_kf(k), u, w, v, y)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    K = args.steps
+    S = args.steps
     ev_s = torch.cuda.Event(enable_timing=True)
     ev_e = torch.cuda.Event(enable_timing=True)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
     launch_count_reset()
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize()
         ev_s.record()
-        for i in range(K):
+        for i in range(S):
             kf = plan.precompute_kf(k)
             ev[i][0].record()
-            if wl["gated"]:
-                plan.gated_fwd(u, w, v, kf, out=y)
-            else:
-                plan.fwd(u, kf, out=y)
+            conv(kf, u, w, v, y)
             ev[i][1].record()
         ev_e.record()
         torch.cuda.synchronize()
@@ -247,36 +292,35 @@ def main():
     if world > 1:
         dist.barrier()
     total_ms = ev_s.elapsed_time(ev_e)
-    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    conv_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
     if world > 1:
-        t = torch.tensor([total_ms, kern_ms], device=dev)
+        t = torch.tensor([total_ms, conv_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, kern_ms = t.tolist()
-    step_ms = total_ms / K
+        total_ms, conv_ms = t.tolist()
+    step_ms = total_ms / S
     value = world * B * H / (step_ms * 1e-3)
 
     # ---------------- end-to-end through the public API with pinned host buffers
-    hu = u.cpu().pin_memory()
-    hw = w.cpu().pin_memory() if w is not None else None
-    hv = v.cpu().pin_memory() if v is not None else None
-    hk = k.cpu().pin_memory()
+    hbuf = {name: t.cpu().pin_memory() for name, t in (("u", u), ("w", w), ("v", v), ("dy", dy), ("k", k))
+            if t is not None}
+    dbuf = {name: torch.empty_like(t) for name, t in (("u", u), ("w", w), ("v", v), ("k", k)) if t is not None}
     hy = torch.empty(y.shape, dtype=y.dtype).pin_memory()
-    du, dw_, dv_, dk = torch.empty_like(u), torch.empty_like(u), torch.empty_like(u), torch.empty_like(k)
-    h2d = hu.numel() * hu.element_size() + hk.numel() * 4 + (2 * hu.numel() * hu.element_size() if w is not None else 0)
+    h2d = sum(t.numel() * t.element_size() for t in hbuf.values())
     d2h = hy.numel() * hy.element_size()
+    if wl["bwd"]:
+        hdu = torch.empty(u.shape, dtype=u.dtype).pin_memory()
+        d2h += hdu.numel() * hdu.element_size() + grads["dk"].numel() * 4
 
     def e2e_step():
-        du.copy_(hu, non_blocking=True)
-        dk.copy_(hk, non_blocking=True)
-        if w is not None:
-            dw_.copy_(hw, non_blocking=True)
-            dv_.copy_(hv, non_blocking=True)
-        kf = plan.precompute_kf(dk)
-        if w is not None:
-            plan.gated_fwd(du, dw_, dv_, kf, out=y)
-        else:
-            plan.fwd(du, kf, out=y)
+        for name, t in dbuf.items():
+            t.copy_(hbuf[name], non_blocking=True)
+        if dy is not None:
+            dy.copy_(hbuf["dy"], non_blocking=True)
+        kf = plan.precompute_kf(dbuf["k"])
+        conv(kf, dbuf["u"], dbuf.get("w"), dbuf.get("v"), y)
         hy.copy_(y, non_blocking=True)
+        if wl["bwd"]:
+            hdu.copy_(grads["du"], non_blocking=True)
 
     for _ in range(2):
         e2e_step()
@@ -299,38 +343,40 @@ def main():
 
     if rank == 0:
         peaks = load_peaks()
-        L = plan.info.fft_size
-        io = 2  # bytes per element
-        bytes_per_launch = B * H * N * io * (4 if wl["gated"] else 2) + H * L * 8  # u,(w,v), y + k_f
-        achieved = bytes_per_launch / (kern_ms * 1e-3) / 1e9
+        bytes_per_call = algorithmic_bytes(wl, H * L * 8)
+        achieved = bytes_per_call / (conv_ms * 1e-3) / 1e9
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_fwd_traffic.json")
+        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(prof):
             try:
-                d = json.load(open(prof))
-                traffic = d.get(args.workload, {}).get("dram_bytes_per_launch")
+                traffic = json.load(open(prof)).get(args.workload, {}).get("dram_bytes_per_launch")
             except Exception:
                 traffic = None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            rate, cores, sample, _ = oracle_rows_per_s(wl)
+            rate, cores, sample, _, _, _ = oracle_rows_per_s(wl)
             cpu = {"value": rate, "unit": "sequences/s", "cores": cores, "kind": "oracle", "sample": sample}
         vs = PAPER_SEQ_S.get(args.workload)
+        regime = {1: "fused", 2: "partial (overlap-save, multipass)", 3: "multipass"}[plan.info.regime]
         out = {
-            "metric": METRIC, "value": value, "unit": "sequences/s", "n_gpus": world, "steps": K,
+            "metric": METRIC, "value": value, "unit": "sequences/s", "n_gpus": world, "steps": S,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": (value / vs) if vs else None,
             "vs_baseline_note": "paper H100-SXM padded gated FFT-2K row (P:1144-1167), another machine: context only"
             if vs else None,
             "dtype": wl["dtype"], "data": "synthetic",
-            "config": {"workload": wl["name"], "B": B, "H": H, "N": N, "fft_size": L, "gated": wl["gated"],
-                       "causal": wl["causal"], "step": "precompute_kf + fused fwd",
-                       "l2": f"inputs larger than L2 ({bytes_per_launch / 1e6:.0f} MB per step)",
+            "config": {"workload": wl["name"], "B": B, "H": H, "N": N, "K": K, "fft_size": L, "gated": wl["gated"],
+                       "causal": True, "backward": wl["bwd"], "regime": regime,
+                       "step": "precompute_kf + conv" + (" fwd+bwd" if wl["bwd"] else " fwd"),
+                       "l2": f"inputs larger than L2 ({bytes_per_call / 1e6:.0f} MB per step)",
                        "parallelism": f"rows sharded, {world} GPU(s), no data-path collective"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm"], "traffic": traffic,
-                         "kernel": "fftconv_fwd_o2_kernel", "kernel_ms": kern_ms,
-                         "algorithmic_bytes_per_launch": bytes_per_launch, "peak_source": peaks["src"]},
+                         "kernel": "conv call (fftconv_fwd_o2_kernel"
+                                   + (" + multipass outer passes" if plan.info.regime != 1 else "")
+                                   + (" + bwd" if wl["bwd"] else "") + ")",
+                         "kernel_ms": conv_ms, "algorithmic_bytes_per_launch": bytes_per_call,
+                         "peak_source": peaks["src"]},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "sequences/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
