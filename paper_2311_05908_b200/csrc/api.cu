@@ -116,6 +116,7 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     MpParams mp{};
     mp.u = u; mp.w = w; mp.v = v; mp.y = y; mp.ws = ws;
     mp.wbase = reinterpret_cast<const float2*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.wbase);
+    mp.wtab = reinterpret_cast<const float2*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.wtab);
     mp.B = B; mp.H = H; mp.N = p->N; mp.L0 = p->L0; mp.Lp = p->Lp;
     mp.gated = gated ? 1 : 0;
     mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
@@ -255,6 +256,7 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   void* scratch = static_cast<uint8_t*>(part) + size_t(H) * p->L0 * size_t(nbt_in) * size_t(p->Lp) * 8;
   MpParams mp{};
   mp.wbase = reinterpret_cast<const float2*>(tab + p->tl.wbase);
+  mp.wtab = reinterpret_cast<const float2*>(tab + p->tl.wtab);
   mp.B = B; mp.H = H; mp.N = p->N; mp.L0 = p->L0; mp.Lp = p->Lp;
   mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
   // pass 1 on g = u (* w) and on dc = dy (* v)

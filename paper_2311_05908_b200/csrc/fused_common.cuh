@@ -57,7 +57,10 @@ struct O2Cfg {
   static constexpr int KA = CAUSAL ? L2 / 2 : L2;
   static constexpr int NOUT = CAUSAL ? L / 2 : L;  // row length N
   static constexpr int CH = NOUT / 8;           // 16-byte chunks per row (16-bit I/O)
-  static constexpr int NA = 3 * L2;             // stage A N: re | im | -im
+  // stage A N: re | im | -im (causal); circular drops the -im block (its
+  // larger K makes the table too big for two warpgroups) and negates in registers
+  static constexpr bool NEG_A = CAUSAL;
+  static constexpr int NA = (NEG_A ? 3 : 2) * L2;
   static constexpr int NB = (3 * L1 + 15) / 16 * 16;  // stage B/B^-1 N: re | im | -im (-re) | pad
   // tables (same offsets as the host image, see plan.cpp)
   static constexpr uint32_t GA_BYTES = NA * 2 * KA * 2;

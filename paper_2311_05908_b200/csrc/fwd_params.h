@@ -43,6 +43,7 @@ struct MpParams {
   void* y;
   void* ws;             // T: fp16 rows (2 * pairs, H * L0, Lp)
   const float2* wbase;  // W_L^{n'}, n' < Lp
+  const float2* wtab;   // W_L^{n' k0}, [k0][n'] (L0 * Lp entries)
   const void* v2;       // pass 3 only: optional second gate (y2 = x * v2)
   void* y2;
   int64_t B, H, N;

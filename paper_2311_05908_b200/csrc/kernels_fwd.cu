@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
       for (int s = 0; s < 2 * C::KA / 16; ++s) {
         const uint64_t ad = dadd(dXA, 256 * s);
 #pragma unroll
-        for (int blk = 0; blk < 3; ++blk) {
+        for (int blk = 0; blk < C::NA / L2; ++blk) {
           const uint32_t row0 = blk * L2 + hh * (L2 / 2);
           const uint64_t bd = dadd(dGA, (row0 / 8) * C::SBO_GA + 256 * s);
           mma_f16_ss(tmem + row0, ad, bd, idesc, s > 0);
@@ -285,11 +285,15 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
         float re[16], im[16], ni[16];
         tmem_ld16(tq + k20, re);
         tmem_ld16(tq + L2 + k20, im);
-        tmem_ld16(tq + 2 * L2 + k20, ni);
+        if constexpr (C::NEG_A) tmem_ld16(tq + 2 * L2 + k20, ni);
         float4 w[8];
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) w[jj] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1, k20 / 2 + jj));
         tmem_ld_wait();
+        if constexpr (!C::NEG_A) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) ni[e] = -im[e];
+        }
         cmul8(re, im, ni, w);
         cmul8(re + 8, im + 8, ni + 8, w + 4);
         if (sub == 0) wait_half(slice ^ 1);

@@ -75,14 +75,62 @@ FC_DEVICE void stockham_pass(const float2* __restrict__ x, float2* __restrict__ 
   }
 }
 
+// In-place variant for L <= 8 * blockDim.x: every thread first reads all of
+// its groups (at most 8 elements) into registers, the block synchronises,
+// then the results are written back -- one L-element buffer instead of two.
+template <int R>
+FC_DEVICE void stockham_pass_inplace(float2* x, const float2* __restrict__ tw, int L, int Ns) {
+  constexpr int GPT = 8 / R;  // groups per thread (L <= 8 * blockDim.x)
+  const int G = L / R;
+  float2 v[GPT][R];
+#pragma unroll
+  for (int g = 0; g < GPT; ++g) {
+    const int j = threadIdx.x + g * blockDim.x;
+    if (j < G) {
+      const int jm = j % Ns;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[g][r] = x[j + r * G];
+      if (Ns > 1) {
+        const int step = L / (Ns * R);
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[g][r] = cmulf(v[g][r], tw[(jm * r * step) & (L - 1)]);
+      }
+      if constexpr (R == 8) dft8(v[g]);
+      else if constexpr (R == 4) dft4(v[g]);
+      else dft2(v[g]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < GPT; ++g) {
+    const int j = threadIdx.x + g * blockDim.x;
+    if (j < G) {
+      const int jm = j % Ns;
+      const int base = (j / Ns) * Ns * R + jm;
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[base + r * Ns] = v[g][r];
+    }
+  }
+  __syncthreads();
+}
+
+// Full forward FFT of xs[0..L) in place (L <= 8 * blockDim.x), natural order.
+FC_DEVICE void fft_inplace(float2* xs, const float2* tws, int L) {
+  int Ns = 1;
+  const int lg = __ffs(L) - 1;
+  const int rem = lg % 3;
+  if (rem == 1) { stockham_pass_inplace<2>(xs, tws, L, Ns); Ns = 2; }
+  if (rem == 2) { stockham_pass_inplace<4>(xs, tws, L, Ns); Ns = 4; }
+  for (; Ns < L; Ns <<= 3) stockham_pass_inplace<8>(xs, tws, L, Ns);
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) {
-  extern __shared__ float2 sm[];  // two L-element ping-pong buffers + L twiddles
+  extern __shared__ float2 sm[];  // L data + L twiddles
   const int h = blockIdx.x;
   const int L = int(prm.L), K = int(prm.K);
-  float2* bufs[2] = {sm, sm + L};
-  float2* tws = sm + 2 * L;
+  float2* tws = sm + L;
   {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.twiddle);
     const uint32_t dst = smem_u32(tws);
@@ -93,22 +141,8 @@ __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) 
   for (int n = threadIdx.x; n < L; n += blockDim.x) sm[n] = make_float2(n < K ? krow[n] : 0.f, 0.f);
   cp_async_wait_all();
   __syncthreads();
-  int cur = 0, Ns = 1;
-  const int lg = __ffs(L) - 1;
-  const int rem = lg % 3;
-  if (rem) {  // leading radix-2/4 pass
-    if (rem == 1) stockham_pass<2>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
-    else stockham_pass<4>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
-    Ns <<= rem;
-    cur ^= 1;
-    __syncthreads();
-  }
-  for (; Ns < L; Ns <<= 3) {
-    stockham_pass<8>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
-    cur ^= 1;
-    __syncthreads();
-  }
-  const float2* xs = bufs[cur];
+  fft_inplace(sm, tws, L);
+  const float2* xs = sm;
   // plan layout: row k2 holds pairs (k1, k1 + 1) as {kr, kr', ki, ki'}
   const int L1 = prm.L1, L2 = prm.L2, cpr = L1 / 2;
   uint8_t* out = reinterpret_cast<uint8_t*>(prm.kf) + int64_t(h) * L2 * tab_stride(uint32_t(cpr));
@@ -130,10 +164,9 @@ __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) 
 // complex values left by step 1 at the start of block (h, k0) and writes the
 // inner plan layout of K_f[k0 + L0 f'] over the same block (in place).
 __global__ void __launch_bounds__(256) mp_kf_rows_kernel(const KfParams prm, int L0, int Lp, size_t block_bytes) {
-  extern __shared__ float2 sm[];
+  extern __shared__ float2 sm[];  // Lp data + Lp twiddles
   const int L = Lp;
-  float2* bufs[2] = {sm, sm + L};
-  float2* tws = sm + 2 * L;
+  float2* tws = sm + L;
   const int64_t blk = blockIdx.x;  // h * L0 + k0
   const int k0 = int(blk % L0);
   uint8_t* block = reinterpret_cast<uint8_t*>(prm.kf) + blk * block_bytes;
@@ -147,22 +180,8 @@ __global__ void __launch_bounds__(256) mp_kf_rows_kernel(const KfParams prm, int
   }
   cp_async_wait_all();
   __syncthreads();
-  int cur = 0, Ns = 1;
-  const int lg = __ffs(L) - 1;
-  const int rem = lg % 3;
-  if (rem) {
-    if (rem == 1) stockham_pass<2>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
-    else stockham_pass<4>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
-    Ns <<= rem;
-    cur ^= 1;
-    __syncthreads();
-  }
-  for (; Ns < L; Ns <<= 3) {
-    stockham_pass<8>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
-    cur ^= 1;
-    __syncthreads();
-  }
-  const float2* xs = bufs[cur];
+  fft_inplace(sm, tws, L);
+  const float2* xs = sm;
   const int L1 = prm.L1, L2 = prm.L2, cpr = L1 / 2;
   for (int q = threadIdx.x; q < L2 * cpr; q += blockDim.x) {
     const int k2 = q / cpr, k1 = 2 * (q % cpr);
@@ -179,7 +198,7 @@ __global__ void __launch_bounds__(256) mp_kf_rows_kernel(const KfParams prm, int
 }
 
 cudaError_t launch_mp_kf_rows(const KfParams& prm, int L0, int Lp, size_t block_bytes, cudaStream_t s) {
-  const size_t smem = size_t(Lp) * sizeof(float2) * 3;
+  const size_t smem = size_t(Lp) * sizeof(float2) * 2;
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(mp_kf_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -197,10 +216,9 @@ cudaError_t launch_mp_kf_rows(const KfParams& prm, int L0, int Lp, size_t block_
 // Multipass regime, step 1: the same per (head, k0) over the inner length Lp,
 // leaving a[k0][n'] = sum_f' acc[k0 + L0 f'] W_Lp^{-n' f'} (complex) in scratch.
 __global__ void __launch_bounds__(256) dk_rows_kernel(const DkParams prm) {
-  extern __shared__ float2 sm[];
+  extern __shared__ float2 sm[];  // Lp data + Lp twiddles
   const int L = prm.Lp;
-  float2* bufs[2] = {sm, sm + L};
-  float2* tws = sm + 2 * L;
+  float2* tws = sm + L;
   const int64_t row = blockIdx.x;  // h * L0 + k0
   const int k0 = int(row % prm.L0);
   {
@@ -226,22 +244,8 @@ __global__ void __launch_bounds__(256) dk_rows_kernel(const DkParams prm) {
   }
   cp_async_wait_all();
   __syncthreads();
-  int cur = 0, Ns = 1;
-  const int lg = __ffs(L) - 1;
-  const int rem = lg % 3;
-  if (rem) {
-    if (rem == 1) stockham_pass<2>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
-    else stockham_pass<4>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
-    Ns <<= rem;
-    cur ^= 1;
-    __syncthreads();
-  }
-  for (; Ns < L; Ns <<= 3) {
-    stockham_pass<8>(bufs[cur], bufs[cur ^ 1], tws, L, Ns);
-    cur ^= 1;
-    __syncthreads();
-  }
-  const float2* xs = bufs[cur];
+  fft_inplace(sm, tws, L);
+  const float2* xs = sm;
   if (prm.L0 == 1) {
     float* dk = prm.dk + row * prm.K;
     for (int t = threadIdx.x; t < prm.K; t += blockDim.x) dk[t] = xs[t].x;
@@ -283,7 +287,7 @@ __global__ void __launch_bounds__(256) dk_cols_kernel(const DkParams prm) {
 
 cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
   if (prm.H <= 0) return cudaSuccess;
-  const size_t smem = size_t(prm.Lp) * sizeof(float2) * 3;
+  const size_t smem = size_t(prm.Lp) * sizeof(float2) * 2;
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(dk_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -299,7 +303,7 @@ cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
 
 cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s) {
   if (prm.H <= 0) return cudaSuccess;
-  const size_t smem = size_t(prm.L) * sizeof(float2) * 3;
+  const size_t smem = size_t(prm.L) * sizeof(float2) * 2;
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(precompute_kf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

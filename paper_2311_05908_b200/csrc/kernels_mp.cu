@@ -98,25 +98,47 @@ __global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
     z0[n0] = make_float2(a.x, c.x);
     z1[n0] = make_float2(a.y, c.y);
   }
-  DftReg<L0, false>::run(z0);
-  DftReg<L0, false>::run(z1);
-  // twiddle W_L^{n' k0} by recurrence from W_L^{n'} (error ~ L0 ulp, fp32)
-  const float2 b0w = prm.wbase[n], b1w = prm.wbase[n + 1];
-  float2 t0 = make_float2(1.f, 0.f), t1 = make_float2(1.f, 0.f);
+  // DFT_L0 over n0.  Causal rows are zero for n0 >= L0/2, so the first
+  // radix-2 stage reduces to X[2m] = DFT_{L0/2}(z)[m],
+  // X[2m+1] = DFT_{L0/2}(z W_L0^{n0})[m].
+  float2 X0[L0], X1[L0];
+  if (!prm.partial) {
+    float2 a0[L0 / 2], b0[L0 / 2], a1[L0 / 2], b1[L0 / 2];
+#pragma unroll
+    for (int n0 = 0; n0 < L0 / 2; ++n0) {
+      const float2 w = w_root<L0>(n0);
+      a0[n0] = z0[n0];
+      a1[n0] = z1[n0];
+      b0[n0] = c_mul(z0[n0], w);
+      b1[n0] = c_mul(z1[n0], w);
+    }
+    DftReg<L0 / 2, false>::run(a0);
+    DftReg<L0 / 2, false>::run(b0);
+    DftReg<L0 / 2, false>::run(a1);
+    DftReg<L0 / 2, false>::run(b1);
+#pragma unroll
+    for (int m = 0; m < L0 / 2; ++m) {
+      X0[2 * m] = a0[m]; X0[2 * m + 1] = b0[m];
+      X1[2 * m] = a1[m]; X1[2 * m + 1] = b1[m];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < L0; ++i) { X0[i] = z0[i]; X1[i] = z1[i]; }
+    DftReg<L0, false>::run(X0);
+    DftReg<L0, false>::run(X1);
+  }
+  // twiddle W_L^{n' k0} from the plan table [k0][n'], scale 1/sqrt(L0)
   const float s = rsqrtf(float(L0));
-  __half* __restrict__ Tw = reinterpret_cast<__half*>(prm.ws);
-  const int64_t HL0 = prm.H * L0;
+  __half* __restrict__ Tre = reinterpret_cast<__half*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
+  __half* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
 #pragma unroll
   for (int k0 = 0; k0 < L0; ++k0) {
-    const float2 a = c_mul(z0[k0], t0), c = c_mul(z1[k0], t1);
-    const int64_t row_re = ((2 * p) * HL0 + h * L0 + k0) * prm.Lp + n;
-    const int64_t row_im = ((2 * p + 1) * HL0 + h * L0 + k0) * prm.Lp + n;
+    const float4 tw = *reinterpret_cast<const float4*>(prm.wtab + int64_t(k0) * prm.Lp + n);
+    const float2 a = c_mul(X0[k0], make_float2(tw.x, tw.y)), c = c_mul(X1[k0], make_float2(tw.z, tw.w));
     if (!prm.row_keep || prm.row_keep[k0]) {  // masked rows are skipped downstream
-      *reinterpret_cast<__half2*>(Tw + row_re) = __floats2half2_rn(a.x * s, c.x * s);
-      *reinterpret_cast<__half2*>(Tw + row_im) = __floats2half2_rn(a.y * s, c.y * s);
+      *reinterpret_cast<__half2*>(Tre + int64_t(k0) * prm.Lp) = __floats2half2_rn(a.x * s, c.x * s);
+      *reinterpret_cast<__half2*>(Tim + int64_t(k0) * prm.Lp) = __floats2half2_rn(a.y * s, c.y * s);
     }
-    t0 = c_mul(t0, b0w);
-    t1 = c_mul(t1, b1w);
   }
 }
 
@@ -130,45 +152,56 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
   const int64_t ph = idx / NP;
   const int64_t h = ph % prm.H, p = ph / prm.H;
   const int n = 2 * cp;
-  const __half* __restrict__ Tw = reinterpret_cast<const __half*>(prm.ws);
-  const int64_t HL0 = prm.H * L0;
-  float2 x0[L0], x1[L0];
-  const float2 b0w = prm.wbase[n], b1w = prm.wbase[n + 1];
-  float2 t0 = make_float2(1.f, 0.f), t1 = make_float2(1.f, 0.f);
+  const __half* __restrict__ Tre =
+      reinterpret_cast<const __half*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
+  const __half* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
+  float2 e0[L0 / 2], o0[L0 / 2], e1[L0 / 2], o1[L0 / 2];  // even / odd k0
 #pragma unroll
   for (int k0 = 0; k0 < L0; ++k0) {
-    const int64_t row_re = ((2 * p) * HL0 + h * L0 + k0) * prm.Lp + n;
-    const int64_t row_im = ((2 * p + 1) * HL0 + h * L0 + k0) * prm.Lp + n;
     const bool kept = !prm.row_keep || prm.row_keep[k0];
-    const float2 re = kept ? __half22float2(*reinterpret_cast<const __half2*>(Tw + row_re)) : make_float2(0.f, 0.f);
-    const float2 im = kept ? __half22float2(*reinterpret_cast<const __half2*>(Tw + row_im)) : make_float2(0.f, 0.f);
-    x0[k0] = c_mulc(make_float2(re.x, im.x), t0);
-    x1[k0] = c_mulc(make_float2(re.y, im.y), t1);
-    t0 = c_mul(t0, b0w);
-    t1 = c_mul(t1, b1w);
+    const float2 re = kept ? __half22float2(*reinterpret_cast<const __half2*>(Tre + int64_t(k0) * prm.Lp))
+                           : make_float2(0.f, 0.f);
+    const float2 im = kept ? __half22float2(*reinterpret_cast<const __half2*>(Tim + int64_t(k0) * prm.Lp))
+                           : make_float2(0.f, 0.f);
+    const float4 tw = *reinterpret_cast<const float4*>(prm.wtab + int64_t(k0) * prm.Lp + n);
+    const float2 a = c_mulc(make_float2(re.x, im.x), make_float2(tw.x, tw.y));
+    const float2 c = c_mulc(make_float2(re.y, im.y), make_float2(tw.z, tw.w));
+    if (k0 & 1) { o0[k0 / 2] = a; o1[k0 / 2] = c; }
+    else { e0[k0 / 2] = a; e1[k0 / 2] = c; }
   }
-  DftReg<L0, true>::run(x0);
-  DftReg<L0, true>::run(x1);
+  // inverse DFT_L0 over k0, half of the outputs: y[n0] = E[n0] +- W_L0^{-n0} O[n0]
+  DftReg<L0 / 2, true>::run(e0);
+  DftReg<L0 / 2, true>::run(o0);
+  DftReg<L0 / 2, true>::run(e1);
+  DftReg<L0 / 2, true>::run(o1);
+  const float sgn = prm.partial ? -1.f : 1.f;  // causal keeps n0 < L0/2, partial n0 >= L0/2
+  float2 x0[L0 / 2], x1[L0 / 2];
+#pragma unroll
+  for (int m = 0; m < L0 / 2; ++m) {
+    float2 w = w_root<L0>(m);
+    w.y = -w.y;
+    w.x *= sgn;
+    w.y *= sgn;
+    x0[m] = c_add(e0[m], c_mul(o0[m], w));
+    x1[m] = c_add(e1[m], c_mul(o1[m], w));
+  }
   const float s = rsqrtf(float(L0));
   const int64_t b0 = 2 * p, b1 = 2 * p + 1;
   const bool has1 = b1 < prm.B;
   T* __restrict__ y = reinterpret_cast<T*>(prm.y);
   const T* __restrict__ v = reinterpret_cast<const T*>(prm.v);
   int64_t r0, r1;
-  int q0 = 0;  // first output block: causal keeps n0 < L0/2, partial keeps n0 >= L0/2
   if (prm.partial) {
     r0 = ((b0 / prm.NC) * prm.H + h) * prm.N + (b0 % prm.NC) * prm.C + n;
     r1 = ((b1 / prm.NC) * prm.H + h) * prm.N + (b1 % prm.NC) * prm.C + n;
-    q0 = L0 / 2;
   } else {
     r0 = (b0 * prm.H + h) * prm.N + n;
     r1 = (b1 * prm.H + h) * prm.N + n;
   }
-  auto emit = [&](auto q0c) {
-    constexpr int Q0 = decltype(q0c)::value;
+  {
   #pragma unroll
       for (int i0 = 0; i0 < L0 / 2; ++i0) {
-        const int n0 = i0 + Q0;
+        const int n0 = i0;
       const int64_t o = int64_t(i0) * prm.Lp;
       float a0 = x0[n0].x * s, a1 = x1[n0].x * s;  // row b
       float c0 = x0[n0].y * s, c1 = x1[n0].y * s;  // row b+1
@@ -193,9 +226,7 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
       st2<T>(y + r0 + o, a0, a1);
       if (has1) st2<T>(y + r1 + o, c0, c1);
     }
-  };
-  if (q0) emit(std::integral_constant<int, L0 / 2>{});
-  else emit(std::integral_constant<int, 0>{});
+  }
 }
 
 // k_f, step 1: per (head, column n'): DFT_L0 of k[n' + L' n0] (n0 < L0/2,

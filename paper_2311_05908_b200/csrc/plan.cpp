@@ -152,7 +152,8 @@ static void put_float(std::vector<uint8_t>& img, size_t off, double x) {
 // inverse pair scales by 1/L and k_f is used unscaled.
 static void build_fused_tables(fftconv_plan_s* p, int64_t L) {
   const int L1 = p->L1, L2 = p->L2, KA = p->KA;
-  const int NA = 3 * L2, NB = (3 * L1 + 15) / 16 * 16;
+  const bool neg_a = KA < L2;  // causal: the -im block of stage A (see O2Cfg::NEG_A)
+  const int NA = (neg_a ? 3 : 2) * L2, NB = (3 * L1 + 15) / 16 * 16;
   TableLayout& t = p->tl;
   size_t off = 0;
   t.ga = off;  t.ga_bytes = size_t(NA) * (2 * KA) * 2;      off = align_up(off + t.ga_bytes, 1024);
@@ -164,12 +165,13 @@ static void build_fused_tables(fftconv_plan_s* p, int64_t L) {
   t.wl = off;  t.wl_bytes = size_t(L) * 8;                  off = align_up(off + t.wl_bytes, 1024);
   const int64_t Lfull = p->L;  // the whole transform (== L unless multipass)
   t.wbase = off; t.wbase_bytes = Lfull != L ? size_t(L) * 8 : 0; off = align_up(off + t.wbase_bytes, 1024);
+  t.wtab = off;  t.wtab_bytes = Lfull != L ? size_t(Lfull) * 8 : 0; off = align_up(off + t.wtab_bytes, 1024);
   t.total = off;
   p->image.assign(t.total, 0);
   std::vector<uint8_t>& img = p->image;
   const double sA = 1.0 / std::sqrt(double(L2)), sB = 1.0 / std::sqrt(double(L1));
   // stage A (forward, contracts n2 -> k2): B^T[(blk,k2)][(c,n2)], n2 < KA
-  for (int blk = 0; blk < 3; ++blk)
+  for (int blk = 0; blk < NA / L2; ++blk)
     for (int k2 = 0; k2 < L2; ++k2)
       for (int ci = 0; ci < 2; ++ci)
         for (int n2 = 0; n2 < KA; ++n2) {
@@ -234,6 +236,14 @@ static void build_fused_tables(fftconv_plan_s* p, int64_t L) {
       put_float(img, t.wbase + size_t(e) * 8, wr);
       put_float(img, t.wbase + size_t(e) * 8 + 4, wi);
     }
+  if (t.wtab_bytes)
+    for (int64_t k0 = 0; k0 < Lfull / L; ++k0)
+      for (int64_t n = 0; n < L; ++n) {
+        double wr, wi;
+        root(n * k0, Lfull, &wr, &wi);
+        put_float(img, t.wtab + size_t(k0 * L + n) * 8, wr);
+        put_float(img, t.wtab + size_t(k0 * L + n) * 8 + 4, wi);
+      }
 }
 
 // A13: keep(f) = prod_j keep_j[digit_j(f)], digits of f on the row-major

@@ -25,6 +25,7 @@ struct TableLayout {
   size_t twt = 0, twt_bytes = 0;  // same values, [k2][n1/2]
   size_t wl = 0, wl_bytes = 0;    // W_L^e, e < L, float2 (k_f precompute)
   size_t wbase = 0, wbase_bytes = 0;  // multipass: W_L^{n'}, n' < L', float2
+  size_t wtab = 0, wtab_bytes = 0;    // multipass: W_L^{n' k0}, [k0][n'], float2
   size_t total = 0;
 };
 
