@@ -46,9 +46,12 @@ WORKLOADS = {
     "cfg5": _wl("cfg5: frequency-sparse causal conv B=8 H=768 N=16384 fp16, 75% of inner Monarch rows skipped",
                 8, 768, 16384, sparse="rows75"),
     "cfg5dense": _wl("cfg5 dense reference: causal conv B=8 H=768 N=16384 fp16", 8, 768, 16384),
+    "cfg5b": _wl("cfg5b: causal conv B=8 H=96 N=4194304 fp16 (fft_size 8M, three outer levels)", 8, 96, 1 << 22),
 }
-for _n in (256, 512, 1024, 2048, 4096, 8192, 16384):
+for _n in (256, 512, 1024, 2048, 4096, 8192, 16384, 32768, 65536):
     WORKLOADS[f"sweep{_n}"] = _wl(f"sweep: causal fp16 conv B*H=49152 N={_n}", 64, 768, _n)
+for _n, _b in ((1 << 18, 16), (1 << 20, 4), (1 << 22, 1)):  # constant elements: B*H = 49152 * 65536 / N
+    WORKLOADS[f"sweep{_n}"] = _wl(f"sweep: causal fp16 conv B*H={_b * 768} N={_n}", _b, 768, _n)
 
 METRIC = "fused FFT-conv sequences/s & % HBM/tensor roofline, N=256–4M, at 1/2/4/8 B200"
 # paper's padded (causal) H100 rows for the same workload, another

@@ -91,9 +91,8 @@ extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float*
   if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
     const size_t block = size_t(p->L2) * tab_stride(uint32_t(p->L1 / 2));
     prm.L = p->Lp;
-    e = launch_mp_precompute_kf(prm, reinterpret_cast<const float2*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.wbase),
-                                p->L0, p->Lp, block, reinterpret_cast<cudaStream_t>(stream));
-    g_launches += H > 0 ? 2 : 0;
+    e = launch_mp_precompute_kf(prm, p->lev_L0, p->nlev, p->L, block, reinterpret_cast<cudaStream_t>(stream));
+    g_launches += H > 0 ? 2 + p->nlev - 1 : 0;
   } else {
     e = launch_precompute_kf(prm, reinterpret_cast<cudaStream_t>(stream));
     g_launches += H > 0 ? 1 : 0;
@@ -115,9 +114,10 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     if (!aligned16(ws)) { set_last_error(std::string(fn) + ": workspace not 16-byte aligned"); return FFTCONV_ERR_MISALIGNED; }
     MpParams mp{};
     mp.u = u; mp.w = w; mp.v = v; mp.y = y; mp.ws = ws;
+    mp.L0 = p->lev_L0[0];
     mp.wbase = reinterpret_cast<const float2*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.wbase);
     mp.wtab = reinterpret_cast<const float2*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.wtab);
-    mp.B = B; mp.H = H; mp.N = p->N; mp.L0 = p->L0; mp.Lp = p->Lp;
+    mp.B = B; mp.H = H; mp.N = p->N; mp.Lp = int32_t(p->L / p->lev_L0[0]);
     mp.gated = gated ? 1 : 0;
     mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
     const bool skip = p->sparse && p->row_map.size() < size_t(p->L0);
@@ -128,12 +128,32 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
       mp.NC = p->N / mp.C;
       mp.B = B * mp.NC;
     }
+    if (p->nlev > 1) mp.wtab = nullptr;  // deep plans: outer twiddles on the fly
+    mp.Llev = p->L;
+    const int64_t rows = 2 * ((mp.B + 1) / 2);
+    const size_t tbytes = size_t(rows) * size_t(H) * size_t(p->L) * 2;
+    void* Tb[2] = {ws, static_cast<uint8_t*>(ws) + tbytes};
     cudaError_t e = launch_mp_pass(mp, 1, st);
     if (e != cudaSuccess) return cuda_fail(fn, e);
-    // pass 2: the fused circular kernel over the complex rows of T, in place
+    // deeper outer levels: complex circular rows, ping-pong between T buffers
+    auto level = [&](int l) {  // params of level l >= 1 (0-based)
+      MpParams q{};
+      int64_t Hl = H, Ll = p->L;
+      for (int j = 0; j < l; ++j) { Hl *= p->lev_L0[j]; Ll /= p->lev_L0[j]; }
+      q.B = rows; q.H = Hl; q.N = Ll; q.L0 = p->lev_L0[l]; q.Lp = int32_t(Ll / p->lev_L0[l]);
+      q.Llev = Ll; q.circ = 1; q.dtype = 0; q.gated = 0;
+      q.u = Tb[(l - 1) & 1]; q.ws = Tb[l & 1]; q.y = Tb[(l - 1) & 1];
+      return q;
+    };
+    for (int l = 1; l < p->nlev; ++l) {
+      e = launch_mp_pass(level(l), 1, st);
+      if (e != cudaSuccess) return cuda_fail(fn, e);
+    }
+    // inner pass: the fused circular kernel over the complex rows, in place
+    void* Tin = Tb[(p->nlev - 1) & 1];
     FwdParams in{};
-    in.u = ws; in.y = ws; in.kf = kf; in.tables = p->d_tables;
-    in.B = 2 * ((mp.B + 1) / 2); in.H = H * p->L0; in.N = p->Lp;
+    in.u = Tin; in.y = Tin; in.kf = kf; in.tables = p->d_tables;
+    in.B = rows; in.H = H * p->L0; in.N = p->Lp;
     in.L1 = p->L1; in.causal = 0; in.gated = 0; in.dtype = 0;
     in.num_sms = num_sms_current();
     if (skip) {  // frequency-sparse: only rows k0 with a non-zero mask are transformed
@@ -143,9 +163,14 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     }
     e = launch_fwd_fused(in, st);
     if (e != cudaSuccess) return cuda_fail(fn, e);
+    for (int l = p->nlev - 1; l >= 1; --l) {
+      e = launch_mp_pass(level(l), 3, st);
+      if (e != cudaSuccess) return cuda_fail(fn, e);
+    }
+    mp.ws = Tb[0];
     e = launch_mp_pass(mp, 3, st);
     if (e != cudaSuccess) return cuda_fail(fn, e);
-    g_launches += 3;
+    g_launches += 1 + 2 * p->nlev;
     return FFTCONV_OK;
   }
   if (p->regime != REGIME_FUSED) { set_last_error(std::string(fn) + ": regime not supported by this build"); return FFTCONV_ERR_UNSUPPORTED; }
@@ -245,7 +270,10 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
     g_launches += 2;
     return FFTCONV_OK;
   }
-  if (p->regime != REGIME_MULTIPASS) { set_last_error("fftconv_bwd: regime not supported by this build"); return FFTCONV_ERR_UNSUPPORTED; }
+  if (p->regime != REGIME_MULTIPASS || p->nlev != 1) {
+    set_last_error("fftconv_bwd: this build supports the backward pass for fft_size <= 32768 (fused and one-level multipass)");
+    return FFTCONV_ERR_UNSUPPORTED;
+  }
   const int64_t rows = 2 * ((B + 1) / 2);
   uint8_t* ws = static_cast<uint8_t*>(d_workspace);
   const size_t tbytes = size_t(rows) * size_t(H) * size_t(p->L) * 2;
@@ -302,7 +330,8 @@ extern "C" fftconv_status_t fftconv_workspace_size(fftconv_plan_t p, int64_t B, 
   if (!p || !bytes || B < 0 || H < 0) { set_last_error("fftconv_workspace_size: bad argument"); return FFTCONV_ERR_INVALID_ARG; }
   size_t n = 0;
   if (for_bwd) n = bwd_ws_bytes(p, B, H);
-  else if (p->regime == REGIME_MULTIPASS) n = size_t(2 * ((B + 1) / 2)) * size_t(H) * size_t(p->L) * 2;
+  else if (p->regime == REGIME_MULTIPASS)
+    n = size_t(p->nlev > 1 ? 2 : 1) * size_t(2 * ((B + 1) / 2)) * size_t(H) * size_t(p->L) * 2;
   else if (p->regime == REGIME_PARTIAL) {
     const int64_t Bv = B * (p->N / (p->L / 2));
     n = size_t(2 * ((Bv + 1) / 2)) * size_t(H) * size_t(p->L) * 2;

@@ -56,6 +56,11 @@ struct MpParams {
   int32_t partial;
   int64_t NC, C;
   const uint8_t* row_keep;  // sparse: L0 flags, rows with 0 are never written/read
+  // recursive levels (N > 16384): complex circular rows of an intermediate in
+  // and out (all n0, no gating, fp16); twiddles W_Llev^{n' k0} computed on
+  // the fly when wtab == nullptr
+  int32_t circ;
+  int64_t Llev;
 };
 cudaError_t launch_mp_pass(const MpParams& prm, int pass, cudaStream_t s);
 
@@ -94,6 +99,7 @@ struct DkParams {
   int32_t L0, Lp;
 };
 cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s);
-cudaError_t launch_mp_precompute_kf(const KfParams& prm, const float2* wbase, int L0, int Lp, size_t block_bytes,
-                                    cudaStream_t s);
+cudaError_t launch_mp_precompute_kf(const KfParams& prm, const int32_t* lev_L0, int nlev, int64_t Lfull,
+                                    size_t block_bytes, cudaStream_t s);
+cudaError_t launch_mp_cols_inverse(float2* data, int L0, int64_t rows, int64_t Lrow, cudaStream_t s);
 }  // namespace fc

@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
   constexpr int NL = L0;
 #pragma unroll
   for (int n0 = 0; n0 < NL; ++n0) {
-    if (!prm.partial && n0 >= L0 / 2) break;
+    if (!prm.partial && !prm.circ && n0 >= L0 / 2) break;
     const int64_t o = int64_t(n0) * prm.Lp;
     const bool ok0 = s0 + o >= 0, ok1 = has1 && s1 + o >= 0;
     float2 a = ok0 ? ld2<T>(u + r0 + o) : make_float2(0.f, 0.f);  // row b, columns n, n+1
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
   // radix-2 stage reduces to X[2m] = DFT_{L0/2}(z)[m],
   // X[2m+1] = DFT_{L0/2}(z W_L0^{n0})[m].
   float2 X0[L0], X1[L0];
-  if (!prm.partial) {
+  if (!prm.partial && !prm.circ) {
     float2 a0[L0 / 2], b0[L0 / 2], a1[L0 / 2], b1[L0 / 2];
 #pragma unroll
     for (int n0 = 0; n0 < L0 / 2; ++n0) {
@@ -131,9 +131,26 @@ __global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
   const float s = rsqrtf(float(L0));
   __half* __restrict__ Tre = reinterpret_cast<__half*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
   __half* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
+  // on-the-fly twiddles (deep levels): W_Llev^{n k0} by recurrence from
+  // W_Llev^{n} (sincospif of an exact dyadic fraction; error ~ L0 ulp)
+  float2 bw0 = make_float2(1.f, 0.f), bw1 = bw0, tw0 = bw0, tw1 = bw0;
+  if (!prm.wtab) {
+    float sn, cs;
+    sincospif(-2.0f * float(n) / float(prm.Llev), &sn, &cs);
+    bw0 = make_float2(cs, sn);
+    sincospif(-2.0f * float(n + 1) / float(prm.Llev), &sn, &cs);
+    bw1 = make_float2(cs, sn);
+  }
 #pragma unroll
   for (int k0 = 0; k0 < L0; ++k0) {
-    const float4 tw = *reinterpret_cast<const float4*>(prm.wtab + int64_t(k0) * prm.Lp + n);
+    float4 tw;
+    if (prm.wtab) {
+      tw = *reinterpret_cast<const float4*>(prm.wtab + int64_t(k0) * prm.Lp + n);
+    } else {
+      tw = make_float4(tw0.x, tw0.y, tw1.x, tw1.y);
+      tw0 = c_mul(tw0, bw0);
+      tw1 = c_mul(tw1, bw1);
+    }
     const float2 a = c_mul(X0[k0], make_float2(tw.x, tw.y)), c = c_mul(X1[k0], make_float2(tw.z, tw.w));
     if (!prm.row_keep || prm.row_keep[k0]) {  // masked rows are skipped downstream
       *reinterpret_cast<__half2*>(Tre + int64_t(k0) * prm.Lp) = __floats2half2_rn(a.x * s, c.x * s);
@@ -156,6 +173,14 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
       reinterpret_cast<const __half*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
   const __half* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
   float2 e0[L0 / 2], o0[L0 / 2], e1[L0 / 2], o1[L0 / 2];  // even / odd k0
+  float2 bw0 = make_float2(1.f, 0.f), bw1 = bw0, tw0 = bw0, tw1 = bw0;
+  if (!prm.wtab) {
+    float sn, cs;
+    sincospif(-2.0f * float(n) / float(prm.Llev), &sn, &cs);
+    bw0 = make_float2(cs, sn);
+    sincospif(-2.0f * float(n + 1) / float(prm.Llev), &sn, &cs);
+    bw1 = make_float2(cs, sn);
+  }
 #pragma unroll
   for (int k0 = 0; k0 < L0; ++k0) {
     const bool kept = !prm.row_keep || prm.row_keep[k0];
@@ -163,7 +188,14 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
                            : make_float2(0.f, 0.f);
     const float2 im = kept ? __half22float2(*reinterpret_cast<const __half2*>(Tim + int64_t(k0) * prm.Lp))
                            : make_float2(0.f, 0.f);
-    const float4 tw = *reinterpret_cast<const float4*>(prm.wtab + int64_t(k0) * prm.Lp + n);
+    float4 tw;
+    if (prm.wtab) {
+      tw = *reinterpret_cast<const float4*>(prm.wtab + int64_t(k0) * prm.Lp + n);
+    } else {
+      tw = make_float4(tw0.x, tw0.y, tw1.x, tw1.y);
+      tw0 = c_mul(tw0, bw0);
+      tw1 = c_mul(tw1, bw1);
+    }
     const float2 a = c_mulc(make_float2(re.x, im.x), make_float2(tw.x, tw.y));
     const float2 c = c_mulc(make_float2(re.y, im.y), make_float2(tw.z, tw.w));
     if (k0 & 1) { o0[k0 / 2] = a; o1[k0 / 2] = c; }
@@ -174,16 +206,17 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
   DftReg<L0 / 2, true>::run(o0);
   DftReg<L0 / 2, true>::run(e1);
   DftReg<L0 / 2, true>::run(o1);
-  const float sgn = prm.partial ? -1.f : 1.f;  // causal keeps n0 < L0/2, partial n0 >= L0/2
-  float2 x0[L0 / 2], x1[L0 / 2];
+  // causal keeps n0 < L0/2 (lo), partial n0 >= L0/2 (hi), circular both
+  float2 x0[L0], x1[L0];
 #pragma unroll
   for (int m = 0; m < L0 / 2; ++m) {
     float2 w = w_root<L0>(m);
     w.y = -w.y;
-    w.x *= sgn;
-    w.y *= sgn;
-    x0[m] = c_add(e0[m], c_mul(o0[m], w));
-    x1[m] = c_add(e1[m], c_mul(o1[m], w));
+    const float2 t0 = c_mul(o0[m], w), t1 = c_mul(o1[m], w);
+    x0[m] = c_add(e0[m], t0);
+    x1[m] = c_add(e1[m], t1);
+    x0[m + L0 / 2] = c_sub(e0[m], t0);
+    x1[m + L0 / 2] = c_sub(e1[m], t1);
   }
   const float s = rsqrtf(float(L0));
   const int64_t b0 = 2 * p, b1 = 2 * p + 1;
@@ -198,10 +231,11 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
     r0 = (b0 * prm.H + h) * prm.N + n;
     r1 = (b1 * prm.H + h) * prm.N + n;
   }
-  {
-  #pragma unroll
-      for (int i0 = 0; i0 < L0 / 2; ++i0) {
-        const int n0 = i0;
+  auto emit = [&](auto q0c, auto noutc) {
+    constexpr int Q0 = decltype(q0c)::value, NOUT = decltype(noutc)::value;
+#pragma unroll
+    for (int i0 = 0; i0 < NOUT; ++i0) {
+      const int n0 = i0 + Q0;
       const int64_t o = int64_t(i0) * prm.Lp;
       float a0 = x0[n0].x * s, a1 = x1[n0].x * s;  // row b
       float c0 = x0[n0].y * s, c1 = x1[n0].y * s;  // row b+1
@@ -225,34 +259,84 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
       }
       st2<T>(y + r0 + o, a0, a1);
       if (has1) st2<T>(y + r1 + o, c0, c1);
-    }
-  }
+        }
+  };
+  if (prm.circ) emit(std::integral_constant<int, 0>{}, std::integral_constant<int, L0>{});
+  else if (prm.partial) emit(std::integral_constant<int, L0 / 2>{}, std::integral_constant<int, L0 / 2>{});
+  else emit(std::integral_constant<int, 0>{}, std::integral_constant<int, L0 / 2>{});
 }
 
-// k_f, step 1: per (head, column n'): DFT_L0 of k[n' + L' n0] (n0 < L0/2,
+// k_f, step 1: per (head, column n'): DFT_L0 of k[n' + Lrow n0] (n0 < L0/2,
 // K <= L/2), twiddle W_L^{n' k0}; fp32 scratch written into the head's k_f
-// blocks (block k0 holds the L' complex values of row k0, unpadded).
+// blocks: element (h, k0, n') lives in 2048-element block
+// (h L0 + k0) * (Lrow / 2048) + n' / 2048 at offset n' % 2048 (unpadded).
 template <int L0>
-__global__ void __launch_bounds__(256) mp_kf_cols_kernel(const KfParams prm, const float2* __restrict__ wbase,
-                                                         int Lp, size_t block_bytes) {
+__global__ void __launch_bounds__(256) mp_kf_cols_kernel(const KfParams prm, int64_t Lrow, int64_t Lfull,
+                                                         size_t block_bytes) {
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= prm.H * Lp) return;
-  const int n = int(idx % Lp);
-  const int64_t h = idx / Lp;
+  if (idx >= prm.H * Lrow) return;
+  const int64_t n = idx % Lrow;
+  const int64_t h = idx / Lrow;
   float2 z[L0];
 #pragma unroll
   for (int n0 = 0; n0 < L0; ++n0) {
-    const int64_t t = int64_t(n) + int64_t(n0) * Lp;
+    const int64_t t = n + int64_t(n0) * Lrow;
     z[n0] = make_float2(t < prm.K ? prm.k[h * prm.K + t] : 0.f, 0.f);
   }
   DftReg<L0, false>::run(z);
-  const float2 bw = wbase[n];
+  float sn, cs;
+  sincospif(-2.0f * float(n) / float(Lfull), &sn, &cs);  // exact dyadic argument
+  const float2 bw = make_float2(cs, sn);
   float2 tw = make_float2(1.f, 0.f);
-  uint8_t* base = reinterpret_cast<uint8_t*>(prm.kf) + h * L0 * block_bytes;
+  const int64_t nb = Lrow / 2048;
+  uint8_t* kf = reinterpret_cast<uint8_t*>(prm.kf);
 #pragma unroll
   for (int k0 = 0; k0 < L0; ++k0) {
-    reinterpret_cast<float2*>(base + k0 * block_bytes)[n] = c_mul(z[k0], tw);
+    const int64_t blk = (h * L0 + k0) * nb + n / 2048;
+    reinterpret_cast<float2*>(kf + blk * block_bytes)[n % 2048] = c_mul(z[k0], tw);
     tw = c_mul(tw, bw);
+  }
+}
+
+// Deeper levels, in place: rows of length Lrow = L0 * Lp (2048-element blocks
+// of block_bytes each); thread (row, n'') reads x[n'' + Lp m], m < L0, and
+// writes DFT_L0 (INV: inverse, unscaled) twiddled by W_Lrow^{+-n'' k0} at
+// k0 Lp + n'' -- the same addresses, so no other thread is touched.
+// Forward applies the twiddle after the DFT, inverse before it.
+template <int L0, bool INV>
+__global__ void __launch_bounds__(256) mp_cols_cplx_kernel(float2* data, int64_t rows, int64_t Lrow,
+                                                           size_t block_bytes) {
+  const int64_t Lp = Lrow / L0;
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= rows * Lp) return;
+  const int64_t n = idx % Lp, r = idx / Lp;
+  const int64_t nb = Lrow / 2048;
+  uint8_t* base = reinterpret_cast<uint8_t*>(data);
+  auto at = [&](int64_t e) -> float2* {
+    return reinterpret_cast<float2*>(base + (r * nb + e / 2048) * int64_t(block_bytes)) + (e % 2048);
+  };
+  float sn, cs;
+  sincospif((INV ? 2.0f : -2.0f) * float(n) / float(Lrow), &sn, &cs);
+  const float2 bw = make_float2(cs, sn);
+  float2 v[L0];
+  float2 tw = make_float2(1.f, 0.f);
+#pragma unroll
+  for (int m = 0; m < L0; ++m) {
+    v[m] = *at(n + Lp * m);
+    if (INV) {  // inverse: twiddle first (index m is k0 here)
+      v[m] = c_mul(v[m], tw);
+      tw = c_mul(tw, bw);
+    }
+  }
+  DftReg<L0, INV>::run(v);
+#pragma unroll
+  for (int m = 0; m < L0; ++m) {
+    float2 o = v[m];
+    if (!INV) {
+      o = c_mul(o, tw);
+      tw = c_mul(tw, bw);
+    }
+    *at(n + Lp * m) = o;
   }
 }
 
@@ -297,20 +381,49 @@ cudaError_t launch_mp_pass(const MpParams& prm, int pass, cudaStream_t s) {
   }
 }
 
-cudaError_t launch_mp_precompute_kf(const KfParams& prm, const float2* wbase, int L0, int Lp, size_t block_bytes,
+template <bool INV>
+static cudaError_t launch_cols_cplx(float2* data, int L0, int64_t rows, int64_t Lrow, size_t block_bytes,
                                     cudaStream_t s) {
-  if (prm.H <= 0) return cudaSuccess;
-  const unsigned grid = unsigned((prm.H * Lp + 255) / 256);
+  const unsigned grid = unsigned((rows * (Lrow / L0) + 255) / 256);
   switch (L0) {
-    case 2: mp_kf_cols_kernel<2><<<grid, 256, 0, s>>>(prm, wbase, Lp, block_bytes); break;
-    case 4: mp_kf_cols_kernel<4><<<grid, 256, 0, s>>>(prm, wbase, Lp, block_bytes); break;
-    case 8: mp_kf_cols_kernel<8><<<grid, 256, 0, s>>>(prm, wbase, Lp, block_bytes); break;
-    case 16: mp_kf_cols_kernel<16><<<grid, 256, 0, s>>>(prm, wbase, Lp, block_bytes); break;
+    case 2: mp_cols_cplx_kernel<2, INV><<<grid, 256, 0, s>>>(data, rows, Lrow, block_bytes); break;
+    case 4: mp_cols_cplx_kernel<4, INV><<<grid, 256, 0, s>>>(data, rows, Lrow, block_bytes); break;
+    case 8: mp_cols_cplx_kernel<8, INV><<<grid, 256, 0, s>>>(data, rows, Lrow, block_bytes); break;
+    case 16: mp_cols_cplx_kernel<16, INV><<<grid, 256, 0, s>>>(data, rows, Lrow, block_bytes); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mp_cols_inverse(float2* data, int L0, int64_t rows, int64_t Lrow, cudaStream_t s) {
+  return launch_cols_cplx<true>(data, L0, rows, Lrow, 2048 * sizeof(float2), s);
+}
+
+cudaError_t launch_mp_precompute_kf(const KfParams& prm, const int32_t* lev_L0, int nlev, int64_t Lfull,
+                                    size_t block_bytes, cudaStream_t s) {
+  if (prm.H <= 0) return cudaSuccess;
+  const int L0 = lev_L0[0];
+  const int64_t Lrow = Lfull / L0;
+  const unsigned grid = unsigned((prm.H * Lrow + 255) / 256);
+  switch (L0) {
+    case 2: mp_kf_cols_kernel<2><<<grid, 256, 0, s>>>(prm, Lrow, Lfull, block_bytes); break;
+    case 4: mp_kf_cols_kernel<4><<<grid, 256, 0, s>>>(prm, Lrow, Lfull, block_bytes); break;
+    case 8: mp_kf_cols_kernel<8><<<grid, 256, 0, s>>>(prm, Lrow, Lfull, block_bytes); break;
+    case 16: mp_kf_cols_kernel<16><<<grid, 256, 0, s>>>(prm, Lrow, Lfull, block_bytes); break;
     default: return cudaErrorInvalidValue;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_mp_kf_rows(prm, L0, Lp, block_bytes, s);
+  int64_t rows = prm.H * L0, Lr = Lrow;
+  for (int l = 1; l < nlev; ++l) {
+    e = launch_cols_cplx<false>(reinterpret_cast<float2*>(prm.kf), lev_L0[l], rows, Lr, block_bytes, s);
+    if (e != cudaSuccess) return e;
+    rows *= lev_L0[l];
+    Lr /= lev_L0[l];
+  }
+  int64_t L0tot = 1;
+  for (int l = 0; l < nlev; ++l) L0tot *= lev_L0[l];
+  return launch_mp_kf_rows(prm, int(L0tot), 2048, block_bytes, s);
 }
 
 }  // namespace fc

@@ -165,7 +165,8 @@ static void build_fused_tables(fftconv_plan_s* p, int64_t L) {
   t.wl = off;  t.wl_bytes = size_t(L) * 8;                  off = align_up(off + t.wl_bytes, 1024);
   const int64_t Lfull = p->L;  // the whole transform (== L unless multipass)
   t.wbase = off; t.wbase_bytes = Lfull != L ? size_t(L) * 8 : 0; off = align_up(off + t.wbase_bytes, 1024);
-  t.wtab = off;  t.wtab_bytes = Lfull != L ? size_t(Lfull) * 8 : 0; off = align_up(off + t.wtab_bytes, 1024);
+  t.wtab = off;  t.wtab_bytes = (Lfull != L && Lfull <= 32768) ? size_t(Lfull) * 8 : 0;
+  off = align_up(off + t.wtab_bytes, 1024);
   t.total = off;
   p->image.assign(t.total, 0);
   std::vector<uint8_t>& img = p->image;
@@ -221,7 +222,9 @@ static void build_fused_tables(fftconv_plan_s* p, int64_t L) {
       put_float(img, t.twt + r + (n1 & 1) * 4, wr);
       put_float(img, t.twt + r + 8 + (n1 & 1) * 4, wi);
     }
-  // full-length twiddles of the (inner) transform for the k_f precompute
+  // full-length twiddles of the (inner) transform for the k_f precompute;
+  // multipass outer twiddles only for a single outer level (deeper levels
+  // compute them on the fly)
   for (int64_t e = 0; e < L; ++e) {
     double wr, wi;
     root(e, L, &wr, &wi);
@@ -338,19 +341,31 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
     p->P = std::max(128 / p->L1, 2);
     build_fused_tables(p, L);
     p->Lp = int32_t(L);
-  } else if (io_ok && causal && L >= 4096 && L <= 32768 &&
-             (fft_size == 2 * N || (p->regime == REGIME_PARTIAL && N % (L / 2) == 0))) {
+  } else if (io_ok && causal && L >= 4096 && L <= (int64_t(1) << 23) &&
+             (fft_size == 2 * N || (p->regime == REGIME_PARTIAL && L <= 32768 && N % (L / 2) == 0))) {
     // multipass; the partial regime (K <= L/2 < N) runs the same passes on
-    // overlap-save windows of length L (A12)
+    // overlap-save windows of length L (A12).  L / 2048 is split
+    // into outer levels of at most 16 (recursive Alg. 4).
     if (p->regime != REGIME_PARTIAL) p->regime = REGIME_MULTIPASS;
-    p->order = 3;
     p->Lp = 2048;
     p->L0 = int32_t(L / 2048);
+    int r = ilog2(L / 2048);
+    p->nlev = (r + 3) / 4;
+    for (int l = 0; l < p->nlev; ++l) {
+      const int el = r / p->nlev + (l < r % p->nlev ? 1 : 0);
+      p->lev_L0[l] = 1 << el;
+    }
+    p->order = 2 + p->nlev;
     p->L2 = 64;
     p->L1 = 32;
     p->KA = 64;  // the inner transform is circular over complex rows
     p->P = 4;
     build_fused_tables(p, p->Lp);
+    if (sparsity && p->nlev > 1) {
+      delete p;
+      set_last_error("fftconv_plan: frequency-sparse plans support fft_size <= 32768 in this build");
+      return FFTCONV_ERR_UNSUPPORTED;
+    }
   } else {
     delete p;
     set_last_error("fftconv_plan: this build supports fp16/bf16 I/O with fft_size 512..2048 (fused; causal "
@@ -400,9 +415,10 @@ extern "C" fftconv_status_t fftconv_plan_info(fftconv_plan_t p, fftconv_plan_inf
   info->regime = p->regime;
   info->order = p->order;
   if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
-    info->factors[0] = p->L0;
-    info->factors[1] = p->L1;
-    info->factors[2] = p->L2;
+    int i = 0;
+    for (int l = 0; l < p->nlev && i < 2; ++l) info->factors[i++] = p->lev_L0[l];
+    info->factors[i++] = p->L1;
+    info->factors[i++] = p->L2;
   } else {
     info->factors[0] = p->L1;
     info->factors[1] = p->L2;

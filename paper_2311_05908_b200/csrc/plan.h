@@ -42,7 +42,9 @@ struct fftconv_plan_s {
   int32_t KA = 0;          // contracted length of stage A (L2/2 causal, L2 circular)
   int32_t P = 0;           // row pairs per tile (two-row real packing)
   int64_t chunk = 0;       // partial regime: chunk length (= L/2)
-  int32_t L0 = 1;          // multipass: outer factor, L = L0 * Lp
+  int32_t L0 = 1;          // multipass: total outer factor, L = L0 * Lp
+  int32_t nlev = 0;        // multipass: outer levels (L0 = prod lev_L0)
+  int32_t lev_L0[4] = {1, 1, 1, 1};
   int32_t Lp = 0;          // multipass: inner (fused) transform length
   fc::TableLayout tl;
   std::vector<uint8_t> image;  // host copy of the table image

@@ -164,3 +164,34 @@ def test_fwd_multipass_cfg3_shape_sampled():
             got.append(y[r, i])
     got, ref = np.array(got), np.array(ref)
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < REL_L2
+
+
+# ---------------------------------------------------------------- recursive multipass (N >= 32768)
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [32768, 262144])
+@pytest.mark.parametrize("dtype,gated", [("f16", False), ("bf16", True)])
+def test_fwd_multilevel_parity(N, dtype, gated):
+    got, ref = _run(N, True, dtype, gated, B=2, H=1)
+    _assert_close(got, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [1 << 20, 1 << 22])
+def test_fwd_multilevel_sampled(N):
+    """N = 1M and 4M (three outer levels): sampled outputs vs direct sums."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    B, H = 2, 2
+    plan = FFTConvPlan(N, dtype=torch.float16)
+    u = synth.quantize(synth.signal(9, "u", B, H, N), "f16")
+    k = synth.decay_filters(9, H, N).astype(np.float32)
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    y = plan.fwd(torch.tensor(u, dtype=torch.float16, device="cuda"), kf).float().cpu().numpy()
+    rng = np.random.default_rng(9)
+    got, ref = [], []
+    for b in range(B):
+        for h in range(H):
+            for i in list(rng.choice(N, 5, replace=False)) + [0, N - 1]:
+                ref.append(orc.direct_point(u[b, h], k[h].astype(np.float64), int(i)))
+                got.append(y[b, h, i])
+    got, ref = np.array(got), np.array(ref)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < REL_L2
