@@ -142,7 +142,7 @@ def _mix_t(x):
     return x
 
 
-def normal_torch(seed: int, tensor: int, row0: int, nrows: int, n: int, device, chunk_rows: int = 4096):
+def normal_torch(seed: int, tensor: int, row0: int, nrows: int, n: int, device, chunk_elems: int = 1 << 25):
     """Same counter-based N(0,1) stream as normal(), generated with int64
     torch ops on `device` (values agree with numpy up to the last bits of
     log/cos); returns float32 (nrows, n)."""
@@ -151,21 +151,30 @@ def normal_torch(seed: int, tensor: int, row0: int, nrows: int, n: int, device, 
     base = _to_i64((seed * 0x9E3779B97F4A7C15 + tensor * 0xD1B54A32D192ED03) % (1 << 64))
     cr = _to_i64(0x8CB92BA72F3D8DD7)
     alt = _to_i64(0xA0761D6478BD642F)
-    cols = torch.arange(n, dtype=torch.int64, device=device)
-    for r0 in range(0, nrows, chunk_rows):
-        r1 = min(nrows, r0 + chunk_rows)
+    cols_per = max(1, min(n, chunk_elems))
+    rows_per = max(1, chunk_elems // n)
+    for r0 in range(0, nrows, rows_per):
+        r1 = min(nrows, r0 + rows_per)
         rows = torch.arange(row0 + r0, row0 + r1, dtype=torch.int64, device=device)
-        k = base + rows[:, None] * cr + cols[None, :]
-        h1 = _mix_t(k)
-        h2 = _mix_t(k ^ alt)
-        u1 = (((h1 >> 11) & ((1 << 53) - 1)).double() + 1.0) * (1.0 / 9007199254740992.0)
-        u2 = ((h2 >> 11) & ((1 << 53) - 1)).double() * (1.0 / 9007199254740992.0)
-        out[r0:r1] = (torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(2.0 * np.pi * u2)).float()
+        for c0 in range(0, n, cols_per):
+            c1 = min(n, c0 + cols_per)
+            cols = torch.arange(c0, c1, dtype=torch.int64, device=device)
+            k = base + rows[:, None] * cr + cols[None, :]
+            h1 = _mix_t(k)
+            h2 = _mix_t(k ^ alt)
+            u1 = (((h1 >> 11) & ((1 << 53) - 1)).double() + 1.0) * (1.0 / 9007199254740992.0)
+            u2 = ((h2 >> 11) & ((1 << 53) - 1)).double() * (1.0 / 9007199254740992.0)
+            out[r0:r1, c0:c1] = (torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(2.0 * np.pi * u2)).float()
     return out
 
 
 def signal_torch(seed: int, name: str, B: int, H: int, N: int, device, dtype, row0: int = 0):
     """(B, H, N) tensor of the given torch dtype on device; rows row0.. of the
     global (b*H + h) numbering (row0 lets ranks generate their own shard)."""
-    x = normal_torch(seed, TENSOR_IDS[name], row0, B * H, N, device)
-    return x.reshape(B, H, N).to(dtype)
+    import torch
+    out = torch.empty(B * H, N, dtype=dtype, device=device)
+    step = max(1, (1 << 27) // N)  # rows per fp32 staging chunk
+    for r in range(0, B * H, step):
+        r1 = min(B * H, r + step)
+        out[r:r1] = normal_torch(seed, TENSOR_IDS[name], row0 + r, r1 - r, N, device).to(dtype)
+    return out.reshape(B, H, N)
