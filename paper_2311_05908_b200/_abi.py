@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfftconv.so")
+LIB_PATH = os.environ.get("FFTCONV_LIB", os.path.join(HERE, "libfftconv.so"))  # override: experiments only
 
 FFTCONV_F16, FFTCONV_BF16, FFTCONV_F32 = 0, 1, 2
 STATUS = {
