@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_slot;
+  const uint32_t tmem = warp_uniform(tmem_slot);
   const uint32_t tq = tmem + (uint32_t(quad * 32) << 16);
   uint32_t phase = 0;
   int64_t cur_h = -1;
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
     fence_async_smem();
     tc_fence_before();
     __syncthreads();
-    if (tid == 0) {
+    if (tid < 32 && elect_one()) {
       tc_fence_after();
       issue_half(0);
       mma_commit(&mma_bar[0]);
@@ -183,17 +183,12 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
 
   // ---- forward stages A, twiddle, B of one spectrum into TMEM columns [rb, rb + 256)
   auto forward_AB = [&](uint32_t rb) {
-    sync_and_issue([&](int hh) {
-      constexpr uint32_t idesc = idesc_f16(128, L2 / 2, true, false);
+    sync_and_issue([&](int hh) {  // TMEM column of (block, k2): (k2 / 32) * NA/2 + 32 * block + k2 % 32
+      constexpr uint32_t idesc = idesc_f16(128, C::NA / 2, true, false);
 #pragma unroll
-      for (int s = 0; s < 2 * C::KA / 16; ++s) {
-        const uint64_t ad = dadd(dXA, 256 * s);
-#pragma unroll
-        for (int blk = 0; blk < C::NA / L2; ++blk) {
-          const uint32_t row0 = blk * L2 + hh * (L2 / 2);
-          mma_f16_ss(tmem + rb + row0, ad, dadd(dGA, (row0 / 8) * C::SBO_GA + 256 * s), idesc, s > 0);
-        }
-      }
+      for (int s = 0; s < 2 * C::KA / 16; ++s)
+        mma_f16_ss(tmem + rb + hh * (C::NA / 2), dadd(dXA, 256 * s),
+                   dadd(dGA, hh * (C::NA / 16) * C::SBO_GA + 256 * s), idesc, s > 0);
     });
     {
       const int p = m / L1, n1 = m % L1;
@@ -201,10 +196,11 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
 #pragma unroll 1
       for (int sub = 0; sub < 2; ++sub) {
         const int k20 = slice * 32 + sub * 16;
+        const uint32_t c0 = rb + slice * (C::NA / 2) + sub * 16;
         float re[16], im[16], ni[16];
-        tmem_ld16(tq + rb + k20, re);
-        tmem_ld16(tq + rb + L2 + k20, im);
-        if constexpr (C::NEG_A) tmem_ld16(tq + rb + 2 * L2 + k20, ni);
+        tmem_ld16(tq + c0, re);
+        tmem_ld16(tq + c0 + 32, im);
+        if constexpr (C::NEG_A) tmem_ld16(tq + c0 + 64, ni);
         float4 w[8];
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) w[jj] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1, k20 / 2 + jj));

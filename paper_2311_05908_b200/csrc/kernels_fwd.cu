@@ -42,6 +42,11 @@
 
 namespace fc {
 
+#ifdef FC_TRACE
+// experiment-only phase timestamps (CTA 0, warpgroup 0, warps 0 and 4)
+__device__ long long fc_trace_buf[2][64][16];
+#endif
+
 // Each CTA runs kWG independent warpgroups; warpgroup g processes tiles
 // t0 + g, t0 + g + kWG, ... of the CTA's contiguous tile range, with its own
 // TMEM columns, mbarriers, named barrier, k_f copy and operand buffer, so one
@@ -60,7 +65,7 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
                  sGAI = base + C::OFF_GAI, sTW = base + C::OFF_TW, sTWT = base + C::OFF_TWT;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wg = warp >> 3;              // warpgroup
+  const int wg = int(warp_uniform(warp >> 3));  // warpgroup
   const int wtid = tid & (kWGThreads - 1);
   const int quad = warp & 3;             // TMEM lane quadrant this warp may access
   const int slice = (warp >> 2) & 1;     // column slice 0..1
@@ -102,7 +107,7 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_slot + wg * C::TMEM_COLS;
+  const uint32_t tmem = warp_uniform(tmem_slot) + wg * C::TMEM_COLS;
   const uint32_t tq = tmem + (uint32_t(quad * 32) << 16);  // this warp's lane quadrant
   uint64_t* bars = mma_bar[wg];
   const uint32_t bar_id = 1 + wg;  // named barrier of this warpgroup
@@ -120,6 +125,14 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
   const uint64_t dXAI = smem_desc(bufX, 128, C::SBO_XA);        // stage A^-1 operand (MN-major B)
   auto dadd = [](uint64_t d, uint32_t off) { return d + uint64_t(off >> 4); };
 
+  int trace_tile = 0;
+  auto stamp = [&](int k) {
+#ifdef FC_TRACE
+    if (blockIdx.x == 0 && wg == 0 && (wtid == 0 || wtid == 128) && trace_tile < 64)
+      fc_trace_buf[wtid >> 7][trace_tile][k] = clock64();
+#endif
+  };
+  int stage_no = 0;
   auto wg_sync = [&] { named_sync(bar_id, kWGThreads); };
   // Operands written -> warpgroup barrier -> one thread issues the stage as
   // two halves, each committed to its own mbarrier so the epilogue of the
@@ -128,13 +141,16 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
     fence_async_smem();
     tc_fence_before();
     wg_sync();
-    if (wtid == 0) {
+    stamp(2 + 3 * stage_no);
+    if (wtid < 32 && elect_one()) {
       tc_fence_after();
       issue_half(0);
       mma_commit(&bars[0]);
       issue_half(1);
       mma_commit(&bars[1]);
     }
+    stamp(3 + 3 * stage_no);
+    ++stage_no;
     phase ^= 1;  // both barriers complete once per stage
   };
   auto wait_half = [&](int hh) {  // parity of the stage issued last
@@ -205,6 +221,8 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
   int64_t hh = (t0 + wg) / nbt, bt = (t0 + wg) % nbt;
   for (int64_t t = t0 + wg; t < t1; t += kWG, bt += kWG) {
     while (bt >= nbt) { bt -= nbt; ++hh; }
+    stage_no = 0;
+    stamp(0);
     const int64_t h = phys_head(hh);
     const int64_t tile_base = (bt * C::R * H + h) * N;  // element offset of row (bt*R, h)
     const int rows_left = int(B - bt * C::R < C::R ? B - bt * C::R : C::R);
@@ -256,20 +274,16 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
     }
     }
     if (new_h) cp_async_wait_all();
+    stamp(1);
 
     // ---------------- stage A: D[(p,n1)][(re|im|-im, k2)] = X[(p,n1)][(c,n2)] * G_A
-    sync_and_issue([&](int hh) {  // half hh: k2 in [32 hh, 32 hh + 32) of each block
-      constexpr uint32_t idesc = idesc_f16(128, L2 / 2, true, false);
+    // TMEM column of (block, k2): (k2 / 32) * NA/2 + 32 * block + k2 % 32
+    sync_and_issue([&](int hh) {  // half hh: k2 in [32 hh, 32 hh + 32) of every block, one MMA per K step
+      constexpr uint32_t idesc = idesc_f16(128, C::NA / 2, true, false);
 #pragma unroll
-      for (int s = 0; s < 2 * C::KA / 16; ++s) {
-        const uint64_t ad = dadd(dXA, 256 * s);
-#pragma unroll
-        for (int blk = 0; blk < C::NA / L2; ++blk) {
-          const uint32_t row0 = blk * L2 + hh * (L2 / 2);
-          const uint64_t bd = dadd(dGA, (row0 / 8) * C::SBO_GA + 256 * s);
-          mma_f16_ss(tmem + row0, ad, bd, idesc, s > 0);
-        }
-      }
+      for (int s = 0; s < 2 * C::KA / 16; ++s)
+        mma_f16_ss(tmem + hh * (C::NA / 2), dadd(dXA, 256 * s),
+                   dadd(dGA, hh * (C::NA / 16) * C::SBO_GA + 256 * s), idesc, s > 0);
     });
 
     // ---------------- epilogue 1: twiddle W^{n1 k2}, transpose -> stage B operand (MN-major)
@@ -282,10 +296,11 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
 #pragma unroll 1
       for (int sub = 0; sub < 2; ++sub) {
         const int k20 = slice * 32 + sub * 16;  // 16 k2 per item
+        const uint32_t c0 = slice * (C::NA / 2) + sub * 16;
         float re[16], im[16], ni[16];
-        tmem_ld16(tq + k20, re);
-        tmem_ld16(tq + L2 + k20, im);
-        if constexpr (C::NEG_A) tmem_ld16(tq + 2 * L2 + k20, ni);
+        tmem_ld16(tq + c0, re);
+        tmem_ld16(tq + c0 + 32, im);
+        if constexpr (C::NEG_A) tmem_ld16(tq + c0 + 64, ni);
         float4 w[8];
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) w[jj] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1, k20 / 2 + jj));
@@ -306,6 +321,7 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
       }
     }
 
+    stamp(4);
     // ---------------- stage B: per group of 128 rows (p,k2), contract n1 -> k1
     sync_and_issue([&](int hh) {
       constexpr uint32_t idesc = idesc_f16(128, C::NB, true, false);
@@ -345,6 +361,7 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
       }
     }
 
+    stamp(7);
     // ---------------- stage B^-1: contract k1 -> n1
     sync_and_issue([&](int hh) {
       constexpr uint32_t idesc = idesc_f16(128, C::NB, false, false);
@@ -385,6 +402,7 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
       }
     }
 
+    stamp(10);
     // ---------------- stage A^-1: D[(c',n2)][(p,n1)] = G_A^-1 * X[(c,k2)][(p,n1)]
     sync_and_issue([&](int hh) {  // half hh: output columns (p, n1) in [64 hh, 64 hh + 64)
       constexpr uint32_t idesc = idesc_f16(128, 64, false, true);
@@ -467,8 +485,11 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
         }
       }
     }
+    stamp(13);
     tc_fence_before();
     wg_sync();  // TMEM columns and bufX are reused by the next tile
+    stamp(14);
+    ++trace_tile;
     prefetched = PF && (t + kWG < t1);
   }
   __syncthreads();
@@ -516,3 +537,9 @@ cudaError_t launch_fwd_fused(const FwdParams& prm, cudaStream_t s) {
 }
 
 }  // namespace fc
+
+#ifdef FC_TRACE
+extern "C" int fc_trace_dump(long long* host) {
+  return int(cudaMemcpyFromSymbol(host, fc::fc_trace_buf, sizeof(fc::fc_trace_buf)));
+}
+#endif

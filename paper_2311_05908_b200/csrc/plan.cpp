@@ -142,7 +142,7 @@ static void put_float(std::vector<uint8_t>& img, size_t off, double x) {
 }
 
 // Table image of the fused order-2 kernel (kernels_fwd.cu, O2Cfg):
-//  GA  : stage A B-operand, K-major rows (re|im|-im, k2) = 3*L2, K (c,n2) = 2*KA
+//  GA  : stage A B-operand, K-major rows (k2 half, re|im|-im, k2 mod 32) = 3*L2, K (c,n2) = 2*KA
 //  GB  : stage B B-operand, rows (re|im|-im|pad, k1) = NB, K (c,n1) = 2*L1
 //  GBI : stage B^-1, rows (re|im|-re|pad, n1) = NB, K (c,k1) = 2*L1
 //  GAI : stage A^-1 A-operand, rows (c',n2) = 2*L2, K (c,k2) = 2*L2
@@ -180,7 +180,9 @@ static void build_fused_tables(fftconv_plan_s* p, int64_t L) {
           root(int64_t(n2) * k2, L2, &fr, &fi);
           const int co = blk == 0 ? 0 : 1;
           const double sgn = blk == 2 ? -1.0 : 1.0;
-          put_half(img, t.ga + kmajor_off(blk * L2 + k2, ci * KA + n2, 2 * KA),
+          // rows ordered (k2 half, blk, k2 mod 32): each stage-A half is one MMA
+          const int row = (k2 / 32) * (NA / 2) + blk * 32 + k2 % 32;
+          put_half(img, t.ga + kmajor_off(row, ci * KA + n2, 2 * KA),
                    sgn * realpair(fr * sA, fi * sA, ci, co));
         }
   // stage B (forward, contracts n1 -> k1; blocks re | im | -im) and

@@ -5,7 +5,8 @@
 // in the SWIZZLE_NONE canonical layout selected by a_mn / b_mn, issues
 // K/16 tcgen05.mma.kind::f16 instructions accumulating into TMEM, and reads
 // D (M x N fp32) back with tcgen05.ld.  Used by tests/test_gpu_primitives.py
-// to pin the descriptor encodings against a host matmul.
+// to pin the descriptor encodings against a host matmul, including the A-in-TMEM
+// (ts) form and the M = 64 lane layout.
 #include <cuda_runtime.h>
 #include "sm100.cuh"
 
@@ -22,17 +23,20 @@ __device__ uint32_t canon_off(int r, int k, int R, int K, bool mn_major) {
   }
 }
 
-__global__ void __launch_bounds__(128, 1)
-    mma_selftest_kernel(const __half* A, const __half* B, float* D, int M, int N, int K, int a_mn, int b_mn) {
+__global__ void __launch_bounds__(128, 1) mma_selftest_kernel(const __half* A, const __half* B, float* D, int M,
+                                                                 int N, int K, int a_mn, int b_mn, int a_tmem,
+                                                                 int d_lane) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base;
   uint8_t* sA = smem;
   uint8_t* sB = smem + M * K * 2;
   const int tid = threadIdx.x;
-  for (int i = tid; i < M * K; i += blockDim.x) {
-    int m = i / K, k = i % K;
-    *reinterpret_cast<__half*>(sA + canon_off(m, k, M, K, a_mn)) = A[i];
+  if (!a_tmem) {
+    for (int i = tid; i < M * K; i += blockDim.x) {
+      int m = i / K, k = i % K;
+      *reinterpret_cast<__half*>(sA + canon_off(m, k, M, K, a_mn)) = A[i];
+    }
   }
   for (int i = tid; i < K * N; i += blockDim.x) {
     int k = i / N, n = i % N;
@@ -42,12 +46,29 @@ __global__ void __launch_bounds__(128, 1)
     fc::mbar_init(&bar, 1);
     fc::fence_barrier_init();
   }
-  if (tid < 32) fc::tmem_alloc<256>(&tmem_base);
+  if (tid < 32) fc::tmem_alloc<512>(&tmem_base);
   fc::fence_async_smem();
   fc::tc_fence_before();
   __syncthreads();
   fc::tc_fence_after();
   const uint32_t tbase = tmem_base;
+  const int warp = tid / 32;
+  const uint32_t a_col = 256;  // A operand columns when staged in TMEM
+  if (a_tmem) {                // row m in lane m (M == 128), two fp16 per column
+    for (int c = 0; c < K / 2; c += 4) {
+      uint32_t v[4];
+      for (int j = 0; j < 4; ++j) {
+        __half2 h = __halves2half2(A[tid * K + 2 * (c + j)], A[tid * K + 2 * (c + j) + 1]);
+        v[j] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      fc::tmem_st4(tbase + ((uint32_t)(warp * 32) << 16) + a_col + c, v[0], v[1], v[2], v[3]);
+    }
+    fc::tmem_st_wait();
+    fc::tc_fence_before();
+    __syncthreads();
+    fc::tc_fence_after();
+  }
+  const uint32_t dt = tbase + ((uint32_t)d_lane << 16);
   if (tid == 0) {
     const uint32_t idesc = fc::idesc_f16(M, N, a_mn, b_mn);
     const uint32_t a0 = fc::smem_u32(sA), b0 = fc::smem_u32(sB);
@@ -57,31 +78,43 @@ __global__ void __launch_bounds__(128, 1)
       else      ad = fc::smem_desc(a0 + s * 256, 128, (K / 8) * 128);
       if (b_mn) bd = fc::smem_desc(b0 + 2 * s * (N / 8) * 128, (N / 8) * 128, 128);
       else      bd = fc::smem_desc(b0 + s * 256, 128, (K / 8) * 128);
-      fc::mma_f16_ss(tbase, ad, bd, idesc, s > 0);
+      if (a_tmem) fc::mma_f16_ts(dt, tbase + a_col + 8 * s, bd, idesc, s > 0);
+      else        fc::mma_f16_ss(dt, ad, bd, idesc, s > 0);
     }
     fc::mma_commit(&bar);
   }
   fc::mbar_wait(&bar, 0);
   fc::tc_fence_after();
-  const int warp = tid / 32;
+  // D row r: lane r (M == 128); lane 32 (r / 16) + r % 16 + d_lane (M == 64)
+  const int lane = tid % 32;
+  int row = -1;
+  if (M == 128) row = tid;
+  else if (lane >= d_lane && lane < d_lane + 16) row = warp * 16 + lane - d_lane;
   for (int c = 0; c < N; c += 8) {
     float v[8];
     fc::tmem_ld8(tbase + ((uint32_t)(warp * 32) << 16) + c, v);
     fc::tmem_ld_wait();
-    for (int j = 0; j < 8; ++j) D[tid * N + c + j] = v[j];
+    if (row >= 0)
+      for (int j = 0; j < 8; ++j) D[row * N + c + j] = v[j];
   }
   fc::tc_fence_before();
   __syncthreads();
-  if (tid < 32) fc::tmem_dealloc<256>(tbase);
+  if (tid < 32) fc::tmem_dealloc<512>(tbase);
 }
 
 }  // namespace
 
-extern "C" int fcst_mma(const void* A, const void* B, void* D, int M, int N, int K, int a_mn, int b_mn) {
-  if (M != 128 || N % 16 || N < 16 || N > 256 || K % 16) return 1;
+// M in {64, 128}; a_tmem: A staged in TMEM (M == 128 only); d_lane: TMEM lane
+// offset of D (0 or 16, M == 64 only).
+extern "C" int fcst_mma(const void* A, const void* B, void* D, int M, int N, int K, int a_mn, int b_mn, int a_tmem,
+                        int d_lane) {
+  if ((M != 128 && M != 64) || N % 16 || N < 16 || N > 256 || K % 16 || K > 128) return 1;
+  if (a_tmem && (M != 128 || a_mn)) return 1;
+  if (M == 128 && d_lane) return 1;
   size_t smem = (size_t)(M + N) * K * 2;
   cudaFuncSetAttribute(mma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  mma_selftest_kernel<<<1, 128, smem>>>((const __half*)A, (const __half*)B, (float*)D, M, N, K, a_mn, b_mn);
+  mma_selftest_kernel<<<1, 128, smem>>>((const __half*)A, (const __half*)B, (float*)D, M, N, K, a_mn, b_mn, a_tmem,
+                                        d_lane);
   cudaError_t e = cudaDeviceSynchronize();
   return e == cudaSuccess ? 0 : 100 + (int)e;
 }
