@@ -57,34 +57,32 @@ struct O2Cfg {
   static constexpr int KA = CAUSAL ? L2 / 2 : L2;
   static constexpr int NOUT = CAUSAL ? L / 2 : L;  // row length N
   static constexpr int CH = NOUT / 8;           // 16-byte chunks per row (16-bit I/O)
-  // stage A N: re | im | -im (causal); circular drops the -im block (its
-  // larger K makes the table too big for two warpgroups) and negates in registers
-  static constexpr bool NEG_A = CAUSAL;
-  static constexpr int NA = (NEG_A ? 3 : 2) * L2;
+  // stage A N: re | im (the -im plane is negated in registers)
+  static constexpr bool NEG_A = false;
+  static constexpr int NA = 2 * L2;
   static constexpr int NB = (3 * L1 + 15) / 16 * 16;  // stage B/B^-1 N: re | im | -im (-re) | pad
-  // tables (same offsets as the host image, see plan.cpp)
+  // table image (same offsets as plan.cpp): GA | GB | GBI | TW | GAI | TWT.
+  // The forward kernel copies the prefix through GAI's first GAI_FWD bytes
+  // (causal: the rows n2 < L2/2 only); the backward copies everything.
   static constexpr uint32_t GA_BYTES = NA * 2 * KA * 2;
   static constexpr uint32_t GB_BYTES = NB * 2 * L1 * 2;
   static constexpr uint32_t GAI_BYTES = 2 * L2 * 2 * L2 * 2;
+  static constexpr uint32_t GAI_FWD_BYTES = (CAUSAL ? L2 : 2 * L2) * 2 * L2 * 2;
   static constexpr uint32_t TW_BYTES = L1 * (L2 / 2 * 16 + 16);    // padded rows, see layout.h
   static constexpr uint32_t TWT_BYTES = L2 * (L1 / 2 * 16 + 16);
   static constexpr uint32_t al(uint32_t x) { return (x + 1023u) / 1024u * 1024u; }
   static constexpr uint32_t OFF_GA = 0;
   static constexpr uint32_t OFF_GB = al(OFF_GA + GA_BYTES);
   static constexpr uint32_t OFF_GBI = al(OFF_GB + GB_BYTES);
-  static constexpr uint32_t OFF_GAI = al(OFF_GBI + GB_BYTES);
-  static constexpr uint32_t OFF_TW = al(OFF_GAI + GAI_BYTES);   // [n1][k2/2] {wr,wr',wi,wi'}
-  static constexpr uint32_t OFF_TWT = al(OFF_TW + TW_BYTES);    // [k2][n1/2] {wr,wr',wi,wi'}
+  static constexpr uint32_t OFF_TW = al(OFF_GBI + GB_BYTES);    // [n1][k2/2] {wr,wr',wi,wi'}
+  static constexpr uint32_t OFF_GAI = al(OFF_TW + TW_BYTES);
+  static constexpr uint32_t OFF_TWT = al(OFF_GAI + GAI_BYTES);  // [k2][n1/2] {wr,wr',wi,wi'}
   static constexpr uint32_t TABLES = al(OFF_TWT + TWT_BYTES);
+  static constexpr uint32_t TABLES_FWD = al(OFF_GAI + GAI_FWD_BYTES);
   // per-warpgroup working buffers
   static constexpr uint32_t KF_BYTES = L2 * (L1 / 2 * 16 + 16); // [k2][k1/2] {kr,kr',ki,ki'}, padded rows
   static constexpr uint32_t BUFX_BYTES = P * L * 4;            // complex fp16 per tile (stage A operand aliases it)
   static constexpr uint32_t WG_BYTES = al(KF_BYTES) + al(BUFX_BYTES);
-  static constexpr uint32_t OFF_WG = TABLES;
-  // two independent tile pipelines when both fit in shared memory, else one
-  static constexpr int WG = (OFF_WG + 2 * WG_BYTES + 1024 <= 227 * 1024) ? 2 : 1;
-  static constexpr int THREADS = WG * kWGThreads;
-  static constexpr uint32_t SMEM = OFF_WG + WG * WG_BYTES + 1024;  // + alignment slack
   // operand strides
   static constexpr uint32_t SBO_A = (2 * KA / 8) * 128;   // stage A operand: MN-group stride (K groups contiguous)
   static constexpr uint32_t LBO_B = (P * L2 / 8) * 128;   // epi1 -> stage B (MN-major, K-group stride)
@@ -94,11 +92,16 @@ struct O2Cfg {
   static constexpr uint32_t SBO_GAI = (2 * L2 / 8) * 128;
   static constexpr uint32_t SBO_XA = (2 * L2 / 8) * 128;  // epi3 -> stage A^-1 (MN-major B, N-group stride)
   static constexpr uint32_t TMEM_COLS = 256;              // per warpgroup
+  // stage B^-1 reads its data operand from TMEM (epilogue 2 writes it into
+  // its own lanes: 2*L1 fp16 = L1 columns per 128-row group) when those
+  // columns fit beside stage B's accumulators; else from shared memory
+  static constexpr uint32_t TS_COLS = (P / 2) * L1;
+  static constexpr bool TS_BI = (P / 2) * NB + TS_COLS <= TMEM_COLS;
+  static constexpr uint32_t CA = TMEM_COLS - TS_COLS;     // first column of that operand
   static_assert(P * L1 == 128, "stage A covers one 128-row MMA group");
   static_assert(P % 4 == 0, "stage B halves hold whole groups of two pairs");
   static_assert((P / 2) * NB <= 256 && NA <= 256, "TMEM budget");
   static_assert(128 * 2 * KA * 2 <= BUFX_BYTES, "stage A operand fits in bufX");
-  static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
 FC_DEVICE void st_half8(uint32_t addr, const float* v) {

@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
   const int64_t HN = H * N;
   const int ld_n2 = tid % KROWS, ld_j = (tid / KROWS) % JC, ld_r0 = tid / (KROWS * JC);
   const int64_t ld_off0 = int64_t(ld_r0) * HN + int64_t(ld_n2 * JC + ld_j) * 8;
-  const int64_t st_off0 = int64_t(m >> 6) * HN + int64_t(L1) * (m & 63);
+  // stage A^-1 output lane m = G_AI row (n2 half, c', n2 mod 32), see plan.cpp
+  const int64_t st_off0 = int64_t((m >> 5) & 1) * HN + int64_t(L1) * ((m >> 6) * 32 + (m & 31));
 
   auto chunk_dst = [&](int r, int n2, int j) -> uint32_t {
     const int k = (r & 1) * C::KA + n2;
@@ -278,8 +279,8 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
 
   // ---- epilogue 4 variants: out1 = o * a1 (or o), out2 = o * a2 (optional)
   auto epi_out = [&](int64_t tile_base, int rows_left, const T* a1, T* out1, const T* a2, T* out2, bool gate) {
-    const int cp = m >> 6;
-    if (!CAUSAL || (m & 63) < L2 / 2) {
+    const int cp = (m >> 5) & 1;
+    if (!CAUSAL || m < 64) {  // warp-uniform
       constexpr int NIT = C::P * (L1 / 8);
       constexpr int PER = NIT / 2;
       wait_half(slice);

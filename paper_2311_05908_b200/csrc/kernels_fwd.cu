@@ -47,22 +47,52 @@ namespace fc {
 __device__ long long fc_trace_buf[2][64][16];
 #endif
 
+// Shared-memory plan of the forward kernel: tables | per-warpgroup (k_f,
+// operand buffer) | input staging.  Causal tiles stage their input rows
+// (u [| w]) and the output gate v through one slot each, filled by bulk
+// (TMA) copies a tile ahead and shared by the warpgroups in tile order.
+template <int L1, bool CAUSAL, bool GATED>
+struct FwdCfg {
+  using C = O2Cfg<L1, CAUSAL>;
+  static constexpr bool STG = CAUSAL;
+  static constexpr uint32_t ROW_BYTES = C::NOUT * 2;  // one 16-bit input row
+  static constexpr uint32_t UW_BYTES = STG ? C::R * ROW_BYTES * (GATED ? 2 : 1) : 0;
+  static constexpr uint32_t V_BYTES = (STG && GATED) ? C::R * ROW_BYTES : 0;
+  static constexpr uint32_t bytes_for(int wg) {
+    return C::al(C::al(C::TABLES_FWD + wg * C::WG_BYTES) + UW_BYTES) + V_BYTES + 1024;  // + alignment slack
+  }
+  static constexpr int WG = bytes_for(2) <= 227 * 1024 ? 2 : 1;
+  static constexpr int THREADS = WG * kWGThreads;
+  static constexpr uint32_t OFF_WG = C::TABLES_FWD;
+  static constexpr uint32_t OFF_UW = C::al(OFF_WG + WG * C::WG_BYTES);
+  static constexpr uint32_t OFF_V = C::al(OFF_UW + UW_BYTES);
+  static constexpr uint32_t SMEM = bytes_for(WG);
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
+
 // Each CTA runs kWG independent warpgroups; warpgroup g processes tiles
 // t0 + g, t0 + g + kWG, ... of the CTA's contiguous tile range, with its own
 // TMEM columns, mbarriers, named barrier, k_f copy and operand buffer, so one
 // warpgroup's MMAs, memory waits and barriers overlap the other's math.
 template <int L1, bool CAUSAL, bool GATED, typename T>
-__global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_kernel(const FwdParams prm) {
+__global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv_fwd_o2_kernel(const FwdParams prm) {
   using C = O2Cfg<L1, CAUSAL>;
-  constexpr int kWG = C::WG;
-  constexpr int kThreads = C::THREADS;
+  using F = FwdCfg<L1, CAUSAL, GATED>;
+  constexpr int kWG = F::WG;
+  constexpr int kThreads = F::THREADS;
+  constexpr bool STG = F::STG;      // input staging by bulk copies
   constexpr int L2 = C::L2;
+  constexpr bool TS = C::TS_BI;     // stage B^-1 data operand in TMEM
+  constexpr bool M64 = CAUSAL;      // stage A^-1 as M = 64 MMAs (rows n2 < L2/2 only)
+
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t mma_bar[kWG][2];  // completion of the first / second half of a stage
+  __shared__ uint64_t stg_bar[2][2];   // [u|w slot, v slot][consuming warpgroup]: bulk copy landed
   __shared__ uint32_t tmem_slot;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;  // 1024-aligned
   const uint32_t sGA = base + C::OFF_GA, sGB = base + C::OFF_GB, sGBI = base + C::OFF_GBI,
-                 sGAI = base + C::OFF_GAI, sTW = base + C::OFF_TW, sTWT = base + C::OFF_TWT;
+                 sGAI = base + C::OFF_GAI, sTW = base + C::OFF_TW;
+  const uint32_t sUW = base + F::OFF_UW, sV = base + F::OFF_V;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wg = int(warp_uniform(warp >> 3));  // warpgroup
@@ -70,7 +100,7 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
   const int quad = warp & 3;             // TMEM lane quadrant this warp may access
   const int slice = (warp >> 2) & 1;     // column slice 0..1
   const int m = quad * 32 + lane;        // TMEM lane / MMA row owned by this thread
-  const uint32_t sKF = base + C::OFF_WG + wg * C::WG_BYTES;
+  const uint32_t sKF = base + F::OFF_WG + wg * C::WG_BYTES;
   const uint32_t bufX = sKF + C::al(C::KF_BYTES);
   const int64_t B = prm.B, H = prm.H, N = prm.N;
   const int64_t nbt = (B + C::R - 1) / C::R;
@@ -91,13 +121,15 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
   // ---- one-time setup: tables -> smem, barriers, TMEM (both warpgroups)
   {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.tables);
-    for (uint32_t o = tid * 16; o < C::TABLES; o += kThreads * 16) cp_async16(base + o, src + o, true);
+    for (uint32_t o = tid * 16; o < C::TABLES_FWD; o += kThreads * 16) cp_async16(base + o, src + o, true);
     cp_async_commit();
   }
   if (tid == 0) {
     for (int g = 0; g < kWG; ++g) {
       mbar_init(&mma_bar[g][0], 1);
       mbar_init(&mma_bar[g][1], 1);
+      mbar_init(&stg_bar[0][g], 1);
+      mbar_init(&stg_bar[1][g], 1);
     }
     fence_barrier_init();
   }
@@ -114,12 +146,45 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
   uint32_t phase = 0;
   int64_t cur_h = -1;
 
+  // Input staging (STG).  Slot `kind` (0: the tile's u [| w] rows, 1: its v
+  // rows) is filled for tile t by one elected thread with one bulk copy per
+  // row, completing on stg_bar[kind][(t - t0) % kWG]; the warpgroup that
+  // consumes tile t refills the slot for tile t + 1 right after it has read
+  // it, so fills (and reads) follow tile order and each slot's fill for the
+  // next warpgroup's tile overlaps the rest of the current tile.
+  auto fill = [&](int kind, int64_t t) {
+    const int64_t th = t / nbt, tb = t % nbt;
+    const int64_t tbase = (tb * C::R * H + phys_head(th)) * N;
+    const int rows = int(B - tb * C::R < C::R ? B - tb * C::R : C::R);
+    uint64_t* bar = &stg_bar[kind][(t - t0) % kWG];
+    const int planes = (kind == 0 && GATED) ? 2 : 1;
+    mbar_arrive_expect_tx(bar, uint32_t(rows * planes) * F::ROW_BYTES);
+    for (int r = 0; r < rows; ++r) {
+      const int64_t go = tbase + r * H * N;
+      if (kind == 0) {
+        bulk_g2s(sUW + r * F::ROW_BYTES, gu + go, F::ROW_BYTES, bar);
+        if (GATED) bulk_g2s(sUW + (C::R + r) * F::ROW_BYTES, gw + go, F::ROW_BYTES, bar);
+      } else {
+        bulk_g2s(sV + r * F::ROW_BYTES, gv + go, F::ROW_BYTES, bar);
+      }
+    }
+  };
+  uint32_t stg_phase[2] = {0, 0};
+  auto stg_wait = [&](int kind) {  // every thread waits (bulk-copied data)
+    mbar_wait(&stg_bar[kind][wg], stg_phase[kind]);
+    stg_phase[kind] ^= 1;
+  };
+  if (STG && tid == 0) {
+    fill(0, t0);
+    if (GATED) fill(1, t0);
+  }
+
   // UMMA shared-memory descriptors: built once, offsets added as (bytes >> 4)
   const uint64_t dXA = smem_desc(bufX, 128, C::SBO_A);          // stage A operand (MN-major)
   const uint64_t dGA = smem_desc(sGA, 128, C::SBO_GA);
   const uint64_t dXB = smem_desc(bufX, C::LBO_B, 128);          // stage B operand (MN-major)
   const uint64_t dGB = smem_desc(sGB, 128, C::SBO_GB);
-  const uint64_t dXBP = smem_desc(bufX, 128, C::SBO_BP);        // stage B^-1 operand (K-major)
+  const uint64_t dXBP = smem_desc(bufX, 128, C::SBO_BP);        // stage B^-1 operand (K-major, !TS)
   const uint64_t dGBI = smem_desc(sGBI, 128, C::SBO_GB);
   const uint64_t dGAI = smem_desc(sGAI, 128, C::SBO_GAI);
   const uint64_t dXAI = smem_desc(bufX, 128, C::SBO_XA);        // stage A^-1 operand (MN-major B)
@@ -134,9 +199,9 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
   };
   int stage_no = 0;
   auto wg_sync = [&] { named_sync(bar_id, kWGThreads); };
-  // Operands written -> warpgroup barrier -> one thread issues the stage as
-  // two halves, each committed to its own mbarrier so the epilogue of the
-  // first half overlaps the MMAs of the second.
+  // Operands written -> warpgroup barrier -> one elected thread issues the
+  // stage as two halves, each committed to its own mbarrier so the epilogue
+  // of the first half overlaps the MMAs of the second.
   auto sync_and_issue = [&](auto&& issue_half) {
     fence_async_smem();
     tc_fence_before();
@@ -158,17 +223,39 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
     tc_fence_after();
   };
 
-  // Per-thread invariants of the input loader: chunk q = wtid + i * 256 maps
-  // to (n2, j, r) with n2, j fixed and r = r0 + i * RSTEP.
-  constexpr int KROWS = C::KA;  // n2 rows per row
+  // Row orders.  Stage A rows (TMEM lanes) m <-> (pair p, n1) and stage B /
+  // B^-1 rows (group gi, lane m) <-> (p, k2) put 4 pairs x 8 consecutive n1
+  // (k2) in each warp, so every twiddle / k_f table word a warp reads is
+  // shared by 4 lanes (one shared-memory wavefront per 8 distinct words).
   constexpr int JC = L1 / 8;    // 8-element n1 chunks
-  constexpr int RSTEP = kWGThreads / (KROWS * JC);
-  static_assert(kWGThreads % (KROWS * JC) == 0, "loader mapping");
+  const int pA = ((m >> 5) / JC) * 4 + ((m >> 3) & 3), n1A = ((m >> 5) % JC) * 8 + (m & 7);
+  auto rowB_p = [&](int gi) { return (gi >> 1) * 4 + ((m >> 3) & 3); };
+  auto rowB_k2 = [&](int gi) { return (gi & 1) * 32 + (m >> 5) * 8 + (m & 7); };
+  // 8-row group of stage-B row (p, k2) (k2 a multiple of 8)
+  auto grpB = [](int p, int k2) { return (((p >> 2) * 2 + (k2 >> 5)) * 16) + ((k2 & 31) >> 3) * 4 + (p & 3); };
+
+  // Input loader: each warp instruction reads 32 consecutive 16 B chunks of
+  // one row (memory chunk cm = n2 * JC + j); lanes are permuted so that each
+  // 8-lane phase writes 8 distinct n2 of one core matrix (conflict-free).
+  // Thread chunk i is row r0 + i * RSTEP with (n2, j) fixed.
+  constexpr int KROWS = C::KA;  // n2 rows per row
+  constexpr int WPR = KROWS * JC / 32;  // warp instructions per row
+  constexpr int RSTEP = 8 / WPR;
+  constexpr int NCH = C::R * C::CH;
+  constexpr int PER_ALL = NCH / kWGThreads;  // chunks per thread and tile
+  static_assert(WPR >= 1 && 8 % WPR == 0 && NCH % kWGThreads == 0, "loader mapping");
   const int64_t HN = H * N;
-  const int ld_n2 = wtid % KROWS, ld_j = (wtid / KROWS) % JC, ld_r0 = wtid / (KROWS * JC);
-  const int64_t ld_off0 = int64_t(ld_r0) * HN + int64_t(ld_n2 * JC + ld_j) * 8;
-  // epilogue-4 invariants: row (2p + cp) of the tile, positions L1*n2 + 8*n1c
-  const int64_t st_off0 = int64_t(m >> 6) * HN + int64_t(L1) * (m & 63);
+  // From staging (STG) the lanes of each 8-lane phase take 8 consecutive n2
+  // and n1 chunks j rotated so that both the staging read (chunk cm mod 8)
+  // and the operand write (n2 mod 8) are bank-conflict-free.
+  constexpr int LJC = JC == 4 ? 2 : JC == 2 ? 1 : 0;
+  const int ld_n2 = STG ? ((wtid >> 5) % WPR) * (32 / JC) + ((lane >> 3) >> LJC) * 8 + (lane & 7)
+                        : (((wtid >> 5) % WPR) * 32 + (lane % (32 / JC)) * JC + lane / (32 / JC)) / JC;
+  const int ld_j = STG ? (((lane & 7) >> (3 - LJC)) + (lane >> 3)) & (JC - 1)
+                       : (((wtid >> 5) % WPR) * 32 + (lane % (32 / JC)) * JC + lane / (32 / JC)) % JC;
+  const int ld_r0 = (wtid >> 5) / WPR;
+  const int ld_cm = ld_n2 * JC + ld_j;
+  const int64_t ld_off0 = int64_t(ld_r0) * HN + int64_t(ld_cm) * 8;
 
   // u (*w) -> fp16 operand chunk of 8 elements
   auto gate8 = [&](uint4 uv, uint4 wv) -> uint4 {
@@ -195,30 +282,60 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
                         pack_half2(g[6], g[7]));
     }
   };
-  // stage A operand address of (row r of the tile, n2, n1 chunk j)
-  auto chunk_dst = [&](int r, int n2, int j) -> uint32_t {
-    const int k = (r & 1) * C::KA + n2;
-    return bufX + ((r >> 1) * JC + j) * C::SBO_A + (k >> 3) * 128 + (k & 7) * 16;
+  // stage A operand address of chunk i of this thread: row r = 2p + c of the
+  // tile, (n2, n1 chunk j) -> K index c*KA + n2, 8-row group of (p, 8j)
+  auto chunk_dst = [&](int i) -> uint32_t {
+    const int r = ld_r0 + i * RSTEP, p = r >> 1;
+    const int k = (r & 1) * C::KA + ld_n2;
+    const int g8 = ((p >> 2) * JC + ld_j) * 4 + (p & 3);
+    return bufX + g8 * C::SBO_A + (k >> 3) * 128 + (k & 7) * 16;
   };
-  // Causal tiles leave TMEM lane quadrants 1 and 3 idle in epilogue 4 (their
-  // rows are the discarded n2 >= L2/2 half): those 4 warps prefetch the next
-  // tile's (gated) input into spare TMEM columns [192, 256) of their own
-  // lanes (the two column slices of a quadrant share lanes: 32 columns each).
-  constexpr bool PF = CAUSAL;
-  const uint32_t PF_COL = 192 + 32 * slice;
-  // live from epilogue 4 of tile t to the start of tile t+1: only stage A^-1
-  // (columns < 128) and the next stage A (< NA) write TMEM in between
-  static_assert(C::NA <= 192, "prefetch columns are free");
-  constexpr int PF_CH = (C::R * C::CH) / 128;  // chunks per idle thread
-  const bool idle4 = CAUSAL && (quad & 1);
-  const int pf_ii = ((quad >> 1) * 2 + slice) * 32 + lane;  // 0..127 among idle threads
-  const int pf_n2 = pf_ii % KROWS, pf_j = (pf_ii / KROWS) % JC, pf_r0 = pf_ii / (KROWS * JC);
-  constexpr int PF_RSTEP = 128 / (KROWS * JC);
-  static_assert(!PF || (128 % (KROWS * JC) == 0 && PF_CH == 8), "prefetch mapping");
-  const int64_t pf_off0 = int64_t(pf_r0) * HN + int64_t(pf_n2 * JC + pf_j) * 8;
-  bool prefetched = false;
+  auto load_chunks = [&](int64_t tbase, int left, uint4* uv, uint4* wv) {
+#pragma unroll
+    for (int i = 0; i < PER_ALL; ++i) {
+      if (ld_r0 + i * RSTEP < left) {
+        const int64_t goff = tbase + ld_off0 + int64_t(i * RSTEP) * HN;
+        uv[i] = *reinterpret_cast<const uint4*>(gu + goff);
+        if (GATED) wv[i] = *reinterpret_cast<const uint4*>(gw + goff);
+      } else {
+        uv[i] = make_uint4(0, 0, 0, 0);
+        wv[i] = make_uint4(0, 0, 0, 0);
+      }
+    }
+  };
+  auto build_from_staging = [&](int left) {  // staging rows -> (gated) stage A operand
+#pragma unroll
+    for (int i = 0; i < PER_ALL; ++i) {
+      const int r = ld_r0 + i * RSTEP;
+      uint4 uv = make_uint4(0, 0, 0, 0), wv = make_uint4(0, 0, 0, 0);
+      if (r < left) {
+        uv = ld_shared_u4(sUW + r * F::ROW_BYTES + ld_cm * 16);
+        if (GATED) wv = ld_shared_u4(sUW + (C::R + r) * F::ROW_BYTES + ld_cm * 16);
+      }
+      const uint4 g = gate8(uv, wv);
+      st_shared_v4(chunk_dst(i), g.x, g.y, g.z, g.w);
+    }
+  };
+  auto store_chunks = [&](const uint4* uv, const uint4* wv) {
+#pragma unroll
+    for (int i = 0; i < PER_ALL; ++i) {
+      const uint4 g = gate8(uv[i], wv[i]);
+      st_shared_v4(chunk_dst(i), g.x, g.y, g.z, g.w);
+    }
+  };
+
+  // Epilogue-4 geometry.  Output lane m holds G_AI row (n2 half, c', n2 mod
+  // 32) (plan.cpp).  Causal: two M = 64 MMAs put column half hh in lanes
+  // 16 hh .. 16 hh + 15 of every quadrant, rows q*16 + lane%16 (n2 < 32).
+  constexpr int OUT_COLS = M64 ? 32 : 64;  // output columns per thread (this slice)
+  const int o_hh = M64 ? (lane >> 4) : slice;
+  const int o_row = M64 ? quad * 16 + (lane & 15) : m;
+  const int o_cp = (o_row >> 5) & 1, o_n2 = (o_row >> 6) * 32 + (o_row & 31);
+  const int o_col0 = M64 ? o_hh * 64 + slice * 32 : slice * 64;  // first (p, n1) column of this thread
+  const uint32_t o_tcol = M64 ? slice * 32 : slice * 64;          // its TMEM column
 
   int64_t hh = (t0 + wg) / nbt, bt = (t0 + wg) % nbt;
+  bool loaded = false;  // the tile's operand was stored by the previous tile's epilogue 4
   for (int64_t t = t0 + wg; t < t1; t += kWG, bt += kWG) {
     while (bt >= nbt) { bt -= nbt; ++hh; }
     stage_no = 0;
@@ -233,57 +350,27 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
       cp_async_commit();
       cur_h = h;
     }
-
-    // ---------------- load (+ gate) the tile's rows straight into the stage A operand
-    if (prefetched) {
-      if (idle4) {
-        uint32_t v[32];
-        tmem_ld16(tq + PF_COL, reinterpret_cast<float*>(v));
-        tmem_ld16(tq + PF_COL + 16, reinterpret_cast<float*>(v + 16));
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < PF_CH; ++i)
-          st_shared_v4(chunk_dst(pf_r0 + i * PF_RSTEP, pf_n2, pf_j), v[4 * i], v[4 * i + 1], v[4 * i + 2],
-                       v[4 * i + 3]);
-      }
-    } else {
-      constexpr int NCH = C::R * C::CH;
-      constexpr int PER_ALL = NCH / kWGThreads;
-      constexpr int PER = PER_ALL < 4 ? PER_ALL : 4;  // loads in flight per batch (register budget)
-#pragma unroll 1
-      for (int i0 = 0; i0 < PER_ALL; i0 += PER) {
-      uint4 uv[PER], wv[PER];
-#pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int r = ld_r0 + (i0 + i) * RSTEP;
-        if (r < rows_left) {
-          const int64_t goff = tile_base + ld_off0 + int64_t((i0 + i) * RSTEP) * HN;
-          uv[i] = *reinterpret_cast<const uint4*>(gu + goff);
-          if (GATED) wv[i] = *reinterpret_cast<const uint4*>(gw + goff);
-        } else {
-          uv[i] = make_uint4(0, 0, 0, 0);
-          wv[i] = make_uint4(0, 0, 0, 0);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        // n2 fastest so 8 consecutive threads fill one 128 B core matrix
-        const uint4 g = gate8(uv[i], wv[i]);
-        st_shared_v4(chunk_dst(ld_r0 + (i0 + i) * RSTEP, ld_n2, ld_j), g.x, g.y, g.z, g.w);
-      }
-    }
+    if constexpr (STG) {
+      stg_wait(0);
+      build_from_staging(rows_left);
+    } else if (!loaded) {
+      uint4 uv[PER_ALL], wv[PER_ALL];
+      load_chunks(tile_base, rows_left, uv, wv);
+      store_chunks(uv, wv);
     }
     if (new_h) cp_async_wait_all();
     stamp(1);
 
     // ---------------- stage A: D[(p,n1)][(re|im|-im, k2)] = X[(p,n1)][(c,n2)] * G_A
     // TMEM column of (block, k2): (k2 / 32) * NA/2 + 32 * block + k2 % 32
-    sync_and_issue([&](int hh) {  // half hh: k2 in [32 hh, 32 hh + 32) of every block, one MMA per K step
+    sync_and_issue([&](int h2) {  // half h2: k2 in [32 h2, 32 h2 + 32) of every block, one MMA per K step
       constexpr uint32_t idesc = idesc_f16(128, C::NA / 2, true, false);
 #pragma unroll
       for (int s = 0; s < 2 * C::KA / 16; ++s)
-        mma_f16_ss(tmem + hh * (C::NA / 2), dadd(dXA, 256 * s),
-                   dadd(dGA, hh * (C::NA / 16) * C::SBO_GA + 256 * s), idesc, s > 0);
+        mma_f16_ss(tmem + h2 * (C::NA / 2), dadd(dXA, 256 * s),
+                   dadd(dGA, h2 * (C::NA / 16) * C::SBO_GA + 256 * s), idesc, s > 0);
+      // the u|w slot has been read by the whole warpgroup: stage the next tile
+      if (STG && h2 == 1 && t + 1 < t1) fill(0, t + 1);
     });
 
     // ---------------- epilogue 1: twiddle W^{n1 k2}, transpose -> stage B operand (MN-major)
@@ -291,7 +378,6 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
     // the stage (the other half's MMAs may still read bufX); math on the
     // first item only needs this warp's half.
     {
-      const int p = m / L1, n1 = m % L1;
       wait_half(slice);
 #pragma unroll 1
       for (int sub = 0; sub < 2; ++sub) {
@@ -303,7 +389,7 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
         if constexpr (C::NEG_A) tmem_ld16(tq + c0 + 64, ni);
         float4 w[8];
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) w[jj] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1, k20 / 2 + jj));
+        for (int jj = 0; jj < 8; ++jj) w[jj] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1A, k20 / 2 + jj));
         tmem_ld_wait();
         if constexpr (!C::NEG_A) {
 #pragma unroll
@@ -314,37 +400,34 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
         if (sub == 0) wait_half(slice ^ 1);
 #pragma unroll
         for (int hh2 = 0; hh2 < 2; ++hh2) {
-          const int mg = p * (L2 / 8) + k20 / 8 + hh2;
-          st_half8(bufX + mg * 128 + (n1 >> 3) * C::LBO_B + (n1 & 7) * 16, re + 8 * hh2);
-          st_half8(bufX + mg * 128 + ((L1 + n1) >> 3) * C::LBO_B + (n1 & 7) * 16, im + 8 * hh2);
+          const int mg = grpB(pA, k20 + 8 * hh2);
+          st_half8(bufX + mg * 128 + (n1A >> 3) * C::LBO_B + (n1A & 7) * 16, re + 8 * hh2);
+          st_half8(bufX + mg * 128 + ((L1 + n1A) >> 3) * C::LBO_B + (n1A & 7) * 16, im + 8 * hh2);
         }
       }
     }
-
     stamp(4);
+
     // ---------------- stage B: per group of 128 rows (p,k2), contract n1 -> k1
-    sync_and_issue([&](int hh) {
+    sync_and_issue([&](int h2) {
       constexpr uint32_t idesc = idesc_f16(128, C::NB, true, false);
 #pragma unroll
-      for (int gi = hh * (C::P / 4); gi < (hh + 1) * (C::P / 4); ++gi) {
+      for (int gi = h2 * (C::P / 4); gi < (h2 + 1) * (C::P / 4); ++gi) {
 #pragma unroll
-        for (int s = 0; s < 2 * L1 / 16; ++s) {
-          uint64_t ad = dadd(dXB, gi * 2048 + 2 * s * C::LBO_B);
-          uint64_t bd = dadd(dGB, 256 * s);
-          mma_f16_ss(tmem + gi * C::NB, ad, bd, idesc, s > 0);
-        }
+        for (int s = 0; s < 2 * L1 / 16; ++s)
+          mma_f16_ss(tmem + gi * C::NB, dadd(dXB, gi * 2048 + 2 * s * C::LBO_B), dadd(dGB, 256 * s), idesc, s > 0);
       }
     });
 
-    // ---------------- epilogue 2: pointwise * k_f -> stage B^-1 operand (K-major, own row)
+    // ---------------- epilogue 2: pointwise * k_f -> stage B^-1 operand (own row: TMEM, else K-major smem)
     {
-      const int k2 = m & 63;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int it = slice + 2 * i;  // items 0..3 in half 0, 4..7 in half 1
-        const int gi = it / (L1 / 8), k1c = it % (L1 / 8);
-        const int row = gi * 128 + m;  // (p, k2) with p = 2 gi + m / 64
+        const int gi = it / JC, k1c = it % JC;
+        const int k2 = rowB_k2(gi);
         if (i == 0) wait_half(0);
+        if (TS && i == 2) wait_half(1);
         const uint32_t col = gi * C::NB + k1c * 8;
         float re[8], im[8], ni[8];
         tmem_ld8(tq + col, re);
@@ -355,142 +438,200 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
         for (int jj = 0; jj < 4; ++jj) kf[jj] = ld_shared_f4(sKF + tab_off<L1 / 2>(k2, k1c * 4 + jj));
         tmem_ld_wait();
         cmul8(re, im, ni, kf);
-        if (i == 0) wait_half(1);  // stores may overwrite operands of the second half
-        st_half8(bufX + (row >> 3) * C::SBO_BP + k1c * 128 + (row & 7) * 16, re);
-        st_half8(bufX + (row >> 3) * C::SBO_BP + (L1 / 8 + k1c) * 128 + (row & 7) * 16, im);
+        if constexpr (TS) {  // K index c*L1 + k1 -> column (c*L1 + k1) / 2
+          const uint32_t ca = tq + C::CA + gi * L1 + k1c * 4;
+          tmem_st4(ca, pack_half2(re[0], re[1]), pack_half2(re[2], re[3]), pack_half2(re[4], re[5]),
+                   pack_half2(re[6], re[7]));
+          tmem_st4(ca + L1 / 2, pack_half2(im[0], im[1]), pack_half2(im[2], im[3]), pack_half2(im[4], im[5]),
+                   pack_half2(im[6], im[7]));
+        } else {
+          if (i == 0) wait_half(1);  // stores may overwrite operands of the second half
+          const int row = gi * 128 + m;
+          st_half8(bufX + (row >> 3) * C::SBO_BP + k1c * 128 + (row & 7) * 16, re);
+          st_half8(bufX + (row >> 3) * C::SBO_BP + (L1 / 8 + k1c) * 128 + (row & 7) * 16, im);
+        }
       }
+      if constexpr (TS) tmem_st_wait();
     }
-
     stamp(7);
+
     // ---------------- stage B^-1: contract k1 -> n1
-    sync_and_issue([&](int hh) {
+    sync_and_issue([&](int h2) {
       constexpr uint32_t idesc = idesc_f16(128, C::NB, false, false);
 #pragma unroll
-      for (int gi = hh * (C::P / 4); gi < (hh + 1) * (C::P / 4); ++gi) {
+      for (int gi = h2 * (C::P / 4); gi < (h2 + 1) * (C::P / 4); ++gi) {
 #pragma unroll
         for (int s = 0; s < 2 * L1 / 16; ++s) {
-          uint64_t ad = dadd(dXBP, gi * 16 * C::SBO_BP + 256 * s);
-          uint64_t bd = dadd(dGBI, 256 * s);
-          mma_f16_ss(tmem + gi * C::NB, ad, bd, idesc, s > 0);
+          if constexpr (TS)
+            mma_f16_ts(tmem + gi * C::NB, tmem + C::CA + gi * L1 + 8 * s, dadd(dGBI, 256 * s), idesc, s > 0);
+          else
+            mma_f16_ss(tmem + gi * C::NB, dadd(dXBP, gi * 16 * C::SBO_BP + 256 * s), dadd(dGBI, 256 * s), idesc,
+                       s > 0);
         }
       }
     });
 
     // ---------------- epilogue 3: conj twiddle, transpose -> stage A^-1 operand (MN-major B)
     {
-      const int k2 = m & 63;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int it = slice + 2 * i;
-        const int gi = it / (L1 / 8), n1c = it % (L1 / 8);
-        const int p = gi * 2 + (m >> 6);
+        const int gi = it / JC, n1c = it % JC;
+        const int p = rowB_p(gi), k2 = rowB_k2(gi);
         if (i == 0) wait_half(0);
+        if (TS && i == 2) wait_half(1);  // bufX is not an operand of stage B^-1 here
         const uint32_t col = gi * C::NB + n1c * 8;
         float re[8], im[8], nr[8];
         tmem_ld8(tq + col, re);
         tmem_ld8(tq + col + L1, im);
         tmem_ld8(tq + col + 2 * L1, nr);
+        // W^{n1 k2} for 8 consecutive n1 at this k2 from TW ([n1][k2/2] pairs
+        // over k2): pick the k2 parity, re-pair over n1
         float4 w[4];
+        {
+          const bool odd = k2 & 1;
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) w[jj] = ld_shared_f4(sTWT + tab_off<L1 / 2>(k2, n1c * 4 + jj));
+          for (int jj = 0; jj < 4; ++jj) {
+            const float4 a = ld_shared_f4(sTW + tab_off<L2 / 2>(n1c * 8 + 2 * jj, k2 >> 1));
+            const float4 b = ld_shared_f4(sTW + tab_off<L2 / 2>(n1c * 8 + 2 * jj + 1, k2 >> 1));
+            w[jj] = odd ? make_float4(a.y, b.y, a.w, b.w) : make_float4(a.x, b.x, a.z, b.z);
+          }
+        }
         tmem_ld_wait();
         cmulc8(re, im, nr, w);
-        if (i == 0) wait_half(1);  // stores may overwrite operands of the second half
+        if (!TS && i == 0) wait_half(1);  // stores may overwrite operands of the second half
         const int ng = (p * L1) / 8 + n1c;
         st_half8(bufX + ng * C::SBO_XA + (k2 >> 3) * 128 + (k2 & 7) * 16, re);
         st_half8(bufX + ng * C::SBO_XA + ((L2 + k2) >> 3) * 128 + (k2 & 7) * 16, im);
       }
     }
-
     stamp(10);
+
     // ---------------- stage A^-1: D[(c',n2)][(p,n1)] = G_A^-1 * X[(c,k2)][(p,n1)]
-    sync_and_issue([&](int hh) {  // half hh: output columns (p, n1) in [64 hh, 64 hh + 64)
-      constexpr uint32_t idesc = idesc_f16(128, 64, false, true);
+    sync_and_issue([&](int h2) {  // half h2: output columns (p, n1) in [64 h2, 64 h2 + 64)
+      constexpr uint32_t idesc = idesc_f16(M64 ? 64 : 128, 64, false, true);
+      const uint32_t dcol = M64 ? tmem + (uint32_t(16 * h2) << 16) : tmem + h2 * 64;
 #pragma unroll
-      for (int s = 0; s < 2 * L2 / 16; ++s) {
-        uint64_t ad = dadd(dGAI, 256 * s);
-        uint64_t bd = dadd(dXAI, hh * 8 * C::SBO_XA + 256 * s);
-        mma_f16_ss(tmem + hh * 64, ad, bd, idesc, s > 0);
-      }
+      for (int s = 0; s < 2 * L2 / 16; ++s)
+        mma_f16_ss(dcol, dadd(dGAI, 256 * s), dadd(dXAI, h2 * 8 * C::SBO_XA + 256 * s), idesc, s > 0);
     });
 
-    // ---------------- epilogue 4: (gate), convert, store y
+    // ---------------- epilogue 4: (gate), convert, store y; load the next tile
+    // v (output gate) and the next tile's input are read with coalesced 16 B
+    // loads issued before the wait.  y leaves TMEM transposed (lane = n2), so
+    // it is staged in natural order through bufX (free once stage A^-1 has
+    // completed; 128 B XOR swizzle, conflict-free both ways) and written back
+    // coalesced.  Gated tiles stage fp32 so y * v is rounded once.
+    // (Circular gated tiles -- fp32 staging would not fit -- store directly.)
     {
-      const int cp = m >> 6;
+      constexpr bool STAGE = CAUSAL || !GATED;
+      using S = typename std::conditional<GATED, float, T>::type;
+      constexpr int OCH = C::R * C::NOUT / 8 / kWGThreads;  // coalesced output chunks per thread
+      static_assert(!STAGE || C::R * C::NOUT * sizeof(S) <= C::BUFX_BYTES, "y staging fits in bufX");
+      constexpr int PER = OUT_COLS / 8;  // transposed 8-column items per thread
+      constexpr int NV = STAGE ? OCH : PER;
       const bool has_next = t + kWG < t1;
-      if (idle4) {  // warp-uniform: prefetch the next tile's input into TMEM
+      uint4 nu[PER_ALL], nw[PER_ALL], vv[NV];
+      auto och_r = [&](int i) { return (i * kWGThreads + wtid) / (C::NOUT / 8); };
+      auto och_n = [&](int i) { return ((i * kWGThreads + wtid) % (C::NOUT / 8)) * 8; };
+      auto item_rn = [&](int i, int& r, int& n) {  // transposed item -> (tile row, position)
+        const int gc = o_col0 + 8 * i;
+        r = 2 * (gc / L1) + o_cp;
+        n = ((gc % L1) / 8) * 8 + L1 * o_n2;
+      };
+      if (GATED && !STG) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          int r, n;
+          if (STAGE) { r = och_r(i); n = och_n(i); } else item_rn(i, r, n);
+          if (r < rows_left) vv[i] = *reinterpret_cast<const uint4*>(gv + tile_base + int64_t(r) * HN + n);
+        }
+      }
+      if (!STG && has_next && (STAGE || !GATED)) {
+        int64_t hh2 = hh, bt2 = bt + kWG;
+        while (bt2 >= nbt) { bt2 -= nbt; ++hh2; }
+        const int64_t base2 = (bt2 * C::R * H + phys_head(hh2)) * N;
+        const int left2 = int(B - bt2 * C::R < C::R ? B - bt2 * C::R : C::R);
+        load_chunks(base2, left2, nu, nw);
+      }
+      wait_half(M64 ? 0 : slice);
+      wait_half(M64 ? 1 : slice ^ 1);  // bufX is rewritten below: both halves done
+      stamp(15);
+      if constexpr (STAGE) {
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          float o[8];
+          tmem_ld8(tq + o_tcol + 8 * i, o);
+          tmem_ld_wait();
+          int r, n;
+          item_rn(i, r, n);
+          const uint32_t off = uint32_t(r * C::NOUT + n) * sizeof(S);
+          if constexpr (GATED) {
+            st_shared_v4(bufX + swz128(off), __float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
+                         __float_as_uint(o[3]));
+            st_shared_v4(bufX + swz128(off + 16), __float_as_uint(o[4]), __float_as_uint(o[5]),
+                         __float_as_uint(o[6]), __float_as_uint(o[7]));
+          } else {
+            st_shared_v4(bufX + swz128(off), IO<T>::pack2(o[0], o[1]), IO<T>::pack2(o[2], o[3]),
+                         IO<T>::pack2(o[4], o[5]), IO<T>::pack2(o[6], o[7]));
+          }
+        }
+        tc_fence_before();
+        if (STG && GATED) stg_wait(1);
+        wg_sync();
+#pragma unroll
+        for (int i = 0; i < OCH; ++i) {
+          const int r = och_r(i), n = och_n(i);
+          const uint32_t off = uint32_t(r * C::NOUT + n) * sizeof(S);
+          uint4 st;
+          if constexpr (GATED) {
+            const float4 a = ld_shared_f4(bufX + swz128(off)), b2 = ld_shared_f4(bufX + swz128(off + 16));
+            float v8[8];
+            if (STG) vv[i] = ld_shared_u4(sV + r * F::ROW_BYTES + n * 2);
+            IO<T>::to_f32x8(vv[i], v8);
+            st = make_uint4(IO<T>::pack2(a.x * v8[0], a.y * v8[1]), IO<T>::pack2(a.z * v8[2], a.w * v8[3]),
+                            IO<T>::pack2(b2.x * v8[4], b2.y * v8[5]), IO<T>::pack2(b2.z * v8[6], b2.w * v8[7]));
+          } else {
+            st = ld_shared_u4(bufX + swz128(off));
+          }
+          if (r < rows_left) *reinterpret_cast<uint4*>(gy + tile_base + int64_t(r) * HN + n) = st;
+        }
+        if (STG && GATED) fence_async_smem();  // v slot reads before its refill (async proxy)
+        wg_sync();  // staging reads done before bufX takes the next tile's operand
+        if (STG && GATED && t + 1 < t1 && wtid < 32 && elect_one()) fill(1, t + 1);
+      } else {
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          float o[8];
+          tmem_ld8(tq + o_tcol + 8 * i, o);
+          tmem_ld_wait();
+          int r, n;
+          item_rn(i, r, n);
+          float v8[8];
+          IO<T>::to_f32x8(vv[i], v8);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] *= v8[e];
+          if (r < rows_left)
+            *reinterpret_cast<uint4*>(gy + tile_base + int64_t(r) * HN + n) =
+                make_uint4(IO<T>::pack2(o[0], o[1]), IO<T>::pack2(o[2], o[3]), IO<T>::pack2(o[4], o[5]),
+                           IO<T>::pack2(o[6], o[7]));
+        }
         if (has_next) {
           int64_t hh2 = hh, bt2 = bt + kWG;
           while (bt2 >= nbt) { bt2 -= nbt; ++hh2; }
-          const int64_t h2 = phys_head(hh2);
-          const int64_t base2 = (bt2 * C::R * H + h2) * N;
+          const int64_t base2 = (bt2 * C::R * H + phys_head(hh2)) * N;
           const int left2 = int(B - bt2 * C::R < C::R ? B - bt2 * C::R : C::R);
-          uint4 uv[PF_CH], wv[PF_CH];
-#pragma unroll
-          for (int i = 0; i < PF_CH; ++i) {
-            const int r = pf_r0 + i * PF_RSTEP;
-            if (r < left2) {
-              const int64_t goff = base2 + pf_off0 + int64_t(i * PF_RSTEP) * HN;
-              uv[i] = *reinterpret_cast<const uint4*>(gu + goff);
-              if (GATED) wv[i] = *reinterpret_cast<const uint4*>(gw + goff);
-            } else {
-              uv[i] = make_uint4(0, 0, 0, 0);
-              wv[i] = make_uint4(0, 0, 0, 0);
-            }
-          }
-          uint32_t v[32];
-#pragma unroll
-          for (int i = 0; i < PF_CH; ++i) {
-            const uint4 g = gate8(uv[i], wv[i]);
-            v[4 * i] = g.x; v[4 * i + 1] = g.y; v[4 * i + 2] = g.z; v[4 * i + 3] = g.w;
-          }
-          tmem_st32(tq + PF_COL, v);
-          tmem_st_wait();
+          load_chunks(base2, left2, nu, nw);
         }
-      } else if (!CAUSAL || (m & 63) < L2 / 2) {  // warp-uniform
-        // this warp's items cover output columns [64 slice, 64 slice + 64)
-        constexpr int NIT = C::P * (L1 / 8);  // (pair, 8-wide n1 chunk) items
-        constexpr int PER = NIT / 2;
-        int64_t goff[PER];
-        bool ok[PER];
-        uint4 vv[PER];
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-          const int it = slice * PER + i;
-          const int p = it / (L1 / 8), n1c = it % (L1 / 8);
-          ok[i] = 2 * p + cp < rows_left;
-          goff[i] = tile_base + st_off0 + int64_t(2 * p) * HN + n1c * 8;
-          if (GATED && ok[i]) vv[i] = *reinterpret_cast<const uint4*>(gv + goff[i]);
-        }
-        wait_half(slice);
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-          const int it = slice * PER + i;
-          const int p = it / (L1 / 8), n1c = it % (L1 / 8);
-          float o[8];
-          tmem_ld8(tq + p * L1 + n1c * 8, o);
-          tmem_ld_wait();
-          if (GATED) {
-            float v8[8];
-            IO<T>::to_f32x8(vv[i], v8);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) o[e] *= v8[e];
-          }
-          uint4 st;
-          st.x = IO<T>::pack2(o[0], o[1]);
-          st.y = IO<T>::pack2(o[2], o[3]);
-          st.z = IO<T>::pack2(o[4], o[5]);
-          st.w = IO<T>::pack2(o[6], o[7]);
-          if (ok[i]) *reinterpret_cast<uint4*>(gy + goff[i]) = st;
-        }
+        tc_fence_before();
+        wg_sync();
       }
+      if (!STG && has_next) store_chunks(nu, nw);
+      loaded = !STG && has_next;
     }
     stamp(13);
-    tc_fence_before();
-    wg_sync();  // TMEM columns and bufX are reused by the next tile
     stamp(14);
     ++trace_tile;
-    prefetched = PF && (t + kWG < t1);
   }
   __syncthreads();
   if (warp == 0) tmem_dealloc<(kWG * C::TMEM_COLS > 512 ? 512 : kWG * C::TMEM_COLS)>(tmem_slot);
@@ -500,10 +641,11 @@ __global__ void __launch_bounds__(O2Cfg<L1, CAUSAL>::THREADS, 1) fftconv_fwd_o2_
 template <int L1, bool CAUSAL, bool GATED, typename T>
 static cudaError_t launch_o2(const FwdParams& prm, cudaStream_t stream) {
   using C = O2Cfg<L1, CAUSAL>;
+  using F = FwdCfg<L1, CAUSAL, GATED>;
   auto kern = fftconv_fwd_o2_kernel<L1, CAUSAL, GATED, T>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(F::SMEM));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -511,7 +653,7 @@ static cudaError_t launch_o2(const FwdParams& prm, cudaStream_t stream) {
   const int64_t tiles = (prm.row_map ? (prm.H / prm.row_L0) * prm.nrow : prm.H) * nbt;
   int grid = int(tiles < prm.num_sms ? tiles : prm.num_sms);
   if (grid < 1) return cudaSuccess;
-  kern<<<grid, C::THREADS, C::SMEM, stream>>>(prm);
+  kern<<<grid, F::THREADS, F::SMEM, stream>>>(prm);
   return cudaGetLastError();
 }
 

@@ -142,25 +142,24 @@ static void put_float(std::vector<uint8_t>& img, size_t off, double x) {
 }
 
 // Table image of the fused order-2 kernel (kernels_fwd.cu, O2Cfg):
-//  GA  : stage A B-operand, K-major rows (k2 half, re|im|-im, k2 mod 32) = 3*L2, K (c,n2) = 2*KA
+//  GA  : stage A B-operand, K-major rows (k2 half, re|im, k2 mod 32) = 2*L2, K (c,n2) = 2*KA
 //  GB  : stage B B-operand, rows (re|im|-im|pad, k1) = NB, K (c,n1) = 2*L1
 //  GBI : stage B^-1, rows (re|im|-re|pad, n1) = NB, K (c,k1) = 2*L1
-//  GAI : stage A^-1 A-operand, rows (c',n2) = 2*L2, K (c,k2) = 2*L2
+//  GAI : stage A^-1 A-operand, rows (n2 half, c', n2 mod 32) = 2*L2, K (c,k2) = 2*L2
 //  TW  : [n1][k2/2] {wr(k2), wr(k2+1), wi(k2), wi(k2+1)} fp32, W = W_L^{n1 k2}
 //  TWT : [k2][n1/2] {wr(n1), wr(n1+1), wi(n1), wi(n1+1)} fp32
 // DFT matrices carry the unitary 1/sqrt(L_i) scale, so the whole forward +
 // inverse pair scales by 1/L and k_f is used unscaled.
 static void build_fused_tables(fftconv_plan_s* p, int64_t L) {
   const int L1 = p->L1, L2 = p->L2, KA = p->KA;
-  const bool neg_a = KA < L2;  // causal: the -im block of stage A (see O2Cfg::NEG_A)
-  const int NA = (neg_a ? 3 : 2) * L2, NB = (3 * L1 + 15) / 16 * 16;
+  const int NA = 2 * L2, NB = (3 * L1 + 15) / 16 * 16;  // O2Cfg::NA, NB
   TableLayout& t = p->tl;
-  size_t off = 0;
+  size_t off = 0;  // order GA | GB | GBI | TW | GAI | TWT (O2Cfg)
   t.ga = off;  t.ga_bytes = size_t(NA) * (2 * KA) * 2;      off = align_up(off + t.ga_bytes, 1024);
   t.gb = off;  t.gb_bytes = size_t(NB) * (2 * L1) * 2;      off = align_up(off + t.gb_bytes, 1024);
   t.gbi = off; t.gbi_bytes = t.gb_bytes;                    off = align_up(off + t.gbi_bytes, 1024);
-  t.gai = off; t.gai_bytes = size_t(2 * L2) * (2 * L2) * 2; off = align_up(off + t.gai_bytes, 1024);
   t.tw = off;  t.tw_bytes = size_t(L1) * tab_stride(L2 / 2); off = align_up(off + t.tw_bytes, 1024);
+  t.gai = off; t.gai_bytes = size_t(2 * L2) * (2 * L2) * 2; off = align_up(off + t.gai_bytes, 1024);
   t.twt = off; t.twt_bytes = size_t(L2) * tab_stride(L1 / 2); off = align_up(off + t.twt_bytes, 1024);
   t.wl = off;  t.wl_bytes = size_t(L) * 8;                  off = align_up(off + t.wl_bytes, 1024);
   const int64_t Lfull = p->L;  // the whole transform (== L unless multipass)
@@ -210,7 +209,10 @@ static void build_fused_tables(fftconv_plan_s* p, int64_t L) {
         for (int k2 = 0; k2 < L2; ++k2) {
           double fr, fi;
           root(-int64_t(k2) * n2, L2, &fr, &fi);
-          put_half(img, t.gai + kmajor_off(co * L2 + n2, ci * L2 + k2, 2 * L2), realpair(fr * sA, fi * sA, ci, co));
+          // rows ordered (n2 half, c', n2 mod 32): the causal forward keeps
+          // only n2 < L2/2, i.e. the first 64 rows (one M = 64 MMA)
+          const int row = (n2 / 32) * 64 + co * 32 + n2 % 32;
+          put_half(img, t.gai + kmajor_off(row, ci * L2 + k2, 2 * L2), realpair(fr * sA, fi * sA, ci, co));
         }
   // twiddles W_L^{n1 k2} as element pairs, padded rows (tab_off_rt)
   for (int n1 = 0; n1 < L1; ++n1)

@@ -118,3 +118,95 @@ extern "C" int fcst_mma(const void* A, const void* B, void* D, int M, int N, int
   cudaError_t e = cudaDeviceSynchronize();
   return e == cudaSuccess ? 0 : 100 + (int)e;
 }
+
+// ---------------------------------------------------------------- microbenchmarks
+// (experiments: TMEM read throughput and back-to-back MMA cost)
+namespace {
+__global__ void __launch_bounds__(512, 1) tmem_ld_bench_kernel(int iters, int nwarps, long long* out) {
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid / 32;
+  if (warp == 0) fc::tmem_alloc<512>(&tmem_base);
+  fc::tc_fence_before();
+  __syncthreads();
+  fc::tc_fence_after();
+  const uint32_t t = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * 64;
+  float acc = 0.f;
+  __syncthreads();
+  long long c0 = clock64();
+  if (warp < nwarps) {
+    for (int i = 0; i < iters; ++i) {
+      float v[32];
+      fc::tmem_ld16(t, v);
+      fc::tmem_ld16(t + 16, v + 16);
+      fc::tmem_ld_wait();
+      for (int j = 0; j < 32; ++j) acc += v[j];
+    }
+  }
+  __syncthreads();
+  long long c1 = clock64();
+  if (tid == 0) out[0] = c1 - c0;
+  if (acc == 12345.f) out[1] = 1;
+  fc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) fc::tmem_dealloc<512>(tmem_base);
+}
+
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int nmma, int N, int ts, long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 16384; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  if (tid == 0) {
+    fc::mbar_init(&bar, 1);
+    fc::fence_barrier_init();
+  }
+  if (tid < 32) fc::tmem_alloc<512>(&tmem_base);
+  fc::fence_async_smem();
+  fc::tc_fence_before();
+  __syncthreads();
+  fc::tc_fence_after();
+  const uint32_t tb = fc::warp_uniform(tmem_base);
+  if (tid < 32 && fc::elect_one()) {
+    const uint32_t a0 = fc::smem_u32(smem), b0 = a0 + 32768;
+    const uint64_t ad = fc::smem_desc(a0, 128, 256), bd = fc::smem_desc(b0, 128, 256);
+    long long c0 = clock64();
+    for (int r = 0; r < 2; ++r) {
+      if (r == 1) c0 = clock64();
+      for (int s = 0; s < nmma; ++s) {
+        const uint32_t idesc = fc::idesc_f16(128, N, false, false);
+        if (ts) fc::mma_f16_ts(tb, tb + 256, bd, idesc, s > 0);
+        else fc::mma_f16_ss(tb, ad, bd, idesc, s > 0);
+      }
+      long long ci = clock64();
+      fc::mma_commit(&bar);
+      fc::mbar_wait(&bar, r);
+      long long c1 = clock64();
+      out[2 * r] = ci - c0;
+      out[2 * r + 1] = c1 - c0;
+    }
+  }
+  fc::tc_fence_before();
+  __syncthreads();
+  if (tid < 32) fc::tmem_dealloc<512>(tb);
+}
+}  // namespace
+
+extern "C" int fcst_tmem_ld_bench(int iters, int nwarps, long long* host_out) {
+  long long* d;
+  cudaMalloc(&d, 16);
+  tmem_ld_bench_kernel<<<1, 512>>>(iters, nwarps, d);
+  cudaError_t e = cudaMemcpy(host_out, d, 8, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e == cudaSuccess ? 0 : 100 + (int)e;
+}
+
+extern "C" int fcst_mma_rate(int nmma, int N, int ts, long long* host_out) {
+  long long* d;
+  cudaMalloc(&d, 32);
+  cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  mma_rate_kernel<<<1, 128, 65536>>>(nmma, N, ts, d);
+  cudaError_t e = cudaMemcpy(host_out, d, 32, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e == cudaSuccess ? 0 : 100 + (int)e;
+}

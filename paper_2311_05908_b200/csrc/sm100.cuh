@@ -44,6 +44,19 @@ FC_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity), "r"(10000000)
       : "memory");
 }
+// Arm an mbarrier with one arrival and an expected transaction byte count.
+FC_DEVICE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// Bulk (TMA, non-tensor) copy global -> shared; completes `bytes` on `bar`.
+// dst, src 16 B aligned, bytes a multiple of 16.
+FC_DEVICE void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 // Named barrier over `nthreads` threads (warp-aligned groups).
 FC_DEVICE void named_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

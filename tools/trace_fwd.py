@@ -29,5 +29,7 @@ for wsel in (0, 1):
     print(f"warp {4*wsel}: tiles {len(d)}  tile cycles median {np.median(buf[wsel,ok,14]-buf[wsel,ok,0]):.0f}")
     for i, nm in enumerate(names):
         print(f"  {nm:8s} {np.median(d[:, i]):8.0f} {np.mean(d[:, i]):8.0f}")
+    e4w = (buf[wsel, ok, 15] - buf[wsel, ok, 12])[2:]
+    print(f"  epi4 until MMA wait done {np.median(e4w):8.0f}")
     nxt = buf[wsel, ok, 0][1:] - buf[wsel, ok, 14][:-1]
     print("  gap to next tile", np.median(nxt))
