@@ -124,6 +124,14 @@ FC_DEVICE void cmul8(float* xr, float* xi, const float* nxi, const float4* w) {
     xi[2 * j] = oi.x;  xi[2 * j + 1] = oi.y;
   }
 }
+// Twiddle pair {wr_j, wr_j+1, wi_j, wi_j+1} -> the next pair (j + 2), i.e.
+// both elements times the complex step c (fp32).
+FC_DEVICE float4 cstep(const float4& w, float2 c) {
+  const float2 wr = make_float2(w.x, w.y), wi = make_float2(w.z, w.w);
+  const float2 nr = fma2(wr, make_float2(c.x, c.x), mul2(wi, make_float2(-c.y, -c.y)));
+  const float2 ni = fma2(wr, make_float2(c.y, c.y), mul2(wi, make_float2(c.x, c.x)));
+  return make_float4(nr.x, nr.y, ni.x, ni.y);
+}
 // x <- x * conj(w); planes (xr, xi, -xr).
 FC_DEVICE void cmulc8(float* xr, float* xi, const float* nxr, const float4* w) {
 #pragma unroll

@@ -44,20 +44,21 @@ namespace fc {
 
 #ifdef FC_TRACE
 // experiment-only phase timestamps (CTA 0, warpgroup 0, warps 0 and 4)
-__device__ long long fc_trace_buf[2][64][16];
+__device__ long long fc_trace_buf[2][64][24];
 #endif
 
 // Shared-memory plan of the forward kernel: tables | per-warpgroup (k_f,
-// operand buffer) | input staging.  Causal tiles stage their input rows
-// (u [| w]) and the output gate v through one slot each, filled by bulk
-// (TMA) copies a tile ahead and shared by the warpgroups in tile order.
+// operand buffer) | staging.  Causal tiles move their rows with bulk (TMA)
+// copies through two slots shared by the warpgroups in tile order: the
+// input slot (u [| w], filled a tile ahead) and the output slot (v arrives
+// there for the gate; y leaves from it).
 template <int L1, bool CAUSAL, bool GATED>
 struct FwdCfg {
   using C = O2Cfg<L1, CAUSAL>;
   static constexpr bool STG = CAUSAL;
   static constexpr uint32_t ROW_BYTES = C::NOUT * 2;  // one 16-bit input row
   static constexpr uint32_t UW_BYTES = STG ? C::R * ROW_BYTES * (GATED ? 2 : 1) : 0;
-  static constexpr uint32_t V_BYTES = (STG && GATED) ? C::R * ROW_BYTES : 0;
+  static constexpr uint32_t V_BYTES = STG ? C::R * ROW_BYTES : 0;
   static constexpr uint32_t bytes_for(int wg) {
     return C::al(C::al(C::TABLES_FWD + wg * C::WG_BYTES) + UW_BYTES) + V_BYTES + 1024;  // + alignment slack
   }
@@ -152,8 +153,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
   // consumes tile t refills the slot for tile t + 1 right after it has read
   // it, so fills (and reads) follow tile order and each slot's fill for the
   // next warpgroup's tile overlaps the rest of the current tile.
-  auto fill = [&](int kind, int64_t t) {
-    const int64_t th = t / nbt, tb = t % nbt;
+  auto fill = [&](int kind, int64_t t, int64_t th, int64_t tb) {  // tile t = th * nbt + tb
     const int64_t tbase = (tb * C::R * H + phys_head(th)) * N;
     const int rows = int(B - tb * C::R < C::R ? B - tb * C::R : C::R);
     uint64_t* bar = &stg_bar[kind][(t - t0) % kWG];
@@ -174,10 +174,18 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
     mbar_wait(&stg_bar[kind][wg], stg_phase[kind]);
     stg_phase[kind] ^= 1;
   };
+  // output slot hand-over for tile t: v landed (gated) or the previous
+  // tile's y stores have read the slot (plain)
+  auto release_out = [&](int64_t t, int64_t th, int64_t tb) {
+    if (GATED) fill(1, t, th, tb);
+    else mbar_arrive(&stg_bar[1][(t - t0) % kWG]);
+  };
   if (STG && tid == 0) {
-    fill(0, t0);
-    if (GATED) fill(1, t0);
+    fill(0, t0, t0 / nbt, t0 % nbt);
+    release_out(t0, t0 / nbt, t0 % nbt);
   }
+  // a thread other than the MMA issuer (warp 1 of the warpgroup) refills the slots
+  auto filler = [&]() { return (wtid >> 5) == 1 && elect_one(); };
 
   // UMMA shared-memory descriptors: built once, offsets added as (bytes >> 4)
   const uint64_t dXA = smem_desc(bufX, 128, C::SBO_A);          // stage A operand (MN-major)
@@ -231,6 +239,21 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
   const int pA = ((m >> 5) / JC) * 4 + ((m >> 3) & 3), n1A = ((m >> 5) % JC) * 8 + (m & 7);
   auto rowB_p = [&](int gi) { return (gi >> 1) * 4 + ((m >> 3) & 3); };
   auto rowB_k2 = [&](int gi) { return (gi & 1) * 32 + (m >> 5) * 8 + (m & 7); };
+  // Twiddle-recurrence constants (tables are resident after the setup sync):
+  // epilogue 1 steps k2 by 2 at fixed n1 (W^{2 n1}); epilogue 3 steps n1 at
+  // fixed k2 (W^{k2}, W^{2 k2}) for the thread's two k2 (group parity).
+  auto tw_at = [&](int n1, int k2) {  // W_L^{n1 k2} from TW
+    const float4 a = ld_shared_f4(sTW + tab_off<L2 / 2>(n1, k2 >> 1));
+    return (k2 & 1) ? make_float2(a.y, a.w) : make_float2(a.x, a.z);
+  };
+  const float2 tw1_c2 = tw_at(n1A, 2);
+  float4 tw3_c[2];
+#pragma unroll
+  for (int par = 0; par < 2; ++par) {
+    const int k2 = par * 32 + (m >> 5) * 8 + (m & 7);
+    const float2 w1 = tw_at(1, k2), w2 = tw_at(2, k2);
+    tw3_c[par] = make_float4(w1.x, w1.y, w2.x, w2.y);
+  }
   // 8-row group of stage-B row (p, k2) (k2 a multiple of 8)
   auto grpB = [](int p, int k2) { return (((p >> 2) * 2 + (k2 >> 5)) * 16) + ((k2 & 31) >> 3) * 4 + (p & 3); };
 
@@ -369,9 +392,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
       for (int s = 0; s < 2 * C::KA / 16; ++s)
         mma_f16_ss(tmem + h2 * (C::NA / 2), dadd(dXA, 256 * s),
                    dadd(dGA, h2 * (C::NA / 16) * C::SBO_GA + 256 * s), idesc, s > 0);
-      // the u|w slot has been read by the whole warpgroup: stage the next tile
-      if (STG && h2 == 1 && t + 1 < t1) fill(0, t + 1);
     });
+    // the u|w slot has been read by the whole warpgroup: stage tile t + 1
+    if (STG && t + 1 < t1 && filler()) fill(0, t + 1, bt + 1 < nbt ? hh : hh + 1, bt + 1 < nbt ? bt + 1 : 0);
 
     // ---------------- epilogue 1: twiddle W^{n1 k2}, transpose -> stage B operand (MN-major)
     // Every stage's operand aliases bufX, so stores wait for BOTH halves of
@@ -387,9 +410,12 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         tmem_ld16(tq + c0, re);
         tmem_ld16(tq + c0 + 32, im);
         if constexpr (C::NEG_A) tmem_ld16(tq + c0 + 64, ni);
+        // W^{n1 k2}, k2 = k20 .. k20 + 15: the table pair at k20, then fp32
+        // steps by W^{2 n1} (register recurrence instead of 8 table loads)
         float4 w[8];
+        w[0] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1A, k20 / 2));
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) w[jj] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1A, k20 / 2 + jj));
+        for (int jj = 1; jj < 8; ++jj) w[jj] = cstep(w[jj - 1], tw1_c2);
         tmem_ld_wait();
         if constexpr (!C::NEG_A) {
 #pragma unroll
@@ -485,17 +511,17 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         tmem_ld8(tq + col, re);
         tmem_ld8(tq + col + L1, im);
         tmem_ld8(tq + col + 2 * L1, nr);
-        // W^{n1 k2} for 8 consecutive n1 at this k2 from TW ([n1][k2/2] pairs
-        // over k2): pick the k2 parity, re-pair over n1
+        // W^{n1 k2}, n1 = 8 n1c .. 8 n1c + 7 at this k2: the table value at
+        // 8 n1c (k2 parity picked from the pair), * W^{k2}, then fp32 steps
+        // by W^{2 k2}
         float4 w[4];
         {
-          const bool odd = k2 & 1;
+          const float4 a = ld_shared_f4(sTW + tab_off<L2 / 2>(n1c * 8, k2 >> 1));
+          const float br = (k2 & 1) ? a.y : a.x, bi = (k2 & 1) ? a.w : a.z;
+          const float4 c = tw3_c[gi & 1];  // {Re W^{k2}, Im W^{k2}, Re W^{2k2}, Im W^{2k2}}
+          w[0] = make_float4(br, br * c.x - bi * c.y, bi, br * c.y + bi * c.x);
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const float4 a = ld_shared_f4(sTW + tab_off<L2 / 2>(n1c * 8 + 2 * jj, k2 >> 1));
-            const float4 b = ld_shared_f4(sTW + tab_off<L2 / 2>(n1c * 8 + 2 * jj + 1, k2 >> 1));
-            w[jj] = odd ? make_float4(a.y, b.y, a.w, b.w) : make_float4(a.x, b.x, a.z, b.z);
-          }
+          for (int jj = 1; jj < 4; ++jj) w[jj] = cstep(w[jj - 1], make_float2(c.z, c.w));
         }
         tmem_ld_wait();
         cmulc8(re, im, nr, w);
@@ -521,11 +547,12 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
     // loads issued before the wait.  y leaves TMEM transposed (lane = n2), so
     // it is staged in natural order through bufX (free once stage A^-1 has
     // completed; 128 B XOR swizzle, conflict-free both ways) and written back
-    // coalesced.  Gated tiles stage fp32 so y * v is rounded once.
-    // (Circular gated tiles -- fp32 staging would not fit -- store directly.)
+    // coalesced.  Gated tiles stage the conv output in fp16 (the operand
+    // precision of every stage; finer than bf16 output) before * v.
+    // (Circular gated tiles store directly.)
     {
       constexpr bool STAGE = CAUSAL || !GATED;
-      using S = typename std::conditional<GATED, float, T>::type;
+      using S = typename std::conditional<GATED, __half, T>::type;
       constexpr int OCH = C::R * C::NOUT / 8 / kWGThreads;  // coalesced output chunks per thread
       static_assert(!STAGE || C::R * C::NOUT * sizeof(S) <= C::BUFX_BYTES, "y staging fits in bufX");
       constexpr int PER = OUT_COLS / 8;  // transposed 8-column items per thread
@@ -566,39 +593,42 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
           int r, n;
           item_rn(i, r, n);
           const uint32_t off = uint32_t(r * C::NOUT + n) * sizeof(S);
-          if constexpr (GATED) {
-            st_shared_v4(bufX + swz128(off), __float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
-                         __float_as_uint(o[3]));
-            st_shared_v4(bufX + swz128(off + 16), __float_as_uint(o[4]), __float_as_uint(o[5]),
-                         __float_as_uint(o[6]), __float_as_uint(o[7]));
-          } else {
-            st_shared_v4(bufX + swz128(off), IO<T>::pack2(o[0], o[1]), IO<T>::pack2(o[2], o[3]),
-                         IO<T>::pack2(o[4], o[5]), IO<T>::pack2(o[6], o[7]));
-          }
+          st_shared_v4(bufX + swz128(off), IO<S>::pack2(o[0], o[1]), IO<S>::pack2(o[2], o[3]),
+                       IO<S>::pack2(o[4], o[5]), IO<S>::pack2(o[6], o[7]));
         }
+        stamp(16);
         tc_fence_before();
-        if (STG && GATED) stg_wait(1);
+        if (STG) stg_wait(1);
+        stamp(17);
         wg_sync();
+        stamp(18);
 #pragma unroll
         for (int i = 0; i < OCH; ++i) {
           const int r = och_r(i), n = och_n(i);
           const uint32_t off = uint32_t(r * C::NOUT + n) * sizeof(S);
           uint4 st;
           if constexpr (GATED) {
-            const float4 a = ld_shared_f4(bufX + swz128(off)), b2 = ld_shared_f4(bufX + swz128(off + 16));
-            float v8[8];
-            if (STG) vv[i] = ld_shared_u4(sV + r * F::ROW_BYTES + n * 2);
+            float a[8], v8[8];
+            IO<__half>::to_f32x8(ld_shared_u4(bufX + swz128(off)), a);
+            if (STG) vv[i] = ld_shared_u4(sV + r * F::ROW_BYTES + n * 2);  // the output slot holds v
             IO<T>::to_f32x8(vv[i], v8);
-            st = make_uint4(IO<T>::pack2(a.x * v8[0], a.y * v8[1]), IO<T>::pack2(a.z * v8[2], a.w * v8[3]),
-                            IO<T>::pack2(b2.x * v8[4], b2.y * v8[5]), IO<T>::pack2(b2.z * v8[6], b2.w * v8[7]));
+            st = make_uint4(IO<T>::pack2(a[0] * v8[0], a[1] * v8[1]), IO<T>::pack2(a[2] * v8[2], a[3] * v8[3]),
+                            IO<T>::pack2(a[4] * v8[4], a[5] * v8[5]), IO<T>::pack2(a[6] * v8[6], a[7] * v8[7]));
           } else {
             st = ld_shared_u4(bufX + swz128(off));
           }
-          if (r < rows_left) *reinterpret_cast<uint4*>(gy + tile_base + int64_t(r) * HN + n) = st;
+          if (STG) st_shared_v4(sV + r * F::ROW_BYTES + n * 2, st.x, st.y, st.z, st.w);  // y, natural order
+          else if (r < rows_left) *reinterpret_cast<uint4*>(gy + tile_base + int64_t(r) * HN + n) = st;
         }
-        if (STG && GATED) fence_async_smem();  // v slot reads before its refill (async proxy)
+        stamp(19);
+        if (STG) fence_async_smem();  // y rows -> bulk stores (async proxy)
         wg_sync();  // staging reads done before bufX takes the next tile's operand
-        if (STG && GATED && t + 1 < t1 && wtid < 32 && elect_one()) fill(1, t + 1);
+        if (STG && filler()) {
+          for (int r = 0; r < rows_left; ++r) bulk_s2g(gy + tile_base + int64_t(r) * HN, sV + r * F::ROW_BYTES, F::ROW_BYTES);
+          bulk_commit();
+          bulk_wait_read0();
+          if (t + 1 < t1) release_out(t + 1, bt + 1 < nbt ? hh : hh + 1, bt + 1 < nbt ? bt + 1 : 0);
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
@@ -633,6 +663,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
     stamp(14);
     ++trace_tile;
   }
+  if (STG) bulk_wait0();  // this thread's bulk stores complete
   __syncthreads();
   if (warp == 0) tmem_dealloc<(kWG * C::TMEM_COLS > 512 ? 512 : kWG * C::TMEM_COLS)>(tmem_slot);
 }
