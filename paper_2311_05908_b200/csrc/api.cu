@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -16,6 +17,18 @@ using namespace fc;
 
 namespace {
 thread_local int64_t g_launches = 0;
+
+// Chunk size of the multipass intermediate kept in L2 (bytes); FFTCONV_CHUNK_MB
+// overrides it for experiments (0 = one chunk, the default: measured on B200,
+// chunks of 16-96 MB were 3-50% slower -- the passes are not HBM-bound).
+size_t chunk_target_bytes() {
+  static size_t v = [] {
+    const char* e = getenv("FFTCONV_CHUNK_MB");
+    const long mb = e ? atol(e) : 0;
+    return mb > 0 ? size_t(mb) << 20 : ~size_t(0) >> 1;
+  }();
+  return v;
+}
 
 int num_sms_current() {
   static int cache[64] = {0};
@@ -91,6 +104,8 @@ extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float*
   if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
     const size_t block = size_t(p->L2) * tab_stride(uint32_t(p->L1 / 2));
     prm.L = p->Lp;
+    if (p->sparse && p->row_map.size() < size_t(p->L0))
+      prm.row_keep = static_cast<const uint8_t*>(p->d_tables) + p->row_keep_off;
     e = launch_mp_precompute_kf(prm, p->lev_L0, p->nlev, p->L, block, reinterpret_cast<cudaStream_t>(stream));
     g_launches += H > 0 ? 2 + p->nlev - 1 : 0;
   } else {
@@ -130,6 +145,53 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     }
     if (p->nlev > 1) mp.wtab = nullptr;  // deep plans: outer twiddles on the fly
     mp.Llev = p->L;
+    if (p->nlev == 1) {
+      // One outer level: run the three passes chunk by chunk over (pairs,
+      // heads) so the chunk's intermediate T stays resident in L2 between
+      // pass 1, the inner pass and pass 3 (Alg. 4's extra I/O, then
+      // never reaches HBM); chunks reuse the start of the workspace.
+      const int64_t Bv = mp.B, pairs = (Bv + 1) / 2;
+      const size_t per_pair_head = size_t(4) * size_t(p->L);  // fp16 re + im planes
+      const size_t target = chunk_target_bytes();
+      int64_t Hc = H, Pc = pairs;
+      if (size_t(pairs) * per_pair_head * size_t(H) > target) {
+        Hc = int64_t(target / (size_t(pairs) * per_pair_head));
+        if (Hc < 1) {
+          Hc = 1;
+          Pc = int64_t(target / per_pair_head);
+          if (Pc < 1) Pc = 1;
+        }
+      }
+      int launches = 0;
+      for (int64_t pc0 = 0; pc0 < pairs; pc0 += Pc) {
+        const int64_t rows_c = (2 * (pc0 + Pc) < Bv ? 2 * Pc : Bv - 2 * pc0);
+        for (int64_t h0 = 0; h0 < H; h0 += Hc) {
+          const int64_t hc = H - h0 < Hc ? H - h0 : Hc;
+          MpParams c = mp;
+          c.B = rows_c; c.H = hc; c.h0 = h0; c.Hg = H; c.pair0 = pc0; c.ws = ws;
+          cudaError_t e = launch_mp_pass(c, 1, st);
+          if (e != cudaSuccess) return cuda_fail(fn, e);
+          FwdParams in{};
+          in.u = ws; in.y = ws; in.tables = p->d_tables;
+          in.kf = static_cast<const uint8_t*>(kf) + size_t(h0) * p->kf_bytes_per_head;
+          in.B = 2 * ((rows_c + 1) / 2); in.H = hc * p->L0; in.N = p->Lp;
+          in.L1 = p->L1; in.causal = 0; in.gated = 0; in.dtype = 0;
+          in.num_sms = num_sms_current();
+          if (skip) {
+            in.row_map = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(p->d_tables) + p->row_map_off);
+            in.nrow = int32_t(p->row_map.size());
+            in.row_L0 = p->L0;
+          }
+          e = launch_fwd_fused(in, st);
+          if (e != cudaSuccess) return cuda_fail(fn, e);
+          e = launch_mp_pass(c, 3, st);
+          if (e != cudaSuccess) return cuda_fail(fn, e);
+          launches += 3;
+        }
+      }
+      g_launches += launches;
+      return FFTCONV_OK;
+    }
     const int64_t rows = 2 * ((mp.B + 1) / 2);
     const size_t tbytes = size_t(rows) * size_t(H) * size_t(p->L) * 2;
     void* Tb[2] = {ws, static_cast<uint8_t*>(ws) + tbytes};

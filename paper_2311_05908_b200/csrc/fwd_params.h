@@ -32,6 +32,9 @@ struct KfParams {
   const float2* twiddle;  // W_L^e, e < L (plan table)
   int64_t H, K, L;
   int32_t L1, L2;
+  // multipass sparse plans: inner rows k0 with row_keep[k0] == 0 are never
+  // read by the inner pass, so their k_f blocks are not computed
+  const uint8_t* row_keep;
 };
 cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s);
 
@@ -61,6 +64,11 @@ struct MpParams {
   // the fly when wtab == nullptr
   int32_t circ;
   int64_t Llev;
+  // chunked execution (L2-resident T): this launch covers pairs
+  // [pair0, pair0 + (B+1)/2) and heads [h0, h0 + H) of a signal with Hg
+  // heads; T is indexed by the chunk-local (pair, head), u/w/v/y by the
+  // global ones.  Hg = 0 means Hg = H (unchunked).
+  int64_t pair0, h0, Hg;
 };
 cudaError_t launch_mp_pass(const MpParams& prm, int pass, cudaStream_t s);
 

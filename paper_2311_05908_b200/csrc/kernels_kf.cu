@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(256) mp_kf_rows_kernel(const KfParams prm, int
   float2* tws = sm + L;
   const int64_t blk = blockIdx.x;  // h * L0 + k0
   const int k0 = int(blk % L0);
+  if (prm.row_keep && !prm.row_keep[k0]) return;  // masked row: never read
   uint8_t* block = reinterpret_cast<uint8_t*>(prm.kf) + blk * block_bytes;
   {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.twiddle);

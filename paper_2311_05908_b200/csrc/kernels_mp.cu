@@ -19,6 +19,7 @@
 #include <type_traits>
 
 #include "dft_small.cuh"
+#include "dft_vec.cuh"
 #include "fwd_params.h"
 #include "sm100.cuh"
 
@@ -47,223 +48,312 @@ FC_DEVICE void st2<__nv_bfloat16>(__nv_bfloat16* p, float a, float b) {
   *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(a, b);
 }
 
-// Each thread owns two adjacent columns (n', n'+1) of one (pair, head).
-template <int L0, bool GATED, typename T>
+// Outer passes.  Each thread owns COLS adjacent columns n' of one (pair,
+// head); every complex value is a column vector (dft_vec.cuh), so the
+// DFT_L0 over n0 runs on packed f32x2 instructions and every global access
+// is a COLS-wide vector (a warp reads/writes 32 * COLS consecutive elements
+// of a row).  MODE: 0 causal (inputs n0 < L0/2, outputs n0 < L0/2),
+// 1 partial (overlap-save window: all inputs, outputs n0 >= L0/2), 2 circular
+// (deep levels: complex rows in and out).
+template <int L0>
+struct PassCfg {
+  static constexpr int COLS = L0 <= 8 ? 4 : 2;
+  static constexpr int C2 = COLS / 2;
+};
+
+template <typename T, int COLS>
+FC_DEVICE void ld_cols(const T* p, float* f) {
+  if constexpr (COLS == 4) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    const float2 a = ld2<T>(reinterpret_cast<const T*>(&v.x)), b = ld2<T>(reinterpret_cast<const T*>(&v.y));
+    f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+  } else {
+    const float2 a = ld2<T>(p);
+    f[0] = a.x; f[1] = a.y;
+  }
+}
+template <typename T, int COLS>
+FC_DEVICE void st_cols(T* p, const float* f) {
+  if constexpr (COLS == 4) {
+    uint2 v;
+    st2<T>(reinterpret_cast<T*>(&v.x), f[0], f[1]);
+    st2<T>(reinterpret_cast<T*>(&v.y), f[2], f[3]);
+    *reinterpret_cast<uint2*>(p) = v;
+  } else {
+    st2<T>(p, f[0], f[1]);
+  }
+}
+
+// per-column twiddle base W_Llev^{n + j}: plan table (W_L^{n'}, n' < Lp) for
+// one-level plans (wtab set), else sincospif of an exact dyadic fraction
+template <int C2>
+FC_DEVICE CV<C2> twiddle_base(const MpParams& prm, int n) {
+  CV<C2> bw;
+#pragma unroll
+  for (int c = 0; c < C2; ++c) {
+    float2 w0, w1;
+    if (prm.wtab) {
+      const float4 q = *reinterpret_cast<const float4*>(prm.wbase + n + 2 * c);
+      w0 = make_float2(q.x, q.y);
+      w1 = make_float2(q.z, q.w);
+    } else {
+      float sn, cs;
+      sincospif(-2.0f * float(n + 2 * c) / float(prm.Llev), &sn, &cs);
+      w0 = make_float2(cs, sn);
+      sincospif(-2.0f * float(n + 2 * c + 1) / float(prm.Llev), &sn, &cs);
+      w1 = make_float2(cs, sn);
+    }
+    bw.r[c] = make_float2(w0.x, w1.x);
+    bw.i[c] = make_float2(w0.y, w1.y);
+  }
+  return bw;
+}
+
+template <int L0, int MODE, bool GATED, typename T>
 __global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
-  const int64_t NP = int64_t(prm.Lp) / 2;  // column pairs per (pair, head)
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t pairs = (prm.B + 1) / 2;
-  if (idx >= pairs * prm.H * NP) return;
-  const int cp = int(idx % NP);
-  const int64_t ph = idx / NP;
-  const int64_t h = ph % prm.H, p = ph / prm.H;
-  const int n = 2 * cp;  // first column n'
+  constexpr int COLS = PassCfg<L0>::COLS, C2 = PassCfg<L0>::C2;
+  constexpr int NIN = MODE == 0 ? L0 / 2 : L0;
+  const int64_t NCH = int64_t(prm.Lp) / COLS;  // column groups per (pair, head)
+  // 32-bit index math (the launcher checks pairs * H * NCH < 2^31); NCH is a power of two
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t pairs = uint32_t((prm.B + 1) / 2);
+  if (idx >= pairs * uint32_t(prm.H) * uint32_t(NCH)) return;
+  const int n = int(idx & uint32_t(NCH - 1)) * COLS;
+  const uint32_t ph = idx >> (31 - __clz(uint32_t(NCH)));
+  const int64_t h = ph % uint32_t(prm.H), p = ph / uint32_t(prm.H);
   const int64_t b0 = 2 * p, b1 = 2 * p + 1;
   const bool has1 = b1 < prm.B;
   const T* __restrict__ u = reinterpret_cast<const T*>(prm.u);
   const T* __restrict__ w = reinterpret_cast<const T*>(prm.w);
   // element offset of sample n0 = 0 of each row; window start (may be < 0)
+  const int64_t Hg = prm.Hg ? prm.Hg : prm.H, hg = h + prm.h0;  // global head
+  const int64_t g0 = b0 + 2 * prm.pair0, g1 = g0 + 1;          // global rows
   int64_t r0, r1, s0 = 0, s1 = 0;
-  if (prm.partial) {
-    const int64_t j0 = b0 % prm.NC, j1 = b1 % prm.NC;
+  if (MODE == 1) {
+    const int64_t j0 = g0 % prm.NC, j1 = g1 % prm.NC;
     s0 = (j0 - 1) * prm.C;
     s1 = (j1 - 1) * prm.C;
-    r0 = ((b0 / prm.NC) * prm.H + h) * prm.N + s0 + n;
-    r1 = ((b1 / prm.NC) * prm.H + h) * prm.N + s1 + n;
+    r0 = ((g0 / prm.NC) * Hg + hg) * prm.N + s0 + n;
+    r1 = ((g1 / prm.NC) * Hg + hg) * prm.N + s1 + n;
   } else {
-    r0 = (b0 * prm.H + h) * prm.N + n;
-    r1 = (b1 * prm.H + h) * prm.N + n;
+    r0 = (g0 * Hg + hg) * prm.N + n;
+    r1 = (g1 * Hg + hg) * prm.N + n;
   }
-  float2 z0[L0], z1[L0];  // column n and n+1, complex z = g_b + i g_{b+1}
+  CV<C2> z[NIN];  // z = g_b + i g_{b+1}
 #pragma unroll
-  for (int n0 = 0; n0 < L0; ++n0) {
-    z0[n0] = make_float2(0.f, 0.f);
-    z1[n0] = make_float2(0.f, 0.f);
-  }
-  // causal: the zero-padded upper half is never loaded; partial: full window
-  constexpr int NL = L0;
-#pragma unroll
-  for (int n0 = 0; n0 < NL; ++n0) {
-    if (!prm.partial && !prm.circ && n0 >= L0 / 2) break;
+  for (int n0 = 0; n0 < NIN; ++n0) {
     const int64_t o = int64_t(n0) * prm.Lp;
-    const bool ok0 = s0 + o >= 0, ok1 = has1 && s1 + o >= 0;
-    float2 a = ok0 ? ld2<T>(u + r0 + o) : make_float2(0.f, 0.f);  // row b, columns n, n+1
-    float2 c = ok1 ? ld2<T>(u + r1 + o) : make_float2(0.f, 0.f);
+    const bool ok0 = MODE != 1 || s0 + o >= 0, ok1 = has1 && (MODE != 1 || s1 + o >= 0);
+    float a[COLS], c[COLS];
+#pragma unroll
+    for (int j = 0; j < COLS; ++j) a[j] = c[j] = 0.f;
+    if (ok0) ld_cols<T, COLS>(u + r0 + o, a);
+    if (ok1) ld_cols<T, COLS>(u + r1 + o, c);
     if (GATED) {
-      const float2 wa = ok0 ? ld2<T>(w + r0 + o) : make_float2(0.f, 0.f);
-      const float2 wc = ok1 ? ld2<T>(w + r1 + o) : make_float2(0.f, 0.f);
-      a.x *= wa.x; a.y *= wa.y;
-      c.x *= wc.x; c.y *= wc.y;
+      float wa[COLS], wc[COLS];
+#pragma unroll
+      for (int j = 0; j < COLS; ++j) wa[j] = wc[j] = 0.f;
+      if (ok0) ld_cols<T, COLS>(w + r0 + o, wa);
+      if (ok1) ld_cols<T, COLS>(w + r1 + o, wc);
+#pragma unroll
+      for (int j = 0; j < COLS; ++j) { a[j] *= wa[j]; c[j] *= wc[j]; }
     }
-    z0[n0] = make_float2(a.x, c.x);
-    z1[n0] = make_float2(a.y, c.y);
+#pragma unroll
+    for (int cc = 0; cc < C2; ++cc) {
+      z[n0].r[cc] = make_float2(a[2 * cc], a[2 * cc + 1]);
+      z[n0].i[cc] = make_float2(c[2 * cc], c[2 * cc + 1]);
+    }
   }
   // DFT_L0 over n0.  Causal rows are zero for n0 >= L0/2, so the first
   // radix-2 stage reduces to X[2m] = DFT_{L0/2}(z)[m],
   // X[2m+1] = DFT_{L0/2}(z W_L0^{n0})[m].
-  float2 X0[L0], X1[L0];
-  if (!prm.partial && !prm.circ) {
-    float2 a0[L0 / 2], b0[L0 / 2], a1[L0 / 2], b1[L0 / 2];
+  CV<C2> X[L0];
+  if constexpr (MODE == 0) {
+    CV<C2> a[L0 / 2], b[L0 / 2];
 #pragma unroll
     for (int n0 = 0; n0 < L0 / 2; ++n0) {
-      const float2 w = w_root<L0>(n0);
-      a0[n0] = z0[n0];
-      a1[n0] = z1[n0];
-      b0[n0] = c_mul(z0[n0], w);
-      b1[n0] = c_mul(z1[n0], w);
+      a[n0] = z[n0];
+      if (n0 == 0) {
+        b[n0] = z[n0];
+      } else if (4 * n0 == L0) {  // * (-i)
+#pragma unroll
+        for (int cc = 0; cc < C2; ++cc) {
+          b[n0].r[cc] = z[n0].i[cc];
+          b[n0].i[cc] = make_float2(-z[n0].r[cc].x, -z[n0].r[cc].y);
+        }
+      } else {
+        const float2 wr = w_root<L0>(n0);
+        b[n0] = cv_mul_s(z[n0], wr.x, wr.y);
+      }
     }
-    DftReg<L0 / 2, false>::run(a0);
-    DftReg<L0 / 2, false>::run(b0);
-    DftReg<L0 / 2, false>::run(a1);
-    DftReg<L0 / 2, false>::run(b1);
+    DftVec<L0 / 2, false, C2>::run(a);
+    DftVec<L0 / 2, false, C2>::run(b);
 #pragma unroll
     for (int m = 0; m < L0 / 2; ++m) {
-      X0[2 * m] = a0[m]; X0[2 * m + 1] = b0[m];
-      X1[2 * m] = a1[m]; X1[2 * m + 1] = b1[m];
+      X[2 * m] = a[m];
+      X[2 * m + 1] = b[m];
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < L0; ++i) { X0[i] = z0[i]; X1[i] = z1[i]; }
-    DftReg<L0, false>::run(X0);
-    DftReg<L0, false>::run(X1);
+    for (int i = 0; i < L0; ++i) X[i] = z[i];
+    DftVec<L0, false, C2>::run(X);
   }
-  // twiddle W_L^{n' k0} from the plan table [k0][n'], scale 1/sqrt(L0)
+  // twiddle W_L^{n' k0} (recurrence over k0 from W_L^{n'}), scale 1/sqrt(L0)
+  const CV<C2> bw = twiddle_base<C2>(prm, n);
   const float s = rsqrtf(float(L0));
+  CV<C2> tw;
+#pragma unroll
+  for (int cc = 0; cc < C2; ++cc) {
+    tw.r[cc] = make_float2(s, s);
+    tw.i[cc] = make_float2(0.f, 0.f);
+  }
   __half* __restrict__ Tre = reinterpret_cast<__half*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
   __half* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
-  // on-the-fly twiddles (deep levels): W_Llev^{n k0} by recurrence from
-  // W_Llev^{n} (sincospif of an exact dyadic fraction; error ~ L0 ulp)
-  float2 bw0 = make_float2(1.f, 0.f), bw1 = bw0, tw0 = bw0, tw1 = bw0;
-  if (!prm.wtab) {
-    float sn, cs;
-    sincospif(-2.0f * float(n) / float(prm.Llev), &sn, &cs);
-    bw0 = make_float2(cs, sn);
-    sincospif(-2.0f * float(n + 1) / float(prm.Llev), &sn, &cs);
-    bw1 = make_float2(cs, sn);
+  uint32_t keep = ~0u;  // masked rows (sparse plans) are skipped downstream
+  if (prm.row_keep) {
+    keep = 0;
+#pragma unroll
+    for (int k0 = 0; k0 < L0; ++k0) keep |= prm.row_keep[k0] ? (1u << k0) : 0u;
   }
 #pragma unroll
   for (int k0 = 0; k0 < L0; ++k0) {
-    float4 tw;
-    if (prm.wtab) {
-      tw = *reinterpret_cast<const float4*>(prm.wtab + int64_t(k0) * prm.Lp + n);
-    } else {
-      tw = make_float4(tw0.x, tw0.y, tw1.x, tw1.y);
-      tw0 = c_mul(tw0, bw0);
-      tw1 = c_mul(tw1, bw1);
-    }
-    const float2 a = c_mul(X0[k0], make_float2(tw.x, tw.y)), c = c_mul(X1[k0], make_float2(tw.z, tw.w));
-    if (!prm.row_keep || prm.row_keep[k0]) {  // masked rows are skipped downstream
-      *reinterpret_cast<__half2*>(Tre + int64_t(k0) * prm.Lp) = __floats2half2_rn(a.x * s, c.x * s);
-      *reinterpret_cast<__half2*>(Tim + int64_t(k0) * prm.Lp) = __floats2half2_rn(a.y * s, c.y * s);
+    const CV<C2> o = cv_mul(X[k0], tw);
+    if (k0 + 1 < L0) tw = cv_mul(tw, bw);
+    if (keep & (1u << k0)) {
+      float fr[COLS], fi[COLS];
+#pragma unroll
+      for (int cc = 0; cc < C2; ++cc) {
+        fr[2 * cc] = o.r[cc].x; fr[2 * cc + 1] = o.r[cc].y;
+        fi[2 * cc] = o.i[cc].x; fi[2 * cc + 1] = o.i[cc].y;
+      }
+      st_cols<__half, COLS>(Tre + int64_t(k0) * prm.Lp, fr);
+      st_cols<__half, COLS>(Tim + int64_t(k0) * prm.Lp, fi);
     }
   }
 }
 
-template <int L0, bool GATED, typename T>
+template <int L0, int MODE, bool GATED, typename T>
 __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
-  const int64_t NP = int64_t(prm.Lp) / 2;
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t pairs = (prm.B + 1) / 2;
-  if (idx >= pairs * prm.H * NP) return;
-  const int cp = int(idx % NP);
-  const int64_t ph = idx / NP;
-  const int64_t h = ph % prm.H, p = ph / prm.H;
-  const int n = 2 * cp;
+  constexpr int COLS = PassCfg<L0>::COLS, C2 = PassCfg<L0>::C2;
+  const int64_t NCH = int64_t(prm.Lp) / COLS;
+  // 32-bit index math (the launcher checks pairs * H * NCH < 2^31); NCH is a power of two
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t pairs = uint32_t((prm.B + 1) / 2);
+  if (idx >= pairs * uint32_t(prm.H) * uint32_t(NCH)) return;
+  const int n = int(idx & uint32_t(NCH - 1)) * COLS;
+  const uint32_t ph = idx >> (31 - __clz(uint32_t(NCH)));
+  const int64_t h = ph % uint32_t(prm.H), p = ph / uint32_t(prm.H);
   const __half* __restrict__ Tre =
       reinterpret_cast<const __half*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
   const __half* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
-  float2 e0[L0 / 2], o0[L0 / 2], e1[L0 / 2], o1[L0 / 2];  // even / odd k0
-  float2 bw0 = make_float2(1.f, 0.f), bw1 = bw0, tw0 = bw0, tw1 = bw0;
-  if (!prm.wtab) {
-    float sn, cs;
-    sincospif(-2.0f * float(n) / float(prm.Llev), &sn, &cs);
-    bw0 = make_float2(cs, sn);
-    sincospif(-2.0f * float(n + 1) / float(prm.Llev), &sn, &cs);
-    bw1 = make_float2(cs, sn);
+  const CV<C2> bw = twiddle_base<C2>(prm, n);
+  const float s = rsqrtf(float(L0));
+  CV<C2> tw;
+#pragma unroll
+  for (int cc = 0; cc < C2; ++cc) {
+    tw.r[cc] = make_float2(s, s);
+    tw.i[cc] = make_float2(0.f, 0.f);
+  }
+  CV<C2> e[L0 / 2], o[L0 / 2];  // even / odd k0, conj-twiddled and scaled
+  // all rows are loaded up front (no load waits on another): dense plans
+  // unconditionally, sparse plans only the kept rows (the others were never
+  // written by pass 1)
+  using RawT = typename std::conditional<COLS == 4, uint2, uint32_t>::type;
+  RawT rr[L0], ri[L0];
+  const bool sparse = prm.row_keep != nullptr;
+#pragma unroll
+  for (int k0 = 0; k0 < L0; ++k0) {
+    if (!sparse || prm.row_keep[k0]) {
+      rr[k0] = *reinterpret_cast<const RawT*>(Tre + int64_t(k0) * prm.Lp);
+      ri[k0] = *reinterpret_cast<const RawT*>(Tim + int64_t(k0) * prm.Lp);
+    } else {
+      rr[k0] = RawT{};
+      ri[k0] = RawT{};
+    }
   }
 #pragma unroll
   for (int k0 = 0; k0 < L0; ++k0) {
-    const bool kept = !prm.row_keep || prm.row_keep[k0];
-    const float2 re = kept ? __half22float2(*reinterpret_cast<const __half2*>(Tre + int64_t(k0) * prm.Lp))
-                           : make_float2(0.f, 0.f);
-    const float2 im = kept ? __half22float2(*reinterpret_cast<const __half2*>(Tim + int64_t(k0) * prm.Lp))
-                           : make_float2(0.f, 0.f);
-    float4 tw;
-    if (prm.wtab) {
-      tw = *reinterpret_cast<const float4*>(prm.wtab + int64_t(k0) * prm.Lp + n);
-    } else {
-      tw = make_float4(tw0.x, tw0.y, tw1.x, tw1.y);
-      tw0 = c_mul(tw0, bw0);
-      tw1 = c_mul(tw1, bw1);
-    }
-    const float2 a = c_mulc(make_float2(re.x, im.x), make_float2(tw.x, tw.y));
-    const float2 c = c_mulc(make_float2(re.y, im.y), make_float2(tw.z, tw.w));
-    if (k0 & 1) { o0[k0 / 2] = a; o1[k0 / 2] = c; }
-    else { e0[k0 / 2] = a; e1[k0 / 2] = c; }
-  }
-  // inverse DFT_L0 over k0, half of the outputs: y[n0] = E[n0] +- W_L0^{-n0} O[n0]
-  DftReg<L0 / 2, true>::run(e0);
-  DftReg<L0 / 2, true>::run(o0);
-  DftReg<L0 / 2, true>::run(e1);
-  DftReg<L0 / 2, true>::run(o1);
-  // causal keeps n0 < L0/2 (lo), partial n0 >= L0/2 (hi), circular both
-  float2 x0[L0], x1[L0];
+    float fr[COLS], fi[COLS];
+    ld_cols<__half, COLS>(reinterpret_cast<const __half*>(&rr[k0]), fr);
+    ld_cols<__half, COLS>(reinterpret_cast<const __half*>(&ri[k0]), fi);
+    CV<C2> x;
 #pragma unroll
-  for (int m = 0; m < L0 / 2; ++m) {
-    float2 w = w_root<L0>(m);
-    w.y = -w.y;
-    const float2 t0 = c_mul(o0[m], w), t1 = c_mul(o1[m], w);
-    x0[m] = c_add(e0[m], t0);
-    x1[m] = c_add(e1[m], t1);
-    x0[m + L0 / 2] = c_sub(e0[m], t0);
-    x1[m + L0 / 2] = c_sub(e1[m], t1);
+    for (int cc = 0; cc < C2; ++cc) {
+      x.r[cc] = make_float2(fr[2 * cc], fr[2 * cc + 1]);
+      x.i[cc] = make_float2(fi[2 * cc], fi[2 * cc + 1]);
+    }
+    x = cv_mulc(x, tw);
+    if (k0 + 1 < L0) tw = cv_mul(tw, bw);
+    if (k0 & 1) o[k0 / 2] = x;
+    else e[k0 / 2] = x;
   }
-  const float s = rsqrtf(float(L0));
+  // inverse DFT_L0 over k0: y[m] = E[m] + W_L0^{-m} O[m], y[m + L0/2] = E[m] - W_L0^{-m} O[m]
+  DftVec<L0 / 2, true, C2>::run(e);
+  DftVec<L0 / 2, true, C2>::run(o);
+  CV<C2> xl[L0 / 2], xh[L0 / 2];
+#pragma unroll
+  for (int m = 0; m < L0 / 2; ++m) cv_bfly<L0, true>(m, e[m], o[m], xl[m], xh[m]);
   const int64_t b0 = 2 * p, b1 = 2 * p + 1;
   const bool has1 = b1 < prm.B;
   T* __restrict__ y = reinterpret_cast<T*>(prm.y);
   const T* __restrict__ v = reinterpret_cast<const T*>(prm.v);
+  const int64_t Hg = prm.Hg ? prm.Hg : prm.H, hg = h + prm.h0;  // global head
+  const int64_t g0 = b0 + 2 * prm.pair0, g1 = g0 + 1;          // global rows
   int64_t r0, r1;
-  if (prm.partial) {
-    r0 = ((b0 / prm.NC) * prm.H + h) * prm.N + (b0 % prm.NC) * prm.C + n;
-    r1 = ((b1 / prm.NC) * prm.H + h) * prm.N + (b1 % prm.NC) * prm.C + n;
+  if (MODE == 1) {
+    r0 = ((g0 / prm.NC) * Hg + hg) * prm.N + (g0 % prm.NC) * prm.C + n;
+    r1 = ((g1 / prm.NC) * Hg + hg) * prm.N + (g1 % prm.NC) * prm.C + n;
   } else {
-    r0 = (b0 * prm.H + h) * prm.N + n;
-    r1 = (b1 * prm.H + h) * prm.N + n;
+    r0 = (g0 * Hg + hg) * prm.N + n;
+    r1 = (g1 * Hg + hg) * prm.N + n;
   }
-  auto emit = [&](auto q0c, auto noutc) {
-    constexpr int Q0 = decltype(q0c)::value, NOUT = decltype(noutc)::value;
+  auto emit = [&](const CV<C2>& x, int64_t off) {
+    float a[COLS], c[COLS];  // rows b (real part), b+1 (imaginary part)
 #pragma unroll
-    for (int i0 = 0; i0 < NOUT; ++i0) {
-      const int n0 = i0 + Q0;
-      const int64_t o = int64_t(i0) * prm.Lp;
-      float a0 = x0[n0].x * s, a1 = x1[n0].x * s;  // row b
-      float c0 = x0[n0].y * s, c1 = x1[n0].y * s;  // row b+1
-      if (GATED) {
-        const float2 va = ld2<T>(v + r0 + o);
-        a0 *= va.x; a1 *= va.y;
-        if (has1) {
-          const float2 vc = ld2<T>(v + r1 + o);
-          c0 *= vc.x; c1 *= vc.y;
-        }
+    for (int cc = 0; cc < C2; ++cc) {
+      a[2 * cc] = x.r[cc].x; a[2 * cc + 1] = x.r[cc].y;
+      c[2 * cc] = x.i[cc].x; c[2 * cc + 1] = x.i[cc].y;
+    }
+    if (prm.y2) {  // second gated output (backward: dw = dg * u)
+      const T* v2 = reinterpret_cast<const T*>(prm.v2);
+      T* y2 = reinterpret_cast<T*>(prm.y2);
+      float g[COLS], q[COLS];
+      ld_cols<T, COLS>(v2 + r0 + off, g);
+#pragma unroll
+      for (int j = 0; j < COLS; ++j) q[j] = a[j] * g[j];
+      st_cols<T, COLS>(y2 + r0 + off, q);
+      if (has1) {
+        ld_cols<T, COLS>(v2 + r1 + off, g);
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) q[j] = c[j] * g[j];
+        st_cols<T, COLS>(y2 + r1 + off, q);
       }
-      if (prm.y2) {  // second gated output (backward: dw = dg * u)
-        const T* v2 = reinterpret_cast<const T*>(prm.v2);
-        T* y2 = reinterpret_cast<T*>(prm.y2);
-        const float2 vb = ld2<T>(v2 + r0 + o);
-        st2<T>(y2 + r0 + o, x0[n0].x * s * vb.x, x1[n0].x * s * vb.y);
-        if (has1) {
-          const float2 vd = ld2<T>(v2 + r1 + o);
-          st2<T>(y2 + r1 + o, x0[n0].y * s * vd.x, x1[n0].y * s * vd.y);
-        }
+    }
+    if (GATED) {
+      float g[COLS];
+      ld_cols<T, COLS>(v + r0 + off, g);
+#pragma unroll
+      for (int j = 0; j < COLS; ++j) a[j] *= g[j];
+      if (has1) {
+        ld_cols<T, COLS>(v + r1 + off, g);
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) c[j] *= g[j];
       }
-      st2<T>(y + r0 + o, a0, a1);
-      if (has1) st2<T>(y + r1 + o, c0, c1);
-        }
+    }
+    st_cols<T, COLS>(y + r0 + off, a);
+    if (has1) st_cols<T, COLS>(y + r1 + off, c);
   };
-  if (prm.circ) emit(std::integral_constant<int, 0>{}, std::integral_constant<int, L0>{});
-  else if (prm.partial) emit(std::integral_constant<int, L0 / 2>{}, std::integral_constant<int, L0 / 2>{});
-  else emit(std::integral_constant<int, 0>{}, std::integral_constant<int, L0 / 2>{});
+  // causal keeps n0 < L0/2 (lo), partial n0 >= L0/2 (hi), circular both;
+  // partial output rows start at the window's second half (offset 0 of y)
+  if (MODE != 1) {
+#pragma unroll
+    for (int m = 0; m < L0 / 2; ++m) emit(xl[m], int64_t(m) * prm.Lp);
+  }
+  if (MODE != 0) {
+    const int64_t q0 = MODE == 2 ? L0 / 2 : 0;
+#pragma unroll
+    for (int m = 0; m < L0 / 2; ++m) emit(xh[m], (q0 + m) * prm.Lp);
+  }
 }
 
 // k_f, step 1: per (head, column n'): DFT_L0 of k[n' + Lrow n0] (n0 < L0/2,
@@ -345,28 +435,36 @@ __global__ void __launch_bounds__(256) mp_cols_cplx_kernel(float2* data, int64_t
 // k_f, step 2 lives in kernels_kf.cu (row FFTs into the inner plan layout).
 cudaError_t launch_mp_kf_rows(const KfParams& prm, int L0, int Lp, size_t block_bytes, cudaStream_t s);
 
+template <int L0, int MODE, bool G, typename T>
+static void launch_pass_k(const MpParams& prm, int pass, unsigned grid, cudaStream_t s) {
+  if (pass == 1) mp_pass1_kernel<L0, MODE, G, T><<<grid, 256, 0, s>>>(prm);
+  else mp_pass3_kernel<L0, MODE, G, T><<<grid, 256, 0, s>>>(prm);
+}
+template <int L0, int MODE>
+static void launch_pass_m(const MpParams& prm, int pass, unsigned grid, cudaStream_t s) {
+  const bool g = prm.gated != 0;
+  if (prm.dtype == 0) {
+    if (g) launch_pass_k<L0, MODE, true, __half>(prm, pass, grid, s);
+    else launch_pass_k<L0, MODE, false, __half>(prm, pass, grid, s);
+  } else {
+    if (g) launch_pass_k<L0, MODE, true, __nv_bfloat16>(prm, pass, grid, s);
+    else launch_pass_k<L0, MODE, false, __nv_bfloat16>(prm, pass, grid, s);
+  }
+}
+
 template <int L0>
 static cudaError_t launch_mp_l0(const MpParams& prm, int pass, cudaStream_t s) {
-  const int64_t total = ((prm.B + 1) / 2) * prm.H * (prm.Lp / 2);
+  const int64_t total = ((prm.B + 1) / 2) * prm.H * (prm.Lp / PassCfg<L0>::COLS);
   const unsigned grid = unsigned((total + 255) / 256);
   if (total == 0) return cudaSuccess;
-  const bool g = prm.gated != 0;
-  if (pass == 1) {
-    if (prm.dtype == 0) {
-      if (g) mp_pass1_kernel<L0, true, __half><<<grid, 256, 0, s>>>(prm);
-      else mp_pass1_kernel<L0, false, __half><<<grid, 256, 0, s>>>(prm);
-    } else {
-      if (g) mp_pass1_kernel<L0, true, __nv_bfloat16><<<grid, 256, 0, s>>>(prm);
-      else mp_pass1_kernel<L0, false, __nv_bfloat16><<<grid, 256, 0, s>>>(prm);
-    }
+  if (total + 255 >= (int64_t(1) << 31) || (prm.Lp & (prm.Lp - 1))) return cudaErrorInvalidValue;
+  if (prm.circ) {  // deep levels: fp16 complex rows, never gated
+    if (prm.dtype != 0 || prm.gated) return cudaErrorInvalidValue;
+    launch_pass_k<L0, 2, false, __half>(prm, pass, grid, s);
+  } else if (prm.partial) {
+    launch_pass_m<L0, 1>(prm, pass, grid, s);
   } else {
-    if (prm.dtype == 0) {
-      if (g) mp_pass3_kernel<L0, true, __half><<<grid, 256, 0, s>>>(prm);
-      else mp_pass3_kernel<L0, false, __half><<<grid, 256, 0, s>>>(prm);
-    } else {
-      if (g) mp_pass3_kernel<L0, true, __nv_bfloat16><<<grid, 256, 0, s>>>(prm);
-      else mp_pass3_kernel<L0, false, __nv_bfloat16><<<grid, 256, 0, s>>>(prm);
-    }
+    launch_pass_m<L0, 0>(prm, pass, grid, s);
   }
   return cudaGetLastError();
 }

@@ -1,5 +1,6 @@
 """Experiment: per-phase clock64 stamps of the fused forward kernel (CTA 0,
-warpgroup 0, warps 0/4) from a -DFC_TRACE build (tools/trace_fwd.sh)."""
+warpgroup 0, warps 0/4) from a -DFC_TRACE build:
+  FFTCONV_LIB=<trace build> python tools/trace_fwd.py N [circular]"""
 import ctypes, os, sys
 import numpy as np
 import torch
@@ -8,28 +9,36 @@ from paper_2311_05908_b200 import FFTConvPlan
 from paper_2311_05908_b200 import _abi
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+circ = len(sys.argv) > 2 and sys.argv[2].startswith("circular")
+gated = not (len(sys.argv) > 2 and sys.argv[2].endswith("plain"))
 B, H = 64, 768
 dev = torch.device("cuda:0")
-plan = FFTConvPlan(N, 2 * N, torch.float16, causal=True)
+plan = FFTConvPlan(N, N if circ else 2 * N, torch.float16, causal=not circ)
 k = torch.randn(H, N, device=dev)
 kf = plan.precompute_kf(k)
 u = torch.randn(B, H, N, device=dev, dtype=torch.float16)
 w = torch.randn_like(u); v = torch.randn_like(u)
 for _ in range(3):
-    y = plan.gated_fwd(u, w, v, kf)
+    y = plan.gated_fwd(u, w, v, kf) if gated else plan.fwd(u, kf)
 torch.cuda.synchronize()
 lib = _abi.lib()
-buf = np.zeros((2, 64, 16), dtype=np.int64)
+buf = np.zeros((2, 64, 24), dtype=np.int64)
 lib.fc_trace_dump(buf.ctypes.data_as(ctypes.c_void_p))
-names = ["load", "syncA", "issA", "epi1", "syncB", "issB", "epi2", "syncBi", "issBi", "epi3", "syncAi", "issAi", "epi4", "endsync"]
+# stamp index -> phase ending there
+seq = [(1, "load/build"), (2, "syncA"), (3, "issA"), (4, "epi1"), (5, "syncB"), (6, "issB"), (7, "epi2"),
+       (8, "syncBi"), (9, "issBi"), (10, "epi3"), (11, "syncAi"), (12, "issAi"), (15, "epi4 wait"),
+       (16, "epi4 tmem->smem"), (17, "epi4 stg wait"), (18, "epi4 sync"), (19, "epi4 out"), (13, "epi4 tail")]
+print(f"N={N} {'circular' if circ else 'causal'} {'gated' if gated else 'plain'}")
 for wsel in (0, 1):
-    d = np.diff(buf[wsel, :, :15], axis=1)
     ok = buf[wsel, :, 0] > 0
-    d = d[ok][2:]
-    print(f"warp {4*wsel}: tiles {len(d)}  tile cycles median {np.median(buf[wsel,ok,14]-buf[wsel,ok,0]):.0f}")
-    for i, nm in enumerate(names):
-        print(f"  {nm:8s} {np.median(d[:, i]):8.0f} {np.mean(d[:, i]):8.0f}")
-    e4w = (buf[wsel, ok, 15] - buf[wsel, ok, 12])[2:]
-    print(f"  epi4 until MMA wait done {np.median(e4w):8.0f}")
+    b = buf[wsel, ok][2:]
+    print(f"warp {4 * wsel}: tiles {len(b)}  tile cycles median {np.median(b[:, 14] - b[:, 0]):.0f}")
+    prev = 0
+    for idx, nm in seq:
+        if np.all(b[:, idx] == 0):
+            continue
+        d = b[:, idx] - b[:, prev]
+        print(f"  {nm:16s} {np.median(d):8.0f}")
+        prev = idx
     nxt = buf[wsel, ok, 0][1:] - buf[wsel, ok, 14][:-1]
     print("  gap to next tile", np.median(nxt))
