@@ -607,7 +607,16 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
           const int r = och_r(i), n = och_n(i);
           const uint32_t off = uint32_t(r * C::NOUT + n) * sizeof(S);
           uint4 st;
-          if constexpr (GATED) {
+          if constexpr (GATED && std::is_same<T, __half>::value) {
+            // fp16 y * fp16 v: HMUL2 rounds the exact product once, the same
+            // value as the fp32 product rounded to fp16
+            st = ld_shared_u4(bufX + swz128(off));
+            if (STG) vv[i] = ld_shared_u4(sV + r * F::ROW_BYTES + n * 2);  // the output slot holds v
+            __half2* a2 = reinterpret_cast<__half2*>(&st);
+            const __half2* v2 = reinterpret_cast<const __half2*>(&vv[i]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) a2[e] = __hmul2(a2[e], v2[e]);
+          } else if constexpr (GATED) {
             float a[8], v8[8];
             IO<__half>::to_f32x8(ld_shared_u4(bufX + swz128(off)), a);
             if (STG) vv[i] = ld_shared_u4(sV + r * F::ROW_BYTES + n * 2);  // the output slot holds v

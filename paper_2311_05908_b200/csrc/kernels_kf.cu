@@ -126,9 +126,13 @@ FC_DEVICE void fft_inplace(float2* xs, const float2* tws, int L) {
 
 }  // namespace
 
+// Two heads per CTA: both filters are real, so one complex transform of
+// z = k_h + i k_{h+1} yields both spectra through the Hermitian split
+// K_h[f] = (Z[f] + conj Z[-f]) / 2, K_{h+1}[f] = (Z[f] - conj Z[-f]) / (2i).
 __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) {
   extern __shared__ float2 sm[];  // L data + L twiddles
-  const int h = blockIdx.x;
+  const int64_t h0 = 2 * int64_t(blockIdx.x);
+  const bool has1 = h0 + 1 < prm.H;
   const int L = int(prm.L), K = int(prm.K);
   float2* tws = sm + L;
   {
@@ -137,26 +141,35 @@ __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) 
     for (int o = threadIdx.x * 16; o < L * 8; o += blockDim.x * 16) cp_async16(dst + o, src + o, true);
     cp_async_commit();
   }
-  const float* krow = prm.k + int64_t(h) * K;
-  for (int n = threadIdx.x; n < L; n += blockDim.x) sm[n] = make_float2(n < K ? krow[n] : 0.f, 0.f);
+  const float* k0row = prm.k + h0 * K;
+  const float* k1row = k0row + K;
+  for (int n = threadIdx.x; n < L; n += blockDim.x)
+    sm[n] = make_float2(n < K ? k0row[n] : 0.f, (n < K && has1) ? k1row[n] : 0.f);
   cp_async_wait_all();
   __syncthreads();
   fft_inplace(sm, tws, L);
   const float2* xs = sm;
   // plan layout: row k2 holds pairs (k1, k1 + 1) as {kr, kr', ki, ki'}
   const int L1 = prm.L1, L2 = prm.L2, cpr = L1 / 2;
-  uint8_t* out = reinterpret_cast<uint8_t*>(prm.kf) + int64_t(h) * L2 * tab_stride(uint32_t(cpr));
+  const size_t hbytes = size_t(L2) * tab_stride(uint32_t(cpr));
+  uint8_t* out0 = reinterpret_cast<uint8_t*>(prm.kf) + h0 * int64_t(hbytes);
+  uint8_t* out1 = out0 + hbytes;
   for (int q = threadIdx.x; q < L2 * cpr; q += blockDim.x) {
     const int k2 = q / cpr, k1 = 2 * (q % cpr);
     const int f0 = k2 + L2 * k1, f1 = f0 + L2;
-    float2 v0 = xs[f0], v1 = xs[f1];
+    const float2 z0 = xs[f0], z1 = xs[f1], m0 = xs[(L - f0) & (L - 1)], m1 = xs[(L - f1) & (L - 1)];
+    float2 a0 = make_float2(0.5f * (z0.x + m0.x), 0.5f * (z0.y - m0.y));
+    float2 a1 = make_float2(0.5f * (z1.x + m1.x), 0.5f * (z1.y - m1.y));
+    float2 b0 = make_float2(0.5f * (z0.y + m0.y), -0.5f * (z0.x - m0.x));
+    float2 b1 = make_float2(0.5f * (z1.y + m1.y), -0.5f * (z1.x - m1.x));
     if (prm.mask) {
-      const float m0 = prm.mask[f0], m1 = prm.mask[f1];
-      v0.x *= m0; v0.y *= m0;
-      v1.x *= m1; v1.y *= m1;
+      const float w0 = prm.mask[f0], w1 = prm.mask[f1];
+      a0.x *= w0; a0.y *= w0; a1.x *= w1; a1.y *= w1;
+      b0.x *= w0; b0.y *= w0; b1.x *= w1; b1.y *= w1;
     }
-    *reinterpret_cast<float4*>(out + tab_off_rt(uint32_t(cpr), uint32_t(k2), uint32_t(k1 / 2))) =
-        make_float4(v0.x, v1.x, v0.y, v1.y);
+    const uint32_t off = tab_off_rt(uint32_t(cpr), uint32_t(k2), uint32_t(k1 / 2));
+    *reinterpret_cast<float4*>(out0 + off) = make_float4(a0.x, a1.x, a0.y, a1.y);
+    if (has1) *reinterpret_cast<float4*>(out1 + off) = make_float4(b0.x, b1.x, b0.y, b1.y);
   }
 }
 
@@ -311,7 +324,7 @@ cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  precompute_kf_kernel<<<unsigned(prm.H), 256, smem, s>>>(prm);
+  precompute_kf_kernel<<<unsigned((prm.H + 1) / 2), 256, smem, s>>>(prm);
   return cudaGetLastError();
 }
 
