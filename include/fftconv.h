@@ -51,7 +51,12 @@ typedef struct fftconv_plan_s* fftconv_plan_t;
 
 /* I/O element type.  Tensor-core operands are always fp16 with fp32
  * accumulation (A16; bf16 operands would miss the 2e-3 bound).
- * FFTCONV_F32 is the validation dtype (fp32 I/O). */
+ * FFTCONV_F32 is the validation build (north star, BASELINE.json: "<= 1e-5
+ * relative L2 on an fp32 validation build"): fp32 I/O and the same plan,
+ * packing, Monarch decomposition and multipass passes with every stage in
+ * fp32 on the CUDA cores (no tensor cores; not a performance path).  It
+ * covers the forward calls for fft_size <= 32768; fftconv_bwd returns
+ * FFTCONV_ERR_UNSUPPORTED for it. */
 typedef enum { FFTCONV_F16 = 0, FFTCONV_BF16 = 1, FFTCONV_F32 = 2 } fftconv_dtype_t;
 
 typedef enum {

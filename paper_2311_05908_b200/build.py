@@ -26,7 +26,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
 LIB = os.path.join(HERE, "libfftconv.so")
 SELFTEST = os.path.join(HERE, "libfftconv_selftest.so")
 
-LIB_SOURCES = ["plan.cpp", "api.cu", "kernels_fwd.cu", "kernels_kf.cu", "kernels_mp.cu", "kernels_bwd.cu"]
+LIB_SOURCES = ["plan.cpp", "api.cu", "kernels_fwd.cu", "kernels_kf.cu", "kernels_mp.cu", "kernels_bwd.cu", "kernels_f32.cu"]
 
 
 def _stale(target, sources):

@@ -30,6 +30,10 @@ size_t chunk_target_bytes() {
   return v;
 }
 
+// bytes per element of the multipass intermediate T (fp16; fp32 in the
+// validation build)
+size_t t_elem_bytes(const fftconv_plan_s* p) { return p->dtype == FFTCONV_F32 ? 4 : 2; }
+
 int num_sms_current() {
   static int cache[64] = {0};
   int dev = 0;
@@ -134,7 +138,7 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     mp.wtab = reinterpret_cast<const float2*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.wtab);
     mp.B = B; mp.H = H; mp.N = p->N; mp.Lp = int32_t(p->L / p->lev_L0[0]);
     mp.gated = gated ? 1 : 0;
-    mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
+    mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : p->dtype == FFTCONV_F32 ? 2 : 0;
     const bool skip = p->sparse && p->row_map.size() < size_t(p->L0);
     if (skip) mp.row_keep = static_cast<const uint8_t*>(p->d_tables) + p->row_keep_off;
     if (p->regime == REGIME_PARTIAL) {  // overlap-save windows as virtual rows
@@ -177,12 +181,18 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
           in.B = 2 * ((rows_c + 1) / 2); in.H = hc * p->L0; in.N = p->Lp;
           in.L1 = p->L1; in.causal = 0; in.gated = 0; in.dtype = 0;
           in.num_sms = num_sms_current();
-          if (skip) {
-            in.row_map = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(p->d_tables) + p->row_map_off);
-            in.nrow = int32_t(p->row_map.size());
-            in.row_L0 = p->L0;
+          if (p->dtype == FFTCONV_F32) {  // validation build: fp32 rows, every inner row
+            in.dtype = 2;
+            in.wl = static_cast<const uint8_t*>(p->d_tables) + p->tl.wl;
+            e = launch_fwd_f32(in, st);
+          } else {
+            if (skip) {
+              in.row_map = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(p->d_tables) + p->row_map_off);
+              in.nrow = int32_t(p->row_map.size());
+              in.row_L0 = p->L0;
+            }
+            e = launch_fwd_fused(in, st);
           }
-          e = launch_fwd_fused(in, st);
           if (e != cudaSuccess) return cuda_fail(fn, e);
           e = launch_mp_pass(c, 3, st);
           if (e != cudaSuccess) return cuda_fail(fn, e);
@@ -249,9 +259,10 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
   prm.L1 = p->L1;
   prm.causal = p->causal;
   prm.gated = gated ? 1 : 0;
-  prm.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
+  prm.dtype = p->dtype == FFTCONV_BF16 ? 1 : p->dtype == FFTCONV_F32 ? 2 : 0;
   prm.num_sms = num_sms_current();
-  cudaError_t e = launch_fwd_fused(prm, st);
+  prm.wl = static_cast<const uint8_t*>(p->d_tables) + p->tl.wl;
+  cudaError_t e = p->dtype == FFTCONV_F32 ? launch_fwd_f32(prm, st) : launch_fwd_fused(prm, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
   g_launches += 1;
   return FFTCONV_OK;
@@ -296,6 +307,10 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   fftconv_status_t chk = gated ? check_signal_args(p, fn, B, H, {d_dy, d_u, d_w, d_v, d_kf, d_du, d_dw, d_dv, d_workspace})
                                : check_signal_args(p, fn, B, H, {d_dy, d_u, d_kf, d_du, d_workspace});
   if (chk != FFTCONV_OK) return chk;
+  if (p->dtype == FFTCONV_F32) {
+    set_last_error("fftconv_bwd: the fp32 validation build covers the forward pass only");
+    return FFTCONV_ERR_UNSUPPORTED;
+  }
   const int64_t kmax = p->causal ? p->L / 2 : p->L;
   if (K < 1 || K > kmax) { set_last_error("fftconv_bwd: K out of range"); return FFTCONV_ERR_KERNEL_TOO_LONG; }
   if (!d_dk && H > 0) { set_last_error("fftconv_bwd: dk is NULL"); return FFTCONV_ERR_INVALID_ARG; }
@@ -393,10 +408,10 @@ extern "C" fftconv_status_t fftconv_workspace_size(fftconv_plan_t p, int64_t B, 
   size_t n = 0;
   if (for_bwd) n = bwd_ws_bytes(p, B, H);
   else if (p->regime == REGIME_MULTIPASS)
-    n = size_t(p->nlev > 1 ? 2 : 1) * size_t(2 * ((B + 1) / 2)) * size_t(H) * size_t(p->L) * 2;
+    n = size_t(p->nlev > 1 ? 2 : 1) * size_t(2 * ((B + 1) / 2)) * size_t(H) * size_t(p->L) * t_elem_bytes(p);
   else if (p->regime == REGIME_PARTIAL) {
     const int64_t Bv = B * (p->N / (p->L / 2));
-    n = size_t(2 * ((Bv + 1) / 2)) * size_t(H) * size_t(p->L) * 2;
+    n = size_t(2 * ((Bv + 1) / 2)) * size_t(H) * size_t(p->L) * t_elem_bytes(p);
   }
   *bytes = n;
   return FFTCONV_OK;

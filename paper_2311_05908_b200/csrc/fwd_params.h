@@ -16,14 +16,17 @@ struct FwdParams {
   int32_t L1;
   int32_t causal;
   int32_t gated;
-  int32_t dtype;  // 0 fp16, 1 bf16
+  int32_t dtype;  // 0 fp16, 1 bf16, 2 fp32 (validation build)
   int32_t num_sms;
   // sparse multipass: iterate over Hi = (H / row_L0) * nrow heads only; head
   // hh maps to tensor head (hh / nrow) * row_L0 + row_map[hh % nrow]
   const int32_t* row_map;
   int32_t nrow, row_L0;
+  const void* wl;  // fp32 validation build: W_L^e, e < L (plan table)
 };
 cudaError_t launch_fwd_fused(const FwdParams& prm, cudaStream_t s);
+// fp32 validation build of the same decomposition on CUDA cores (kernels_f32.cu)
+cudaError_t launch_fwd_f32(const FwdParams& prm, cudaStream_t s);
 
 struct KfParams {
   const float* k;     // (H, K)

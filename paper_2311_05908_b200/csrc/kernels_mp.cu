@@ -37,8 +37,16 @@ template <>
 FC_DEVICE float2 ld2<__nv_bfloat16>(const __nv_bfloat16* p) {
   return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
 }
+template <>
+FC_DEVICE float2 ld2<float>(const float* p) {
+  return *reinterpret_cast<const float2*>(p);
+}
 template <typename T>
 FC_DEVICE void st2(T* p, float a, float b);
+template <>
+FC_DEVICE void st2<float>(float* p, float a, float b) {
+  *reinterpret_cast<float2*>(p) = make_float2(a, b);
+}
 template <>
 FC_DEVICE void st2<__half>(__half* p, float a, float b) {
   *reinterpret_cast<__half2*>(p) = __floats2half2_rn(a, b);
@@ -61,27 +69,38 @@ struct PassCfg {
   static constexpr int C2 = COLS / 2;
 };
 
+// COLS adjacent elements of type T as one vector access
+template <int BYTES>
+struct RawVec;
+template <>
+struct RawVec<4> { using type = uint32_t; };
+template <>
+struct RawVec<8> { using type = uint2; };
+template <>
+struct RawVec<16> { using type = uint4; };
 template <typename T, int COLS>
-FC_DEVICE void ld_cols(const T* p, float* f) {
-  if constexpr (COLS == 4) {
-    const uint2 v = *reinterpret_cast<const uint2*>(p);
-    const float2 a = ld2<T>(reinterpret_cast<const T*>(&v.x)), b = ld2<T>(reinterpret_cast<const T*>(&v.y));
-    f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
-  } else {
-    const float2 a = ld2<T>(p);
-    f[0] = a.x; f[1] = a.y;
+using Raw = typename RawVec<int(sizeof(T)) * COLS>::type;
+
+template <typename T, int COLS>
+FC_DEVICE void unpack_cols(const Raw<T, COLS>& v, float* f) {
+  const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+  for (int j = 0; j < COLS; j += 2) {
+    const float2 a = ld2<T>(e + j);
+    f[j] = a.x; f[j + 1] = a.y;
   }
 }
 template <typename T, int COLS>
+FC_DEVICE void ld_cols(const T* p, float* f) {
+  unpack_cols<T, COLS>(*reinterpret_cast<const Raw<T, COLS>*>(p), f);
+}
+template <typename T, int COLS>
 FC_DEVICE void st_cols(T* p, const float* f) {
-  if constexpr (COLS == 4) {
-    uint2 v;
-    st2<T>(reinterpret_cast<T*>(&v.x), f[0], f[1]);
-    st2<T>(reinterpret_cast<T*>(&v.y), f[2], f[3]);
-    *reinterpret_cast<uint2*>(p) = v;
-  } else {
-    st2<T>(p, f[0], f[1]);
-  }
+  Raw<T, COLS> v;
+  T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+  for (int j = 0; j < COLS; j += 2) st2<T>(e + j, f[j], f[j + 1]);
+  *reinterpret_cast<Raw<T, COLS>*>(p) = v;
 }
 
 // per-column twiddle base W_Llev^{n + j}: plan table (W_L^{n'}, n' < Lp) for
@@ -109,7 +128,7 @@ FC_DEVICE CV<C2> twiddle_base(const MpParams& prm, int n) {
   return bw;
 }
 
-template <int L0, int MODE, bool GATED, typename T>
+template <int L0, int MODE, bool GATED, typename T, typename TT>
 __global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
   constexpr int COLS = PassCfg<L0>::COLS, C2 = PassCfg<L0>::C2;
   constexpr int NIN = MODE == 0 ? L0 / 2 : L0;
@@ -207,8 +226,8 @@ __global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
     tw.r[cc] = make_float2(s, s);
     tw.i[cc] = make_float2(0.f, 0.f);
   }
-  __half* __restrict__ Tre = reinterpret_cast<__half*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
-  __half* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
+  TT* __restrict__ Tre = reinterpret_cast<TT*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
+  TT* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
   uint32_t keep = ~0u;  // masked rows (sparse plans) are skipped downstream
   if (prm.row_keep) {
     keep = 0;
@@ -226,13 +245,13 @@ __global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
         fr[2 * cc] = o.r[cc].x; fr[2 * cc + 1] = o.r[cc].y;
         fi[2 * cc] = o.i[cc].x; fi[2 * cc + 1] = o.i[cc].y;
       }
-      st_cols<__half, COLS>(Tre + int64_t(k0) * prm.Lp, fr);
-      st_cols<__half, COLS>(Tim + int64_t(k0) * prm.Lp, fi);
+      st_cols<TT, COLS>(Tre + int64_t(k0) * prm.Lp, fr);
+      st_cols<TT, COLS>(Tim + int64_t(k0) * prm.Lp, fi);
     }
   }
 }
 
-template <int L0, int MODE, bool GATED, typename T>
+template <int L0, int MODE, bool GATED, typename T, typename TT>
 __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
   constexpr int COLS = PassCfg<L0>::COLS, C2 = PassCfg<L0>::C2;
   const int64_t NCH = int64_t(prm.Lp) / COLS;
@@ -243,9 +262,9 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
   const int n = int(idx & uint32_t(NCH - 1)) * COLS;
   const uint32_t ph = idx >> (31 - __clz(uint32_t(NCH)));
   const int64_t h = ph % uint32_t(prm.H), p = ph / uint32_t(prm.H);
-  const __half* __restrict__ Tre =
-      reinterpret_cast<const __half*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
-  const __half* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
+  const TT* __restrict__ Tre =
+      reinterpret_cast<const TT*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
+  const TT* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
   const CV<C2> bw = twiddle_base<C2>(prm, n);
   const float s = rsqrtf(float(L0));
   CV<C2> tw;
@@ -258,7 +277,7 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
   // all rows are loaded up front (no load waits on another): dense plans
   // unconditionally, sparse plans only the kept rows (the others were never
   // written by pass 1)
-  using RawT = typename std::conditional<COLS == 4, uint2, uint32_t>::type;
+  using RawT = Raw<TT, COLS>;
   RawT rr[L0], ri[L0];
   const bool sparse = prm.row_keep != nullptr;
 #pragma unroll
@@ -274,8 +293,8 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
 #pragma unroll
   for (int k0 = 0; k0 < L0; ++k0) {
     float fr[COLS], fi[COLS];
-    ld_cols<__half, COLS>(reinterpret_cast<const __half*>(&rr[k0]), fr);
-    ld_cols<__half, COLS>(reinterpret_cast<const __half*>(&ri[k0]), fi);
+    unpack_cols<TT, COLS>(rr[k0], fr);
+    unpack_cols<TT, COLS>(ri[k0], fi);
     CV<C2> x;
 #pragma unroll
     for (int cc = 0; cc < C2; ++cc) {
@@ -435,15 +454,20 @@ __global__ void __launch_bounds__(256) mp_cols_cplx_kernel(float2* data, int64_t
 // k_f, step 2 lives in kernels_kf.cu (row FFTs into the inner plan layout).
 cudaError_t launch_mp_kf_rows(const KfParams& prm, int L0, int Lp, size_t block_bytes, cudaStream_t s);
 
+// T: I/O type; the intermediate is fp16 except in the fp32 validation build
 template <int L0, int MODE, bool G, typename T>
 static void launch_pass_k(const MpParams& prm, int pass, unsigned grid, cudaStream_t s) {
-  if (pass == 1) mp_pass1_kernel<L0, MODE, G, T><<<grid, 256, 0, s>>>(prm);
-  else mp_pass3_kernel<L0, MODE, G, T><<<grid, 256, 0, s>>>(prm);
+  using TT = typename std::conditional<std::is_same<T, float>::value, float, __half>::type;
+  if (pass == 1) mp_pass1_kernel<L0, MODE, G, T, TT><<<grid, 256, 0, s>>>(prm);
+  else mp_pass3_kernel<L0, MODE, G, T, TT><<<grid, 256, 0, s>>>(prm);
 }
 template <int L0, int MODE>
 static void launch_pass_m(const MpParams& prm, int pass, unsigned grid, cudaStream_t s) {
   const bool g = prm.gated != 0;
-  if (prm.dtype == 0) {
+  if (prm.dtype == 2) {  // fp32 validation build
+    if (g) launch_pass_k<L0, MODE, true, float>(prm, pass, grid, s);
+    else launch_pass_k<L0, MODE, false, float>(prm, pass, grid, s);
+  } else if (prm.dtype == 0) {
     if (g) launch_pass_k<L0, MODE, true, __half>(prm, pass, grid, s);
     else launch_pass_k<L0, MODE, false, __half>(prm, pass, grid, s);
   } else {

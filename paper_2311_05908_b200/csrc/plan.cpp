@@ -336,7 +336,7 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
   //  fused     : L = L1 * 64, L1 in {8, 16, 32}; causal L = 2N or circular L = N
   //  multipass : causal, L = L0 * 2048 with L0 in {2, 4, 8, 16} (N = 2048..16384)
   const int64_t L = fft_size;
-  const bool io_ok = dtype != FFTCONV_F32;
+  const bool io_ok = true;  // fp16 / bf16 I/O, or the fp32 validation build
   if (io_ok && p->regime == REGIME_FUSED && L >= 512 && L <= 2048 && (!causal || fft_size == 2 * N)) {
     p->order = 2;
     p->L2 = 64;
@@ -365,6 +365,11 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
     p->KA = 64;  // the inner transform is circular over complex rows
     p->P = 4;
     build_fused_tables(p, p->Lp);
+    if (dtype == FFTCONV_F32 && p->nlev > 1) {
+      delete p;
+      set_last_error("fftconv_plan: the fp32 validation build supports fft_size <= 32768");
+      return FFTCONV_ERR_UNSUPPORTED;
+    }
     if (sparsity && p->nlev > 1) {
       delete p;
       set_last_error("fftconv_plan: frequency-sparse plans support fft_size <= 32768 in this build");
@@ -372,7 +377,7 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
     }
   } else {
     delete p;
-    set_last_error("fftconv_plan: this build supports fp16/bf16 I/O with fft_size 512..2048 (fused; causal "
+    set_last_error("fftconv_plan: this build supports fft_size 512..2048 (fused; causal "
                    "fft_size == 2N or circular), causal fft_size 4096..32768 == 2N (multipass) and partial "
                    "convolutions with fft_size 4096..32768 < 2N dividing 2N (overlap-save)");
     return FFTCONV_ERR_UNSUPPORTED;

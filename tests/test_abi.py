@@ -130,3 +130,13 @@ def test_no_cpu_fallback_in_product():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "liboracle" not in txt, f
+
+
+def test_f32_validation_plans(lib):
+    # the fp32 validation build: fused and one-level multipass sizes plan;
+    # recursive (fft_size > 32768) does not
+    for N, L in ((256, 512), (1024, 2048), (8192, 16384)):
+        rc, h = _plan(lib, N, L, dtype=2)
+        assert rc == 0, (N, L)
+        lib.fftconv_plan_destroy(h)
+    assert _plan(lib, 32768, 65536, dtype=2)[0] == 5
