@@ -182,8 +182,13 @@ __global__ void __launch_bounds__(256) mp_kf_rows_kernel(const KfParams prm, int
   float2* tws = sm + L;
   const int64_t blk = blockIdx.x;  // h * L0 + k0
   const int k0 = int(blk % L0);
-  if (prm.row_keep && !prm.row_keep[k0]) return;  // masked row: never read
   uint8_t* block = reinterpret_cast<uint8_t*>(prm.kf) + blk * block_bytes;
+  if (prm.row_keep && !prm.row_keep[k0]) {  // masked row: zeros, no transform (the
+    // forward pass never reads it; the backward reads finite zeros)
+    for (int o = threadIdx.x * 16; o < int(block_bytes); o += blockDim.x * 16)
+      *reinterpret_cast<float4*>(block + o) = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
   {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.twiddle);
     const uint32_t dst = smem_u32(tws);

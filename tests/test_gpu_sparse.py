@@ -64,3 +64,36 @@ def test_sparse_all_masked_is_zero():
     dims, keeps = [16384], [np.zeros(16384, bool)]
     plan, got, ref, m = _run(N, dims, keeps, B=2, H=2)
     assert np.all(got == 0) and np.all(ref == 0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,dims,zeroed", [
+    (16384, [2048, 16], None),                 # cfg 5 row pattern (75% of inner rows skipped forward)
+    (1024, [32, 64], [16, 32]),                # fused regime
+])
+def test_sparse_backward(N, dims, zeroed):
+    """Backward of a frequency-sparse conv (NEXT-3): the oracle's gradients
+    with the same mask (dg uses conj(K_f) * m, dk = Re IFFT(m * sum DC conj G))."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    if zeroed is None:
+        keep_k0 = np.zeros(16, bool)
+        keep_k0[[0, 1, 8, 15]] = True
+        keeps = [np.ones(2048, bool), keep_k0]
+    else:
+        keeps = orc.keep_masks_from_zero_counts(dims, zeroed)
+    B, H, seed = 3, 2, 31
+    plan = FFTConvPlan(N, dtype=torch.float16, causal=True, sparsity=(dims, keeps))
+    q = lambda name: synth.quantize(synth.signal(seed, name, B, H, N), "f16")
+    u, w, v, dy = q("u"), q("w"), q("v"), q("dy")
+    k = synth.decay_filters(seed, H, N).astype(np.float32)
+    t = lambda a: torch.tensor(a, dtype=torch.float16, device="cuda")
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    g = plan.bwd(t(dy), t(u), kf, N, w=t(w), v=t(v))
+    torch.cuda.synchronize()
+    m = orc.frequency_mask(dims, keeps)
+    ref = orc.conv_bwd(dy, u, k.astype(np.float64), w=w, v=v, mask=m)
+    for key in ("du", "dw", "dv", "dk"):
+        got = g[key].float().cpu().numpy().astype(np.float64)
+        assert np.all(np.isfinite(got)), key
+        rel = np.linalg.norm(got - ref[key]) / np.linalg.norm(ref[key])
+        assert rel < REL_L2, (key, rel)
