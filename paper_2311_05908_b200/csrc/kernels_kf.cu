@@ -11,6 +11,7 @@
 // padded rows (layout.h).  No cuFFT.
 #include <cuda_runtime.h>
 
+#include "dft_small.cuh"
 #include "fwd_params.h"
 #include "sm100.cuh"
 
@@ -275,32 +276,29 @@ __global__ void __launch_bounds__(256) dk_rows_kernel(const DkParams prm) {
 }
 
 // Multipass regime, step 2: per (head, n'):
-// dk[n' + Lp n0] = Re sum_k0 W_L^{-n' k0} W_L0^{-n0 k0} a[k0][n'].
+// dk[n' + Lp n0] = Re sum_k0 W_L^{-n' k0} W_L0^{-n0 k0} a[k0][n'],
+// i.e. an inverse DFT_L0 (in registers) of the conj-twiddled column.
+template <int L0>
 __global__ void __launch_bounds__(256) dk_cols_kernel(const DkParams prm) {
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= prm.H * prm.Lp) return;
   const int n = int(idx % prm.Lp);
   const int64_t h = idx / prm.Lp;
-  const int L0 = prm.L0;
   const float2 bw = prm.wbase[n];
   float2 tw = make_float2(1.f, 0.f);
-  float2 x[16];
+  float2 x[L0];
+#pragma unroll
+  for (int k0 = 0; k0 < L0; ++k0) x[k0] = prm.scratch[(h * L0 + k0) * prm.Lp + n];
+#pragma unroll
   for (int k0 = 0; k0 < L0; ++k0) {
-    const float2 a = prm.scratch[(h * L0 + k0) * prm.Lp + n];
-    x[k0] = make_float2(a.x * tw.x + a.y * tw.y, a.y * tw.x - a.x * tw.y);  // a * conj(tw)
-    const float2 t2 = make_float2(tw.x * bw.x - tw.y * bw.y, tw.x * bw.y + tw.y * bw.x);
-    tw = t2;
+    x[k0] = c_mulc(x[k0], tw);  // a * conj(W_L^{n' k0})
+    tw = c_mul(tw, bw);
   }
+  DftReg<L0, true>::run(x);  // sum_k0 x[k0] W_L0^{-n0 k0}
+#pragma unroll
   for (int n0 = 0; n0 < L0; ++n0) {
     const int64_t t = int64_t(n) + int64_t(n0) * prm.Lp;
-    if (t >= prm.K) break;
-    float s = 0.f;
-    for (int k0 = 0; k0 < L0; ++k0) {
-      float sn, cs;
-      sincospif(2.0f * float((n0 * k0) % L0) / float(L0), &sn, &cs);  // W_L0^{-n0 k0}
-      s += x[k0].x * cs - x[k0].y * sn;
-    }
-    prm.dk[h * prm.K + t] = s;
+    if (t < prm.K) prm.dk[h * prm.K + t] = x[n0].x;
   }
 }
 
@@ -316,7 +314,14 @@ cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
   dk_rows_kernel<<<unsigned(prm.H * prm.L0), 256, smem, s>>>(prm);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || prm.L0 == 1) return e;
-  dk_cols_kernel<<<unsigned((prm.H * prm.Lp + 255) / 256), 256, 0, s>>>(prm);
+  const unsigned grid = unsigned((prm.H * prm.Lp + 255) / 256);
+  switch (prm.L0) {
+    case 2: dk_cols_kernel<2><<<grid, 256, 0, s>>>(prm); break;
+    case 4: dk_cols_kernel<4><<<grid, 256, 0, s>>>(prm); break;
+    case 8: dk_cols_kernel<8><<<grid, 256, 0, s>>>(prm); break;
+    case 16: dk_cols_kernel<16><<<grid, 256, 0, s>>>(prm); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

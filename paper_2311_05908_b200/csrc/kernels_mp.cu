@@ -129,7 +129,7 @@ FC_DEVICE CV<C2> twiddle_base(const MpParams& prm, int n) {
 }
 
 template <int L0, int MODE, bool GATED, typename T, typename TT>
-__global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
+__global__ void __launch_bounds__(256, 3) mp_pass1_kernel(const MpParams prm) {
   constexpr int COLS = PassCfg<L0>::COLS, C2 = PassCfg<L0>::C2;
   constexpr int NIN = MODE == 0 ? L0 / 2 : L0;
   const int64_t NCH = int64_t(prm.Lp) / COLS;  // column groups per (pair, head)
@@ -148,12 +148,14 @@ __global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
   const int64_t Hg = prm.Hg ? prm.Hg : prm.H, hg = h + prm.h0;  // global head
   const int64_t g0 = b0 + 2 * prm.pair0, g1 = g0 + 1;          // global rows
   int64_t r0, r1, s0 = 0, s1 = 0;
-  if (MODE == 1) {
-    const int64_t j0 = g0 % prm.NC, j1 = g1 % prm.NC;
+  if (MODE == 1) {  // virtual rows < 2^31 (launcher): 32-bit division
+    const uint32_t nc = uint32_t(prm.NC);
+    const int64_t q0 = uint32_t(g0) / nc, q1 = uint32_t(g1) / nc;
+    const int64_t j0 = g0 - q0 * nc, j1 = g1 - q1 * nc;
     s0 = (j0 - 1) * prm.C;
     s1 = (j1 - 1) * prm.C;
-    r0 = ((g0 / prm.NC) * Hg + hg) * prm.N + s0 + n;
-    r1 = ((g1 / prm.NC) * Hg + hg) * prm.N + s1 + n;
+    r0 = (q0 * Hg + hg) * prm.N + s0 + n;
+    r1 = (q1 * Hg + hg) * prm.N + s1 + n;
   } else {
     r0 = (g0 * Hg + hg) * prm.N + n;
     r1 = (g1 * Hg + hg) * prm.N + n;
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(256) mp_pass1_kernel(const MpParams prm) {
 }
 
 template <int L0, int MODE, bool GATED, typename T, typename TT>
-__global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
+__global__ void __launch_bounds__(256, 3) mp_pass3_kernel(const MpParams prm) {
   constexpr int COLS = PassCfg<L0>::COLS, C2 = PassCfg<L0>::C2;
   const int64_t NCH = int64_t(prm.Lp) / COLS;
   // 32-bit index math (the launcher checks pairs * H * NCH < 2^31); NCH is a power of two
@@ -319,9 +321,11 @@ __global__ void __launch_bounds__(256) mp_pass3_kernel(const MpParams prm) {
   const int64_t Hg = prm.Hg ? prm.Hg : prm.H, hg = h + prm.h0;  // global head
   const int64_t g0 = b0 + 2 * prm.pair0, g1 = g0 + 1;          // global rows
   int64_t r0, r1;
-  if (MODE == 1) {
-    r0 = ((g0 / prm.NC) * Hg + hg) * prm.N + (g0 % prm.NC) * prm.C + n;
-    r1 = ((g1 / prm.NC) * Hg + hg) * prm.N + (g1 % prm.NC) * prm.C + n;
+  if (MODE == 1) {  // virtual rows < 2^31 (launcher): 32-bit division
+    const uint32_t nc = uint32_t(prm.NC);
+    const int64_t q0 = uint32_t(g0) / nc, q1 = uint32_t(g1) / nc;
+    r0 = (q0 * Hg + hg) * prm.N + (g0 - q0 * nc) * prm.C + n;
+    r1 = (q1 * Hg + hg) * prm.N + (g1 - q1 * nc) * prm.C + n;
   } else {
     r0 = (g0 * Hg + hg) * prm.N + n;
     r1 = (g1 * Hg + hg) * prm.N + n;
@@ -482,6 +486,7 @@ static cudaError_t launch_mp_l0(const MpParams& prm, int pass, cudaStream_t s) {
   const unsigned grid = unsigned((total + 255) / 256);
   if (total == 0) return cudaSuccess;
   if (total + 255 >= (int64_t(1) << 31) || (prm.Lp & (prm.Lp - 1))) return cudaErrorInvalidValue;
+  if (2 * (prm.pair0 + (prm.B + 1) / 2) >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   if (prm.circ) {  // deep levels: fp16 complex rows, never gated
     if (prm.dtype != 0 || prm.gated) return cudaErrorInvalidValue;
     launch_pass_k<L0, 2, false, __half>(prm, pass, grid, s);
