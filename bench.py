@@ -248,7 +248,7 @@ def main():
     w = synth.signal_torch(0, "w", B, H, N, dev, tdt, row0=row0) if wl["gated"] else None
     v = synth.signal_torch(0, "v", B, H, N, dev, tdt, row0=row0) if wl["gated"] else None
     dy = synth.signal_torch(0, "dy", B, H, N, dev, tdt, row0=row0) if wl["bwd"] else None
-    k = torch.tensor(synth.decay_filters(rank, H, K), dtype=torch.float32, device=dev)
+    k = synth.decay_filters_torch(rank, H, K, dev)
     y = torch.empty_like(u)
     ws_f = plan.workspace(B, H, device=dev)
     ws_b = plan.workspace(B, H, for_bwd=True, device=dev) if wl["bwd"] else None
@@ -271,8 +271,9 @@ def main():
                 plan._h, _ptr(dy), _ptr(uu), _ptr(ww), _ptr(vv), _ptr(kf), _ptr(grads["du"]), _ptr(grads["dw"]),
                 _ptr(grads["dv"]), _ptr(grads["dk"]), B, H, K, _ptr(ws_b), _stream(dev)))
 
+    kfb = plan.kf_buffer(H, dev)  # reused every step (N = 4M: 64 MB of fp32 k_f per head)
     for _ in range(args.warmup):
-        conv(plan.precompute_kf(k), u, w, v, y)
+        conv(plan.precompute_kf(k, out=kfb), u, w, v, y)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -285,7 +286,7 @@ def main():
         torch.cuda.synchronize()
         ev_s.record()
         for i in range(S):
-            kf = plan.precompute_kf(k)
+            kf = plan.precompute_kf(k, out=kfb)
             ev[i][0].record()
             conv(kf, u, w, v, y)
             ev[i][1].record()
@@ -304,7 +305,12 @@ def main():
     value = world * B * H / (step_ms * 1e-3)
 
     # ---------------- end-to-end through the public API with pinned host buffers
-    hbuf = {name: t.cpu().pin_memory() for name, t in (("u", u), ("w", w), ("v", v), ("dy", dy), ("k", k))
+    def pinned_copy(t):  # straight into pinned host memory (no pageable staging copy)
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        return h
+
+    hbuf = {name: pinned_copy(t) for name, t in (("u", u), ("w", w), ("v", v), ("dy", dy), ("k", k))
             if t is not None}
     dbuf = {name: torch.empty_like(t) for name, t in (("u", u), ("w", w), ("v", v), ("k", k)) if t is not None}
     hy = torch.empty(y.shape, dtype=y.dtype).pin_memory()
@@ -319,7 +325,7 @@ def main():
             t.copy_(hbuf[name], non_blocking=True)
         if dy is not None:
             dy.copy_(hbuf["dy"], non_blocking=True)
-        kf = plan.precompute_kf(dbuf["k"])
+        kf = plan.precompute_kf(dbuf["k"], out=kfb)
         conv(kf, dbuf["u"], dbuf.get("w"), dbuf.get("v"), y)
         hy.copy_(y, non_blocking=True)
         if wl["bwd"]:

@@ -84,6 +84,13 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
   constexpr bool STG = F::STG;      // input staging by bulk copies
   constexpr int L2 = C::L2;
   constexpr bool TS = C::TS_BI;     // stage B^-1 data operand in TMEM
+#ifndef FC_NEG_B
+#define FC_NEG_B 0
+#endif
+  // Stage B / B^-1 N: re | im only (the negated plane the complex multiply
+  // needs is a sign folded into the f32x2 multiplies); FC_NEG_B=1 has the
+  // tensor core emit it as a third block of the G_B table instead.
+  constexpr int NBF = FC_NEG_B ? C::NB : (2 * L1 + 15) / 16 * 16;
   constexpr bool M64 = CAUSAL;      // stage A^-1 as M = 64 MMAs (rows n2 < L2/2 only)
 
   extern __shared__ uint8_t smem_raw[];
@@ -413,9 +420,17 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         // W^{n1 k2}, k2 = k20 .. k20 + 15: the table pair at k20, then fp32
         // steps by W^{2 n1} (register recurrence instead of 8 table loads)
         float4 w[8];
-        w[0] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1A, k20 / 2));
+#ifndef FC_TW1_TABLE
+#define FC_TW1_TABLE 0
+#endif
+        if constexpr (FC_TW1_TABLE) {  // 8 conflict-free table reads
 #pragma unroll
-        for (int jj = 1; jj < 8; ++jj) w[jj] = cstep(w[jj - 1], tw1_c2);
+          for (int jj = 0; jj < 8; ++jj) w[jj] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1A, k20 / 2 + jj));
+        } else {
+          w[0] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1A, k20 / 2));
+#pragma unroll
+          for (int jj = 1; jj < 8; ++jj) w[jj] = cstep(w[jj - 1], tw1_c2);
+        }
         tmem_ld_wait();
         if constexpr (!C::NEG_A) {
 #pragma unroll
@@ -436,12 +451,12 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
 
     // ---------------- stage B: per group of 128 rows (p,k2), contract n1 -> k1
     sync_and_issue([&](int h2) {
-      constexpr uint32_t idesc = idesc_f16(128, C::NB, true, false);
+      constexpr uint32_t idesc = idesc_f16(128, NBF, true, false);
 #pragma unroll
       for (int gi = h2 * (C::P / 4); gi < (h2 + 1) * (C::P / 4); ++gi) {
 #pragma unroll
         for (int s = 0; s < 2 * L1 / 16; ++s)
-          mma_f16_ss(tmem + gi * C::NB, dadd(dXB, gi * 2048 + 2 * s * C::LBO_B), dadd(dGB, 256 * s), idesc, s > 0);
+          mma_f16_ss(tmem + gi * NBF, dadd(dXB, gi * 2048 + 2 * s * C::LBO_B), dadd(dGB, 256 * s), idesc, s > 0);
       }
     });
 
@@ -454,15 +469,19 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         const int k2 = rowB_k2(gi);
         if (i == 0) wait_half(0);
         if (TS && i == 2) wait_half(1);
-        const uint32_t col = gi * C::NB + k1c * 8;
+        const uint32_t col = gi * NBF + k1c * 8;
         float re[8], im[8], ni[8];
         tmem_ld8(tq + col, re);
         tmem_ld8(tq + col + L1, im);
-        tmem_ld8(tq + col + 2 * L1, ni);
+        if constexpr (FC_NEG_B) tmem_ld8(tq + col + 2 * L1, ni);
         float4 kf[4];
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) kf[jj] = ld_shared_f4(sKF + tab_off<L1 / 2>(k2, k1c * 4 + jj));
         tmem_ld_wait();
+        if constexpr (!FC_NEG_B) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) ni[e] = -im[e];
+        }
         cmul8(re, im, ni, kf);
         if constexpr (TS) {  // K index c*L1 + k1 -> column (c*L1 + k1) / 2
           const uint32_t ca = tq + C::CA + gi * L1 + k1c * 4;
@@ -483,15 +502,15 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
 
     // ---------------- stage B^-1: contract k1 -> n1
     sync_and_issue([&](int h2) {
-      constexpr uint32_t idesc = idesc_f16(128, C::NB, false, false);
+      constexpr uint32_t idesc = idesc_f16(128, NBF, false, false);
 #pragma unroll
       for (int gi = h2 * (C::P / 4); gi < (h2 + 1) * (C::P / 4); ++gi) {
 #pragma unroll
         for (int s = 0; s < 2 * L1 / 16; ++s) {
           if constexpr (TS)
-            mma_f16_ts(tmem + gi * C::NB, tmem + C::CA + gi * L1 + 8 * s, dadd(dGBI, 256 * s), idesc, s > 0);
+            mma_f16_ts(tmem + gi * NBF, tmem + C::CA + gi * L1 + 8 * s, dadd(dGBI, 256 * s), idesc, s > 0);
           else
-            mma_f16_ss(tmem + gi * C::NB, dadd(dXBP, gi * 16 * C::SBO_BP + 256 * s), dadd(dGBI, 256 * s), idesc,
+            mma_f16_ss(tmem + gi * NBF, dadd(dXBP, gi * 16 * C::SBO_BP + 256 * s), dadd(dGBI, 256 * s), idesc,
                        s > 0);
         }
       }
@@ -506,11 +525,11 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         const int p = rowB_p(gi), k2 = rowB_k2(gi);
         if (i == 0) wait_half(0);
         if (TS && i == 2) wait_half(1);  // bufX is not an operand of stage B^-1 here
-        const uint32_t col = gi * C::NB + n1c * 8;
+        const uint32_t col = gi * NBF + n1c * 8;
         float re[8], im[8], nr[8];
         tmem_ld8(tq + col, re);
         tmem_ld8(tq + col + L1, im);
-        tmem_ld8(tq + col + 2 * L1, nr);
+        if constexpr (FC_NEG_B) tmem_ld8(tq + col + 2 * L1, nr);
         // W^{n1 k2}, n1 = 8 n1c .. 8 n1c + 7 at this k2: the table value at
         // 8 n1c (k2 parity picked from the pair), * W^{k2}, then fp32 steps
         // by W^{2 k2}
@@ -524,6 +543,10 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
           for (int jj = 1; jj < 4; ++jj) w[jj] = cstep(w[jj - 1], make_float2(c.z, c.w));
         }
         tmem_ld_wait();
+        if constexpr (!FC_NEG_B) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) nr[e] = -re[e];
+        }
         cmulc8(re, im, nr, w);
         if (!TS && i == 0) wait_half(1);  // stores may overwrite operands of the second half
         const int ng = (p * L1) / 8 + n1c;

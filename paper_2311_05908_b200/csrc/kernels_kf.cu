@@ -53,48 +53,46 @@ FC_DEVICE void dft8(float2* v) {
   }
 }
 
-template <int R>
-FC_DEVICE void stockham_pass(const float2* __restrict__ x, float2* __restrict__ y, const float2* __restrict__ tw,
-                             int L, int Ns) {
-  const int G = L / R;  // butterfly groups per pass
-  for (int j = threadIdx.x; j < G; j += blockDim.x) {
-    float2 v[R];
-    const int jm = j % Ns;
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = x[j + r * G];
-    if (Ns > 1) {
-      const int step = L / (Ns * R);  // W_{Ns R}^{jm r} = W_L^{jm r step}
-#pragma unroll
-      for (int r = 1; r < R; ++r) v[r] = cmulf(v[r], tw[(jm * r * step) & (L - 1)]);
-    }
-    if constexpr (R == 8) dft8(v);
-    else if constexpr (R == 4) dft4(v);
-    else dft2(v);
-    const int base = (j / Ns) * Ns * R + jm;
-#pragma unroll
-    for (int r = 0; r < R; ++r) y[base + r * Ns] = v[r];
-  }
-}
+// Compile-time Stockham FFT for 256-thread blocks and L in {512, 1024,
+// 2048}: every index and twiddle exponent is a constant expression of the
+// thread index.  Data live at padded positions pd(i) = i + i/8 (one spare
+// float2 per 8) so the strided butterfly stores of the early passes do not
+// pile onto one shared-memory bank; a butterfly reads 3 twiddles
+// (W^e, W^2e, W^4e) and forms the other 4 by at most two fp32 products.
+FC_DEVICE int pd(int i) { return i + (i >> 3); }
+template <int L>
+constexpr int padded_len() { return L + L / 8; }
 
-// In-place variant for L <= 8 * blockDim.x: every thread first reads all of
-// its groups (at most 8 elements) into registers, the block synchronises,
-// then the results are written back -- one L-element buffer instead of two.
-template <int R>
-FC_DEVICE void stockham_pass_inplace(float2* x, const float2* __restrict__ tw, int L, int Ns) {
-  constexpr int GPT = 8 / R;  // groups per thread (L <= 8 * blockDim.x)
-  const int G = L / R;
+template <int R, int L, int NS>
+FC_DEVICE void stockham_pass_ct(float2* x, const float2* __restrict__ tw) {
+  constexpr int G = L / R, GPT = (G + 255) / 256;
   float2 v[GPT][R];
 #pragma unroll
   for (int g = 0; g < GPT; ++g) {
-    const int j = threadIdx.x + g * blockDim.x;
-    if (j < G) {
-      const int jm = j % Ns;
+    const int j = threadIdx.x + g * 256;
+    if (G % 256 == 0 || j < G) {
+      const int jm = j % NS;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[g][r] = x[j + r * G];
-      if (Ns > 1) {
-        const int step = L / (Ns * R);
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[g][r] = cmulf(v[g][r], tw[(jm * r * step) & (L - 1)]);
+      for (int r = 0; r < R; ++r) v[g][r] = x[pd(j + r * G)];
+      if (NS > 1) {
+        constexpr int step = L / (NS * R);  // W_{NS R}^{jm r} = W_L^{jm r step}
+        const int e = jm * step;
+        const float2 w1 = tw[pd(e & (L - 1))];
+        if constexpr (R == 2) {
+          v[g][1] = cmulf(v[g][1], w1);
+        } else {
+          const float2 w2 = tw[pd((2 * e) & (L - 1))];
+          v[g][1] = cmulf(v[g][1], w1);
+          v[g][2] = cmulf(v[g][2], w2);
+          v[g][3] = cmulf(v[g][3], cmulf(w1, w2));
+          if constexpr (R == 8) {
+            const float2 w4 = tw[pd((4 * e) & (L - 1))];
+            v[g][4] = cmulf(v[g][4], w4);
+            v[g][5] = cmulf(v[g][5], cmulf(w1, w4));
+            v[g][6] = cmulf(v[g][6], cmulf(w2, w4));
+            v[g][7] = cmulf(v[g][7], cmulf(cmulf(w1, w2), w4));
+          }
+        }
       }
       if constexpr (R == 8) dft8(v[g]);
       else if constexpr (R == 4) dft4(v[g]);
@@ -104,25 +102,52 @@ FC_DEVICE void stockham_pass_inplace(float2* x, const float2* __restrict__ tw, i
   __syncthreads();
 #pragma unroll
   for (int g = 0; g < GPT; ++g) {
-    const int j = threadIdx.x + g * blockDim.x;
-    if (j < G) {
-      const int jm = j % Ns;
-      const int base = (j / Ns) * Ns * R + jm;
+    const int j = threadIdx.x + g * 256;
+    if (G % 256 == 0 || j < G) {
+      const int jm = j % NS;
+      const int base = (j / NS) * NS * R + jm;
 #pragma unroll
-      for (int r = 0; r < R; ++r) x[base + r * Ns] = v[g][r];
+      for (int r = 0; r < R; ++r) x[pd(base + r * NS)] = v[g][r];
     }
   }
   __syncthreads();
 }
-
-// Full forward FFT of xs[0..L) in place (L <= 8 * blockDim.x), natural order.
-FC_DEVICE void fft_inplace(float2* xs, const float2* tws, int L) {
-  int Ns = 1;
-  const int lg = __ffs(L) - 1;
-  const int rem = lg % 3;
-  if (rem == 1) { stockham_pass_inplace<2>(xs, tws, L, Ns); Ns = 2; }
-  if (rem == 2) { stockham_pass_inplace<4>(xs, tws, L, Ns); Ns = 4; }
-  for (; Ns < L; Ns <<= 3) stockham_pass_inplace<8>(xs, tws, L, Ns);
+template <int L>
+FC_DEVICE void fft_inplace_ct(float2* xs, const float2* tws) {
+  static_assert(L == 512 || L == 1024 || L == 2048, "compile-time FFT sizes");
+  if constexpr (L == 512) {  // 8 * 8 * 8
+    stockham_pass_ct<8, L, 1>(xs, tws);
+    stockham_pass_ct<8, L, 8>(xs, tws);
+    stockham_pass_ct<8, L, 64>(xs, tws);
+  } else if constexpr (L == 1024) {  // 2 * 8 * 8 * 8
+    stockham_pass_ct<2, L, 1>(xs, tws);
+    stockham_pass_ct<8, L, 2>(xs, tws);
+    stockham_pass_ct<8, L, 16>(xs, tws);
+    stockham_pass_ct<8, L, 128>(xs, tws);
+  } else {  // 4 * 8 * 8 * 8
+    stockham_pass_ct<4, L, 1>(xs, tws);
+    stockham_pass_ct<8, L, 4>(xs, tws);
+    stockham_pass_ct<8, L, 32>(xs, tws);
+    stockham_pass_ct<8, L, 256>(xs, tws);
+  }
+}
+// Forward FFT of the padded buffer xs (natural order; twiddles W_L^e also
+// padded); the launchers use
+// 256-thread blocks and L in {512, 1024, 2048} only.
+FC_DEVICE void fft_inplace_any(float2* xs, const float2* tws, int L) {
+  if (L == 2048) fft_inplace_ct<2048>(xs, tws);
+  else if (L == 1024) fft_inplace_ct<1024>(xs, tws);
+  else fft_inplace_ct<512>(xs, tws);
+}
+// shared memory of the FFT kernels: padded data + L twiddles
+inline size_t fft_smem_bytes(int64_t L) { return size_t(2 * (L + L / 8)) * sizeof(float2); }
+// L float2 from global (16-byte aligned) into the padded layout
+FC_DEVICE void load_padded(float2* dst, const float2* src, int L) {
+  for (int c = threadIdx.x; c < L / 2; c += blockDim.x) {
+    const float4 q = reinterpret_cast<const float4*>(src)[c];
+    dst[pd(2 * c)] = make_float2(q.x, q.y);
+    dst[pd(2 * c + 1)] = make_float2(q.z, q.w);
+  }
 }
 
 }  // namespace
@@ -131,24 +156,21 @@ FC_DEVICE void fft_inplace(float2* xs, const float2* tws, int L) {
 // z = k_h + i k_{h+1} yields both spectra through the Hermitian split
 // K_h[f] = (Z[f] + conj Z[-f]) / 2, K_{h+1}[f] = (Z[f] - conj Z[-f]) / (2i).
 __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) {
-  extern __shared__ float2 sm[];  // L data + L twiddles
+  extern __shared__ float2 sm[];  // padded L data + L twiddles
   const int64_t h0 = 2 * int64_t(blockIdx.x);
   const bool has1 = h0 + 1 < prm.H;
   const int L = int(prm.L), K = int(prm.K);
-  float2* tws = sm + L;
+  float2* tws = sm + L + L / 8;
   {
-    const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.twiddle);
-    const uint32_t dst = smem_u32(tws);
-    for (int o = threadIdx.x * 16; o < L * 8; o += blockDim.x * 16) cp_async16(dst + o, src + o, true);
-    cp_async_commit();
+    load_padded(tws, prm.twiddle, L);
   }
   const float* k0row = prm.k + h0 * K;
   const float* k1row = k0row + K;
   for (int n = threadIdx.x; n < L; n += blockDim.x)
-    sm[n] = make_float2(n < K ? k0row[n] : 0.f, (n < K && has1) ? k1row[n] : 0.f);
+    sm[pd(n)] = make_float2(n < K ? k0row[n] : 0.f, (n < K && has1) ? k1row[n] : 0.f);
   cp_async_wait_all();
   __syncthreads();
-  fft_inplace(sm, tws, L);
+  fft_inplace_any(sm, tws, L);
   const float2* xs = sm;
   // plan layout: row k2 holds pairs (k1, k1 + 1) as {kr, kr', ki, ki'}
   const int L1 = prm.L1, L2 = prm.L2, cpr = L1 / 2;
@@ -156,9 +178,13 @@ __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) 
   uint8_t* out0 = reinterpret_cast<uint8_t*>(prm.kf) + h0 * int64_t(hbytes);
   uint8_t* out1 = out0 + hbytes;
   for (int q = threadIdx.x; q < L2 * cpr; q += blockDim.x) {
-    const int k2 = q / cpr, k1 = 2 * (q % cpr);
+    // a warp covers 8 consecutive k2 x 4 column pairs: shared-memory reads
+    // of consecutive f, 64-byte runs of each output row
+    const int w = q >> 5, lane = q & 31;
+    const int k2 = (w % (L2 / 8)) * 8 + (lane & 7);
+    const int k1 = 2 * ((w / (L2 / 8)) * 4 + (lane >> 3));
     const int f0 = k2 + L2 * k1, f1 = f0 + L2;
-    const float2 z0 = xs[f0], z1 = xs[f1], m0 = xs[(L - f0) & (L - 1)], m1 = xs[(L - f1) & (L - 1)];
+    const float2 z0 = xs[pd(f0)], z1 = xs[pd(f1)], m0 = xs[pd((L - f0) & (L - 1))], m1 = xs[pd((L - f1) & (L - 1))];
     float2 a0 = make_float2(0.5f * (z0.x + m0.x), 0.5f * (z0.y - m0.y));
     float2 a1 = make_float2(0.5f * (z1.x + m1.x), 0.5f * (z1.y - m1.y));
     float2 b0 = make_float2(0.5f * (z0.y + m0.y), -0.5f * (z0.x - m0.x));
@@ -178,9 +204,9 @@ __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) 
 // complex values left by step 1 at the start of block (h, k0) and writes the
 // inner plan layout of K_f[k0 + L0 f'] over the same block (in place).
 __global__ void __launch_bounds__(256) mp_kf_rows_kernel(const KfParams prm, int L0, int Lp, size_t block_bytes) {
-  extern __shared__ float2 sm[];  // Lp data + Lp twiddles
+  extern __shared__ float2 sm[];  // padded Lp data + Lp twiddles
   const int L = Lp;
-  float2* tws = sm + L;
+  float2* tws = sm + L + L / 8;
   const int64_t blk = blockIdx.x;  // h * L0 + k0
   const int k0 = int(blk % L0);
   uint8_t* block = reinterpret_cast<uint8_t*>(prm.kf) + blk * block_bytes;
@@ -191,22 +217,28 @@ __global__ void __launch_bounds__(256) mp_kf_rows_kernel(const KfParams prm, int
     return;
   }
   {
-    const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.twiddle);
-    const uint32_t dst = smem_u32(tws);
-    for (int o = threadIdx.x * 16; o < L * 8; o += blockDim.x * 16) cp_async16(dst + o, src + o, true);
-    const uint32_t dd = smem_u32(sm);
-    for (int o = threadIdx.x * 16; o < L * 8; o += blockDim.x * 16) cp_async16(dd + o, block + o, true);
-    cp_async_commit();
+    load_padded(tws, prm.twiddle, L);
+    // data: 16-byte loads into the padded layout (pd() breaks 16-byte
+    // alignment of the shared destination, so no cp.async here)
+    for (int c = threadIdx.x; c < L / 2; c += blockDim.x) {
+      const float4 q = reinterpret_cast<const float4*>(block)[c];
+      sm[pd(2 * c)] = make_float2(q.x, q.y);
+      sm[pd(2 * c + 1)] = make_float2(q.z, q.w);
+    }
   }
   cp_async_wait_all();
   __syncthreads();
-  fft_inplace(sm, tws, L);
+  fft_inplace_any(sm, tws, L);
   const float2* xs = sm;
   const int L1 = prm.L1, L2 = prm.L2, cpr = L1 / 2;
   for (int q = threadIdx.x; q < L2 * cpr; q += blockDim.x) {
-    const int k2 = q / cpr, k1 = 2 * (q % cpr);
+    // a warp covers 8 consecutive k2 x 4 column pairs: shared-memory reads
+    // of consecutive f, 64-byte runs of each output row
+    const int w = q >> 5, lane = q & 31;
+    const int k2 = (w % (L2 / 8)) * 8 + (lane & 7);
+    const int k1 = 2 * ((w / (L2 / 8)) * 4 + (lane >> 3));
     const int f0 = k2 + L2 * k1, f1 = f0 + L2;
-    float2 v0 = xs[f0], v1 = xs[f1];
+    float2 v0 = xs[pd(f0)], v1 = xs[pd(f1)];
     if (prm.mask) {
       const float m0 = prm.mask[k0 + int64_t(L0) * f0], m1 = prm.mask[k0 + int64_t(L0) * f1];
       v0.x *= m0; v0.y *= m0;
@@ -218,7 +250,7 @@ __global__ void __launch_bounds__(256) mp_kf_rows_kernel(const KfParams prm, int
 }
 
 cudaError_t launch_mp_kf_rows(const KfParams& prm, int L0, int Lp, size_t block_bytes, cudaStream_t s) {
-  const size_t smem = size_t(Lp) * sizeof(float2) * 2;
+  const size_t smem = fft_smem_bytes(Lp);
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(mp_kf_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -236,16 +268,13 @@ cudaError_t launch_mp_kf_rows(const KfParams& prm, int L0, int Lp, size_t block_
 // Multipass regime, step 1: the same per (head, k0) over the inner length Lp,
 // leaving a[k0][n'] = sum_f' acc[k0 + L0 f'] W_Lp^{-n' f'} (complex) in scratch.
 __global__ void __launch_bounds__(256) dk_rows_kernel(const DkParams prm) {
-  extern __shared__ float2 sm[];  // Lp data + Lp twiddles
+  extern __shared__ float2 sm[];  // padded Lp data + Lp twiddles
   const int L = prm.Lp;
-  float2* tws = sm + L;
+  float2* tws = sm + L + L / 8;
   const int64_t row = blockIdx.x;  // h * L0 + k0
   const int k0 = int(row % prm.L0);
   {
-    const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.twiddle);
-    const uint32_t dst = smem_u32(tws);
-    for (int o = threadIdx.x * 16; o < L * 8; o += blockDim.x * 16) cp_async16(dst + o, src + o, true);
-    cp_async_commit();
+    load_padded(tws, prm.twiddle, L);
   }
   const float2* part = prm.part + row * prm.nbt * L;
   for (int f = threadIdx.x; f < L; f += blockDim.x) {
@@ -260,18 +289,18 @@ __global__ void __launch_bounds__(256) dk_rows_kernel(const DkParams prm) {
       a.x *= mk;
       a.y *= mk;
     }
-    sm[f] = make_float2(a.x, -a.y);  // conj: inverse transform via the forward one
+    sm[pd(f)] = make_float2(a.x, -a.y);  // conj: inverse transform via the forward one
   }
   cp_async_wait_all();
   __syncthreads();
-  fft_inplace(sm, tws, L);
+  fft_inplace_any(sm, tws, L);
   const float2* xs = sm;
   if (prm.L0 == 1) {
     float* dk = prm.dk + row * prm.K;
-    for (int t = threadIdx.x; t < prm.K; t += blockDim.x) dk[t] = xs[t].x;
+    for (int t = threadIdx.x; t < prm.K; t += blockDim.x) dk[t] = xs[pd(t)].x;
   } else {
     float2* a = prm.scratch + row * L;
-    for (int t = threadIdx.x; t < L; t += blockDim.x) a[t] = make_float2(xs[t].x, -xs[t].y);  // undo conj
+    for (int t = threadIdx.x; t < L; t += blockDim.x) a[t] = make_float2(xs[pd(t)].x, -xs[pd(t)].y);  // undo conj
   }
 }
 
@@ -304,7 +333,7 @@ __global__ void __launch_bounds__(256) dk_cols_kernel(const DkParams prm) {
 
 cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
   if (prm.H <= 0) return cudaSuccess;
-  const size_t smem = size_t(prm.Lp) * sizeof(float2) * 2;
+  const size_t smem = fft_smem_bytes(prm.Lp);
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(dk_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -327,7 +356,7 @@ cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
 
 cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s) {
   if (prm.H <= 0) return cudaSuccess;
-  const size_t smem = size_t(prm.L) * sizeof(float2) * 2;
+  const size_t smem = fft_smem_bytes(prm.L);
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(precompute_kf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

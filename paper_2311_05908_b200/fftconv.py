@@ -97,12 +97,21 @@ class FFTConvPlan:
             self._h = None
 
     # ------------------------------------------------------------------ calls
-    def precompute_kf(self, k: torch.Tensor) -> torch.Tensor:
-        """k: (H, K) fp32 on device -> opaque k_f buffer (H * kf_bytes_per_head)."""
+    def kf_buffer(self, H: int, device=None) -> torch.Tensor:
+        """An opaque k_f buffer for H heads (reusable across precompute_kf calls)."""
+        return _aligned_empty(max(H, 1) * self.info.kf_bytes_per_head, device or self.device, 16)
+
+    def precompute_kf(self, k: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """k: (H, K) fp32 on device -> opaque k_f buffer (H * kf_bytes_per_head),
+        written into `out` (from kf_buffer) when given."""
         assert k.dtype == torch.float32 and k.is_cuda and k.dim() == 2
         k = k.contiguous()
         H, K = k.shape
-        kf = _aligned_empty(max(H, 1) * self.info.kf_bytes_per_head, k.device, 16)
+        if out is not None:
+            assert out.numel() >= max(H, 1) * self.info.kf_bytes_per_head and out.data_ptr() % 16 == 0
+            kf = out
+        else:
+            kf = _aligned_empty(max(H, 1) * self.info.kf_bytes_per_head, k.device, 16)
         _abi.check(_abi.lib().fftconv_precompute_kf(self._h, _ptr(k), H, K, _ptr(kf), _stream(k.device)))
         return kf
 

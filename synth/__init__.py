@@ -178,3 +178,20 @@ def signal_torch(seed: int, name: str, B: int, H: int, N: int, device, dtype, ro
         r1 = min(B * H, r + step)
         out[r:r1] = normal_torch(seed, TENSOR_IDS[name], row0 + r, r1 - r, N, device).to(dtype)
     return out.reshape(B, H, N)
+
+
+def decay_filters_torch(seed: int, H: int, K: int, device, lam_lo: float = 0.5, lam_hi: float = 50.0):
+    """decay_filters() generated on `device` (float32 (H, K)); same stream and
+    recipe, for workloads whose filters do not fit host memory comfortably."""
+    import torch
+    out = normal_torch(seed, TENSOR_IDS["k"], 0, H, K, device)
+    lam = np.exp(np.linspace(np.log(lam_lo), np.log(lam_hi), max(H, 1)))[:H]
+    step = max(1, (1 << 26) // max(K, 1))
+    for h0 in range(0, H, step):
+        h1 = min(H, h0 + step)
+        t = torch.arange(K, dtype=torch.float64, device=device)
+        lt = torch.tensor(lam[h0:h1], dtype=torch.float64, device=device)
+        env = torch.exp(-lt[:, None] * t[None, :] / max(K, 1))
+        nrm = torch.sqrt((env ** 2).sum(dim=1, keepdim=True))
+        out[h0:h1] = (out[h0:h1].double() * env / nrm).float()
+    return out
