@@ -148,6 +148,25 @@ fftconv_status_t fftconv_gated_fwd(fftconv_plan_t plan, const void* d_u, const v
                                    const void* d_kf, void* d_y, int64_t B, int64_t H, void* d_workspace,
                                    fftconv_stream_t stream);
 
+/* End-to-end forward from HOST buffers (plain when h_w == h_v == NULL,
+ * gated otherwise).  h_u, h_w, h_v, h_y: (B, H, N) row-major in the plan
+ * dtype, preferably pinned (pageable memory makes the copies synchronous).
+ * The B batch rows are streamed through the caller-owned device staging
+ * buffer d_stage in chunks of rows_per_chunk (rounded up to even, so rows
+ * keep their packing partner and the result is bitwise that of the device
+ * call; two slots): the host->device
+ * copy of chunk i+1, the convolution of chunk i and the device->host copy of
+ * chunk i-1 run concurrently on library streams (copy engines beside the
+ * SMs).  d_kf: device k_f from fftconv_precompute_kf.  Ordered after earlier
+ * work on `stream`; work queued on `stream` after this call sees h_y
+ * complete.  stage_bytes >= fftconv_host_stage_size(plan, H, rows_per_chunk,
+ * gated).  Errors as fftconv_fwd; FFTCONV_ERR_INVALID_ARG for a short stage. */
+fftconv_status_t fftconv_fwd_host(fftconv_plan_t plan, const void* h_u, const void* h_w, const void* h_v,
+                                  const void* d_kf, void* h_y, int64_t B, int64_t H, int64_t rows_per_chunk,
+                                  void* d_stage, size_t stage_bytes, fftconv_stream_t stream);
+fftconv_status_t fftconv_host_stage_size(fftconv_plan_t plan, int64_t H, int64_t rows_per_chunk, int gated,
+                                         size_t* bytes);
+
 /* Backward of <y, dy> with recomputation (A15).  Plain when
  * d_w == d_v == NULL (then d_dw, d_dv ignored); gated when both are given.
  * d_dk (H, K) fp32 is OVERWRITTEN with the batch sum.  d_workspace:

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -278,6 +279,129 @@ extern "C" fftconv_status_t fftconv_gated_fwd(fftconv_plan_t p, const void* d_u,
                                               fftconv_stream_t stream) {
   if (!d_w || !d_v) { set_last_error("fftconv_gated_fwd: w and v are required"); return FFTCONV_ERR_INVALID_ARG; }
   return run_fwd(p, d_u, d_w, d_v, d_kf, d_y, B, H, d_workspace, stream, "fftconv_gated_fwd");
+}
+
+// ---------------------------------------------------------------- host streaming
+// Device staging slot for `rows` batch rows: u | (w | v) | y | workspace.
+static size_t elem_bytes(const fftconv_plan_s* p) { return p->dtype == FFTCONV_F32 ? 4 : 2; }
+static size_t slot_bytes(fftconv_plan_t p, int64_t H, int64_t rows, bool gated, size_t* ws_bytes) {
+  const size_t t = (size_t(rows) * size_t(H) * size_t(p->N) * elem_bytes(p) + 1023) / 1024 * 1024;
+  size_t ws = 0;
+  fftconv_workspace_size(p, rows, H, 0, &ws);
+  ws = (ws + 1023) / 1024 * 1024;
+  if (ws_bytes) *ws_bytes = ws;
+  return t * (gated ? 4 : 2) + ws;
+}
+
+extern "C" fftconv_status_t fftconv_host_stage_size(fftconv_plan_t p, int64_t H, int64_t rows_per_chunk, int gated,
+                                                    size_t* bytes) {
+  if (!p || !bytes || H < 0 || rows_per_chunk < 1) {
+    set_last_error("fftconv_host_stage_size: bad argument");
+    return FFTCONV_ERR_INVALID_ARG;
+  }
+  const int64_t rc = rows_per_chunk + (rows_per_chunk & 1);  // chunks keep row pairs together
+  *bytes = 2 * slot_bytes(p, H, rc, gated != 0, nullptr) + 1024;
+  return FFTCONV_OK;
+}
+
+namespace {
+// Per-device copy-in / copy-out streams and chunk events, created once.
+struct HostPipe {
+  cudaStream_t in = nullptr, out = nullptr;
+  cudaEvent_t start = nullptr, done = nullptr;
+  cudaEvent_t loaded[2] = {}, computed[2] = {}, freed[2] = {};
+};
+std::mutex g_pipe_mu;
+HostPipe g_pipes[64];
+cudaError_t host_pipe(HostPipe** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  HostPipe& hp = g_pipes[dev];
+  if (!hp.in) {
+    const unsigned f = cudaStreamNonBlocking, ef = cudaEventDisableTiming;
+    if ((e = cudaStreamCreateWithFlags(&hp.in, f)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&hp.out, f)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&hp.start, ef)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&hp.done, ef)) != cudaSuccess) return e;
+    for (int i = 0; i < 2; ++i) {
+      if ((e = cudaEventCreateWithFlags(&hp.loaded[i], ef)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&hp.computed[i], ef)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&hp.freed[i], ef)) != cudaSuccess) return e;
+    }
+  }
+  *out = &hp;
+  return cudaSuccess;
+}
+}  // namespace
+
+extern "C" fftconv_status_t fftconv_fwd_host(fftconv_plan_t p, const void* h_u, const void* h_w, const void* h_v,
+                                             const void* d_kf, void* h_y, int64_t B, int64_t H,
+                                             int64_t rows_per_chunk, void* d_stage, size_t stage_bytes,
+                                             fftconv_stream_t stream) {
+  const char* fn = "fftconv_fwd_host";
+  if (!p) { set_last_error("fftconv_fwd_host: plan is NULL"); return FFTCONV_ERR_INVALID_ARG; }
+  const bool gated = h_w != nullptr || h_v != nullptr;
+  if (gated && !(h_w && h_v)) { set_last_error("fftconv_fwd_host: gated needs both w and v"); return FFTCONV_ERR_INVALID_ARG; }
+  if (B < 0 || H < 0 || rows_per_chunk < 1) { set_last_error("fftconv_fwd_host: bad sizes"); return FFTCONV_ERR_INVALID_ARG; }
+  if (B * H == 0) return FFTCONV_OK;
+  if (!h_u || !h_y || !d_kf || !d_stage) { set_last_error("fftconv_fwd_host: NULL pointer"); return FFTCONV_ERR_INVALID_ARG; }
+  if (!aligned16(d_stage)) { set_last_error("fftconv_fwd_host: stage not 16-byte aligned"); return FFTCONV_ERR_MISALIGNED; }
+  // chunks hold an even number of rows so every row keeps its packing
+  // partner (two real rows per complex transform): results are bitwise
+  // those of one fftconv_fwd / fftconv_gated_fwd call on all B rows
+  const int64_t rpc = rows_per_chunk + (rows_per_chunk & 1);
+  const int64_t rc = rpc < B ? rpc : B;
+  size_t ws_bytes = 0;
+  const size_t slot = slot_bytes(p, H, rc, gated, &ws_bytes);
+  if (stage_bytes < 2 * slot) { set_last_error("fftconv_fwd_host: staging buffer too small"); return FFTCONV_ERR_INVALID_ARG; }
+  HostPipe* hp = nullptr;
+  cudaError_t e = host_pipe(&hp);
+  if (e != cudaSuccess) return cuda_fail(fn, e);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  // the pipeline starts after earlier work on the caller's stream
+  if ((e = cudaEventRecord(hp->start, cs)) != cudaSuccess) return cuda_fail(fn, e);
+  if ((e = cudaStreamWaitEvent(hp->in, hp->start, 0)) != cudaSuccess) return cuda_fail(fn, e);
+  if ((e = cudaStreamWaitEvent(hp->out, hp->start, 0)) != cudaSuccess) return cuda_fail(fn, e);
+  const size_t row_bytes = size_t(H) * size_t(p->N) * elem_bytes(p);
+  const size_t t = (size_t(rc) * row_bytes + 1023) / 1024 * 1024;
+  uint8_t* base = static_cast<uint8_t*>(d_stage);
+  const int64_t nchunks = (B + rc - 1) / rc;
+  for (int64_t i = 0; i < nchunks; ++i) {
+    const int s = int(i & 1);
+    const int64_t b0 = i * rc, rows = (B - b0 < rc ? B - b0 : rc);
+    const size_t off = size_t(b0) * row_bytes, nb = size_t(rows) * row_bytes;
+    uint8_t* sl = base + size_t(s) * slot;
+    uint8_t *du = sl, *dw = sl + t, *dv = sl + 2 * t, *dy = sl + (gated ? 3 : 1) * t, *dws = sl + (gated ? 4 : 2) * t;
+    // copy in (slot reusable once the copy-out of chunk i-2 has finished)
+    if (i >= 2 && (e = cudaStreamWaitEvent(hp->in, hp->freed[s], 0)) != cudaSuccess) return cuda_fail(fn, e);
+    if ((e = cudaMemcpyAsync(du, static_cast<const uint8_t*>(h_u) + off, nb, cudaMemcpyHostToDevice, hp->in)) != cudaSuccess)
+      return cuda_fail(fn, e);
+    if (gated) {
+      if ((e = cudaMemcpyAsync(dw, static_cast<const uint8_t*>(h_w) + off, nb, cudaMemcpyHostToDevice, hp->in)) != cudaSuccess)
+        return cuda_fail(fn, e);
+      if ((e = cudaMemcpyAsync(dv, static_cast<const uint8_t*>(h_v) + off, nb, cudaMemcpyHostToDevice, hp->in)) != cudaSuccess)
+        return cuda_fail(fn, e);
+    }
+    if ((e = cudaEventRecord(hp->loaded[s], hp->in)) != cudaSuccess) return cuda_fail(fn, e);
+    // convolution on the caller's stream
+    if ((e = cudaStreamWaitEvent(cs, hp->loaded[s], 0)) != cudaSuccess) return cuda_fail(fn, e);
+    fftconv_status_t st = run_fwd(p, du, gated ? dw : nullptr, gated ? dv : nullptr, d_kf, dy, rows, H,
+                                  ws_bytes ? dws : nullptr, stream, fn);
+    if (st != FFTCONV_OK) return st;
+    if ((e = cudaEventRecord(hp->computed[s], cs)) != cudaSuccess) return cuda_fail(fn, e);
+    // copy out
+    if ((e = cudaStreamWaitEvent(hp->out, hp->computed[s], 0)) != cudaSuccess) return cuda_fail(fn, e);
+    if ((e = cudaMemcpyAsync(static_cast<uint8_t*>(h_y) + off, dy, nb, cudaMemcpyDeviceToHost, hp->out)) != cudaSuccess)
+      return cuda_fail(fn, e);
+    if ((e = cudaEventRecord(hp->freed[s], hp->out)) != cudaSuccess) return cuda_fail(fn, e);
+  }
+  // later work on the caller's stream sees every chunk of h_y
+  if ((e = cudaEventRecord(hp->done, hp->out)) != cudaSuccess) return cuda_fail(fn, e);
+  if ((e = cudaStreamWaitEvent(cs, hp->done, 0)) != cudaSuccess) return cuda_fail(fn, e);
+  return FFTCONV_OK;
 }
 
 // Workspace layout of the backward pass (bytes):

@@ -148,6 +148,32 @@ class FFTConvPlan:
                                                 _ptr(ws), _stream(u.device)))
         return y
 
+    def fwd_host(self, u: torch.Tensor, kf: torch.Tensor, w=None, v=None, out=None, rows_per_chunk: int = 8,
+                 stage=None) -> torch.Tensor:
+        """End-to-end forward from (pinned) host tensors through fftconv_fwd_host:
+        batch rows are streamed through a device staging buffer with the
+        copies of neighbouring chunks overlapping the convolution."""
+        for t in (u, w, v):
+            if t is not None:
+                assert not t.is_cuda and t.dtype == self.dtype and t.is_contiguous() and t.dim() == 3
+        B, H, N = u.shape
+        assert N == self.info.N
+        out = torch.empty_like(u, pin_memory=u.is_pinned()) if out is None else out
+        gated = w is not None
+        n = ctypes.c_size_t()
+        _abi.check(_abi.lib().fftconv_host_stage_size(self._h, H, rows_per_chunk, int(gated), ctypes.byref(n)))
+        if stage is None or stage.numel() < n.value:
+            stage = _aligned_empty(int(n.value), kf.device, 1024)
+        _abi.check(_abi.lib().fftconv_fwd_host(self._h, _ptr(u), _ptr(w), _ptr(v), _ptr(kf), _ptr(out), B, H,
+                                               rows_per_chunk, _ptr(stage), stage.numel(), _stream(kf.device)))
+        self._stage = stage  # keep the staging buffer alive while the copies run
+        return out
+
+    def host_stage(self, H: int, rows_per_chunk: int = 8, gated: bool = False, device=None):
+        n = ctypes.c_size_t()
+        _abi.check(_abi.lib().fftconv_host_stage_size(self._h, H, rows_per_chunk, int(gated), ctypes.byref(n)))
+        return _aligned_empty(int(n.value), device or self.device, 1024)
+
     def bwd(self, dy, u, kf, K, w=None, v=None):
         """Gradients of <y, dy>: returns du, dw, dv (None when ungated) and dk (H, K)."""
         self._check_sig(dy, u)
