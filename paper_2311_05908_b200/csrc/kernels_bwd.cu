@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
 
   constexpr int NK1C = (L1 / 8) / 2 > 0 ? (L1 / 8) / 2 : 1;  // distinct k1 chunks per thread
   int64_t h = t0 / nbt, bt = t0 % nbt;
+  uint4 nxa[PER_ALL], nya[PER_ALL];  // g rows of the next tile (prefetched)
   for (int64_t t = t0; t < t1; ++t, ++bt) {
     while (bt >= nbt) { bt -= nbt; ++h; }
     const int64_t tile_base = (bt * C::R * H + h) * N;
@@ -335,9 +336,10 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
       cur_h = h;
     }
     uint4 xa[PER_ALL], ya[PER_ALL];
-    // 1. G = FFT(g)
-    load_rows(gu, gw, GATE_IO, tile_base, rows_left, xa, ya);
-    store_rows(xa, ya, GATE_IO);
+    // 1. G = FFT(g) (its rows were prefetched during the previous tile's
+    // last epilogue)
+    if (t == t0) load_rows(gu, gw, GATE_IO, tile_base, rows_left, nxa, nya);
+    store_rows(nxa, nya, GATE_IO);
     cp_async_wait_all();
     forward_AB(0);
     // 2. DC = FFT(dc): issue loads, then wait until stage B(G) has read bufX
@@ -460,6 +462,12 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
       }
     }
     inverse_BA();
+    if (t + 1 < t1) {  // prefetch the next tile's g rows behind the last epilogue
+      int64_t h2 = h, bt2 = bt + 1;
+      if (bt2 >= nbt) { bt2 = 0; ++h2; }
+      const int64_t base2 = (bt2 * C::R * H + h2) * N;
+      load_rows(gu, gw, GATE_IO, base2, int(B - bt2 * C::R < C::R ? B - bt2 * C::R : C::R), nxa, nya);
+    }
     if (GATE_IO) epi_out(tile_base, rows_left, gw, gdu, gu, gdw, true);
     else epi_out(tile_base, rows_left, nullptr, gdu, nullptr, nullptr, false);
     tc_fence_before();
