@@ -43,6 +43,8 @@ WORKLOADS = {
                 dtype="bf16", bwd=True),
     "cfg4": _wl("cfg4: HyenaDNA partial conv B=1 H=256 N=1048576 K=8192 fp16 (fft_size 16384, overlap-save)",
                 1, 256, 1 << 20, fft=16384, K=8192),
+    "cfg4bwd": _wl("cfg4 fwd+bwd: HyenaDNA partial conv B=1 H=256 N=1048576 K=8192 fp16 (fft_size 16384)",
+                   1, 256, 1 << 20, fft=16384, K=8192, bwd=True),
     "cfg5": _wl("cfg5: frequency-sparse causal conv B=8 H=768 N=16384 fp16, 75% of inner Monarch rows skipped",
                 8, 768, 16384, sparse="rows75"),
     "cfg5dense": _wl("cfg5 dense reference: causal conv B=8 H=768 N=16384 fp16", 8, 768, 16384),

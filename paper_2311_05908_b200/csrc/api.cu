@@ -409,8 +409,9 @@ extern "C" fftconv_status_t fftconv_fwd_host(fftconv_plan_t p, const void* h_u, 
 //  multipass : [T_g][T_dc] (fp16 rows, 2 * ceil(B/2) * H * L each)
 //              [partials: H * L0 * nbt' * Lp complex fp32][scratch: H * L complex fp32]
 static size_t bwd_ws_bytes(const fftconv_plan_s* p, int64_t B, int64_t H) {
-  if (p->regime == REGIME_MULTIPASS) {
-    const int64_t rows = 2 * ((B + 1) / 2);
+  if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
+    const int64_t Bv = p->regime == REGIME_PARTIAL ? B * (p->N / (p->L / 2)) : B;
+    const int64_t rows = 2 * ((Bv + 1) / 2);
     const size_t t = size_t(rows) * size_t(H) * size_t(p->L) * 2;
     const size_t part = size_t(H) * p->L0 * size_t(bwd_tiles_per_head(rows, p->L1)) * size_t(p->Lp) * 8;
     return 2 * t + part + size_t(H) * size_t(p->L) * 8;
@@ -471,11 +472,21 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
     g_launches += 2;
     return FFTCONV_OK;
   }
-  if (p->regime != REGIME_MULTIPASS || p->nlev != 1) {
-    set_last_error("fftconv_bwd: this build supports the backward pass for fft_size <= 32768 (fused and one-level multipass)");
+  if ((p->regime != REGIME_MULTIPASS && p->regime != REGIME_PARTIAL) || p->nlev != 1) {
+    set_last_error("fftconv_bwd: this build supports the backward pass for fft_size <= 32768 (fused, one-level "
+                   "multipass and partial)");
     return FFTCONV_ERR_UNSUPPORTED;
   }
-  const int64_t rows = 2 * ((B + 1) / 2);
+  // Partial (overlap-save, A12): the rows are the virtual windows b * NC + j.
+  // c (for dv) is the second half of each window's circular result as in the
+  // forward; dc windows hold only their second half (block j), so the
+  // window's correlation with k is block j's contribution to dg over both
+  // halves (overlap-add in pass 3) and Sum_windows DC conj(G) is exactly
+  // Sum_i dc[i] g[i - t] for t < K <= C (dk).
+  const bool partial = p->regime == REGIME_PARTIAL;
+  const int64_t NCw = partial ? p->N / (p->L / 2) : 1;
+  const int64_t Bv = B * NCw;
+  const int64_t rows = 2 * ((Bv + 1) / 2);
   uint8_t* ws = static_cast<uint8_t*>(d_workspace);
   const size_t tbytes = size_t(rows) * size_t(H) * size_t(p->L) * 2;
   void* Tg = ws;
@@ -486,15 +497,17 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   MpParams mp{};
   mp.wbase = reinterpret_cast<const float2*>(tab + p->tl.wbase);
   mp.wtab = reinterpret_cast<const float2*>(tab + p->tl.wtab);
-  mp.B = B; mp.H = H; mp.N = p->N; mp.L0 = p->L0; mp.Lp = p->Lp;
+  mp.B = Bv; mp.H = H; mp.N = p->N; mp.L0 = p->L0; mp.Lp = p->Lp;
   mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
+  if (partial) { mp.partial = 1; mp.C = p->L / 2; mp.NC = NCw; }
   // pass 1 on g = u (* w) and on dc = dy (* v)
   mp.u = d_u; mp.w = d_w; mp.gated = gated ? 1 : 0; mp.ws = Tg;
   e = launch_mp_pass(mp, 1, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
-  mp.u = d_dy; mp.w = d_v; mp.ws = Tdc;
+  mp.u = d_dy; mp.w = d_v; mp.ws = Tdc; mp.win_hi_only = partial ? 1 : 0;
   e = launch_mp_pass(mp, 1, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
+  mp.win_hi_only = 0;
   // inner backward on the complex rows (circular), in place
   BwdParams b{};
   b.u = Tg; b.dy = Tdc; b.dv = Tg; b.du = Tdc;
@@ -513,6 +526,7 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   } else {
     mp.ws = Tdc; mp.gated = 0; mp.v = nullptr; mp.y = d_du; mp.v2 = nullptr; mp.y2 = nullptr;
   }
+  mp.ola = partial ? 1 : 0;  // partial: dg = overlap-add of neighbouring windows
   e = launch_mp_pass(mp, 3, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
   dk.part = static_cast<const float2*>(part);

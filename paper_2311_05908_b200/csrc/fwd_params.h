@@ -72,6 +72,9 @@ struct MpParams {
   // heads; T is indexed by the chunk-local (pair, head), u/w/v/y by the
   // global ones.  Hg = 0 means Hg = H (unchunked).
   int64_t pair0, h0, Hg;
+  // backward of the partial conv: pass 1 loads only the second half of each
+  // window (dc blocks); pass 3 overlap-adds neighbouring windows (dg)
+  int32_t win_hi_only, ola;
 };
 cudaError_t launch_mp_pass(const MpParams& prm, int pass, cudaStream_t s);
 

@@ -164,7 +164,11 @@ __global__ void __launch_bounds__(256, 3) mp_pass1_kernel(const MpParams prm) {
 #pragma unroll
   for (int n0 = 0; n0 < NIN; ++n0) {
     const int64_t o = int64_t(n0) * prm.Lp;
-    const bool ok0 = MODE != 1 || s0 + o >= 0, ok1 = has1 && (MODE != 1 || s1 + o >= 0);
+    // partial: the window's first half may precede the row (zeros); the
+    // backward's dc windows keep only their second half (win_hi_only)
+    const bool hi_only = MODE == 1 && prm.win_hi_only && n0 < L0 / 2;
+    const bool ok0 = !hi_only && (MODE != 1 || s0 + o >= 0);
+    const bool ok1 = !hi_only && has1 && (MODE != 1 || s1 + o >= 0);
     float a[COLS], c[COLS];
 #pragma unroll
     for (int j = 0; j < COLS; ++j) a[j] = c[j] = 0.f;
@@ -379,6 +383,109 @@ __global__ void __launch_bounds__(256, 3) mp_pass3_kernel(const MpParams prm) {
   }
 }
 
+// Backward of the partial convolution, dg by overlap-add: the circular
+// correlation of window j (dc block j in its second half, zeros in its
+// first) with k spans positions [(j-1)C, (j+1)C) of dg, so
+// dg[jC : (j+1)C] = hi(window j) + lo(window j+1) (no wrap: K <= C).  A thread
+// owns pair p = windows (2p, 2p+1) of one batch row (NC is even): block 2p is
+// hi(re) + lo(im) of pair p, block 2p+1 is hi(im) of pair p + lo(re) of pair
+// p+1 (absent for the row's last window).
+template <int L0, typename TT, int C2>
+FC_DEVICE void pair_idft(const MpParams& prm, int64_t p, int64_t h, int n, const CV<C2>& bw, CV<C2>* xl,
+                         CV<C2>* xh) {
+  constexpr int COLS = 2 * C2;
+  const TT* Tre = reinterpret_cast<const TT*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
+  const TT* Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
+  using RawT = Raw<TT, COLS>;
+  RawT rr[L0], ri[L0];
+#pragma unroll
+  for (int k0 = 0; k0 < L0; ++k0) {
+    rr[k0] = *reinterpret_cast<const RawT*>(Tre + int64_t(k0) * prm.Lp);
+    ri[k0] = *reinterpret_cast<const RawT*>(Tim + int64_t(k0) * prm.Lp);
+  }
+  const float s = rsqrtf(float(L0));
+  CV<C2> tw;
+#pragma unroll
+  for (int cc = 0; cc < C2; ++cc) {
+    tw.r[cc] = make_float2(s, s);
+    tw.i[cc] = make_float2(0.f, 0.f);
+  }
+  CV<C2> e[L0 / 2], o[L0 / 2];
+#pragma unroll
+  for (int k0 = 0; k0 < L0; ++k0) {
+    float fr[COLS], fi[COLS];
+    unpack_cols<TT, COLS>(rr[k0], fr);
+    unpack_cols<TT, COLS>(ri[k0], fi);
+    CV<C2> x;
+#pragma unroll
+    for (int cc = 0; cc < C2; ++cc) {
+      x.r[cc] = make_float2(fr[2 * cc], fr[2 * cc + 1]);
+      x.i[cc] = make_float2(fi[2 * cc], fi[2 * cc + 1]);
+    }
+    x = cv_mulc(x, tw);
+    if (k0 + 1 < L0) tw = cv_mul(tw, bw);
+    if (k0 & 1) o[k0 / 2] = x;
+    else e[k0 / 2] = x;
+  }
+  DftVec<L0 / 2, true, C2>::run(e);
+  DftVec<L0 / 2, true, C2>::run(o);
+#pragma unroll
+  for (int m = 0; m < L0 / 2; ++m) cv_bfly<L0, true>(m, e[m], o[m], xl[m], xh[m]);
+}
+
+template <int L0, bool GATED, typename T, typename TT>
+__global__ void __launch_bounds__(256, 2) mp_pass3_ola_kernel(const MpParams prm) {
+  constexpr int COLS = PassCfg<L0>::COLS, C2 = PassCfg<L0>::C2;
+  const int64_t NCH = int64_t(prm.Lp) / COLS;
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t pairs = uint32_t((prm.B + 1) / 2);
+  if (idx >= pairs * uint32_t(prm.H) * uint32_t(NCH)) return;
+  const int n = int(idx & uint32_t(NCH - 1)) * COLS;
+  const uint32_t ph = idx >> (31 - __clz(uint32_t(NCH)));
+  const int64_t h = ph % uint32_t(prm.H), p = ph / uint32_t(prm.H);
+  const CV<C2> bw = twiddle_base<C2>(prm, n);
+  CV<C2> xl[L0 / 2], xh[L0 / 2], nl[L0 / 2], nh[L0 / 2];
+  pair_idft<L0, TT, C2>(prm, p, h, n, bw, xl, xh);
+  const uint32_t nc = uint32_t(prm.NC);
+  const int64_t g0 = 2 * p, b = uint32_t(g0) / nc, j0 = g0 - b * int64_t(nc);
+  const bool has_next = j0 + 2 < int64_t(nc);  // window j0 + 2 belongs to the same row
+  if (has_next) pair_idft<L0, TT, C2>(prm, p + 1, h, n, bw, nl, nh);
+  const int64_t Hg = prm.Hg ? prm.Hg : prm.H, hg = h + prm.h0;
+  const int64_t row = (b * Hg + hg) * prm.N + n;
+  T* __restrict__ y = reinterpret_cast<T*>(prm.y);
+  auto emit = [&](float* a, int64_t off) {  // one output row segment of COLS
+    if (prm.y2) {
+      float g[COLS], q[COLS];
+      ld_cols<T, COLS>(reinterpret_cast<const T*>(prm.v2) + off, g);
+#pragma unroll
+      for (int j = 0; j < COLS; ++j) q[j] = a[j] * g[j];
+      st_cols<T, COLS>(reinterpret_cast<T*>(prm.y2) + off, q);
+    }
+    if (GATED) {
+      float g[COLS];
+      ld_cols<T, COLS>(reinterpret_cast<const T*>(prm.v) + off, g);
+#pragma unroll
+      for (int j = 0; j < COLS; ++j) a[j] *= g[j];
+    }
+    st_cols<T, COLS>(y + off, a);
+  };
+#pragma unroll
+  for (int m = 0; m < L0 / 2; ++m) {
+    float a[COLS], c[COLS];
+#pragma unroll
+    for (int cc = 0; cc < C2; ++cc) {
+      // block j0: hi(window j0) + lo(window j0 + 1)
+      a[2 * cc] = xh[m].r[cc].x + xl[m].i[cc].x;
+      a[2 * cc + 1] = xh[m].r[cc].y + xl[m].i[cc].y;
+      // block j0 + 1: hi(window j0 + 1) + lo(window j0 + 2)
+      c[2 * cc] = xh[m].i[cc].x + (has_next ? nl[m].r[cc].x : 0.f);
+      c[2 * cc + 1] = xh[m].i[cc].y + (has_next ? nl[m].r[cc].y : 0.f);
+    }
+    emit(a, row + j0 * prm.C + int64_t(m) * prm.Lp);
+    emit(c, row + (j0 + 1) * prm.C + int64_t(m) * prm.Lp);
+  }
+}
+
 // k_f, step 1: per (head, column n'): DFT_L0 of k[n' + Lrow n0] (n0 < L0/2,
 // K <= L/2), twiddle W_L^{n' k0}; fp32 scratch written into the head's k_f
 // blocks: element (h, k0, n') lives in 2048-element block
@@ -490,6 +597,18 @@ static cudaError_t launch_mp_l0(const MpParams& prm, int pass, cudaStream_t s) {
   if (prm.circ) {  // deep levels: fp16 complex rows, never gated
     if (prm.dtype != 0 || prm.gated) return cudaErrorInvalidValue;
     launch_pass_k<L0, 2, false, __half>(prm, pass, grid, s);
+  } else if (prm.partial && prm.ola && pass == 3) {  // backward dg of the partial conv
+    if ((prm.NC & 1) || prm.pair0 || prm.h0) return cudaErrorInvalidValue;
+    const bool g = prm.gated != 0;
+    if (prm.dtype == 0) {
+      if (g) mp_pass3_ola_kernel<L0, true, __half, __half><<<grid, 256, 0, s>>>(prm);
+      else mp_pass3_ola_kernel<L0, false, __half, __half><<<grid, 256, 0, s>>>(prm);
+    } else if (prm.dtype == 1) {
+      if (g) mp_pass3_ola_kernel<L0, true, __nv_bfloat16, __half><<<grid, 256, 0, s>>>(prm);
+      else mp_pass3_ola_kernel<L0, false, __nv_bfloat16, __half><<<grid, 256, 0, s>>>(prm);
+    } else {
+      return cudaErrorInvalidValue;
+    }
   } else if (prm.partial) {
     launch_pass_m<L0, 1>(prm, pass, grid, s);
   } else {

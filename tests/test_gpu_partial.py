@@ -52,3 +52,33 @@ def test_partial_cfg4_shape_sampled():
             got.append(y[0, h, i])
     got, ref = np.array(got), np.array(ref)
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < REL_L2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,L,K", [(16384, 4096, 2048), (16384, 4096, 700), (32768, 16384, 8192)])
+@pytest.mark.parametrize("dtype,gated", [("f16", False), ("bf16", True)])
+def test_partial_backward(N, L, K, dtype, gated):
+    """Backward of the partial convolution (NEXT-3): dv from the windows'
+    second halves, dg by overlap-add of the dc windows' correlations, dk from
+    Sum_windows DC conj(G); against the oracle's causal-conv gradients with the
+    truncated filter (A12, A15)."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    B, H = 3, 2
+    plan = FFTConvPlan(N, fft_size=L, dtype=TDT[dtype], causal=True)
+    assert plan.info.regime == 2
+    q = lambda name: synth.quantize(synth.signal(13, name, B, H, N), dtype)
+    u, dy = q("u"), q("dy")
+    w, v = (q("w"), q("v")) if gated else (None, None)
+    k = synth.decay_filters(13, H, K).astype(np.float32)
+    t = lambda a: torch.tensor(a, dtype=TDT[dtype], device="cuda") if a is not None else None
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    g = plan.bwd(t(dy), t(u), kf, K, w=t(w), v=t(v))
+    torch.cuda.synchronize()
+    ref = orc.conv_bwd(dy, u, k.astype(np.float64), w=w, v=v)
+    for key in ("du", "dw", "dv", "dk"):
+        if ref[key] is None:
+            continue
+        got = g[key].float().cpu().numpy().astype(np.float64)
+        assert np.all(np.isfinite(got)), key
+        rel = np.linalg.norm(got - ref[key]) / np.linalg.norm(ref[key])
+        assert rel < REL_L2, (key, rel)
