@@ -45,6 +45,8 @@ WORKLOADS = {
                 1, 256, 1 << 20, fft=16384, K=8192),
     "cfg4bwd": _wl("cfg4 fwd+bwd: HyenaDNA partial conv B=1 H=256 N=1048576 K=8192 fp16 (fft_size 16384)",
                    1, 256, 1 << 20, fft=16384, K=8192, bwd=True),
+    "long1m": _wl("long gated causal conv B=8 H=96 N=1048576 bf16, fwd+bwd (two outer levels)", 8, 96, 1 << 20,
+                  gated=True, dtype="bf16", bwd=True),
     "cfg5": _wl("cfg5: frequency-sparse causal conv B=8 H=768 N=16384 fp16, 75% of inner Monarch rows skipped",
                 8, 768, 16384, sparse="rows75"),
     "cfg5dense": _wl("cfg5 dense reference: causal conv B=8 H=768 N=16384 fp16", 8, 768, 16384),

@@ -414,7 +414,7 @@ static size_t bwd_ws_bytes(const fftconv_plan_s* p, int64_t B, int64_t H) {
     const int64_t rows = 2 * ((Bv + 1) / 2);
     const size_t t = size_t(rows) * size_t(H) * size_t(p->L) * 2;
     const size_t part = size_t(H) * p->L0 * size_t(bwd_tiles_per_head(rows, p->L1)) * size_t(p->Lp) * 8;
-    return 2 * t + part + size_t(H) * size_t(p->L) * 8;
+    return (p->nlev > 1 ? 4 : 2) * t + part + size_t(H) * size_t(p->L) * 8;
   }
   return size_t(H) * size_t(bwd_tiles_per_head(B, p->L1)) * size_t(p->L) * 8;
 }
@@ -472,9 +472,8 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
     g_launches += 2;
     return FFTCONV_OK;
   }
-  if ((p->regime != REGIME_MULTIPASS && p->regime != REGIME_PARTIAL) || p->nlev != 1) {
-    set_last_error("fftconv_bwd: this build supports the backward pass for fft_size <= 32768 (fused, one-level "
-                   "multipass and partial)");
+  if (p->regime != REGIME_MULTIPASS && p->regime != REGIME_PARTIAL) {
+    set_last_error("fftconv_bwd: regime not supported by this build");
     return FFTCONV_ERR_UNSUPPORTED;
   }
   // Partial (overlap-save, A12): the rows are the virtual windows b * NC + j.
@@ -487,57 +486,93 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   const int64_t NCw = partial ? p->N / (p->L / 2) : 1;
   const int64_t Bv = B * NCw;
   const int64_t rows = 2 * ((Bv + 1) / 2);
+  const int nlev = p->nlev;
   uint8_t* ws = static_cast<uint8_t*>(d_workspace);
   const size_t tbytes = size_t(rows) * size_t(H) * size_t(p->L) * 2;
-  void* Tg = ws;
-  void* Tdc = ws + tbytes;
-  void* part = ws + 2 * tbytes;
+  // T buffers of g and dc; recursive plans ping-pong between two of each
+  void* Tg[2] = {ws, ws + (nlev > 1 ? 2 : 1) * tbytes};
+  void* Tdc[2] = {ws + tbytes, ws + 3 * tbytes};
+  if (nlev == 1) { Tg[1] = Tg[0]; Tdc[1] = Tdc[0]; }
+  void* part = ws + (nlev > 1 ? 4 : 2) * tbytes;
   const int64_t nbt_in = bwd_tiles_per_head(rows, p->L1);
   void* scratch = static_cast<uint8_t*>(part) + size_t(H) * p->L0 * size_t(nbt_in) * size_t(p->Lp) * 8;
   MpParams mp{};
   mp.wbase = reinterpret_cast<const float2*>(tab + p->tl.wbase);
   mp.wtab = reinterpret_cast<const float2*>(tab + p->tl.wtab);
-  mp.B = Bv; mp.H = H; mp.N = p->N; mp.L0 = p->L0; mp.Lp = p->Lp;
+  mp.B = Bv; mp.H = H; mp.N = p->N; mp.L0 = p->lev_L0[0]; mp.Lp = int32_t(p->L / p->lev_L0[0]);
   mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
+  mp.Llev = p->L;
+  if (nlev > 1) mp.wtab = nullptr;  // outer twiddles on the fly, as in the forward
   if (partial) { mp.partial = 1; mp.C = p->L / 2; mp.NC = NCw; }
-  // pass 1 on g = u (* w) and on dc = dy (* v)
-  mp.u = d_u; mp.w = d_w; mp.gated = gated ? 1 : 0; mp.ws = Tg;
+  // deeper outer levels (recursive plans): complex circular fp16 rows
+  auto level = [&](int l, void* const* T) {
+    MpParams q{};
+    int64_t Hl = H, Ll = p->L;
+    for (int j = 0; j < l; ++j) { Hl *= p->lev_L0[j]; Ll /= p->lev_L0[j]; }
+    q.B = rows; q.H = Hl; q.N = Ll; q.L0 = p->lev_L0[l]; q.Lp = int32_t(Ll / p->lev_L0[l]);
+    q.Llev = Ll; q.circ = 1; q.dtype = 0; q.gated = 0;
+    q.u = T[(l - 1) & 1]; q.ws = T[l & 1]; q.y = T[(l - 1) & 1];
+    return q;
+  };
+  int launches = 0;
+  // pass 1 on g = u (* w) and on dc = dy (* v), then the deeper levels
+  mp.u = d_u; mp.w = d_w; mp.gated = gated ? 1 : 0; mp.ws = Tg[0];
   e = launch_mp_pass(mp, 1, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
-  mp.u = d_dy; mp.w = d_v; mp.ws = Tdc; mp.win_hi_only = partial ? 1 : 0;
+  mp.u = d_dy; mp.w = d_v; mp.ws = Tdc[0]; mp.win_hi_only = partial ? 1 : 0;
   e = launch_mp_pass(mp, 1, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
   mp.win_hi_only = 0;
+  launches += 2;
+  for (int l = 1; l < nlev; ++l) {
+    if ((e = launch_mp_pass(level(l, Tg), 1, st)) != cudaSuccess) return cuda_fail(fn, e);
+    if ((e = launch_mp_pass(level(l, Tdc), 1, st)) != cudaSuccess) return cuda_fail(fn, e);
+    launches += 2;
+  }
   // inner backward on the complex rows (circular), in place
+  void* Tgi = Tg[(nlev - 1) & 1];
+  void* Tdci = Tdc[(nlev - 1) & 1];
   BwdParams b{};
-  b.u = Tg; b.dy = Tdc; b.dv = Tg; b.du = Tdc;
+  b.u = Tgi; b.dy = Tdci; b.dv = Tgi; b.du = Tdci;
   b.kf = d_kf; b.tables = p->d_tables; b.acc = part;
   b.B = rows; b.H = H * p->L0; b.N = p->Lp; b.L1 = p->L1; b.causal = 0;
   b.gate_io = 0; b.need_c = gated ? 1 : 0; b.dtype = 0;
   b.num_sms = num_sms_current();
   e = launch_bwd_fused(b, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
+  launches += 1;
+  // deeper levels back (c only when gated: dv needs it)
+  for (int l = nlev - 1; l >= 1; --l) {
+    if (gated && (e = launch_mp_pass(level(l, Tg), 3, st)) != cudaSuccess) return cuda_fail(fn, e);
+    if ((e = launch_mp_pass(level(l, Tdc), 3, st)) != cudaSuccess) return cuda_fail(fn, e);
+    launches += gated ? 2 : 1;
+  }
   // pass 3: dv = dy * c ; du = dg * w (or dg), dw = dg * u
   if (gated) {
-    mp.ws = Tg; mp.gated = 1; mp.v = d_dy; mp.y = d_dv; mp.v2 = nullptr; mp.y2 = nullptr;
+    mp.ws = Tg[0]; mp.gated = 1; mp.v = d_dy; mp.y = d_dv; mp.v2 = nullptr; mp.y2 = nullptr;
     e = launch_mp_pass(mp, 3, st);
     if (e != cudaSuccess) return cuda_fail(fn, e);
-    mp.ws = Tdc; mp.v = d_w; mp.y = d_du; mp.v2 = d_u; mp.y2 = d_dw;
+    mp.ws = Tdc[0]; mp.v = d_w; mp.y = d_du; mp.v2 = d_u; mp.y2 = d_dw;
+    launches += 1;
   } else {
-    mp.ws = Tdc; mp.gated = 0; mp.v = nullptr; mp.y = d_du; mp.v2 = nullptr; mp.y2 = nullptr;
+    mp.ws = Tdc[0]; mp.gated = 0; mp.v = nullptr; mp.y = d_du; mp.v2 = nullptr; mp.y2 = nullptr;
   }
   mp.ola = partial ? 1 : 0;  // partial: dg = overlap-add of neighbouring windows
   e = launch_mp_pass(mp, 3, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
+  launches += 1;
   dk.part = static_cast<const float2*>(part);
   dk.scratch = static_cast<float2*>(scratch);
-  dk.wbase = mp.wbase;
+  dk.wbase = nlev > 1 ? nullptr : mp.wbase;
   dk.nbt = nbt_in;
   dk.L0 = p->L0;
   dk.Lp = p->Lp;
+  dk.lev_L0 = p->lev_L0;
+  dk.nlev = nlev;
+  dk.Lfull = p->L;
   e = launch_dk_finalize(dk, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
-  g_launches += gated ? 7 : 6;
+  g_launches += launches + 1 + nlev;
   return FFTCONV_OK;
 }
 

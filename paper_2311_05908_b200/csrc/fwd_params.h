@@ -111,6 +111,12 @@ struct DkParams {
   const float2* wbase;    // multipass: W_L^{n'}, n' < Lp
   int64_t H, K, nbt;
   int32_t L0, Lp;
+  // recursive plans (nlev > 1): L0 above is the product of the levels; the
+  // deeper levels are inverted in place on scratch, then level 0 (twiddles
+  // W_Lfull^{n'} on the fly when wbase is null)
+  const int32_t* lev_L0;
+  int32_t nlev;
+  int64_t Lfull;
 };
 cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s);
 cudaError_t launch_mp_precompute_kf(const KfParams& prm, const int32_t* lev_L0, int nlev, int64_t Lfull,

@@ -313,7 +313,14 @@ __global__ void __launch_bounds__(256) dk_cols_kernel(const DkParams prm) {
   if (idx >= prm.H * prm.Lp) return;
   const int n = int(idx % prm.Lp);
   const int64_t h = idx / prm.Lp;
-  const float2 bw = prm.wbase[n];
+  float2 bw;
+  if (prm.wbase) {
+    bw = prm.wbase[n];
+  } else {  // W_Lfull^{n}, exact dyadic argument
+    float sn, cs;
+    sincospif(-2.0f * float(n) / float(prm.Lfull), &sn, &cs);
+    bw = make_float2(cs, sn);
+  }
   float2 tw = make_float2(1.f, 0.f);
   float2 x[L0];
 #pragma unroll
@@ -343,12 +350,24 @@ cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
   dk_rows_kernel<<<unsigned(prm.H * prm.L0), 256, smem, s>>>(prm);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || prm.L0 == 1) return e;
-  const unsigned grid = unsigned((prm.H * prm.Lp + 255) / 256);
-  switch (prm.L0) {
-    case 2: dk_cols_kernel<2><<<grid, 256, 0, s>>>(prm); break;
-    case 4: dk_cols_kernel<4><<<grid, 256, 0, s>>>(prm); break;
-    case 8: dk_cols_kernel<8><<<grid, 256, 0, s>>>(prm); break;
-    case 16: dk_cols_kernel<16><<<grid, 256, 0, s>>>(prm); break;
+  DkParams c = prm;
+  if (prm.nlev > 1) {  // invert the deeper levels in place, deepest first
+    for (int l = prm.nlev - 1; l >= 1; --l) {
+      int64_t rows = prm.H, Lrow = prm.Lfull;
+      for (int j = 0; j < l; ++j) { rows *= prm.lev_L0[j]; Lrow /= prm.lev_L0[j]; }
+      e = launch_mp_cols_inverse(prm.scratch, prm.lev_L0[l], rows, Lrow, s);
+      if (e != cudaSuccess) return e;
+    }
+    c.L0 = prm.lev_L0[0];
+    c.Lp = int32_t(prm.Lfull / prm.lev_L0[0]);
+    c.wbase = nullptr;
+  }
+  const unsigned grid = unsigned((c.H * c.Lp + 255) / 256);
+  switch (c.L0) {
+    case 2: dk_cols_kernel<2><<<grid, 256, 0, s>>>(c); break;
+    case 4: dk_cols_kernel<4><<<grid, 256, 0, s>>>(c); break;
+    case 8: dk_cols_kernel<8><<<grid, 256, 0, s>>>(c); break;
+    case 16: dk_cols_kernel<16><<<grid, 256, 0, s>>>(c); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

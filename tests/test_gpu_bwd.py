@@ -54,3 +54,18 @@ def test_bwd_deterministic():
     for key in a:
         if a[key] is not None:
             assert np.array_equal(a[key], b[key]), key
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [32768, 131072])
+@pytest.mark.parametrize("dtype,gated", [("f16", False), ("bf16", True)])
+def test_bwd_multilevel_parity(N, dtype, gated):
+    """Backward of recursive multipass plans (two outer levels): both T
+    chains through every level, the inner backward, and dk inverted level by
+    level (deepest first)."""
+    got, ref = _run(N, dtype, gated, B=2, H=1, seed=4)
+    for key in ("du", "dw", "dv", "dk"):
+        if ref[key] is None:
+            continue
+        assert np.all(np.isfinite(got[key])), key
+        assert _rel(got[key], ref[key]) < REL_L2, (key, _rel(got[key], ref[key]))
