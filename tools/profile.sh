@@ -5,19 +5,22 @@ tag=${1:-r01}
 d=gpurun_out/prof_$tag
 mkdir -p $d
 K='regex:fftconv|precompute|mp_|dk_|kf_'
-# 1. launch lists (cold-cache, serialised: compare shares, not absolutes)
-for w in ${WORKLOADS:-cfg2 cfg3 cfg4 cfg5 sweep2048 sweep8192}; do
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -c 40 --csv \
-      --log-file $d/launches_$w.csv python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 3 > /dev/null 2>&1
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__issue_active.avg.pct_of_peak_sustained_elapsed,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed
+# 1. launch lists of one warm step (cold-cache, serialised: compare shares, not absolutes)
+for w in ${WORKLOADS:-cfg2 cfg3 cfg4 cfg4bwd cfg5 sweep1024 sweep8192 long1m}; do
+  timeout 900 ncu --metrics $M --clock-control none -k "$K" -c 60 --csv \
+      --log-file $d/launches_$w.csv python bench.py --workload $w --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 3 > /dev/null 2>&1
 done
 # 2. full sections of the dominant kernels
 if [ -z "$NOFULL" ]; then
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:fftconv_fwd_o2 -s 3 -c 1 -o $d/fwd_cfg2 \
-    python bench.py --workload cfg2 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 3 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:fftconv_bwd_o2 -s 1 -c 1 -o $d/bwd_cfg3 \
-    python bench.py --workload cfg3 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 3 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none -k regex:"mp_pass|fftconv_fwd_o2" -s 3 -c 3 -o $d/mp_sweep8192 \
-    python bench.py --workload sweep8192 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 3 > /dev/null 2>&1
+full() {  # name workload kernel-regex skip count
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$3" -s $4 -c $5 -o $d/$1 \
+      python bench.py --workload $2 --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 3 > /dev/null 2>&1
+}
+full fwd_cfg2 cfg2 fftconv_fwd_o2 3 1
+full kf_cfg2 cfg2 precompute_kf 3 1
+full bwd_cfg3 cfg3 fftconv_bwd_o2 2 1
+full mp_sweep8192 sweep8192 "mp_pass|fftconv_fwd_o2" 3 3
 fi
 # 3. text summaries
 for r in $d/*.ncu-rep; do
