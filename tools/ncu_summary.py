@@ -21,6 +21,8 @@ def rows(path):
 
 def raw_summary(path):
     r = rows(path)
+    if len(r) < 3:
+        return []
     hdr, units = r[0], r[1]
     out = []
     for row in r[2:]:
@@ -30,14 +32,18 @@ def raw_summary(path):
     return out
 
 
+UNIT = {"ns": 1.0, "nsecond": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "s": 1e9, "second": 1e9}
+
+
 def launches(path):
     r = rows(path)
     hdr = r[0]
-    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    ki, vi, mi, ui = (hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name"),
+                      hdr.index("Metric Unit"))
     agg = collections.OrderedDict()
     for row in r[1:]:
-        if len(row) > vi:
-            agg.setdefault(row[ki], []).append(float(row[vi].replace(",", "")))
+        if len(row) > vi and row[mi] == "gpu__time_duration.sum":
+            agg.setdefault(row[ki], []).append(float(row[vi].replace(",", "")) * UNIT.get(row[ui], 1.0))
     tot = sum(sum(v) for v in agg.values())
     return [(k, len(v), sum(v) / len(v), sum(v) / tot) for k, v in agg.items()]
 

@@ -43,7 +43,7 @@ def main(d, out):
         if r is None:
             continue
         res[w] = {"dram_bytes_per_launch": r[0], "kernels_per_call": r[1],
-                  "source": os.path.join("profiles", os.path.basename(d) + "_" + os.path.basename(p)),
+                  "source": os.path.join("profiles", "r01_final", os.path.basename(p)),
                   "note": "sum of dram__bytes_read+write over the conv call's kernels (one step; k_f precompute excluded)"}
     json.dump(res, open(out, "w"), indent=1)
 
