@@ -388,7 +388,6 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
       load_chunks(tile_base, rows_left, uv, wv);
       store_chunks(uv, wv);
     }
-    if (new_h) cp_async_wait_all();
     stamp(1);
 
     // ---------------- stage A: D[(p,n1)][(re|im|-im, k2)] = X[(p,n1)][(c,n2)] * G_A
@@ -449,6 +448,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
     }
     stamp(4);
 
+    // the new head's k_f copy is first read in epilogue 2: wait for this
+    // thread's copies here, the warpgroup barrier of stage B publishes them
+    if (new_h) cp_async_wait_all();
     // ---------------- stage B: per group of 128 rows (p,k2), contract n1 -> k1
     sync_and_issue([&](int h2) {
       constexpr uint32_t idesc = idesc_f16(128, NBF, true, false);
