@@ -576,7 +576,13 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
     // precision of every stage; finer than bf16 output) before * v.
     // (Circular gated tiles store directly.)
     {
-      constexpr bool STAGE = CAUSAL || !GATED;
+#ifndef FC_CIRC_DIRECT
+#define FC_CIRC_DIRECT 0
+#endif
+      // circular tiles (the multipass inner pass) may store straight from
+      // TMEM registers (16 B per item, 64 B apart within a warp) instead of
+      // staging through bufX for fully coalesced rows (FC_CIRC_DIRECT)
+      constexpr bool STAGE = CAUSAL || (!GATED && !FC_CIRC_DIRECT);
       using S = typename std::conditional<GATED, __half, T>::type;
       constexpr int OCH = C::R * C::NOUT / 8 / kWGThreads;  // coalesced output chunks per thread
       static_assert(!STAGE || C::R * C::NOUT * sizeof(S) <= C::BUFX_BYTES, "y staging fits in bufX");
@@ -671,16 +677,18 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
           tmem_ld_wait();
           int r, n;
           item_rn(i, r, n);
-          float v8[8];
-          IO<T>::to_f32x8(vv[i], v8);
+          if constexpr (GATED) {
+            float v8[8];
+            IO<T>::to_f32x8(vv[i], v8);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) o[e] *= v8[e];
+            for (int e = 0; e < 8; ++e) o[e] *= v8[e];
+          }
           if (r < rows_left)
             *reinterpret_cast<uint4*>(gy + tile_base + int64_t(r) * HN + n) =
                 make_uint4(IO<T>::pack2(o[0], o[1]), IO<T>::pack2(o[2], o[3]), IO<T>::pack2(o[4], o[5]),
                            IO<T>::pack2(o[6], o[7]));
         }
-        if (has_next) {
+        if (GATED && has_next) {  // (plain tiles prefetched these before the wait)
           int64_t hh2 = hh, bt2 = bt + kWG;
           while (bt2 >= nbt) { bt2 -= nbt; ++hh2; }
           const int64_t base2 = (bt2 * C::R * H + phys_head(hh2)) * N;
