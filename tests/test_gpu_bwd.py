@@ -69,3 +69,30 @@ def test_bwd_multilevel_parity(N, dtype, gated):
             continue
         assert np.all(np.isfinite(got[key])), key
         assert _rel(got[key], ref[key]) < REL_L2, (key, _rel(got[key], ref[key]))
+
+
+@pytest.mark.gpu
+def test_bwd_cfg3_full_size_sampled():
+    """cfg 3 backward at full size (gated causal bf16, B=16, H=768, N=8192),
+    bench.py's launch configuration: du, dw, dv on sampled (b, h) rows and dk of
+    sampled heads (batch sums over all 16 rows) against the oracle run on
+    just those rows / heads."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    B, H, N = 16, 768, 8192
+    plan = FFTConvPlan(N, dtype=torch.bfloat16, causal=True)
+    q = lambda name: synth.quantize(synth.signal(8, name, B, H, N), "bf16")
+    u, w, v, dy = q("u"), q("w"), q("v"), q("dy")
+    k = synth.decay_filters(8, H, N).astype(np.float32)
+    t = lambda a: torch.tensor(a, dtype=torch.bfloat16, device="cuda")
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    g = plan.bwd(t(dy), t(u), kf, N, w=t(w), v=t(v))
+    torch.cuda.synchronize()
+    got = {key: g[key].float().cpu().numpy() for key in ("du", "dw", "dv", "dk")}
+    rng = np.random.default_rng(9)
+    for h in rng.choice(H, 3, replace=False):
+        sl = (slice(None), slice(h, h + 1), slice(None))
+        ref = orc.conv_bwd(dy[sl], u[sl], k[h:h + 1].astype(np.float64), w=w[sl], v=v[sl])
+        assert _rel(got["dk"][h:h + 1], ref["dk"]) < REL_L2
+        for b in rng.choice(B, 3, replace=False):
+            for key in ("du", "dw", "dv"):
+                assert _rel(got[key][b, h], ref[key][b, 0]) < REL_L2, (key, b, h)

@@ -97,3 +97,30 @@ def test_sparse_backward(N, dims, zeroed):
         assert np.all(np.isfinite(got)), key
         rel = np.linalg.norm(got - ref[key]) / np.linalg.norm(ref[key])
         assert rel < REL_L2, (key, rel)
+
+
+@pytest.mark.gpu
+def test_sparse_cfg5_full_size_sampled_rows():
+    """cfg 5 at full size (B=8, H=768, N=16384, fp16, 75 % of the inner rows
+    skipped), bench.py's launch configuration; 16 sampled (b, h) rows compared
+    whole against the oracle's masked convolution of those rows."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    B, H, N = 8, 768, 16384
+    keep_k0 = np.zeros(16, bool)
+    keep_k0[[0, 1, 8, 15]] = True
+    dims, keeps = [2048, 16], [np.ones(2048, bool), keep_k0]
+    plan = FFTConvPlan(N, dtype=torch.float16, causal=True, sparsity=(dims, keeps))
+    u = torch.empty(B, H, N, dtype=torch.float16, device="cuda")
+    rows = np.sort(np.random.default_rng(5).choice(B * H, 16, replace=False))
+    uh = synth.quantize(synth.signal(6, "u", B, H, N), "f16")
+    u.copy_(torch.tensor(uh, dtype=torch.float16))
+    k = synth.decay_filters(6, H, N).astype(np.float32)
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    y = plan.fwd(u, kf).float().cpu().numpy().reshape(B * H, N)
+    m = orc.frequency_mask(dims, keeps)
+    u2 = uh.reshape(B * H, N)
+    for r in rows:
+        h = r % H
+        ref = orc.conv_fwd(u2[r][None, None, :], k[h:h + 1].astype(np.float64), mask=m)[0, 0]
+        rel = np.linalg.norm(y[r] - ref) / np.linalg.norm(ref)
+        assert rel < REL_L2, (r, rel)
