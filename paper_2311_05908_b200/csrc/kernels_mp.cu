@@ -129,7 +129,10 @@ FC_DEVICE CV<C2> twiddle_base(const MpParams& prm, int n) {
 }
 
 template <int L0, int MODE, bool GATED, typename T, typename TT>
-__global__ void __launch_bounds__(256, 3) mp_pass1_kernel(const MpParams prm) {
+#ifndef FC_PASS_MINB
+#define FC_PASS_MINB 3
+#endif
+__global__ void __launch_bounds__(256, FC_PASS_MINB) mp_pass1_kernel(const MpParams prm) {
   constexpr int COLS = PassCfg<L0>::COLS, C2 = PassCfg<L0>::C2;
   constexpr int NIN = MODE == 0 ? L0 / 2 : L0;
   const int64_t NCH = int64_t(prm.Lp) / COLS;  // column groups per (pair, head)
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(256, 3) mp_pass1_kernel(const MpParams prm) {
 }
 
 template <int L0, int MODE, bool GATED, typename T, typename TT>
-__global__ void __launch_bounds__(256, 3) mp_pass3_kernel(const MpParams prm) {
+__global__ void __launch_bounds__(256, FC_PASS_MINB) mp_pass3_kernel(const MpParams prm) {
   constexpr int COLS = PassCfg<L0>::COLS, C2 = PassCfg<L0>::C2;
   const int64_t NCH = int64_t(prm.Lp) / COLS;
   // 32-bit index math (the launcher checks pairs * H * NCH < 2^31); NCH is a power of two
