@@ -68,3 +68,22 @@ def test_f32_partial():
     rel, plan = _run(16384, True, False, B=2, H=2, seed=24, fft_size=4096, K=1500)
     assert plan.info.regime == 2
     assert rel <= REL_L2, rel
+
+
+@pytest.mark.gpu
+def test_f32_sparse_multipass():
+    """fp32 validation build with a frequency-sparse plan (masked k_f rows
+    are zero-filled; the fp32 inner pass transforms every row)."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    N, B, H = 16384, 3, 2
+    keep_k0 = np.zeros(16, bool)
+    keep_k0[[0, 1, 8, 15]] = True
+    dims, keeps = [2048, 16], [np.ones(2048, bool), keep_k0]
+    plan = FFTConvPlan(N, dtype=torch.float32, causal=True, sparsity=(dims, keeps))
+    u = synth.quantize(synth.signal(25, "u", B, H, N), "f32")
+    k = synth.decay_filters(25, H, N).astype(np.float32)
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    y = plan.fwd(torch.tensor(u, dtype=torch.float32, device="cuda"), kf).cpu().numpy()
+    ref = orc.conv_fwd(u, k.astype(np.float64), mask=orc.frequency_mask(dims, keeps))
+    rel = np.linalg.norm(y - ref) / np.linalg.norm(ref)
+    assert rel <= REL_L2, rel

@@ -82,3 +82,28 @@ def test_partial_backward(N, L, K, dtype, gated):
         assert np.all(np.isfinite(got)), key
         rel = np.linalg.norm(got - ref[key]) / np.linalg.norm(ref[key])
         assert rel < REL_L2, (key, rel)
+
+
+@pytest.mark.gpu
+def test_partial_cfg4_backward_full_size_sampled():
+    """cfg 4 backward at full size (B=1, H=256, N=2^20, K=8192, fp16), bench's
+    launch configuration: du rows and dk of sampled heads against the oracle
+    run on those heads."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    B, H, N, K, L = 1, 256, 1 << 20, 8192, 16384
+    plan = FFTConvPlan(N, fft_size=L, dtype=torch.float16, causal=True)
+    u = synth.quantize(synth.dna_like(4, B, H, N), "f16")
+    dy = synth.quantize(synth.signal(4, "dy", B, H, N), "f16")
+    k = synth.decay_filters(4, H, K).astype(np.float32)
+    t = lambda a: torch.tensor(a, dtype=torch.float16, device="cuda")
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    g = plan.bwd(t(dy), t(u), kf, K)
+    torch.cuda.synchronize()
+    du = g["du"].float().cpu().numpy()
+    dk = g["dk"].cpu().numpy()
+    for h in np.random.default_rng(2).choice(H, 2, replace=False):
+        sl = (slice(None), slice(h, h + 1), slice(None))
+        ref = orc.conv_bwd(dy[sl], u[sl], k[h:h + 1].astype(np.float64))
+        for key, got in (("du", du[sl]), ("dk", dk[h:h + 1])):
+            rel = np.linalg.norm(got - ref[key]) / np.linalg.norm(ref[key])
+            assert rel < REL_L2, (key, h, rel)
