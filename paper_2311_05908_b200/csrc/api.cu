@@ -31,6 +31,32 @@ size_t chunk_target_bytes() {
   return v;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return EncodeTiledFn(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// The multipass inner pass stores its tiles with TMA tensor stores unless
+// FFTCONV_TMA_Y=0 (experiments).
+bool tma_y_enabled() {
+  static bool v = [] {
+    const char* e = getenv("FFTCONV_TMA_Y");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // bytes per element of the multipass intermediate T (fp16; fp32 in the
 // validation build)
 size_t t_elem_bytes(const fftconv_plan_s* p) { return p->dtype == FFTCONV_F32 ? 4 : 2; }
@@ -84,6 +110,22 @@ extern "C" fftconv_status_t fftconv_plan_upload(fftconv_plan_t p, void* d_tables
   p->d_tables = d_tables;
   return FFTCONV_OK;
 }
+
+namespace fc {
+cudaError_t make_tmap_rows(CUtensorMap* map, void* base, int64_t rows, int64_t heads, int64_t Lp, int R) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return cudaErrorNotSupported;
+  // dims by increasing stride: element in a 128 B segment, segment, head, row
+  const cuuint64_t dim[4] = {64, cuuint64_t(Lp / 64), cuuint64_t(heads), cuuint64_t(rows)};
+  const cuuint64_t stride[3] = {128, cuuint64_t(Lp) * 2, cuuint64_t(heads) * cuuint64_t(Lp) * 2};
+  const cuuint32_t box[4] = {64, cuuint32_t(Lp / 64), 1, cuuint32_t(R)};
+  const cuuint32_t estride[4] = {1, 1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dim, stride, box, estride,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+}  // namespace fc
 
 extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float* d_k, int64_t H, int64_t K,
                                                   void* d_kf, fftconv_stream_t stream) {
@@ -178,6 +220,9 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
           if (e != cudaSuccess) return cuda_fail(fn, e);
           FwdParams in{};
           in.u = ws; in.y = ws; in.tables = p->d_tables;
+          if (tma_y_enabled() && p->dtype != FFTCONV_F32 &&
+              make_tmap_rows(&in.tmap_y, ws, 2 * ((rows_c + 1) / 2), hc * p->L0, p->Lp, 8) == cudaSuccess)
+            in.tma_y = 1;
           in.kf = static_cast<const uint8_t*>(kf) + size_t(h0) * p->kf_bytes_per_head;
           in.B = 2 * ((rows_c + 1) / 2); in.H = hc * p->L0; in.N = p->Lp;
           in.L1 = p->L1; in.causal = 0; in.gated = 0; in.dtype = 0;
@@ -226,6 +271,7 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     void* Tin = Tb[(p->nlev - 1) & 1];
     FwdParams in{};
     in.u = Tin; in.y = Tin; in.kf = kf; in.tables = p->d_tables;
+    if (tma_y_enabled() && make_tmap_rows(&in.tmap_y, Tin, rows, H * p->L0, p->Lp, 8) == cudaSuccess) in.tma_y = 1;
     in.B = rows; in.H = H * p->L0; in.N = p->Lp;
     in.L1 = p->L1; in.causal = 0; in.gated = 0; in.dtype = 0;
     in.num_sms = num_sms_current();

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace fc {
@@ -23,7 +24,14 @@ struct FwdParams {
   const int32_t* row_map;
   int32_t nrow, row_L0;
   const void* wl;  // fp32 validation build: W_L^e, e < L (plan table)
+  // circular (multipass inner) tiles: y leaves the SMEM staging buffer by one
+  // TMA tensor store (4-D box {64, Lp/64, 1 head, R rows}, 128 B swizzle)
+  int32_t tma_y;
+  CUtensorMap tmap_y;
 };
+// Encode tmap_y for fp16 rows (rows, heads, n) of length n = Lp (in elements),
+// row stride heads * Lp; box of R rows of one head.
+cudaError_t make_tmap_rows(CUtensorMap* map, void* base, int64_t rows, int64_t heads, int64_t Lp, int R);
 cudaError_t launch_fwd_fused(const FwdParams& prm, cudaStream_t s);
 // fp32 validation build of the same decomposition on CUDA cores (kernels_f32.cu)
 cudaError_t launch_fwd_f32(const FwdParams& prm, cudaStream_t s);

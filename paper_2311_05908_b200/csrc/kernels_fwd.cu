@@ -76,7 +76,7 @@ struct FwdCfg {
 // TMEM columns, mbarriers, named barrier, k_f copy and operand buffer, so one
 // warpgroup's MMAs, memory waits and barriers overlap the other's math.
 template <int L1, bool CAUSAL, bool GATED, typename T>
-__global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv_fwd_o2_kernel(const FwdParams prm) {
+__global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv_fwd_o2_kernel(const __grid_constant__ FwdParams prm) {
   using C = O2Cfg<L1, CAUSAL>;
   using F = FwdCfg<L1, CAUSAL, GATED>;
   constexpr int kWG = F::WG;
@@ -628,6 +628,21 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
                        IO<S>::pack2(o[4], o[5]), IO<S>::pack2(o[6], o[7]));
         }
         stamp(16);
+        // circular plain tiles (the multipass inner pass): the staged tile
+        // leaves by one TMA tensor store; the staging layout is the 128 B
+        // swizzle of the {64, Lp/64, 1, R} box
+        const bool tma_out = (!CAUSAL && !GATED) && prm.tma_y;
+        if (tma_out) {
+          fence_async_smem();
+          tc_fence_before();
+          wg_sync();
+          if (wtid == 0) {
+            tma_store_4d(&prm.tmap_y, bufX, 0, 0, int(h), int(bt * C::R));
+            bulk_commit();
+            bulk_wait_read0();
+          }
+          wg_sync();  // the TMA has read the staging before bufX takes the next operand
+        } else {
         tc_fence_before();
         if (STG) stg_wait(1);
         stamp(17);
@@ -669,6 +684,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
           bulk_wait_read0();
           if (t + 1 < t1) release_out(t + 1, bt + 1 < nbt ? hh : hh + 1, bt + 1 < nbt ? bt + 1 : 0);
         }
+        }  // !tma_out
       } else {
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
@@ -705,7 +721,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
     stamp(14);
     ++trace_tile;
   }
-  if (STG) bulk_wait0();  // this thread's bulk stores complete
+  if (STG || prm.tma_y) bulk_wait0();  // this thread's bulk stores complete
   __syncthreads();
   if (warp == 0) tmem_dealloc<(kWG * C::TMEM_COLS > 512 ? 512 : kWG * C::TMEM_COLS)>(tmem_slot);
 }
