@@ -192,6 +192,7 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     }
     if (p->nlev > 1) mp.wtab = nullptr;  // deep plans: outer twiddles on the fly
     mp.Llev = p->L;
+    mp.circ = p->causal ? 0 : 1;  // circular plan: every n0 in and out
     if (p->nlev == 1) {
       // One outer level: run the three passes chunk by chunk over (pairs,
       // heads) so the chunk's intermediate T stays resident in L2 between
@@ -548,6 +549,7 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   mp.B = Bv; mp.H = H; mp.N = p->N; mp.L0 = p->lev_L0[0]; mp.Lp = int32_t(p->L / p->lev_L0[0]);
   mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
   mp.Llev = p->L;
+  mp.circ = p->causal ? 0 : 1;
   if (nlev > 1) mp.wtab = nullptr;  // outer twiddles on the fly, as in the forward
   if (partial) { mp.partial = 1; mp.C = p->L / 2; mp.NC = NCw; }
   // deeper outer levels (recursive plans): complex circular fp16 rows

@@ -597,9 +597,8 @@ static cudaError_t launch_mp_l0(const MpParams& prm, int pass, cudaStream_t s) {
   if (total == 0) return cudaSuccess;
   if (total + 255 >= (int64_t(1) << 31) || (prm.Lp & (prm.Lp - 1))) return cudaErrorInvalidValue;
   if (2 * (prm.pair0 + (prm.B + 1) / 2) >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
-  if (prm.circ) {  // deep levels: fp16 complex rows, never gated
-    if (prm.dtype != 0 || prm.gated) return cudaErrorInvalidValue;
-    launch_pass_k<L0, 2, false, __half>(prm, pass, grid, s);
+  if (prm.circ) {  // circular: deep levels (fp16 complex rows) or a circular plan's top level
+    launch_pass_m<L0, 2>(prm, pass, grid, s);
   } else if (prm.partial && prm.ola && pass == 3) {  // backward dg of the partial conv
     if ((prm.NC & 1) || prm.pair0 || prm.h0) return cudaErrorInvalidValue;
     const bool g = prm.gated != 0;

@@ -345,8 +345,11 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
     p->P = std::max(128 / p->L1, 2);
     build_fused_tables(p, L);
     p->Lp = int32_t(L);
-  } else if (io_ok && causal && L >= 4096 && L <= (int64_t(1) << 23) &&
-             (fft_size == 2 * N || (p->regime == REGIME_PARTIAL && L <= 32768 && N % (L / 2) == 0))) {
+  } else if (io_ok && L >= 4096 && L <= (int64_t(1) << 23) &&
+             ((causal && (fft_size == 2 * N || (p->regime == REGIME_PARTIAL && L <= 32768 && N % (L / 2) == 0))) ||
+              (!causal && fft_size == N))) {
+    // (circular plans, fft_size == N: the paper's circular benchmark rows,
+    // P:1243-1244; the outer passes keep every n0 in and out)
     // multipass; the partial regime (K <= L/2 < N) runs the same passes on
     // overlap-save windows of length L (A12).  L / 2048 is split
     // into outer levels of at most 16 (recursive Alg. 4).

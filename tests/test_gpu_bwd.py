@@ -96,3 +96,23 @@ def test_bwd_cfg3_full_size_sampled():
         for b in rng.choice(B, 3, replace=False):
             for key in ("du", "dw", "dv"):
                 assert _rel(got[key][b, h], ref[key][b, 0]) < REL_L2, (key, b, h)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [4096, 65536])
+def test_bwd_circular_multipass(N):
+    from paper_2311_05908_b200 import FFTConvPlan
+    B, H = 3, 2
+    plan = FFTConvPlan(N, fft_size=N, dtype=torch.float16, causal=False)
+    q = lambda name: synth.quantize(synth.signal(12, name, B, H, N), "f16")
+    u, w, v, dy = q("u"), q("w"), q("v"), q("dy")
+    k = synth.decay_filters(12, H, N).astype(np.float32)
+    t = lambda a: torch.tensor(a, dtype=torch.float16, device="cuda")
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    g = plan.bwd(t(dy), t(u), kf, N, w=t(w), v=t(v))
+    torch.cuda.synchronize()
+    ref = orc.conv_bwd(dy, u, k.astype(np.float64), causal=False, w=w, v=v)
+    for key in ("du", "dw", "dv", "dk"):
+        got = g[key].float().cpu().numpy().astype(np.float64)
+        assert np.all(np.isfinite(got)), key
+        assert _rel(got, ref[key]) < REL_L2, (key, _rel(got, ref[key]))

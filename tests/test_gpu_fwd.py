@@ -195,3 +195,14 @@ def test_fwd_multilevel_sampled(N):
                 got.append(y[b, h, i])
     got, ref = np.array(got), np.array(ref)
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < REL_L2
+
+
+# ---------------------------------------------------------------- circular multipass (fft_size == N >= 4096)
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [4096, 16384, 65536])
+@pytest.mark.parametrize("dtype,gated", [("f16", False), ("bf16", True)])
+def test_fwd_circular_multipass_parity(N, dtype, gated):
+    """The paper's circular benchmark rows (FFT size = input length,
+    P:1243-1244) beyond the fused sizes: outer passes keep every n0."""
+    got, ref = _run(N, False, dtype, gated, B=3, H=2)
+    _assert_close(got, ref)
