@@ -30,9 +30,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 
-def _wl(name, B, H, N, gated=False, dtype="f16", bwd=False, fft=None, K=None, sparse=None):
-    return dict(name=name, B=B, H=H, N=N, gated=gated, causal=True, dtype=dtype, bwd=bwd,
-                fft=fft or 2 * N, K=K or N, sparse=sparse)
+def _wl(name, B, H, N, gated=False, dtype="f16", bwd=False, fft=None, K=None, sparse=None, causal=True):
+    return dict(name=name, B=B, H=H, N=N, gated=gated, causal=causal, dtype=dtype, bwd=bwd,
+                fft=fft or (2 * N if causal else N), K=K or N, sparse=sparse)
 
 
 WORKLOADS = {
@@ -56,11 +56,20 @@ for _n in (256, 512, 1024, 2048, 4096, 8192, 16384, 32768, 65536):
     WORKLOADS[f"sweep{_n}"] = _wl(f"sweep: causal fp16 conv B*H=49152 N={_n}", 64, 768, _n)
 for _n, _b in ((1 << 18, 16), (1 << 20, 4), (1 << 22, 1)):  # constant elements: B*H = 49152 * 65536 / N
     WORKLOADS[f"sweep{_n}"] = _wl(f"sweep: causal fp16 conv B*H={_b * 768} N={_n}", _b, 768, _n)
+# the paper's circular forward table (FFT size = input length, B=64, H=768)
+for _n, _b in ((512, 64), (1024, 64), (4096, 64), (16384, 64), (65536, 64), (1 << 18, 16), (1 << 20, 4),
+               (1 << 22, 1)):
+    WORKLOADS[f"circ{_n}"] = _wl(f"circular fp16 conv (fft_size = N) B*H={_b * 768} N={_n}", _b, 768, _n,
+                                 causal=False)
 
 METRIC = "fused FFT-conv sequences/s & % HBM/tensor roofline, N=256–4M, at 1/2/4/8 B200"
 # paper's padded (causal) H100 rows for the same workload, another
 # machine: context only.  cfg2 = gated FFT-2K row 0.59 ms.
 PAPER_SEQ_S = {"cfg2": 49152 / 0.59e-3}
+# circular table rows (FlashFFTConv ms on H100 for 49,152 rows)
+for _n, _ms in ((512, 0.15), (1024, 0.24), (4096, 1.37), (16384, 9.27), (65536, 67.96), (1 << 18, 308.48),
+                (1 << 20, 1492.84), (1 << 22, 7586.96)):
+    PAPER_SEQ_S[f"circ{_n}"] = 49152 / (_ms * 1e-3)
 
 
 def sparsity_spec(kind, fft):
@@ -154,10 +163,10 @@ def _oracle_sample(wl, Bs, rows=None):
         dims, keeps = sparsity_spec(wl["sparse"], wl["fft"])
         mask = orc.frequency_mask(dims, keeps)
     t = time.perf_counter()
-    orc.conv_fwd(u, k, causal=True, mask=mask, **kw)
+    orc.conv_fwd(u, k, causal=wl["causal"], mask=mask, **kw)
     if wl["bwd"]:
         dy = q("dy")
-        orc.conv_bwd(dy, u, k, causal=True, mask=mask, **kw)
+        orc.conv_bwd(dy, u, k, causal=wl["causal"], mask=mask, **kw)
     return time.perf_counter() - t
 
 
@@ -245,7 +254,7 @@ def main():
 
     B, H, N, K, L = wl["B"], wl["H"], wl["N"], wl["K"], wl["fft"]
     tdt = {"f16": torch.float16, "bf16": torch.bfloat16}[wl["dtype"]]
-    plan = FFTConvPlan(N, fft_size=L, dtype=tdt, causal=True, device=dev,
+    plan = FFTConvPlan(N, fft_size=L, dtype=tdt, causal=wl["causal"], device=dev,
                        sparsity=sparsity_spec(wl["sparse"], L))
     row0 = rank * B * H  # this rank's rows of the global problem (weak scaling)
     u = synth.signal_torch(0, "u", B, H, N, dev, tdt, row0=row0)
@@ -387,11 +396,13 @@ def main():
             "metric": METRIC, "value": value, "unit": "sequences/s", "n_gpus": world, "steps": S,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": (value / vs) if vs else None,
-            "vs_baseline_note": "paper H100-SXM padded gated FFT-2K row (P:1144-1167), another machine: context only"
+            "vs_baseline_note": ("paper H100-SXM " + ("padded gated FFT-2K row (P:1144-1167)" if args.workload == "cfg2"
+                                                       else "circular forward row (P:1072-1095)")
+                                 + ", conv only there, k_f precompute included here; another machine: context only")
             if vs else None,
             "dtype": wl["dtype"], "data": "synthetic",
             "config": {"workload": wl["name"], "B": B, "H": H, "N": N, "K": K, "fft_size": L, "gated": wl["gated"],
-                       "causal": True, "backward": wl["bwd"], "regime": regime,
+                       "causal": wl["causal"], "backward": wl["bwd"], "regime": regime,
                        "step": "precompute_kf + conv" + (" fwd+bwd" if wl["bwd"] else " fwd"),
                        "l2": f"inputs larger than L2 ({bytes_per_call / 1e6:.0f} MB per step)",
                        "parallelism": f"rows sharded, {world} GPU(s), no data-path collective"},
