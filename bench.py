@@ -218,6 +218,48 @@ def algorithmic_bytes(wl, H_L8):
     return fwd + bwd
 
 
+# ----------------------------------------------------------------- B1 baseline
+def torch_fft_baseline(wl, u, w, v, k, dy, steps, mask=None):
+    """cuFFT + PyTorch, the Hyena reference fftconv (inputs
+    upcast to fp32, rfft of the padded rows, pointwise k_f, irfft, crop,
+    gate); the filter FFT is inside the step as in ours; backward workloads
+    through autograd.  Returns (ms per step, peak extra device bytes)."""
+    import torch
+    L, N = wl["fft"], wl["N"]
+    if wl["causal"] and L < 2 * N:
+        L = 2 * N  # partial conv: the plain FFT conv with the truncated filter
+    m = None if mask is None else torch.tensor(mask[: L // 2 + 1], dtype=torch.float32, device=u.device)
+
+    def step():
+        rg = wl["bwd"]
+        kk = k.detach().requires_grad_(rg)
+        uu = u.float().requires_grad_(rg)
+        g = uu * w.float().requires_grad_(rg) if w is not None else uu
+        kf = torch.fft.rfft(kk, n=L)
+        if m is not None:
+            kf = kf * m
+        y = torch.fft.irfft(torch.fft.rfft(g, n=L) * kf, n=L)[..., :N]
+        if v is not None:
+            y = y * v.float().requires_grad_(rg)
+        if wl["bwd"]:
+            y.backward(dy.float())
+        return y.to(u.dtype)
+
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    step()
+    step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps, torch.cuda.max_memory_allocated() - base
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -227,6 +269,7 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-torch-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = WORKLOADS[args.workload]
@@ -392,6 +435,24 @@ def main():
             cpu = {"value": rate, "unit": "sequences/s", "cores": cores, "kind": "oracle", "sample": sample}
         vs = PAPER_SEQ_S.get(args.workload)
         regime = {1: "fused", 2: "partial (overlap-save, multipass)", 3: "multipass"}[plan.info.regime]
+        # device memory of this library for the step vs the cuFFT+PyTorch reference (NEXT-3)
+        lib_bytes = kfb.numel() + (ws_f.numel() if ws_f is not None else 0) + (ws_b.numel() if ws_b is not None else 0)
+        lib_bytes += plan.info.table_bytes
+        tb = None
+        if not args.no_torch_baseline:
+            spec = B * H * (max(L, 2 * N) // 2 + 1) * 8  # one complex64 spectrum of the batch
+            free, _ = torch.cuda.mem_get_info(dev)
+            if spec * (10 if wl["bwd"] else 6) < free:
+                try:  # (sparse workloads: dense spectrum product, the mask multiply is the same cost)
+                    ms_b, peak_b = torch_fft_baseline(wl, u, w, v, k, dy, min(S, 20))
+                    tb = {"value": B * H / (ms_b * 1e-3), "unit": "sequences/s", "ms_per_step": ms_b,
+                          "peak_extra_bytes": int(peak_b),
+                          "kind": "torch.fft (cuFFT) fp32 Hyena-style fftconv" + (" + autograd bwd" if wl["bwd"] else ""),
+                          "speedup_of_this": (B * H / (step_ms * 1e-3)) / (B * H / (ms_b * 1e-3))}
+                except torch.OutOfMemoryError:
+                    tb = {"value": None, "unavailable": "out of memory"}
+            else:
+                tb = {"value": None, "unavailable": "would not fit beside this run's buffers"}
         out = {
             "metric": METRIC, "value": value, "unit": "sequences/s", "n_gpus": world, "steps": S,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
@@ -414,6 +475,9 @@ def main():
                          "kernel_ms": conv_ms, "algorithmic_bytes_per_launch": bytes_per_call,
                          "peak_source": peaks["src"]},
             "cpu_baseline": cpu,
+            "cufft_baseline": tb,
+            "memory": {"library_device_bytes": int(lib_bytes),
+                       "note": "k_f + workspace(s) + plan tables; caller-owned, reused every step"},
             "e2e": None if not E else {"value": e2e_value, "unit": "sequences/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                     "path": (f"fftconv_fwd_host, {(B + rpc - 1) // rpc} chunks of {rpc} batch rows, copies overlapped"
