@@ -167,6 +167,21 @@ fftconv_status_t fftconv_fwd_host(fftconv_plan_t plan, const void* h_u, const vo
 fftconv_status_t fftconv_host_stage_size(fftconv_plan_t plan, int64_t H, int64_t rows_per_chunk, int gated,
                                          size_t* bytes);
 
+/* Sequence streaming for rows longer than device buffers (NEXT-4; partial
+ * plans only, K <= C = fft_size/2, plan N = segment length, a multiple of C):
+ * (B, H, N_total) host rows are convolved segment by segment.  Segment i
+ * produces outputs [i S, (i+1) S), S = N - C, from a device buffer holding
+ * u[i S - C, i S + S) (zeros outside the row), so the overlap-save windows see
+ * the C samples of history they need; copies of neighbouring segments overlap
+ * the convolution as in fftconv_fwd_host.  h_w, h_v NULL = plain.  Result
+ * equals the partial convolution of the full rows.  stage_bytes >=
+ * fftconv_stream_stage_size(plan, B, H, gated).  FFTCONV_ERR_UNSUPPORTED for
+ * non-partial plans. */
+fftconv_status_t fftconv_fwd_stream(fftconv_plan_t plan, const void* h_u, const void* h_w, const void* h_v,
+                                    const void* d_kf, void* h_y, int64_t B, int64_t H, int64_t N_total,
+                                    void* d_stage, size_t stage_bytes, fftconv_stream_t stream);
+fftconv_status_t fftconv_stream_stage_size(fftconv_plan_t plan, int64_t B, int64_t H, int gated, size_t* bytes);
+
 /* Backward of <y, dy> with recomputation (A15).  Plain when
  * d_w == d_v == NULL (then d_dw, d_dv ignored); gated when both are given.
  * d_dk (H, K) fp32 is OVERWRITTEN with the batch sum.  d_workspace:

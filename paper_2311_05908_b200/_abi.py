@@ -28,7 +28,7 @@ ABI_SYMBOLS = [
     "fftconv_plan", "fftconv_plan_info", "fftconv_plan_upload", "fftconv_precompute_kf",
     "fftconv_fwd", "fftconv_gated_fwd", "fftconv_bwd", "fftconv_plan_destroy",
     "fftconv_last_error", "fftconv_launch_count_reset", "fftconv_workspace_size",
-    "fftconv_fwd_host", "fftconv_host_stage_size",
+    "fftconv_fwd_host", "fftconv_host_stage_size", "fftconv_fwd_stream", "fftconv_stream_stage_size",
 ]
 
 
@@ -80,6 +80,10 @@ def lib():
         L.fftconv_fwd_host.restype = ctypes.c_int
         L.fftconv_host_stage_size.argtypes = [P, i64, i64, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]
         L.fftconv_host_stage_size.restype = ctypes.c_int
+        L.fftconv_fwd_stream.argtypes = [P, P, P, P, P, P, i64, i64, i64, P, ctypes.c_size_t, P]
+        L.fftconv_fwd_stream.restype = ctypes.c_int
+        L.fftconv_stream_stage_size.argtypes = [P, i64, i64, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]
+        L.fftconv_stream_stage_size.restype = ctypes.c_int
         L.fftconv_workspace_size.restype = ctypes.c_int
         for f in ("fftconv_plan", "fftconv_plan_info", "fftconv_plan_upload", "fftconv_precompute_kf",
                   "fftconv_fwd", "fftconv_gated_fwd", "fftconv_bwd"):

@@ -451,6 +451,91 @@ extern "C" fftconv_status_t fftconv_fwd_host(fftconv_plan_t p, const void* h_u, 
   return FFTCONV_OK;
 }
 
+// ---------------------------------------------------------------- sequence streaming (NEXT-4)
+// Partial plans only (K <= C = fft_size/2): rows longer than the plan's N are
+// streamed from host memory in segments.  Segment i covers outputs
+// [i S, (i+1) S) with S = N - C; its device buffer holds u[i S - C, i S + S)
+// (zeros before 0 and past the end), so the overlap-save windows of the plan
+// see the C-sample history they need and outputs C.. of the buffer are exact.
+extern "C" fftconv_status_t fftconv_stream_stage_size(fftconv_plan_t p, int64_t B, int64_t H, int gated,
+                                                      size_t* bytes) {
+  if (!p || !bytes || B < 1 || H < 1) { set_last_error("fftconv_stream_stage_size: bad argument"); return FFTCONV_ERR_INVALID_ARG; }
+  if (p->regime != REGIME_PARTIAL) { set_last_error("fftconv_stream_stage_size: needs a partial plan"); return FFTCONV_ERR_UNSUPPORTED; }
+  *bytes = 2 * slot_bytes(p, H, B, gated != 0, nullptr) + 1024;
+  return FFTCONV_OK;
+}
+
+extern "C" fftconv_status_t fftconv_fwd_stream(fftconv_plan_t p, const void* h_u, const void* h_w, const void* h_v,
+                                               const void* d_kf, void* h_y, int64_t B, int64_t H, int64_t N_total,
+                                               void* d_stage, size_t stage_bytes, fftconv_stream_t stream) {
+  const char* fn = "fftconv_fwd_stream";
+  if (!p) { set_last_error("fftconv_fwd_stream: plan is NULL"); return FFTCONV_ERR_INVALID_ARG; }
+  if (p->regime != REGIME_PARTIAL) { set_last_error("fftconv_fwd_stream: needs a partial plan (fft_size < 2N)"); return FFTCONV_ERR_UNSUPPORTED; }
+  const bool gated = h_w != nullptr || h_v != nullptr;
+  if (gated && !(h_w && h_v)) { set_last_error("fftconv_fwd_stream: gated needs both w and v"); return FFTCONV_ERR_INVALID_ARG; }
+  if (B < 0 || H < 0 || N_total < 0) { set_last_error("fftconv_fwd_stream: bad sizes"); return FFTCONV_ERR_INVALID_ARG; }
+  if (B * H * N_total == 0) return FFTCONV_OK;
+  if (!h_u || !h_y || !d_kf || !d_stage) { set_last_error("fftconv_fwd_stream: NULL pointer"); return FFTCONV_ERR_INVALID_ARG; }
+  if (!aligned16(d_stage)) { set_last_error("fftconv_fwd_stream: stage not 16-byte aligned"); return FFTCONV_ERR_MISALIGNED; }
+  size_t ws_bytes = 0;
+  const size_t slot = slot_bytes(p, H, B, gated, &ws_bytes);
+  if (stage_bytes < 2 * slot) { set_last_error("fftconv_fwd_stream: staging buffer too small"); return FFTCONV_ERR_INVALID_ARG; }
+  HostPipe* hp = nullptr;
+  cudaError_t e = host_pipe(&hp);
+  if (e != cudaSuccess) return cuda_fail(fn, e);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if ((e = cudaEventRecord(hp->start, cs)) != cudaSuccess) return cuda_fail(fn, e);
+  if ((e = cudaStreamWaitEvent(hp->in, hp->start, 0)) != cudaSuccess) return cuda_fail(fn, e);
+  if ((e = cudaStreamWaitEvent(hp->out, hp->start, 0)) != cudaSuccess) return cuda_fail(fn, e);
+  const int64_t Nseg = p->N, C = p->L / 2, S = Nseg - C, rows = B * H;
+  const size_t es = elem_bytes(p);
+  const size_t t = (size_t(rows) * size_t(Nseg) * es + 1023) / 1024 * 1024;
+  uint8_t* base = static_cast<uint8_t*>(d_stage);
+  const int64_t nseg = (N_total + S - 1) / S;
+  for (int64_t i = 0; i < nseg; ++i) {
+    const int sl_i = int(i & 1);
+    uint8_t* sl = base + size_t(sl_i) * slot;
+    uint8_t *du = sl, *dw = sl + t, *dv = sl + 2 * t, *dy = sl + (gated ? 3 : 1) * t, *dws = sl + (gated ? 4 : 2) * t;
+    const int64_t s0 = i * S;              // first output position of the segment
+    const int64_t a = s0 - C;              // first input position in the buffer
+    const int64_t lo = a < 0 ? 0 : a;      // first valid input position
+    const int64_t hi = s0 + S < N_total ? s0 + S : N_total;  // end of valid input
+    const int64_t off = lo - a;            // its column in the buffer
+    const int64_t ncols = hi - lo;
+    if (i >= 2 && (e = cudaStreamWaitEvent(hp->in, hp->freed[sl_i], 0)) != cudaSuccess) return cuda_fail(fn, e);
+    const void* src[3] = {h_u, h_w, h_v};
+    uint8_t* dst[3] = {du, dw, dv};
+    for (int q = 0; q < (gated ? 3 : 1); ++q) {
+      // zero the columns this segment does not fill (history before 0, tail past the end)
+      if (off > 0 || off + ncols < Nseg) {
+        if ((e = cudaMemsetAsync(dst[q], 0, size_t(rows) * size_t(Nseg) * es, hp->in)) != cudaSuccess)
+          return cuda_fail(fn, e);
+      }
+      if ((e = cudaMemcpy2DAsync(dst[q] + size_t(off) * es, size_t(Nseg) * es,
+                                 static_cast<const uint8_t*>(src[q]) + size_t(lo) * es, size_t(N_total) * es,
+                                 size_t(ncols) * es, size_t(rows), cudaMemcpyHostToDevice, hp->in)) != cudaSuccess)
+        return cuda_fail(fn, e);
+    }
+    if ((e = cudaEventRecord(hp->loaded[sl_i], hp->in)) != cudaSuccess) return cuda_fail(fn, e);
+    if ((e = cudaStreamWaitEvent(cs, hp->loaded[sl_i], 0)) != cudaSuccess) return cuda_fail(fn, e);
+    fftconv_status_t st = run_fwd(p, du, gated ? dw : nullptr, gated ? dv : nullptr, d_kf, dy, B, H,
+                                  ws_bytes ? dws : nullptr, stream, fn);
+    if (st != FFTCONV_OK) return st;
+    if ((e = cudaEventRecord(hp->computed[sl_i], cs)) != cudaSuccess) return cuda_fail(fn, e);
+    if ((e = cudaStreamWaitEvent(hp->out, hp->computed[sl_i], 0)) != cudaSuccess) return cuda_fail(fn, e);
+    // outputs s0 .. min(s0 + S, N_total) live at buffer columns C ..
+    const int64_t nout = (s0 + S < N_total ? s0 + S : N_total) - s0;
+    if ((e = cudaMemcpy2DAsync(static_cast<uint8_t*>(h_y) + size_t(s0) * es, size_t(N_total) * es,
+                               dy + size_t(C) * es, size_t(Nseg) * es, size_t(nout) * es, size_t(rows),
+                               cudaMemcpyDeviceToHost, hp->out)) != cudaSuccess)
+      return cuda_fail(fn, e);
+    if ((e = cudaEventRecord(hp->freed[sl_i], hp->out)) != cudaSuccess) return cuda_fail(fn, e);
+  }
+  if ((e = cudaEventRecord(hp->done, hp->out)) != cudaSuccess) return cuda_fail(fn, e);
+  if ((e = cudaStreamWaitEvent(cs, hp->done, 0)) != cudaSuccess) return cuda_fail(fn, e);
+  return FFTCONV_OK;
+}
+
 // Workspace layout of the backward pass (bytes):
 //  fused     : [partials: H * nbt * L complex fp32]
 //  multipass : [T_g][T_dc] (fp16 rows, 2 * ceil(B/2) * H * L each)

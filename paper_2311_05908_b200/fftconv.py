@@ -169,6 +169,23 @@ class FFTConvPlan:
         self._stage = stage  # keep the staging buffer alive while the copies run
         return out
 
+    def fwd_stream(self, u: torch.Tensor, kf: torch.Tensor, w=None, v=None, out=None, stage=None) -> torch.Tensor:
+        """Partial plans: host rows (B, H, N_total) of any length streamed in
+        segments of the plan's N through fftconv_fwd_stream."""
+        for t in (u, w, v):
+            if t is not None:
+                assert not t.is_cuda and t.dtype == self.dtype and t.is_contiguous() and t.dim() == 3
+        B, H, NT = u.shape
+        out = torch.empty_like(u, pin_memory=u.is_pinned()) if out is None else out
+        n = ctypes.c_size_t()
+        _abi.check(_abi.lib().fftconv_stream_stage_size(self._h, B, H, int(w is not None), ctypes.byref(n)))
+        if stage is None or stage.numel() < n.value:
+            stage = _aligned_empty(int(n.value), kf.device, 1024)
+        _abi.check(_abi.lib().fftconv_fwd_stream(self._h, _ptr(u), _ptr(w), _ptr(v), _ptr(kf), _ptr(out), B, H, NT,
+                                                 _ptr(stage), stage.numel(), _stream(kf.device)))
+        self._stage = stage
+        return out
+
     def host_stage(self, H: int, rows_per_chunk: int = 8, gated: bool = False, device=None):
         n = ctypes.c_size_t()
         _abi.check(_abi.lib().fftconv_host_stage_size(self._h, H, rows_per_chunk, int(gated), ctypes.byref(n)))

@@ -28,3 +28,33 @@ def test_fwd_host_matches_device(N, gated, B, rpc):
         got = plan.fwd_host(u.pin_memory(), kf, rows_per_chunk=rpc)
     torch.cuda.synchronize()
     assert torch.equal(got, ref.cpu())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,gated", [("f16", False), ("bf16", True)])
+def test_fwd_stream_partial_long_rows(dtype, gated):
+    """fftconv_fwd_stream (NEXT-4): rows of N_total = 32768 streamed through a
+    partial plan with N = 8192, fft_size 4096 (C = 2048, segments of 6144
+    outputs, the last one ragged) equal the causal convolution of the whole
+    rows with the truncated filter (K = 700)."""
+    from oracle import oracle as orc
+    from paper_2311_05908_b200 import FFTConvPlan
+    tdt = {"f16": torch.float16, "bf16": torch.bfloat16}[dtype]
+    B, H, NT, K = 2, 3, 32768, 700
+    plan = FFTConvPlan(8192, fft_size=4096, dtype=tdt, causal=True)
+    assert plan.info.regime == 2
+    q = lambda name: synth.quantize(synth.signal(15, name, B, H, NT), dtype)
+    u, w, v = q("u"), q("w"), q("v")
+    k = synth.decay_filters(15, H, K).astype(np.float32)
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    th = lambda a: torch.tensor(a, dtype=tdt).pin_memory()
+    if gated:
+        y = plan.fwd_stream(th(u), kf, w=th(w), v=th(v))
+        ref = orc.conv_fwd(u, k.astype(np.float64), w=w, v=v)
+    else:
+        y = plan.fwd_stream(th(u), kf)
+        ref = orc.conv_fwd(u, k.astype(np.float64))
+    torch.cuda.synchronize()
+    got = y.float().numpy().astype(np.float64)
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert rel < 2e-3, rel
