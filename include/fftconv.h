@@ -55,8 +55,7 @@ typedef struct fftconv_plan_s* fftconv_plan_t;
  * relative L2 on an fp32 validation build"): fp32 I/O and the same plan,
  * packing, Monarch decomposition and multipass passes with every stage in
  * fp32 on the CUDA cores (no tensor cores; not a performance path).  It
- * covers the forward calls for fft_size <= 32768; fftconv_bwd returns
- * FFTCONV_ERR_UNSUPPORTED for it. */
+ * covers the forward and backward calls for fft_size <= 32768. */
 typedef enum { FFTCONV_F16 = 0, FFTCONV_BF16 = 1, FFTCONV_F32 = 2 } fftconv_dtype_t;
 
 typedef enum {

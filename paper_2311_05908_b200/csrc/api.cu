@@ -544,11 +544,13 @@ static size_t bwd_ws_bytes(const fftconv_plan_s* p, int64_t B, int64_t H) {
   if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
     const int64_t Bv = p->regime == REGIME_PARTIAL ? B * (p->N / (p->L / 2)) : B;
     const int64_t rows = 2 * ((Bv + 1) / 2);
-    const size_t t = size_t(rows) * size_t(H) * size_t(p->L) * 2;
-    const size_t part = size_t(H) * p->L0 * size_t(bwd_tiles_per_head(rows, p->L1)) * size_t(p->Lp) * 8;
+    const size_t t = size_t(rows) * size_t(H) * size_t(p->L) * t_elem_bytes(p);
+    const int64_t units = p->dtype == FFTCONV_F32 ? bwd_f32_units_per_head(rows) : bwd_tiles_per_head(rows, p->L1);
+    const size_t part = size_t(H) * p->L0 * size_t(units) * size_t(p->Lp) * 8;
     return (p->nlev > 1 ? 4 : 2) * t + part + size_t(H) * size_t(p->L) * 8;
   }
-  return size_t(H) * size_t(bwd_tiles_per_head(B, p->L1)) * size_t(p->L) * 8;
+  const int64_t units = p->dtype == FFTCONV_F32 ? bwd_f32_units_per_head(B) : bwd_tiles_per_head(B, p->L1);
+  return size_t(H) * size_t(units) * size_t(p->L) * 8;
 }
 
 extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, const void* d_u, const void* d_w,
@@ -564,10 +566,6 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   fftconv_status_t chk = gated ? check_signal_args(p, fn, B, H, {d_dy, d_u, d_w, d_v, d_kf, d_du, d_dw, d_dv, d_workspace})
                                : check_signal_args(p, fn, B, H, {d_dy, d_u, d_kf, d_du, d_workspace});
   if (chk != FFTCONV_OK) return chk;
-  if (p->dtype == FFTCONV_F32) {
-    set_last_error("fftconv_bwd: the fp32 validation build covers the forward pass only");
-    return FFTCONV_ERR_UNSUPPORTED;
-  }
   const int64_t kmax = p->causal ? p->L / 2 : p->L;
   if (K < 1 || K > kmax) { set_last_error("fftconv_bwd: K out of range"); return FFTCONV_ERR_KERNEL_TOO_LONG; }
   if (!d_dk && H > 0) { set_last_error("fftconv_bwd: dk is NULL"); return FFTCONV_ERR_INVALID_ARG; }
@@ -593,10 +591,11 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
     b.gate_io = gated ? 1 : 0; b.need_c = gated ? 1 : 0;
     b.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
     b.num_sms = num_sms_current();
-    e = launch_bwd_fused(b, st);
+    const bool f32 = p->dtype == FFTCONV_F32;
+    e = f32 ? launch_bwd_f32(b, tab + p->tl.wl, st) : launch_bwd_fused(b, st);
     if (e != cudaSuccess) return cuda_fail(fn, e);
     dk.part = static_cast<const float2*>(d_workspace);
-    dk.nbt = bwd_tiles_per_head(B, p->L1);
+    dk.nbt = f32 ? bwd_f32_units_per_head(B) : bwd_tiles_per_head(B, p->L1);
     dk.L0 = 1;
     dk.Lp = int32_t(p->L);
     e = launch_dk_finalize(dk, st);
@@ -620,19 +619,21 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   const int64_t rows = 2 * ((Bv + 1) / 2);
   const int nlev = p->nlev;
   uint8_t* ws = static_cast<uint8_t*>(d_workspace);
-  const size_t tbytes = size_t(rows) * size_t(H) * size_t(p->L) * 2;
+  const bool f32 = p->dtype == FFTCONV_F32;
+  if (f32 && nlev > 1) { set_last_error("fftconv_bwd: the fp32 validation build supports fft_size <= 32768"); return FFTCONV_ERR_UNSUPPORTED; }
+  const size_t tbytes = size_t(rows) * size_t(H) * size_t(p->L) * t_elem_bytes(p);
   // T buffers of g and dc; recursive plans ping-pong between two of each
   void* Tg[2] = {ws, ws + (nlev > 1 ? 2 : 1) * tbytes};
   void* Tdc[2] = {ws + tbytes, ws + 3 * tbytes};
   if (nlev == 1) { Tg[1] = Tg[0]; Tdc[1] = Tdc[0]; }
   void* part = ws + (nlev > 1 ? 4 : 2) * tbytes;
-  const int64_t nbt_in = bwd_tiles_per_head(rows, p->L1);
+  const int64_t nbt_in = f32 ? bwd_f32_units_per_head(rows) : bwd_tiles_per_head(rows, p->L1);
   void* scratch = static_cast<uint8_t*>(part) + size_t(H) * p->L0 * size_t(nbt_in) * size_t(p->Lp) * 8;
   MpParams mp{};
   mp.wbase = reinterpret_cast<const float2*>(tab + p->tl.wbase);
   mp.wtab = reinterpret_cast<const float2*>(tab + p->tl.wtab);
   mp.B = Bv; mp.H = H; mp.N = p->N; mp.L0 = p->lev_L0[0]; mp.Lp = int32_t(p->L / p->lev_L0[0]);
-  mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
+  mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : f32 ? 2 : 0;
   mp.Llev = p->L;
   mp.circ = p->causal ? 0 : 1;
   if (nlev > 1) mp.wtab = nullptr;  // outer twiddles on the fly, as in the forward
@@ -669,9 +670,9 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   b.u = Tgi; b.dy = Tdci; b.dv = Tgi; b.du = Tdci;
   b.kf = d_kf; b.tables = p->d_tables; b.acc = part;
   b.B = rows; b.H = H * p->L0; b.N = p->Lp; b.L1 = p->L1; b.causal = 0;
-  b.gate_io = 0; b.need_c = gated ? 1 : 0; b.dtype = 0;
+  b.gate_io = 0; b.need_c = gated ? 1 : 0; b.dtype = f32 ? 2 : 0;
   b.num_sms = num_sms_current();
-  e = launch_bwd_fused(b, st);
+  e = f32 ? launch_bwd_f32(b, tab + p->tl.wl, st) : launch_bwd_fused(b, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
   launches += 1;
   // deeper levels back (c only when gated: dv needs it)

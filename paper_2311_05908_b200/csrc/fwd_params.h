@@ -107,6 +107,10 @@ struct BwdParams {
   int32_t num_sms;
 };
 cudaError_t launch_bwd_fused(const BwdParams& prm, cudaStream_t s);
+// fp32 validation build of the backward (kernels_f32.cu): per (pair, head)
+// partial spectra [h][pair][L]; wl = W_L^e (plan table)
+cudaError_t launch_bwd_f32(const BwdParams& prm, const void* wl, cudaStream_t s);
+int64_t bwd_f32_units_per_head(int64_t B);
 int64_t bwd_tiles_per_head(int64_t B, int L1);
 
 // dk = Re IFFT(mask * sum of partial spectra)[:K] (kernels_kf.cu)

@@ -608,8 +608,9 @@ static cudaError_t launch_mp_l0(const MpParams& prm, int pass, cudaStream_t s) {
     } else if (prm.dtype == 1) {
       if (g) mp_pass3_ola_kernel<L0, true, __nv_bfloat16, __half><<<grid, 256, 0, s>>>(prm);
       else mp_pass3_ola_kernel<L0, false, __nv_bfloat16, __half><<<grid, 256, 0, s>>>(prm);
-    } else {
-      return cudaErrorInvalidValue;
+    } else {  // fp32 validation build
+      if (g) mp_pass3_ola_kernel<L0, true, float, float><<<grid, 256, 0, s>>>(prm);
+      else mp_pass3_ola_kernel<L0, false, float, float><<<grid, 256, 0, s>>>(prm);
     }
   } else if (prm.partial) {
     launch_pass_m<L0, 1>(prm, pass, grid, s);
