@@ -153,6 +153,8 @@ extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float*
     prm.L = p->Lp;
     if (p->sparse && p->row_map.size() < size_t(p->L0))
       prm.row_keep = static_cast<const uint8_t*>(p->d_tables) + p->row_keep_off;
+    prm.nlev = p->nlev;
+    for (int l = 0; l < 4; ++l) prm.lev[l] = p->lev_L0[l];
     e = launch_mp_precompute_kf(prm, p->lev_L0, p->nlev, p->L, block, reinterpret_cast<cudaStream_t>(stream));
     g_launches += H > 0 ? 2 + p->nlev - 1 : 0;
   } else {
@@ -703,6 +705,7 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   dk.Lp = p->Lp;
   dk.lev_L0 = p->lev_L0;
   dk.nlev = nlev;
+  for (int l = 0; l < 4; ++l) dk.lev[l] = p->lev_L0[l];
   dk.Lfull = p->L;
   e = launch_dk_finalize(dk, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);

@@ -5,6 +5,12 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#if defined(__CUDACC__)
+#define FC_HD_PARAMS __host__ __device__ __forceinline__
+#else
+#define FC_HD_PARAMS inline
+#endif
+
 namespace fc {
 struct FwdParams {
   const void* u;
@@ -46,7 +52,20 @@ struct KfParams {
   // multipass sparse plans: inner rows k0 with row_keep[k0] == 0 are never
   // read by the inner pass, so their k_f blocks are not computed
   const uint8_t* row_keep;
+  // recursive plans: outer level sizes (inner row r -> frequency digit k0(r))
+  int32_t nlev;
+  int32_t lev[4];
 };
+// frequency digit k0 + L0 f' of inner row r of a recursive plan: rows nest
+// level 0 outermost, frequencies have level 0 fastest
+FC_HD_PARAMS int32_t row_freq_digit(int32_t r, int32_t nlev, const int32_t* lev) {
+  if (nlev <= 1) return r;
+  int32_t d[4] = {0, 0, 0, 0};
+  for (int l = nlev - 1; l >= 0; --l) { d[l] = r % lev[l]; r /= lev[l]; }
+  int32_t k = 0, m = 1;
+  for (int l = 0; l < nlev; ++l) { k += d[l] * m; m *= lev[l]; }
+  return k;
+}
 cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s);
 
 // multipass regime (kernels_mp.cu)
@@ -129,6 +148,7 @@ struct DkParams {
   const int32_t* lev_L0;
   int32_t nlev;
   int64_t Lfull;
+  int32_t lev[4];  // device copy of lev_L0 (mask digit mapping)
 };
 cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s);
 cudaError_t launch_mp_precompute_kf(const KfParams& prm, const int32_t* lev_L0, int nlev, int64_t Lfull,

@@ -240,7 +240,8 @@ __global__ void __launch_bounds__(256) mp_kf_rows_kernel(const KfParams prm, int
     const int f0 = k2 + L2 * k1, f1 = f0 + L2;
     float2 v0 = xs[pd(f0)], v1 = xs[pd(f1)];
     if (prm.mask) {
-      const float m0 = prm.mask[k0 + int64_t(L0) * f0], m1 = prm.mask[k0 + int64_t(L0) * f1];
+      const int64_t kd = row_freq_digit(k0, prm.nlev, prm.lev);
+      const float m0 = prm.mask[kd + int64_t(L0) * f0], m1 = prm.mask[kd + int64_t(L0) * f1];
       v0.x *= m0; v0.y *= m0;
       v1.x *= m1; v1.y *= m1;
     }
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(256) dk_rows_kernel(const DkParams prm) {
       a.y += v.y;
     }
     if (prm.mask) {
-      const float mk = prm.mask[k0 + int64_t(prm.L0) * f];
+      const float mk = prm.mask[row_freq_digit(k0, prm.nlev, prm.lev) + int64_t(prm.L0) * f];
       a.x *= mk;
       a.y *= mk;
     }

@@ -287,7 +287,13 @@ static fftconv_status_t build_mask(fftconv_plan_s* p, const fftconv_sparsity_t* 
   // spectrum is masked contributes nothing and is skipped ("skip one
   // iteration of the outer loop").  The fused regime skips nothing yet.
   p->row_map.clear();
-  if (p->L0 > 1) {
+  if (p->L0 > 1 && p->nlev > 1) {
+    // recursive plans: the mask acts through k_f only (inner row r holds the
+    // frequencies k0(r) + L0 f', k0(r) the level-digit reversal of r); no row
+    // is skipped
+    for (int k0 = 0; k0 < p->L0; ++k0) p->row_map.push_back(k0);
+    p->skip_fraction = 0.0;
+  } else if (p->L0 > 1) {
     for (int k0 = 0; k0 < p->L0; ++k0) {
       bool any = false;
       for (int64_t fp = 0; fp < p->Lp && !any; ++fp) any = p->mask[size_t(k0 + int64_t(p->L0) * fp)] != 0.0f;
@@ -371,11 +377,6 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
     if (dtype == FFTCONV_F32 && p->nlev > 1) {
       delete p;
       set_last_error("fftconv_plan: the fp32 validation build supports fft_size <= 32768");
-      return FFTCONV_ERR_UNSUPPORTED;
-    }
-    if (sparsity && p->nlev > 1) {
-      delete p;
-      set_last_error("fftconv_plan: frequency-sparse plans support fft_size <= 32768 in this build");
       return FFTCONV_ERR_UNSUPPORTED;
     }
   } else {

@@ -124,3 +124,35 @@ def test_sparse_cfg5_full_size_sampled_rows():
         ref = orc.conv_fwd(u2[r][None, None, :], k[h:h + 1].astype(np.float64), mask=m)[0, 0]
         rel = np.linalg.norm(y[r] - ref) / np.linalg.norm(ref)
         assert rel < REL_L2, (r, rel)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,dims,zeroed", [
+    (32768, [8, 8, 16, 64], [4, 0, 8, 16]),
+    (1 << 20, [32, 32, 32, 64], [16, 8, 0, 32]),   # the paper's 2M-length kernel grid
+])
+def test_sparse_recursive_plans(N, dims, zeroed):
+    """Frequency-sparse plans with more than one outer level: the mask acts
+    through k_f with inner row r mapped to its frequency digits (level 0
+    fastest); forward and, at 32K, backward against the masked oracle."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    keeps = orc.keep_masks_from_zero_counts(dims, zeroed)
+    B, H, seed = 2, 1, 33
+    plan = FFTConvPlan(N, dtype=torch.float16, causal=True, sparsity=(dims, keeps))
+    q = lambda name: synth.quantize(synth.signal(seed, name, B, H, N), "f16")
+    u, dy = q("u"), q("dy")
+    k = synth.decay_filters(seed, H, N).astype(np.float32)
+    t = lambda a: torch.tensor(a, dtype=torch.float16, device="cuda")
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    y = plan.fwd(t(u), kf).float().cpu().numpy()
+    m = orc.frequency_mask(dims, keeps)
+    ref = orc.conv_fwd(u, k.astype(np.float64), mask=m)
+    assert np.linalg.norm(y - ref) / np.linalg.norm(ref) < REL_L2
+    if N <= 32768:
+        g = plan.bwd(t(dy), t(u), kf, N)
+        torch.cuda.synchronize()
+        rb = orc.conv_bwd(dy, u, k.astype(np.float64), mask=m)
+        for key in ("du", "dk"):
+            got = g[key].float().cpu().numpy()
+            rel = np.linalg.norm(got - rb[key]) / np.linalg.norm(rb[key])
+            assert rel < REL_L2, (key, rel)
