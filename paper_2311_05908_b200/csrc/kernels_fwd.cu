@@ -408,7 +408,11 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
     // first item only needs this warp's half.
     {
       wait_half(slice);
-#pragma unroll 1
+      // both 16-k2 items unrolled (more ILP, 122 registers) measured 1-2 %
+      // faster for gated causal and circular tiles and ~1 % slower for plain
+      // causal ones on B200
+      constexpr int kEpi1Unroll = (GATED || !CAUSAL) ? 2 : 1;
+#pragma unroll kEpi1Unroll
       for (int sub = 0; sub < 2; ++sub) {
         const int k20 = slice * 32 + sub * 16;  // 16 k2 per item
         const uint32_t c0 = slice * (C::NA / 2) + sub * 16;
