@@ -12,6 +12,7 @@
 // No CUDA calls happen here except in fftconv_plan_upload (api.cu).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -367,6 +368,21 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
     for (int l = 0; l < p->nlev; ++l) {
       const int el = r / p->nlev + (l < r % p->nlev ? 1 : 0);
       p->lev_L0[l] = 1 << el;
+    }
+    // experiments: FFTCONV_LEVELS="a,b[,c]" overrides the outer split (the
+    // product must be L / 2048, each factor in {2, 4, 8, 16})
+    if (const char* env = getenv("FFTCONV_LEVELS")) {
+      int32_t lv[4] = {1, 1, 1, 1}, n = 0;
+      int64_t prod = 1;
+      for (const char* c = env; *c && n < 4;) {
+        const long v = strtol(c, const_cast<char**>(&c), 10);
+        if (v == 2 || v == 4 || v == 8 || v == 16) { lv[n++] = int32_t(v); prod *= v; }
+        if (*c == ',') ++c; else break;
+      }
+      if (n > 0 && prod == L / 2048) {
+        p->nlev = n;
+        for (int l = 0; l < 4; ++l) p->lev_L0[l] = lv[l];
+      }
     }
     p->order = 2 + p->nlev;
     p->L2 = 64;
