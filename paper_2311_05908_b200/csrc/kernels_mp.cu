@@ -516,7 +516,8 @@ __global__ void __launch_bounds__(256) mp_kf_cols_kernel(const KfParams prm, int
 #pragma unroll
   for (int k0 = 0; k0 < L0; ++k0) {
     const int64_t blk = (h * L0 + k0) * nb + n / 2048;
-    reinterpret_cast<float2*>(kf + blk * block_bytes)[n % 2048] = c_mul(z[k0], tw);
+    if (!prm.row_keep || prm.row_keep[k0])  // masked rows: zero-filled by the rows step
+      reinterpret_cast<float2*>(kf + blk * block_bytes)[n % 2048] = c_mul(z[k0], tw);
     tw = c_mul(tw, bw);
   }
 }
