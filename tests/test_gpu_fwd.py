@@ -206,3 +206,31 @@ def test_fwd_circular_multipass_parity(N, dtype, gated):
     P:1243-1244) beyond the fused sizes: outer passes keep every n0."""
     got, ref = _run(N, False, dtype, gated, B=3, H=2)
     _assert_close(got, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,fft", [(4096, None), (65536, None), (16384, 4096)])
+def test_edge_single_row_and_empty(N, fft):
+    """Multipass / recursive / partial plans with B = 1 (the row pairs with a
+    zero partner) and H = 1, and empty batches for forward, backward and the
+    host entry points (no launch, no error)."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    plan = FFTConvPlan(N, fft_size=fft, dtype=torch.float16)
+    K = (fft // 2) if fft else N
+    u = synth.quantize(synth.signal(17, "u", 1, 1, N), "f16")
+    dy = synth.quantize(synth.signal(17, "dy", 1, 1, N), "f16")
+    k = synth.decay_filters(17, 1, K).astype(np.float32)
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    t = lambda a: torch.tensor(a, dtype=torch.float16, device="cuda")
+    y = plan.fwd(t(u), kf).float().cpu().numpy()
+    _assert_close(y.astype(np.float64), orc.conv_fwd(u, k.astype(np.float64)))
+    g = plan.bwd(t(dy), t(u), kf, K)
+    ref = orc.conv_bwd(dy, u, k.astype(np.float64))
+    for key in ("du", "dk"):
+        got = g[key].float().cpu().numpy().astype(np.float64)
+        assert np.linalg.norm(got - ref[key]) / np.linalg.norm(ref[key]) < REL_L2, key
+    empty = torch.zeros(0, 1, N, dtype=torch.float16, device="cuda")
+    assert plan.fwd(empty, kf).shape == (0, 1, N)
+    ge = plan.bwd(empty, empty, kf, K)
+    assert ge["du"].shape == (0, 1, N) and float(ge["dk"].abs().max()) == 0.0
+    assert plan.fwd_host(torch.zeros(0, 1, N, dtype=torch.float16), kf).shape == (0, 1, N)
