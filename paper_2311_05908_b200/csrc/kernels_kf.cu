@@ -143,10 +143,20 @@ FC_DEVICE void fft_inplace_any(float2* xs, const float2* tws, int L) {
 inline size_t fft_smem_bytes(int64_t L) { return size_t(2 * (L + L / 8)) * sizeof(float2); }
 // L float2 from global (16-byte aligned) into the padded layout
 FC_DEVICE void load_padded(float2* dst, const float2* src, int L) {
-  for (int c = threadIdx.x; c < L / 2; c += blockDim.x) {
-    const float4 q = reinterpret_cast<const float4*>(src)[c];
-    dst[pd(2 * c)] = make_float2(q.x, q.y);
-    dst[pd(2 * c + 1)] = make_float2(q.z, q.w);
+  // 256 threads, L <= 2048: at most 4 16-byte loads per thread, all issued first
+  float4 q[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = threadIdx.x + i * 256;
+    if (c < L / 2) q[i] = reinterpret_cast<const float4*>(src)[c];
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = threadIdx.x + i * 256;
+    if (c < L / 2) {
+      dst[pd(2 * c)] = make_float2(q[i].x, q[i].y);
+      dst[pd(2 * c + 1)] = make_float2(q[i].z, q[i].w);
+    }
   }
 }
 
@@ -166,8 +176,22 @@ __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) 
   }
   const float* k0row = prm.k + h0 * K;
   const float* k1row = k0row + K;
-  for (int n = threadIdx.x; n < L; n += blockDim.x)
-    sm[pd(n)] = make_float2(n < K ? k0row[n] : 0.f, (n < K && has1) ? k1row[n] : 0.f);
+  // all of this thread's filter loads are issued before any is stored
+  // (L <= 2048 = 8 per thread), so their latencies overlap
+  {
+    float2 kv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int n = threadIdx.x + i * 256;
+      kv[i] = make_float2(0.f, 0.f);
+      if (n < L && n < K) kv[i] = make_float2(k0row[n], has1 ? k1row[n] : 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int n = threadIdx.x + i * 256;
+      if (n < L) sm[pd(n)] = kv[i];
+    }
+  }
   cp_async_wait_all();
   __syncthreads();
   fft_inplace_any(sm, tws, L);
@@ -220,11 +244,7 @@ __global__ void __launch_bounds__(256) mp_kf_rows_kernel(const KfParams prm, int
     load_padded(tws, prm.twiddle, L);
     // data: 16-byte loads into the padded layout (pd() breaks 16-byte
     // alignment of the shared destination, so no cp.async here)
-    for (int c = threadIdx.x; c < L / 2; c += blockDim.x) {
-      const float4 q = reinterpret_cast<const float4*>(block)[c];
-      sm[pd(2 * c)] = make_float2(q.x, q.y);
-      sm[pd(2 * c + 1)] = make_float2(q.z, q.w);
-    }
+    load_padded(sm, reinterpret_cast<const float2*>(block), L);
   }
   cp_async_wait_all();
   __syncthreads();
