@@ -175,10 +175,14 @@ def oracle_rows_per_s(wl, target_s=8.0):
     rows, on this host's cores.  Returns (rows/s, cores, sample text, seconds, Bs, Hs)."""
     from oracle import oracle as orc
     H, N = wl["H"], wl["N"]
-    Hs = H if N <= 16384 else 2  # long rows: a couple of heads only
-    dt = _oracle_sample(wl, 1, Hs)
-    Bs = max(1, min(wl["B"], int(target_s / max(dt, 1e-3))))
-    if Bs > 1:
+    h0 = min(H, 4)
+    dt = _oracle_sample(wl, 1, h0)  # calibration: a few rows
+    rows = max(1.0, target_s / max(dt / h0, 1e-6))  # rows that fit the per-step budget
+    if rows < H:
+        Bs, Hs = 1, max(1, int(rows))
+    else:
+        Bs, Hs = max(1, min(wl["B"], int(rows / H))), H
+    if (Bs, Hs) != (1, h0):
         dt = _oracle_sample(wl, Bs, Hs)
     what = ("gated " if wl["gated"] else "") + ("fwd+bwd" if wl["bwd"] else "fwd")
     sample = f"{Bs}x{Hs} rows of N={N} ({what} causal conv + k_f per head), fp64 oracle, {orc.num_threads()} threads"
@@ -188,7 +192,9 @@ def oracle_rows_per_s(wl, target_s=8.0):
 def run_reference(args, wl, rank, world):
     if rank != 0:
         return
-    rate, cores, sample, dt, Bs, Hs = oracle_rows_per_s(wl, target_s=min(20.0, 2.0 + 0.5 * args.steps))
+    # each step a bounded sample sized so the whole run stays around two minutes
+    per_step = min(20.0, max(0.02, 120.0 / max(1, args.steps + min(args.warmup, 1))))
+    rate, cores, sample, dt, Bs, Hs = oracle_rows_per_s(wl, target_s=per_step)
     for _ in range(min(args.warmup, 1)):
         _oracle_sample(wl, 1, Hs)
     ts = [_oracle_sample(wl, Bs, Hs) for _ in range(args.steps)]
