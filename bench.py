@@ -144,28 +144,39 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- CPU oracle
+_ORACLE_INPUTS = {}
+
+
+def _oracle_inputs(wl, Bs, Hs):
+    """Seeded inputs of a Bs x Hs sample of the workload (generated once per
+    shape; generation is never timed)."""
+    key = (wl["name"], Bs, Hs)
+    if key not in _ORACLE_INPUTS:
+        import synth
+        from oracle import oracle as orc
+        H, N, K = wl["H"], wl["N"], wl["K"]
+        k = synth.decay_filters(0, Hs, K).astype(np.float32).astype(np.float64)
+        rows = np.array([b * H + h for b in range(Bs) for h in range(Hs)])
+        q = lambda name: synth.quantize(synth.normal(0, synth.TENSOR_IDS[name], rows, N).reshape(Bs, Hs, N),
+                                        wl["dtype"])
+        kw = dict(w=q("w"), v=q("v")) if wl["gated"] else {}
+        mask = None
+        if wl["sparse"]:
+            dims, keeps = sparsity_spec(wl["sparse"], wl["fft"])
+            mask = orc.frequency_mask(dims, keeps)
+        _ORACLE_INPUTS.clear()  # keep one sample resident
+        _ORACLE_INPUTS[key] = (q("u"), k, kw, mask, q("dy") if wl["bwd"] else None)
+    return _ORACLE_INPUTS[key]
+
+
 def _oracle_sample(wl, Bs, rows=None):
     """Run the fp64 oracle on Bs x (rows or H) rows of the workload; seconds."""
-    import synth
     from oracle import oracle as orc
-    H, N, K = wl["H"], wl["N"], wl["K"]
-    Hs = H if rows is None else rows
-    k = synth.decay_filters(0, H, K)[:Hs].astype(np.float32).astype(np.float64)
-    rows = np.array([b * H + h for b in range(Bs) for h in range(Hs)])
-    q = lambda name: synth.quantize(synth.normal(0, synth.TENSOR_IDS[name], rows, N).reshape(Bs, Hs, N),
-                                    wl["dtype"])
-    u = q("u")
-    kw = {}
-    if wl["gated"]:
-        kw = dict(w=q("w"), v=q("v"))
-    mask = None
-    if wl["sparse"]:
-        dims, keeps = sparsity_spec(wl["sparse"], wl["fft"])
-        mask = orc.frequency_mask(dims, keeps)
+    Hs = wl["H"] if rows is None else rows
+    u, k, kw, mask, dy = _oracle_inputs(wl, Bs, Hs)
     t = time.perf_counter()
     orc.conv_fwd(u, k, causal=wl["causal"], mask=mask, **kw)
     if wl["bwd"]:
-        dy = q("dy")
         orc.conv_bwd(dy, u, k, causal=wl["causal"], mask=mask, **kw)
     return time.perf_counter() - t
 
@@ -175,8 +186,8 @@ def oracle_rows_per_s(wl, target_s=8.0):
     rows, on this host's cores.  Returns (rows/s, cores, sample text, seconds, Bs, Hs)."""
     from oracle import oracle as orc
     H, N = wl["H"], wl["N"]
-    h0 = min(H, 4)
-    dt = _oracle_sample(wl, 1, h0)  # calibration: a few rows
+    h0 = max(1, min(H, (1 << 20) // N))  # calibration: ~1M samples (per-call overhead amortised)
+    dt = _oracle_sample(wl, 1, h0)
     rows = max(1.0, target_s / max(dt / h0, 1e-6))  # rows that fit the per-step budget
     if rows < H:
         Bs, Hs = 1, max(1, int(rows))
@@ -196,7 +207,7 @@ def run_reference(args, wl, rank, world):
     per_step = min(20.0, max(0.02, 120.0 / max(1, args.steps + min(args.warmup, 1))))
     rate, cores, sample, dt, Bs, Hs = oracle_rows_per_s(wl, target_s=per_step)
     for _ in range(min(args.warmup, 1)):
-        _oracle_sample(wl, 1, Hs)
+        _oracle_sample(wl, Bs, Hs)
     ts = [_oracle_sample(wl, Bs, Hs) for _ in range(args.steps)]
     step = statistics.mean(ts)
     value = Bs * Hs / step
