@@ -22,6 +22,7 @@
 
 #include "fused_common.cuh"
 #include "fwd_params.h"
+#include "launch_util.h"
 #include "sm100.cuh"
 
 namespace fc {
@@ -486,12 +487,8 @@ template <int L1, bool CAUSAL, bool GATE_IO, bool NEED_C, typename T>
 static cudaError_t launch_bwd_t(const BwdParams& prm, cudaStream_t s) {
   using BC = BwdCfg<L1, CAUSAL>;
   auto kern = fftconv_bwd_o2_kernel<L1, CAUSAL, GATE_IO, NEED_C, T>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(BC::SMEM));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static int attr[64] = {0};
+  if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(BC::SMEM), attr)) return e;
   const int64_t tiles = prm.H * bwd_tiles_per_head(prm.B, L1);
   const int grid = int(tiles < prm.num_sms ? tiles : prm.num_sms);
   if (grid < 1) return cudaSuccess;

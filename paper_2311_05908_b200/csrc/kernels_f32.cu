@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include "fwd_params.h"
+#include "launch_util.h"
 #include "layout.h"
 #include "sm100.cuh"
 
@@ -253,8 +254,8 @@ cudaError_t launch_bwd_f32_t(const BwdParams& prm, const float2* wl, cudaStream_
   const int L = prm.L1 * 64;
   const size_t smem = size_t(5) * size_t(L) * sizeof(float2);
   auto kern = fftconv_bwd_f32_kernel<CAUSAL, GATE_IO, NEED_C>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
+  static int attr[64] = {0};
+  if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(smem), attr)) return e;
   const int64_t units = ((prm.B + 1) / 2) * prm.H;
   const int64_t cap = int64_t(prm.num_sms) * 2;
   const unsigned grid = unsigned(units < cap ? units : cap);
@@ -268,8 +269,8 @@ cudaError_t launch_f32_t(const FwdParams& prm, cudaStream_t s) {
   const int L = prm.L1 * 64;
   const size_t smem = size_t(3) * size_t(L) * sizeof(float2);
   auto kern = fftconv_f32_kernel<CAUSAL, GATED>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
+  static int attr[64] = {0};
+  if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(smem), attr)) return e;
   const int64_t units = ((prm.B + 1) / 2) * prm.H;
   const int64_t cap = int64_t(prm.num_sms) * 4;
   const unsigned grid = unsigned(units < cap ? units : cap);

@@ -38,6 +38,7 @@
 
 #include "fused_common.cuh"
 #include "fwd_params.h"
+#include "launch_util.h"
 #include "sm100.cuh"
 
 namespace fc {
@@ -736,12 +737,8 @@ static cudaError_t launch_o2(const FwdParams& prm, cudaStream_t stream) {
   using C = O2Cfg<L1, CAUSAL>;
   using F = FwdCfg<L1, CAUSAL, GATED>;
   auto kern = fftconv_fwd_o2_kernel<L1, CAUSAL, GATED, T>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(F::SMEM));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static int attr[64] = {0};
+  if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(F::SMEM), attr)) return e;
   const int64_t nbt = (prm.B + C::R - 1) / C::R;
   const int64_t tiles = (prm.row_map ? (prm.H / prm.row_L0) * prm.nrow : prm.H) * nbt;
   int grid = int(tiles < prm.num_sms ? tiles : prm.num_sms);

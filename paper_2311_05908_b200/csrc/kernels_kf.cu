@@ -13,6 +13,7 @@
 
 #include "dft_small.cuh"
 #include "fwd_params.h"
+#include "launch_util.h"
 #include "sm100.cuh"
 
 namespace fc {
@@ -272,12 +273,8 @@ __global__ void __launch_bounds__(256) mp_kf_rows_kernel(const KfParams prm, int
 
 cudaError_t launch_mp_kf_rows(const KfParams& prm, int L0, int Lp, size_t block_bytes, cudaStream_t s) {
   const size_t smem = fft_smem_bytes(Lp);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(mp_kf_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  static int attr[64] = {0};
+  if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(mp_kf_rows_kernel), int(smem), attr)) return e;
   mp_kf_rows_kernel<<<unsigned(prm.H * L0), 256, smem, s>>>(prm, L0, Lp, block_bytes);
   return cudaGetLastError();
 }
@@ -362,12 +359,8 @@ __global__ void __launch_bounds__(256) dk_cols_kernel(const DkParams prm) {
 cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
   if (prm.H <= 0) return cudaSuccess;
   const size_t smem = fft_smem_bytes(prm.Lp);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(dk_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  static int attr[64] = {0};
+  if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(dk_rows_kernel), int(smem), attr)) return e;
   dk_rows_kernel<<<unsigned(prm.H * prm.L0), 256, smem, s>>>(prm);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || prm.L0 == 1) return e;
@@ -397,12 +390,8 @@ cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
 cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s) {
   if (prm.H <= 0) return cudaSuccess;
   const size_t smem = fft_smem_bytes(prm.L);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(precompute_kf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  static int attr[64] = {0};
+  if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_kernel), int(smem), attr)) return e;
   precompute_kf_kernel<<<unsigned((prm.H + 1) / 2), 256, smem, s>>>(prm);
   return cudaGetLastError();
 }
