@@ -185,7 +185,13 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     mp.gated = gated ? 1 : 0;
     mp.dtype = p->dtype == FFTCONV_BF16 ? 1 : p->dtype == FFTCONV_F32 ? 2 : 0;
     const bool skip = p->sparse && p->row_map.size() < size_t(p->L0);
-    if (skip) mp.row_keep = static_cast<const uint8_t*>(p->d_tables) + p->row_keep_off;
+    if (skip) {
+      mp.row_keep = static_cast<const uint8_t*>(p->d_tables) + p->row_keep_off;
+      if (p->nlev == 1) {  // outer passes produce / consume only the kept rows
+        mp.row_map = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(p->d_tables) + p->row_map_off);
+        mp.nrow = int32_t(p->row_map.size());
+      }
+    }
     if (p->regime == REGIME_PARTIAL) {  // overlap-save windows as virtual rows
       mp.partial = 1;
       mp.C = p->L / 2;

@@ -89,6 +89,8 @@ struct MpParams {
   int32_t partial;
   int64_t NC, C;
   const uint8_t* row_keep;  // sparse: L0 flags, rows with 0 are never written/read
+  const int32_t* row_map;   // sparse one-level plans: the kept rows k0 (nrow of them)
+  int32_t nrow;
   // recursive levels (N > 16384): complex circular rows of an intermediate in
   // and out (all n0, no gating, fp16); twiddles W_Llev^{n' k0} computed on
   // the fly when wtab == nullptr

@@ -386,6 +386,209 @@ __global__ void __launch_bounds__(256, FC_PASS_MINB) mp_pass3_kernel(const MpPar
   }
 }
 
+// Frequency-sparse one-level plans: only the nrow kept outer rows k0 are
+// produced (pass 1) and consumed (pass 3), each as a direct sum over n0 with
+// W_L0^{n0 k0} from the constant root table and W_L^{n' k0} from the plan's
+// [k0][n'] table -- a quarter of the work of the full DFT_L0 for cfg 5's
+// 4-of-16 pattern, with 4-column vectors at every L0.
+template <int NPT>
+FC_DEVICE float2 w_full(int k) {  // W_NPT^k, any k
+  k &= NPT - 1;
+  if (k < NPT / 2) return w_root<NPT>(k);
+  const float2 w = w_root<NPT>(k - NPT / 2);
+  return make_float2(-w.x, -w.y);
+}
+
+template <int L0, int MODE, bool GATED, typename T, typename TT>
+__global__ void __launch_bounds__(256, 2) mp_pass1_sparse_kernel(const MpParams prm) {
+  constexpr int COLS = 4, C2 = 2;
+  constexpr int NIN = MODE == 0 ? L0 / 2 : L0;
+  const int64_t NCH = int64_t(prm.Lp) / COLS;
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t pairs = uint32_t((prm.B + 1) / 2);
+  if (idx >= pairs * uint32_t(prm.H) * uint32_t(NCH)) return;
+  const int n = int(idx & uint32_t(NCH - 1)) * COLS;
+  const uint32_t ph = idx >> (31 - __clz(uint32_t(NCH)));
+  const int64_t h = ph % uint32_t(prm.H), p = ph / uint32_t(prm.H);
+  const int64_t b0 = 2 * p, b1 = 2 * p + 1;
+  const bool has1 = b1 < prm.B;
+  const T* __restrict__ u = reinterpret_cast<const T*>(prm.u);
+  const T* __restrict__ w = reinterpret_cast<const T*>(prm.w);
+  const int64_t Hg = prm.Hg ? prm.Hg : prm.H, hg = h + prm.h0;
+  const int64_t g0 = b0 + 2 * prm.pair0, g1 = g0 + 1;
+  int64_t r0, r1, s0 = 0, s1 = 0;
+  if (MODE == 1) {
+    const uint32_t nc = uint32_t(prm.NC);
+    const int64_t q0 = uint32_t(g0) / nc, q1 = uint32_t(g1) / nc;
+    s0 = (g0 - q0 * nc - 1) * prm.C;
+    s1 = (g1 - q1 * nc - 1) * prm.C;
+    r0 = (q0 * Hg + hg) * prm.N + s0 + n;
+    r1 = (q1 * Hg + hg) * prm.N + s1 + n;
+  } else {
+    r0 = (g0 * Hg + hg) * prm.N + n;
+    r1 = (g1 * Hg + hg) * prm.N + n;
+  }
+  CV<C2> z[NIN];
+#pragma unroll
+  for (int n0 = 0; n0 < NIN; ++n0) {
+    const int64_t o = int64_t(n0) * prm.Lp;
+    const bool hi_only = MODE == 1 && prm.win_hi_only && n0 < L0 / 2;
+    const bool ok0 = !hi_only && (MODE != 1 || s0 + o >= 0);
+    const bool ok1 = !hi_only && has1 && (MODE != 1 || s1 + o >= 0);
+    float a[COLS], c[COLS];
+#pragma unroll
+    for (int j = 0; j < COLS; ++j) a[j] = c[j] = 0.f;
+    if (ok0) ld_cols<T, COLS>(u + r0 + o, a);
+    if (ok1) ld_cols<T, COLS>(u + r1 + o, c);
+    if (GATED) {
+      float wa[COLS], wc[COLS];
+#pragma unroll
+      for (int j = 0; j < COLS; ++j) wa[j] = wc[j] = 0.f;
+      if (ok0) ld_cols<T, COLS>(w + r0 + o, wa);
+      if (ok1) ld_cols<T, COLS>(w + r1 + o, wc);
+#pragma unroll
+      for (int j = 0; j < COLS; ++j) { a[j] *= wa[j]; c[j] *= wc[j]; }
+    }
+#pragma unroll
+    for (int cc = 0; cc < C2; ++cc) {
+      z[n0].r[cc] = make_float2(a[2 * cc], a[2 * cc + 1]);
+      z[n0].i[cc] = make_float2(c[2 * cc], c[2 * cc + 1]);
+    }
+  }
+  const float s = rsqrtf(float(L0));
+  TT* __restrict__ Tre = reinterpret_cast<TT*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
+  TT* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
+  for (int q = 0; q < prm.nrow; ++q) {
+    const int k0 = prm.row_map[q];
+    CV<C2> acc;
+#pragma unroll
+    for (int cc = 0; cc < C2; ++cc) acc.r[cc] = acc.i[cc] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int n0 = 0; n0 < NIN; ++n0) {
+      const float2 wr = w_full<L0>(n0 * k0);
+      const CV<C2> t = cv_mul_s(z[n0], wr.x, wr.y);
+#pragma unroll
+      for (int cc = 0; cc < C2; ++cc) { acc.r[cc] = add2(acc.r[cc], t.r[cc]); acc.i[cc] = add2(acc.i[cc], t.i[cc]); }
+    }
+    // twiddle W_L^{n' k0} (plan table), scale 1/sqrt(L0)
+    const float4 q01 = *reinterpret_cast<const float4*>(prm.wtab + int64_t(k0) * prm.Lp + n);
+    const float4 q23 = *reinterpret_cast<const float4*>(prm.wtab + int64_t(k0) * prm.Lp + n + 2);
+    CV<C2> tw;
+    tw.r[0] = make_float2(q01.x * s, q01.z * s); tw.i[0] = make_float2(q01.y * s, q01.w * s);
+    tw.r[1] = make_float2(q23.x * s, q23.z * s); tw.i[1] = make_float2(q23.y * s, q23.w * s);
+    const CV<C2> o = cv_mul(acc, tw);
+    float fr[COLS], fi[COLS];
+#pragma unroll
+    for (int cc = 0; cc < C2; ++cc) {
+      fr[2 * cc] = o.r[cc].x; fr[2 * cc + 1] = o.r[cc].y;
+      fi[2 * cc] = o.i[cc].x; fi[2 * cc + 1] = o.i[cc].y;
+    }
+    st_cols<TT, COLS>(Tre + int64_t(k0) * prm.Lp, fr);
+    st_cols<TT, COLS>(Tim + int64_t(k0) * prm.Lp, fi);
+  }
+}
+
+template <int L0, int MODE, bool GATED, typename T, typename TT>
+__global__ void __launch_bounds__(256, 2) mp_pass3_sparse_kernel(const MpParams prm) {
+  constexpr int COLS = 4, C2 = 2;
+  constexpr int NOUT = MODE == 2 ? L0 : L0 / 2;      // output rows n0
+  constexpr int Q0 = MODE == 1 ? L0 / 2 : 0;         // first output n0
+  const int64_t NCH = int64_t(prm.Lp) / COLS;
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t pairs = uint32_t((prm.B + 1) / 2);
+  if (idx >= pairs * uint32_t(prm.H) * uint32_t(NCH)) return;
+  const int n = int(idx & uint32_t(NCH - 1)) * COLS;
+  const uint32_t ph = idx >> (31 - __clz(uint32_t(NCH)));
+  const int64_t h = ph % uint32_t(prm.H), p = ph / uint32_t(prm.H);
+  const TT* __restrict__ Tre =
+      reinterpret_cast<const TT*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
+  const TT* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
+  const float s = rsqrtf(float(L0));
+  CV<C2> x[NOUT];
+#pragma unroll
+  for (int m = 0; m < NOUT; ++m)
+#pragma unroll
+    for (int cc = 0; cc < C2; ++cc) x[m].r[cc] = x[m].i[cc] = make_float2(0.f, 0.f);
+  for (int q = 0; q < prm.nrow; ++q) {
+    const int k0 = prm.row_map[q];
+    float fr[COLS], fi[COLS];
+    ld_cols<TT, COLS>(Tre + int64_t(k0) * prm.Lp, fr);
+    ld_cols<TT, COLS>(Tim + int64_t(k0) * prm.Lp, fi);
+    const float4 q01 = *reinterpret_cast<const float4*>(prm.wtab + int64_t(k0) * prm.Lp + n);
+    const float4 q23 = *reinterpret_cast<const float4*>(prm.wtab + int64_t(k0) * prm.Lp + n + 2);
+    CV<C2> v, tw;
+#pragma unroll
+    for (int cc = 0; cc < C2; ++cc) {
+      v.r[cc] = make_float2(fr[2 * cc], fr[2 * cc + 1]);
+      v.i[cc] = make_float2(fi[2 * cc], fi[2 * cc + 1]);
+    }
+    tw.r[0] = make_float2(q01.x * s, q01.z * s); tw.i[0] = make_float2(q01.y * s, q01.w * s);
+    tw.r[1] = make_float2(q23.x * s, q23.z * s); tw.i[1] = make_float2(q23.y * s, q23.w * s);
+    v = cv_mulc(v, tw);  // conj twiddle and 1/sqrt(L0)
+#pragma unroll
+    for (int m = 0; m < NOUT; ++m) {
+      const float2 wr = w_full<L0>((Q0 + m) * k0);
+      const CV<C2> t = cv_mul_s(v, wr.x, -wr.y);  // W_L0^{-n0 k0}
+#pragma unroll
+      for (int cc = 0; cc < C2; ++cc) { x[m].r[cc] = add2(x[m].r[cc], t.r[cc]); x[m].i[cc] = add2(x[m].i[cc], t.i[cc]); }
+    }
+  }
+  const int64_t b0 = 2 * p, b1 = 2 * p + 1;
+  const bool has1 = b1 < prm.B;
+  T* __restrict__ y = reinterpret_cast<T*>(prm.y);
+  const T* __restrict__ v = reinterpret_cast<const T*>(prm.v);
+  const int64_t Hg = prm.Hg ? prm.Hg : prm.H, hg = h + prm.h0;
+  const int64_t g0 = b0 + 2 * prm.pair0, g1 = g0 + 1;
+  int64_t r0, r1;
+  if (MODE == 1) {
+    const uint32_t nc = uint32_t(prm.NC);
+    const int64_t q0 = uint32_t(g0) / nc, q1 = uint32_t(g1) / nc;
+    r0 = (q0 * Hg + hg) * prm.N + (g0 - q0 * nc) * prm.C + n;
+    r1 = (q1 * Hg + hg) * prm.N + (g1 - q1 * nc) * prm.C + n;
+  } else {
+    r0 = (g0 * Hg + hg) * prm.N + n;
+    r1 = (g1 * Hg + hg) * prm.N + n;
+  }
+#pragma unroll
+  for (int m = 0; m < NOUT; ++m) {
+    const int64_t off = int64_t(m) * prm.Lp;  // partial: rows start at the window's second half
+    float a[COLS], c[COLS];
+#pragma unroll
+    for (int cc = 0; cc < C2; ++cc) {
+      a[2 * cc] = x[m].r[cc].x; a[2 * cc + 1] = x[m].r[cc].y;
+      c[2 * cc] = x[m].i[cc].x; c[2 * cc + 1] = x[m].i[cc].y;
+    }
+    if (prm.y2) {
+      const T* v2 = reinterpret_cast<const T*>(prm.v2);
+      T* y2 = reinterpret_cast<T*>(prm.y2);
+      float g[COLS], qv[COLS];
+      ld_cols<T, COLS>(v2 + r0 + off, g);
+#pragma unroll
+      for (int j = 0; j < COLS; ++j) qv[j] = a[j] * g[j];
+      st_cols<T, COLS>(y2 + r0 + off, qv);
+      if (has1) {
+        ld_cols<T, COLS>(v2 + r1 + off, g);
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) qv[j] = c[j] * g[j];
+        st_cols<T, COLS>(y2 + r1 + off, qv);
+      }
+    }
+    if (GATED) {
+      float g[COLS];
+      ld_cols<T, COLS>(v + r0 + off, g);
+#pragma unroll
+      for (int j = 0; j < COLS; ++j) a[j] *= g[j];
+      if (has1) {
+        ld_cols<T, COLS>(v + r1 + off, g);
+#pragma unroll
+        for (int j = 0; j < COLS; ++j) c[j] *= g[j];
+      }
+    }
+    st_cols<T, COLS>(y + r0 + off, a);
+    if (has1) st_cols<T, COLS>(y + r1 + off, c);
+  }
+}
+
 // Backward of the partial convolution, dg by overlap-add: the circular
 // correlation of window j (dc block j in its second half, zeros in its
 // first) with k spans positions [(j-1)C, (j+1)C) of dg, so
@@ -573,6 +776,13 @@ cudaError_t launch_mp_kf_rows(const KfParams& prm, int L0, int Lp, size_t block_
 template <int L0, int MODE, bool G, typename T>
 static void launch_pass_k(const MpParams& prm, int pass, unsigned grid, cudaStream_t s) {
   using TT = typename std::conditional<std::is_same<T, float>::value, float, __half>::type;
+  if (prm.row_map && prm.wtab) {  // sparse one-level plans: kept rows only
+    const int64_t total = ((prm.B + 1) / 2) * prm.H * (prm.Lp / 4);
+    const unsigned g4 = unsigned((total + 255) / 256);
+    if (pass == 1) mp_pass1_sparse_kernel<L0, MODE, G, T, TT><<<g4, 256, 0, s>>>(prm);
+    else mp_pass3_sparse_kernel<L0, MODE, G, T, TT><<<g4, 256, 0, s>>>(prm);
+    return;
+  }
   if (pass == 1) mp_pass1_kernel<L0, MODE, G, T, TT><<<grid, 256, 0, s>>>(prm);
   else mp_pass3_kernel<L0, MODE, G, T, TT><<<grid, 256, 0, s>>>(prm);
 }
