@@ -39,9 +39,24 @@ def _stale(target, sources):
 
 
 def _nvcc(out, sources, extra=()):
+    """Compile every source to an object in parallel, then link the shared
+    library (the sources share no device symbols)."""
+    from concurrent.futures import ThreadPoolExecutor
     tmp = out + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, *COMMON, *extra, "-o", tmp, *sources]
-    subprocess.check_call(cmd)
+    objdir = os.path.join(os.path.dirname(out), "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in COMMON if f != "-shared"]
+
+    def one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + f".{os.getpid()}.o")
+        subprocess.check_call([NVCC, *ARCH, *compile_flags, *extra, "-c", "-o", obj, src])
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(sources), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(one, sources))
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs])
+    for o in objs:
+        os.remove(o)
     os.replace(tmp, out)
 
 
