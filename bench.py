@@ -235,6 +235,36 @@ def algorithmic_bytes(wl, H_L8):
     return fwd + bwd
 
 
+def min_tensor_flops_per_row(wl):
+    """the method's own minimum tensor-core work per row --
+    Monarch stages over the packed complex length M = L/2, 8 M M_i real flops
+    per stage and direction (fwd + inv), the causal halves of the first
+    forward and last inverse stage removed, minimised over p <= 4 orders with
+    factors >= 8 (powers of two).  Backward: x1.5 (plain) or x2 (gated)."""
+    import itertools
+    M = wl["fft"] // 2
+    lg = M.bit_length() - 1
+    best = None
+    for p in (2, 3, 4):
+        for parts in itertools.product(range(3, lg + 1), repeat=p):
+            if sum(parts) != lg:
+                continue
+            f = [1 << e for e in parts]
+            fl = sum(8 * M * m for m in f) * 2
+            if wl["causal"]:
+                fl -= 8 * M * f[0] // 2 * 2  # first forward stage (half K) and last inverse (half outputs)
+            best = fl if best is None else min(best, fl)
+    if best is None:
+        return 0.0
+    rows_per_row = 1.0
+    if wl["causal"] and wl["fft"] < 2 * wl["N"]:  # partial: N / C windows of length L per row
+        rows_per_row = wl["N"] / (wl["fft"] // 2)
+    fl = best * rows_per_row  # M = L/2 is already the per-row packed length
+    if wl["bwd"]:
+        fl *= 3.0 if wl["gated"] else 2.5  # fwd + bwd (x2 gated, x1.5 plain)
+    return fl
+
+
 # ----------------------------------------------------------------- B1 baseline
 def torch_fft_baseline(wl, u, w, v, k, dy, steps, mask=None):
     """cuFFT + PyTorch, the Hyena reference fftconv (inputs
@@ -450,6 +480,14 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             rate, cores, sample, _, _, _ = oracle_rows_per_s(wl)
             cpu = {"value": rate, "unit": "sequences/s", "cores": cores, "kind": "oracle", "sample": sample}
+        # governing roofline = max(bytes / BW, min tensor flops / peak)
+        tflops = min_tensor_flops_per_row(wl) * B * H
+        t_hbm = bytes_per_call / (peaks["hbm"] * 1e9)
+        t_tc = tflops / (peaks["tc"] * 1e12)
+        governing = {"bound": "hbm" if t_hbm >= t_tc else "tensor", "frac": max(t_hbm, t_tc) / (conv_ms * 1e-3),
+                     "min_tensor_flops_per_call": tflops, "tensor_peak_tflops": peaks["tc"],
+                     "note": "fraction of the governing roofline (HBM bytes vs the method's minimum Monarch "
+                             "tensor flops, p <= 4, SURVEY 8(d))"}
         vs = PAPER_SEQ_S.get(args.workload)
         regime = {1: "fused", 2: "partial (overlap-save, multipass)", 3: "multipass"}[plan.info.regime]
         # device memory of this library for the step vs the cuFFT+PyTorch reference (NEXT-3)
@@ -490,7 +528,8 @@ def main():
                                    + (" + multipass outer passes" if plan.info.regime != 1 else "")
                                    + (" + bwd" if wl["bwd"] else "") + ")",
                          "kernel_ms": conv_ms, "algorithmic_bytes_per_launch": bytes_per_call,
-                         "peak_source": peaks["src"]},
+                         "peak_source": peaks["src"],
+                         "governing": governing},
             "cpu_baseline": cpu,
             "cufft_baseline": tb,
             "memory": {"library_device_bytes": int(lib_bytes),
