@@ -295,19 +295,32 @@ __global__ void __launch_bounds__(256) dk_rows_kernel(const DkParams prm) {
     load_padded(tws, prm.twiddle, L);
   }
   const float2* part = prm.part + row * prm.nbt * L;
-  for (int f = threadIdx.x; f < L; f += blockDim.x) {
-    float2 a = make_float2(0.f, 0.f);
+  {  // 256 threads, L <= 2048: each thread's 8 columns summed over the tiles in
+     // tile order (deterministic), one tile's loads in flight together
+    float2 a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = make_float2(0.f, 0.f);
     for (int64_t j = 0; j < prm.nbt; ++j) {
-      const float2 v = part[j * L + f];
-      a.x += v.x;
-      a.y += v.y;
+      float2 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int f = threadIdx.x + i * 256;
+        v[i] = f < L ? part[j * L + f] : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { a[i].x += v[i].x; a[i].y += v[i].y; }
     }
-    if (prm.mask) {
-      const float mk = prm.mask[row_freq_digit(k0, prm.nlev, prm.lev) + int64_t(prm.L0) * f];
-      a.x *= mk;
-      a.y *= mk;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int f = threadIdx.x + i * 256;
+      if (f >= L) continue;
+      if (prm.mask) {
+        const float mk = prm.mask[row_freq_digit(k0, prm.nlev, prm.lev) + int64_t(prm.L0) * f];
+        a[i].x *= mk;
+        a[i].y *= mk;
+      }
+      sm[pd(f)] = make_float2(a[i].x, -a[i].y);  // conj: inverse transform via the forward one
     }
-    sm[pd(f)] = make_float2(a.x, -a.y);  // conj: inverse transform via the forward one
   }
   cp_async_wait_all();
   __syncthreads();
