@@ -103,10 +103,12 @@ typedef struct {
 
 /* Create a plan (host only, no CUDA calls).
  *  N        input length per row, power of two, 256 <= N.
- *  fft_size L, power of two.  causal=1: L >= 2N is the full causal conv
- *           (K <= N); L < 2N selects the partial (chunked overlap-add) conv
- *           with K <= L/2 (A12).  causal=0: circular, L == N == K
- *           (A2).
+ *  fft_size L, power of two.  causal=1: L == 2N is the full causal conv
+ *           (K <= N; N up to 4M); L < 2N selects the partial (overlap-save)
+ *           conv with K <= L/2, L <= 32768 (A12).  causal=0:
+ *           circular, L == N == K, N = 512 .. 8M (A2).
+ *  dtype    FFTCONV_F16 / FFTCONV_BF16 I/O (fp16 tensor-core operands, fp32
+ *           accumulation), or FFTCONV_F32 (validation build, L <= 32768).
  *  sparsity NULL for dense; else see fftconv_sparsity_t (prod dims == L).
  * Returns NOT_POW2 / INVALID_ARG / BAD_SPARSITY / UNSUPPORTED on bad input;
  * *out is set only on success. */
@@ -131,8 +133,10 @@ fftconv_status_t fftconv_precompute_kf(fftconv_plan_t plan, const float* d_k, in
 
 /* Device workspace the forward (for_bwd = 0) or backward (for_bwd = 1) call
  * needs for a (B, H) problem.  The fused regime's forward needs none; the
- * multipass regime (regime 3, Alg. 4) keeps its fp16 intermediate
- * there (2 * ceil(B/2) * H * fft_size * 2 bytes). */
+ * multipass and partial regimes (Alg. 4) keep their fp16
+ * intermediate there (2 * ceil(B'/2) * H * fft_size * 2 bytes, B' = B or the
+ * number of overlap-save windows; twice that for recursive plans and for the
+ * fp32 build); the backward adds the per-tile partial spectra of dk. */
 fftconv_status_t fftconv_workspace_size(fftconv_plan_t plan, int64_t B, int64_t H, int for_bwd, size_t* bytes);
 
 /* y = u conv k (Alg. 1; real packing, causal padding and the
@@ -181,10 +185,12 @@ fftconv_status_t fftconv_fwd_stream(fftconv_plan_t plan, const void* h_u, const 
                                     void* d_stage, size_t stage_bytes, fftconv_stream_t stream);
 fftconv_status_t fftconv_stream_stage_size(fftconv_plan_t plan, int64_t B, int64_t H, int gated, size_t* bytes);
 
-/* Backward of <y, dy> with recomputation (A15).  Plain when
- * d_w == d_v == NULL (then d_dw, d_dv ignored); gated when both are given.
- * d_dk (H, K) fp32 is OVERWRITTEN with the batch sum.  d_workspace:
- * H * workspace_bytes_per_head bytes (required). */
+/* Backward of <y, dy> with recomputation (A15) for every plan the
+ * forward accepts (fused, multipass incl. recursive, partial, circular,
+ * frequency-sparse, fp32 build).  Plain when d_w == d_v == NULL (then d_dw,
+ * d_dv ignored); gated when both are given.  d_dk (H, K) fp32 is OVERWRITTEN
+ * with the batch sum (deterministic: fixed-order reductions, no atomics).
+ * d_workspace: fftconv_workspace_size(plan, B, H, 1) bytes (required). */
 fftconv_status_t fftconv_bwd(fftconv_plan_t plan, const void* d_dy, const void* d_u, const void* d_w,
                              const void* d_v, const void* d_kf, void* d_du, void* d_dw, void* d_dv, float* d_dk,
                              int64_t B, int64_t H, int64_t K, void* d_workspace, fftconv_stream_t stream);
