@@ -170,8 +170,11 @@ __global__ void __launch_bounds__(256, FC_PASS_MINB) mp_pass1_kernel(const MpPar
     // partial: the window's first half may precede the row (zeros); the
     // backward's dc windows keep only their second half (win_hi_only)
     const bool hi_only = MODE == 1 && prm.win_hi_only && n0 < L0 / 2;
+    // a pair's two windows are consecutive (j, j+1) of one row: the second
+    // window's first half is the first window's second half (copied below)
+    const bool reused = MODE == 1 && !prm.win_hi_only && n0 < L0 / 2;
     const bool ok0 = !hi_only && (MODE != 1 || s0 + o >= 0);
-    const bool ok1 = !hi_only && has1 && (MODE != 1 || s1 + o >= 0);
+    const bool ok1 = !hi_only && !reused && has1 && (MODE != 1 || s1 + o >= 0);
     float a[COLS], c[COLS];
 #pragma unroll
     for (int j = 0; j < COLS; ++j) a[j] = c[j] = 0.f;
@@ -191,6 +194,12 @@ __global__ void __launch_bounds__(256, FC_PASS_MINB) mp_pass1_kernel(const MpPar
       z[n0].r[cc] = make_float2(a[2 * cc], a[2 * cc + 1]);
       z[n0].i[cc] = make_float2(c[2 * cc], c[2 * cc + 1]);
     }
+  }
+  if (MODE == 1 && !prm.win_hi_only && has1) {
+#pragma unroll
+    for (int n0 = 0; n0 < L0 / 2; ++n0)
+#pragma unroll
+      for (int cc = 0; cc < C2; ++cc) z[n0].i[cc] = z[n0 + L0 / 2].r[cc];
   }
   // DFT_L0 over n0.  Causal rows are zero for n0 >= L0/2, so the first
   // radix-2 stage reduces to X[2m] = DFT_{L0/2}(z)[m],
@@ -433,8 +442,11 @@ __global__ void __launch_bounds__(256, 2) mp_pass1_sparse_kernel(const MpParams 
   for (int n0 = 0; n0 < NIN; ++n0) {
     const int64_t o = int64_t(n0) * prm.Lp;
     const bool hi_only = MODE == 1 && prm.win_hi_only && n0 < L0 / 2;
+    // a pair's two windows are consecutive (j, j+1) of one row: the second
+    // window's first half is the first window's second half (copied below)
+    const bool reused = MODE == 1 && !prm.win_hi_only && n0 < L0 / 2;
     const bool ok0 = !hi_only && (MODE != 1 || s0 + o >= 0);
-    const bool ok1 = !hi_only && has1 && (MODE != 1 || s1 + o >= 0);
+    const bool ok1 = !hi_only && !reused && has1 && (MODE != 1 || s1 + o >= 0);
     float a[COLS], c[COLS];
 #pragma unroll
     for (int j = 0; j < COLS; ++j) a[j] = c[j] = 0.f;
@@ -454,6 +466,12 @@ __global__ void __launch_bounds__(256, 2) mp_pass1_sparse_kernel(const MpParams 
       z[n0].r[cc] = make_float2(a[2 * cc], a[2 * cc + 1]);
       z[n0].i[cc] = make_float2(c[2 * cc], c[2 * cc + 1]);
     }
+  }
+  if (MODE == 1 && !prm.win_hi_only && has1) {
+#pragma unroll
+    for (int n0 = 0; n0 < L0 / 2; ++n0)
+#pragma unroll
+      for (int cc = 0; cc < C2; ++cc) z[n0].i[cc] = z[n0 + L0 / 2].r[cc];
   }
   const float s = rsqrtf(float(L0));
   TT* __restrict__ Tre = reinterpret_cast<TT*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
