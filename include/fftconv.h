@@ -82,6 +82,8 @@ typedef struct {
   const uint8_t* keep[4]; /* host arrays of dims[j] bytes */
 } fftconv_sparsity_t;
 
+#define FFTCONV_MAX_ORDER 6
+
 typedef struct {
   int64_t N;                 /* input/output length per row                   */
   int64_t fft_size;          /* L                                             */
@@ -90,8 +92,11 @@ typedef struct {
   int32_t regime;            /* 1 fused single pass, 2 partial (chunked),
                                 3 multipass (outer L0-point passes + fused
                                 inner transform, Alg. 4)                     */
-  int32_t order;             /* Monarch order p of the complex transform      */
-  int32_t factors[4];        /* L = prod factors[0..order)                    */
+  int32_t order;             /* number of transform levels: order-2 Monarch
+                                (L1, L2) plus one per outer multipass level
+                                (Alg. 4), order <= FFTCONV_MAX_ORDER         */
+  int32_t factors[6];        /* L = prod factors[0..order), slowest level
+                                first (outer levels, then L1, L2)            */
   int32_t rows_per_tile;     /* batch rows one CTA work unit processes        */
   int64_t max_kernel_len;    /* largest K accepted by precompute_kf           */
   size_t table_bytes;        /* device bytes for fftconv_plan_upload          */
@@ -163,7 +168,12 @@ fftconv_status_t fftconv_gated_fwd(fftconv_plan_t plan, const void* d_u, const v
  * SMs).  d_kf: device k_f from fftconv_precompute_kf.  Ordered after earlier
  * work on `stream`; work queued on `stream` after this call sees h_y
  * complete.  stage_bytes >= fftconv_host_stage_size(plan, H, rows_per_chunk,
- * gated).  Errors as fftconv_fwd; FFTCONV_ERR_INVALID_ARG for a short stage. */
+ * gated).  Errors as fftconv_fwd; FFTCONV_ERR_INVALID_ARG for a short stage.
+ * Argument errors are reported before any copy is enqueued; a failure after
+ * that still orders `stream` after the copies already queued.  Concurrent
+ * calls from several host threads on one device are safe: the library's copy
+ * streams and events are per device, and each call holds that device's pipe
+ * lock while it enqueues (the calls' copies then run one after another). */
 fftconv_status_t fftconv_fwd_host(fftconv_plan_t plan, const void* h_u, const void* h_w, const void* h_v,
                                   const void* d_kf, void* h_y, int64_t B, int64_t H, int64_t rows_per_chunk,
                                   void* d_stage, size_t stage_bytes, fftconv_stream_t stream);
@@ -179,7 +189,7 @@ fftconv_status_t fftconv_host_stage_size(fftconv_plan_t plan, int64_t H, int64_t
  * the convolution as in fftconv_fwd_host.  h_w, h_v NULL = plain.  Result
  * equals the partial convolution of the full rows.  stage_bytes >=
  * fftconv_stream_stage_size(plan, B, H, gated).  FFTCONV_ERR_UNSUPPORTED for
- * non-partial plans. */
+ * non-partial plans.  Thread safety and error ordering as fftconv_fwd_host. */
 fftconv_status_t fftconv_fwd_stream(fftconv_plan_t plan, const void* h_u, const void* h_w, const void* h_v,
                                     const void* d_kf, void* h_y, int64_t B, int64_t H, int64_t N_total,
                                     void* d_stage, size_t stage_bytes, fftconv_stream_t stream);

@@ -213,24 +213,35 @@ def sparsity_fraction(dims, zeroed) -> float:
 
 
 def keep_masks_from_zero_counts(dims, zeroed):
-    """Per-dimension keep masks: index i of dim j kept iff i < d_j - a_j."""
+    """Per-dimension keep masks for the slicing `k_f[..., x:, ...] = 0` of
+    P:1036-1038: the zeroed entries of dim j are its TRAILING a_j entries
+    (indices >= d_j - a_j), the count reading A13(i) that reproduces
+    tab:sparsity_fraction.  Pinned by the hand-enumerated
+    golden masks in tests/golden/sparsity_masks.json."""
     return [np.arange(d) < (d - a) for d, a in zip(dims, zeroed)]
 
 
-def frequency_mask(dims, keeps) -> np.ndarray:
-    """0/1 mask over the length-L spectrum, L = prod(dims), digit grid slowest
-    first (A13(ii)); applied Hermitian-symmetrically m[f] = keep(f) or
-    keep((L - f) mod L) so the output stays real (A13(iii))."""
+def keep_set(dims, keeps) -> np.ndarray:
+    """keep(f) before the Hermitian closure: frequency f of the length-L
+    spectrum, L = prod(dims), written in the digit grid of the reshape
+    `k_f.reshape(d_0, d_1, ...)` (row-major: dim 0 is the SLOWEST
+    digit, A13(ii)), is kept iff every digit is kept in its dimension."""
     dims = [int(d) for d in dims]
     L = int(np.prod(dims))
-    f = np.arange(L)
-    def keep_of(idx):
-        ok = np.ones(L, dtype=bool)
-        rem = idx.copy()
-        for j in range(len(dims) - 1, -1, -1):
-            digit = rem % dims[j]
-            rem = rem // dims[j]
-            ok &= np.asarray(keeps[j], dtype=bool)[digit]
-        return ok
-    m = keep_of(f) | keep_of((L - f) % L)
+    ok = np.ones(L, dtype=bool)
+    rem = np.arange(L)
+    for j in range(len(dims) - 1, -1, -1):  # fastest digit first
+        digit = rem % dims[j]
+        rem = rem // dims[j]
+        ok &= np.asarray(keeps[j], dtype=bool)[digit]
+    return ok
+
+
+def frequency_mask(dims, keeps) -> np.ndarray:
+    """0/1 mask over the length-L spectrum: keep_set applied
+    Hermitian-symmetrically, m[f] = keep(f) or keep((L - f) mod L), so the
+    output stays real (A13(iii); the paper is silent on real output)."""
+    k = keep_set(dims, keeps)
+    L = k.size
+    m = k | k[(L - np.arange(L)) % L]
     return m.astype(np.float64)

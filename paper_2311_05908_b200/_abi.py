@@ -47,7 +47,7 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [
         ("N", ctypes.c_int64), ("fft_size", ctypes.c_int64), ("causal", ctypes.c_int32),
         ("dtype", ctypes.c_int32), ("regime", ctypes.c_int32), ("order", ctypes.c_int32),
-        ("factors", ctypes.c_int32 * 4), ("rows_per_tile", ctypes.c_int32),
+        ("factors", ctypes.c_int32 * 6), ("rows_per_tile", ctypes.c_int32),
         ("max_kernel_len", ctypes.c_int64), ("table_bytes", ctypes.c_size_t),
         ("kf_bytes_per_head", ctypes.c_size_t), ("workspace_bytes_per_head", ctypes.c_size_t),
         ("mask_fraction", ctypes.c_double), ("skip_fraction", ctypes.c_double),

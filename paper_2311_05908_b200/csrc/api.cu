@@ -361,7 +361,13 @@ extern "C" fftconv_status_t fftconv_host_stage_size(fftconv_plan_t p, int64_t H,
 
 namespace {
 // Per-device copy-in / copy-out streams and chunk events, created once.
+// The pipe's events are re-recorded by every call, so a call holds the
+// pipe's mutex for its whole enqueue sequence: a second host thread on the
+// same device cannot re-record computed[s] / start between another call's
+// record and wait (its copies queue behind the first call's on the same
+// copy streams).
 struct HostPipe {
+  std::mutex mu;
   cudaStream_t in = nullptr, out = nullptr;
   cudaEvent_t start = nullptr, done = nullptr;
   cudaEvent_t loaded[2] = {}, computed[2] = {}, freed[2] = {};
@@ -390,6 +396,13 @@ cudaError_t host_pipe(HostPipe** out) {
   *out = &hp;
   return cudaSuccess;
 }
+// A failed call still orders the caller's stream after every copy it queued,
+// so the caller may free its buffers once its stream has drained.
+fftconv_status_t drain_pipe(HostPipe* hp, cudaStream_t cs, fftconv_status_t st) {
+  if (cudaEventRecord(hp->done, hp->in) == cudaSuccess) cudaStreamWaitEvent(cs, hp->done, 0);
+  if (cudaEventRecord(hp->done, hp->out) == cudaSuccess) cudaStreamWaitEvent(cs, hp->done, 0);
+  return st;
+}
 }  // namespace
 
 extern "C" fftconv_status_t fftconv_fwd_host(fftconv_plan_t p, const void* h_u, const void* h_w, const void* h_v,
@@ -412,9 +425,14 @@ extern "C" fftconv_status_t fftconv_fwd_host(fftconv_plan_t p, const void* h_u, 
   size_t ws_bytes = 0;
   const size_t slot = slot_bytes(p, H, rc, gated, &ws_bytes);
   if (stage_bytes < 2 * slot) { set_last_error("fftconv_fwd_host: staging buffer too small"); return FFTCONV_ERR_INVALID_ARG; }
+  {  // every argument run_fwd checks, before any copy is enqueued (the staged pointers stand in for the chunk buffers)
+    fftconv_status_t chk = check_signal_args(p, fn, rc, H, {d_stage, d_kf});
+    if (chk != FFTCONV_OK) return chk;
+  }
   HostPipe* hp = nullptr;
   cudaError_t e = host_pipe(&hp);
   if (e != cudaSuccess) return cuda_fail(fn, e);
+  std::lock_guard<std::mutex> pipe_lock(hp->mu);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   // the pipeline starts after earlier work on the caller's stream
   if ((e = cudaEventRecord(hp->start, cs)) != cudaSuccess) return cuda_fail(fn, e);
@@ -445,7 +463,7 @@ extern "C" fftconv_status_t fftconv_fwd_host(fftconv_plan_t p, const void* h_u, 
     if ((e = cudaStreamWaitEvent(cs, hp->loaded[s], 0)) != cudaSuccess) return cuda_fail(fn, e);
     fftconv_status_t st = run_fwd(p, du, gated ? dw : nullptr, gated ? dv : nullptr, d_kf, dy, rows, H,
                                   ws_bytes ? dws : nullptr, stream, fn);
-    if (st != FFTCONV_OK) return st;
+    if (st != FFTCONV_OK) return drain_pipe(hp, cs, st);
     if ((e = cudaEventRecord(hp->computed[s], cs)) != cudaSuccess) return cuda_fail(fn, e);
     // copy out
     if ((e = cudaStreamWaitEvent(hp->out, hp->computed[s], 0)) != cudaSuccess) return cuda_fail(fn, e);
@@ -488,9 +506,14 @@ extern "C" fftconv_status_t fftconv_fwd_stream(fftconv_plan_t p, const void* h_u
   size_t ws_bytes = 0;
   const size_t slot = slot_bytes(p, H, B, gated, &ws_bytes);
   if (stage_bytes < 2 * slot) { set_last_error("fftconv_fwd_stream: staging buffer too small"); return FFTCONV_ERR_INVALID_ARG; }
+  {
+    fftconv_status_t chk = check_signal_args(p, fn, B, H, {d_stage, d_kf});
+    if (chk != FFTCONV_OK) return chk;
+  }
   HostPipe* hp = nullptr;
   cudaError_t e = host_pipe(&hp);
   if (e != cudaSuccess) return cuda_fail(fn, e);
+  std::lock_guard<std::mutex> pipe_lock(hp->mu);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   if ((e = cudaEventRecord(hp->start, cs)) != cudaSuccess) return cuda_fail(fn, e);
   if ((e = cudaStreamWaitEvent(hp->in, hp->start, 0)) != cudaSuccess) return cuda_fail(fn, e);
@@ -528,7 +551,7 @@ extern "C" fftconv_status_t fftconv_fwd_stream(fftconv_plan_t p, const void* h_u
     if ((e = cudaStreamWaitEvent(cs, hp->loaded[sl_i], 0)) != cudaSuccess) return cuda_fail(fn, e);
     fftconv_status_t st = run_fwd(p, du, gated ? dw : nullptr, gated ? dv : nullptr, d_kf, dy, B, H,
                                   ws_bytes ? dws : nullptr, stream, fn);
-    if (st != FFTCONV_OK) return st;
+    if (st != FFTCONV_OK) return drain_pipe(hp, cs, st);
     if ((e = cudaEventRecord(hp->computed[sl_i], cs)) != cudaSuccess) return cuda_fail(fn, e);
     if ((e = cudaStreamWaitEvent(hp->out, hp->computed[sl_i], 0)) != cudaSuccess) return cuda_fail(fn, e);
     // outputs s0 .. min(s0 + S, N_total) live at buffer columns C ..

@@ -44,8 +44,8 @@
 namespace fc {
 
 #ifdef FC_TRACE
-// experiment-only phase timestamps (CTA 0, warpgroup 0, warps 0 and 4)
-__device__ long long fc_trace_buf[2][64][24];
+// experiment-only phase timestamps (CTA 0, warpgroup 0, lane 0 of warps 0..7)
+__device__ long long fc_trace_buf[8][64][24];
 #endif
 
 // Shared-memory plan of the forward kernel: tables | per-warpgroup (k_f,
@@ -209,8 +209,8 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
   int trace_tile = 0;
   auto stamp = [&](int k) {
 #ifdef FC_TRACE
-    if (blockIdx.x == 0 && wg == 0 && (wtid == 0 || wtid == 128) && trace_tile < 64)
-      fc_trace_buf[wtid >> 7][trace_tile][k] = clock64();
+    if (blockIdx.x == 0 && wg == 0 && (wtid & 31) == 0 && trace_tile < 64)
+      fc_trace_buf[wtid >> 5][trace_tile][k] = clock64();
 #endif
   };
   int stage_no = 0;

@@ -842,6 +842,9 @@ static cudaError_t launch_mp_l0(const MpParams& prm, int pass, cudaStream_t s) {
       else mp_pass3_ola_kernel<L0, false, float, float><<<grid, 256, 0, s>>>(prm);
     }
   } else if (prm.partial) {
+    // pass 1 pairs windows (2p, 2p+1) of one row (a pair's second window
+    // reuses the first one's second half): needs an even window count
+    if (pass == 1 && !prm.win_hi_only && (prm.NC & 1)) return cudaErrorInvalidValue;
     launch_pass_m<L0, 1>(prm, pass, grid, s);
   } else {
     launch_pass_m<L0, 0>(prm, pass, grid, s);

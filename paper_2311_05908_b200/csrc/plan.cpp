@@ -445,7 +445,7 @@ extern "C" fftconv_status_t fftconv_plan_info(fftconv_plan_t p, fftconv_plan_inf
   info->order = p->order;
   if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
     int i = 0;
-    for (int l = 0; l < p->nlev && i < 2; ++l) info->factors[i++] = p->lev_L0[l];
+    for (int l = 0; l < p->nlev && i < FFTCONV_MAX_ORDER - 2; ++l) info->factors[i++] = p->lev_L0[l];
     info->factors[i++] = p->L1;
     info->factors[i++] = p->L2;
   } else {

@@ -104,11 +104,13 @@ class FFTConvPlan:
     def precompute_kf(self, k: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """k: (H, K) fp32 on device -> opaque k_f buffer (H * kf_bytes_per_head),
         written into `out` (from kf_buffer) when given."""
-        assert k.dtype == torch.float32 and k.is_cuda and k.dim() == 2
+        if not (isinstance(k, torch.Tensor) and k.dtype == torch.float32 and k.is_cuda and k.dim() == 2):
+            raise ValueError("k must be an (H, K) float32 CUDA tensor")
         k = k.contiguous()
         H, K = k.shape
         if out is not None:
-            assert out.numel() >= max(H, 1) * self.info.kf_bytes_per_head and out.data_ptr() % 16 == 0
+            if not (out.numel() * out.element_size() >= max(H, 1) * self.info.kf_bytes_per_head and out.data_ptr() % 16 == 0):
+                raise ValueError("kf out buffer too small or not 16-byte aligned")
             kf = out
         else:
             kf = _aligned_empty(max(H, 1) * self.info.kf_bytes_per_head, k.device, 16)
@@ -116,9 +118,49 @@ class FFTConvPlan:
         return kf
 
     def _check_sig(self, *ts):
+        """Signal tensors (B, H, N): plan dtype, contiguous, on one CUDA
+        device, all the same shape (the C ABI takes raw pointers: a mismatch
+        here would be an out-of-bounds device access there)."""
+        ref = None
         for t in ts:
-            assert t.is_cuda and t.dtype == self.dtype and t.is_contiguous() and t.dim() == 3
-            assert t.shape[-1] == self.info.N, (t.shape, self.info.N)
+            if t is None:
+                continue
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == self.dtype and t.is_contiguous()
+                    and t.dim() == 3 and t.shape[-1] == self.info.N):
+                raise ValueError(f"signal tensor must be a contiguous CUDA (B, H, {self.info.N}) {self.dtype} "
+                                 f"tensor, got {getattr(t, 'shape', None)} {getattr(t, 'dtype', None)}")
+            if ref is None:
+                ref = t
+            elif t.shape != ref.shape or t.device != ref.device:
+                raise ValueError(f"signal tensors disagree: {tuple(t.shape)}@{t.device} vs "
+                                 f"{tuple(ref.shape)}@{ref.device}")
+        return ref
+
+    def _check_kf(self, kf, H, device):
+        need = max(H, 1) * self.info.kf_bytes_per_head
+        if not (isinstance(kf, torch.Tensor) and kf.is_cuda and kf.device == device and kf.is_contiguous()):
+            raise ValueError("kf must be a contiguous CUDA buffer from precompute_kf on the signals' device")
+        if kf.numel() * kf.element_size() < need:
+            raise ValueError(f"kf holds {kf.numel() * kf.element_size()} bytes, {H} heads need {need}")
+
+    def _check_out(self, out, like, name="out"):
+        if out is None:
+            return torch.empty_like(like)
+        if not (isinstance(out, torch.Tensor) and out.shape == like.shape and out.dtype == like.dtype
+                and out.device == like.device and out.is_contiguous()):
+            raise ValueError(f"{name} must be a contiguous {like.dtype} tensor of shape {tuple(like.shape)} "
+                             f"on {like.device}")
+        return out
+
+    def _check_ws(self, ws, B, H, for_bwd, device):
+        need = self.workspace_bytes(B, H, for_bwd)
+        if ws is None:
+            return self.workspace(B, H, for_bwd, device=device)
+        if not (isinstance(ws, torch.Tensor) and ws.is_cuda and ws.device == device and ws.is_contiguous()):
+            raise ValueError("workspace must be a contiguous CUDA buffer on the signals' device")
+        if ws.numel() * ws.element_size() < need:
+            raise ValueError(f"workspace holds {ws.numel() * ws.element_size()} bytes, needs {need}")
+        return ws
 
     def workspace_bytes(self, B: int, H: int, for_bwd: bool = False) -> int:
         n = ctypes.c_size_t()
@@ -134,16 +176,20 @@ class FFTConvPlan:
     def fwd(self, u: torch.Tensor, kf: torch.Tensor, out: torch.Tensor | None = None, workspace=None) -> torch.Tensor:
         self._check_sig(u)
         B, H, _ = u.shape
-        y = torch.empty_like(u) if out is None else out
-        ws = workspace if workspace is not None else self.workspace(B, H, device=u.device)
+        self._check_kf(kf, H, u.device)
+        y = self._check_out(out, u)
+        ws = self._check_ws(workspace, B, H, False, u.device)
         _abi.check(_abi.lib().fftconv_fwd(self._h, _ptr(u), _ptr(kf), _ptr(y), B, H, _ptr(ws), _stream(u.device)))
         return y
 
     def gated_fwd(self, u, w, v, kf, out=None, workspace=None):
+        if w is None or v is None:
+            raise ValueError("gated_fwd needs both gates w and v")
         self._check_sig(u, w, v)
         B, H, _ = u.shape
-        y = torch.empty_like(u) if out is None else out
-        ws = workspace if workspace is not None else self.workspace(B, H, device=u.device)
+        self._check_kf(kf, H, u.device)
+        y = self._check_out(out, u)
+        ws = self._check_ws(workspace, B, H, False, u.device)
         _abi.check(_abi.lib().fftconv_gated_fwd(self._h, _ptr(u), _ptr(w), _ptr(v), _ptr(kf), _ptr(y), B, H,
                                                 _ptr(ws), _stream(u.device)))
         return y
@@ -153,11 +199,9 @@ class FFTConvPlan:
         """End-to-end forward from (pinned) host tensors through fftconv_fwd_host:
         batch rows are streamed through a device staging buffer with the
         copies of neighbouring chunks overlapping the convolution."""
-        for t in (u, w, v):
-            if t is not None:
-                assert not t.is_cuda and t.dtype == self.dtype and t.is_contiguous() and t.dim() == 3
+        self._check_host(u, w, v, out, n=self.info.N)
         B, H, N = u.shape
-        assert N == self.info.N
+        self._check_kf(kf, H, kf.device)
         out = torch.empty_like(u, pin_memory=u.is_pinned()) if out is None else out
         gated = w is not None
         n = ctypes.c_size_t()
@@ -172,10 +216,9 @@ class FFTConvPlan:
     def fwd_stream(self, u: torch.Tensor, kf: torch.Tensor, w=None, v=None, out=None, stage=None) -> torch.Tensor:
         """Partial plans: host rows (B, H, N_total) of any length streamed in
         segments of the plan's N through fftconv_fwd_stream."""
-        for t in (u, w, v):
-            if t is not None:
-                assert not t.is_cuda and t.dtype == self.dtype and t.is_contiguous() and t.dim() == 3
+        self._check_host(u, w, v, out)
         B, H, NT = u.shape
+        self._check_kf(kf, H, kf.device)
         out = torch.empty_like(u, pin_memory=u.is_pinned()) if out is None else out
         n = ctypes.c_size_t()
         _abi.check(_abi.lib().fftconv_stream_stage_size(self._h, B, H, int(w is not None), ctypes.byref(n)))
@@ -186,6 +229,20 @@ class FFTConvPlan:
         self._stage = stage
         return out
 
+    def _check_host(self, u, w, v, out, n=None):
+        """Host signal tensors: plan dtype, contiguous, CPU, one shape; both
+        gates or none."""
+        if (w is None) != (v is None):
+            raise ValueError("gated host calls need both w and v")
+        for t in (u, w, v, out):
+            if t is None:
+                continue
+            if not (isinstance(t, torch.Tensor) and not t.is_cuda and t.dtype == self.dtype and t.is_contiguous()
+                    and t.shape == u.shape and t.dim() == 3):
+                raise ValueError(f"host tensors must be contiguous CPU {self.dtype} tensors of shape {tuple(u.shape)}")
+        if n is not None and u.shape[-1] != n:
+            raise ValueError(f"row length {u.shape[-1]} != plan N {n}")
+
     def host_stage(self, H: int, rows_per_chunk: int = 8, gated: bool = False, device=None):
         n = ctypes.c_size_t()
         _abi.check(_abi.lib().fftconv_host_stage_size(self._h, H, rows_per_chunk, int(gated), ctypes.byref(n)))
@@ -193,8 +250,11 @@ class FFTConvPlan:
 
     def bwd(self, dy, u, kf, K, w=None, v=None):
         """Gradients of <y, dy>: returns du, dw, dv (None when ungated) and dk (H, K)."""
-        self._check_sig(dy, u)
+        if (w is None) != (v is None):
+            raise ValueError("bwd: the gated backward needs both w and v")
+        self._check_sig(dy, u, w, v)
         B, H, _ = u.shape
+        self._check_kf(kf, H, u.device)
         du = torch.empty_like(u)
         dw = torch.empty_like(u) if w is not None else None
         dv = torch.empty_like(u) if v is not None else None

@@ -53,6 +53,22 @@ def test_plan_validation(lib):
     assert lib.fftconv_last_error() is not None
 
 
+@pytest.mark.parametrize("N,fft,causal", [(1024, 2048, 1), (8192, 16384, 1), (1 << 15, 1 << 16, 1),
+                                          (1 << 20, 1 << 21, 1), (1 << 22, 1 << 23, 1), (1 << 23, 1 << 23, 0),
+                                          (1 << 20, 16384, 1)])
+def test_plan_info_factors_cover_L(lib, N, fft, causal):
+    """plan_info reports every level: prod(factors[:order]) == fft_size for
+    fused, one-level, recursive (up to three outer levels) and partial plans."""
+    from paper_2311_05908_b200 import _abi
+    rc, h = _plan(lib, N, fft, causal=causal)
+    assert rc == 0
+    info = _abi.PlanInfo()
+    assert lib.fftconv_plan_info(h, ctypes.byref(info)) == 0
+    assert 2 <= info.order <= len(info.factors)
+    assert int(np.prod([info.factors[i] for i in range(info.order)])) == fft
+    lib.fftconv_plan_destroy(h)
+
+
 def test_plan_info_and_calls_without_upload(lib):
     from paper_2311_05908_b200 import _abi
     rc, h = _plan(lib, 1024, 2048)

@@ -5,6 +5,7 @@ import pytest
 
 import synth
 from oracle import oracle as orc
+from parity import assert_parity, assert_parity_f32  # noqa: F401
 
 torch = pytest.importorskip("torch")
 
@@ -44,7 +45,7 @@ def test_bwd_parity(N, dtype, gated):
             assert got[key] is None
             continue
         assert np.all(np.isfinite(got[key])), key
-        assert _rel(got[key], ref[key]) < REL_L2, (key, _rel(got[key], ref[key]))
+        assert_parity(got[key], ref[key], str(key))
 
 
 @pytest.mark.gpu
@@ -68,7 +69,7 @@ def test_bwd_multilevel_parity(N, dtype, gated):
         if ref[key] is None:
             continue
         assert np.all(np.isfinite(got[key])), key
-        assert _rel(got[key], ref[key]) < REL_L2, (key, _rel(got[key], ref[key]))
+        assert_parity(got[key], ref[key], str(key))
 
 
 @pytest.mark.gpu
@@ -92,10 +93,10 @@ def test_bwd_cfg3_full_size_sampled():
     for h in rng.choice(H, 3, replace=False):
         sl = (slice(None), slice(h, h + 1), slice(None))
         ref = orc.conv_bwd(dy[sl], u[sl], k[h:h + 1].astype(np.float64), w=w[sl], v=v[sl])
-        assert _rel(got["dk"][h:h + 1], ref["dk"]) < REL_L2
+        assert_parity(got["dk"][h:h + 1], ref["dk"])
         for b in rng.choice(B, 3, replace=False):
             for key in ("du", "dw", "dv"):
-                assert _rel(got[key][b, h], ref[key][b, 0]) < REL_L2, (key, b, h)
+                assert_parity(got[key][b, h], ref[key][b, 0], str((key, b, h)))
 
 
 @pytest.mark.gpu
@@ -115,4 +116,4 @@ def test_bwd_circular_multipass(N):
     for key in ("du", "dw", "dv", "dk"):
         got = g[key].float().cpu().numpy().astype(np.float64)
         assert np.all(np.isfinite(got)), key
-        assert _rel(got, ref[key]) < REL_L2, (key, _rel(got, ref[key]))
+        assert_parity(got, ref[key], str(key))

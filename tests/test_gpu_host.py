@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 import synth
+from parity import assert_parity
 
 torch = pytest.importorskip("torch")
 
@@ -56,5 +57,4 @@ def test_fwd_stream_partial_long_rows(dtype, gated):
         ref = orc.conv_fwd(u, k.astype(np.float64))
     torch.cuda.synchronize()
     got = y.float().numpy().astype(np.float64)
-    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
-    assert rel < 2e-3, rel
+    assert_parity(got, ref)

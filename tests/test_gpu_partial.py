@@ -6,6 +6,7 @@ import pytest
 
 import synth
 from oracle import oracle as orc
+from parity import assert_parity, assert_parity_f32  # noqa: F401
 
 torch = pytest.importorskip("torch")
 REL_L2 = 2e-3
@@ -29,8 +30,7 @@ def test_partial_parity(N, L, K, dtype, gated):
     y = plan.gated_fwd(t(u), t(w), t(v), kf) if gated else plan.fwd(t(u), kf)
     got = y.float().cpu().numpy().astype(np.float64)
     ref = orc.conv_fwd(u, k.astype(np.float64), causal=True, w=w, v=v)
-    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
-    assert rel < REL_L2, rel
+    assert_parity(got, ref)
 
 
 @pytest.mark.gpu
@@ -51,7 +51,7 @@ def test_partial_cfg4_shape_sampled():
             ref.append(orc.direct_point(u[0, h], k[h].astype(np.float64), int(i)))
             got.append(y[0, h, i])
     got, ref = np.array(got), np.array(ref)
-    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < REL_L2
+    assert_parity(got, ref)
 
 
 @pytest.mark.gpu
@@ -80,8 +80,7 @@ def test_partial_backward(N, L, K, dtype, gated):
             continue
         got = g[key].float().cpu().numpy().astype(np.float64)
         assert np.all(np.isfinite(got)), key
-        rel = np.linalg.norm(got - ref[key]) / np.linalg.norm(ref[key])
-        assert rel < REL_L2, (key, rel)
+        assert_parity(got, ref[key], str(key))
 
 
 @pytest.mark.gpu
@@ -105,5 +104,4 @@ def test_partial_cfg4_backward_full_size_sampled():
         sl = (slice(None), slice(h, h + 1), slice(None))
         ref = orc.conv_bwd(dy[sl], u[sl], k[h:h + 1].astype(np.float64))
         for key, got in (("du", du[sl]), ("dk", dk[h:h + 1])):
-            rel = np.linalg.norm(got - ref[key]) / np.linalg.norm(ref[key])
-            assert rel < REL_L2, (key, h, rel)
+            assert_parity(got, ref[key], str((key, h)))

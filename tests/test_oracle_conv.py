@@ -134,6 +134,40 @@ def test_sparsity_fraction_table(golden_dir):
         assert int(np.floor(100 * S + 0.5)) == row["S_percent"], (row, S)
 
 
+def test_sparsity_masks_golden(golden_dir):
+    """keep_masks_from_zero_counts + keep_set + frequency_mask against masks
+    enumerated by hand from P:1035-1038 (tests/golden/sparsity_masks.json):
+    pins which entries are zeroed (trailing) and the digit order (dim 0
+    slowest)."""
+    g = json.load(open(os.path.join(golden_dir, "sparsity_masks.json")))
+    for case in g["cases"]:
+        dims, zeroed = case["dims"], case["zeroed"]
+        L = int(np.prod(dims))
+        keeps = orc.keep_masks_from_zero_counts(dims, zeroed)
+        got_keep = np.flatnonzero(orc.keep_set(dims, keeps)).tolist()
+        assert got_keep == case["keep"], (case, got_keep)
+        m = orc.frequency_mask(dims, keeps)
+        assert m.shape == (L,)
+        assert np.flatnonzero(m).tolist() == case["mask"], (case, np.flatnonzero(m).tolist())
+
+
+def test_sparsity_fraction_of_constructed_mask(golden_dir):
+    """tab:sparsity_fraction on the paper's own 32x32x32x64
+    grid of the 2M-length kernel: the kept fraction of the mask the
+    oracle BUILDS (keep(f) before the Hermitian closure) reproduces S for
+    all six printed rows."""
+    g = json.load(open(os.path.join(golden_dir, "sparsity_fraction.json")))
+    dims = g["dims"]
+    assert int(np.prod(dims)) == 1 << 21
+    for row in g["rows"]:
+        keep = orc.keep_set(dims, orc.keep_masks_from_zero_counts(dims, row["zeroed"]))
+        S = 1.0 - keep.mean()
+        assert int(np.floor(100 * S + 0.5)) == row["S_percent"], (row, S)
+        # the closure only adds mirror frequencies: kept set grows, never shrinks
+        m = orc.frequency_mask(dims, orc.keep_masks_from_zero_counts(dims, row["zeroed"]))
+        assert np.all(m[keep] == 1.0)
+
+
 def test_masked_conv_against_naive_dft():
     N = 16
     L = 2 * N
