@@ -54,8 +54,19 @@ WORKLOADS = {
 }
 for _n in (256, 512, 1024, 2048, 4096, 8192, 16384, 32768, 65536):
     WORKLOADS[f"sweep{_n}"] = _wl(f"sweep: causal fp16 conv B*H=49152 N={_n}", 64, 768, _n)
-for _n, _b in ((1 << 18, 16), (1 << 20, 4), (1 << 22, 1)):  # constant elements: B*H = 49152 * 65536 / N
-    WORKLOADS[f"sweep{_n}"] = _wl(f"sweep: causal fp16 conv B*H={_b * 768} N={_n}", _b, 768, _n)
+# constant elements (B*H = 49152 * 65536 / N) with B >= 8 (k_f is
+# fp32 per head, so B=1 rows would be dominated by k_f bytes)
+for _n, _b, _h in ((1 << 18, 16, 768), (1 << 20, 8, 384), (1 << 22, 8, 96)):
+    WORKLOADS[f"sweep{_n}"] = _wl(f"sweep: causal fp16 conv B={_b} H={_h} N={_n}", _b, _h, _n)
+# gated fp16 sweep points (B=64, H=768): cfg2's path at other N
+for _n in (256, 512, 2048, 4096, 8192, 16384):
+    WORKLOADS[f"gsweep{_n}"] = _wl(f"sweep: gated causal fp16 conv B*H=49152 N={_n}", 64, 768, _n, gated=True)
+# default sweep carried in the bench line (every regime of the metric)
+SWEEP = ["sweep256", "sweep512", "sweep1024", "sweep2048", "sweep4096", "sweep8192", "sweep16384",
+         "sweep32768", "sweep65536", "sweep262144", "sweep1048576", "sweep4194304",
+         "gsweep2048", "gsweep8192", "cfg3", "cfg4", "cfg4bwd", "cfg5", "cfg5dense", "circ1024", "circ16384"]
+# row-sharded fixed problems (--shard): SURVEY 8(e)
+SHARD = {"cfg4": "cfg4", "cfg5b": "cfg5b"}
 # the paper's circular forward table (FFT size = input length, B=64, H=768)
 for _n, _b in ((512, 64), (1024, 64), (4096, 64), (16384, 64), (65536, 64), (1 << 18, 16), (1 << 20, 4),
                (1 << 22, 1)):
@@ -307,6 +318,232 @@ def torch_fft_baseline(wl, u, w, v, k, dy, steps, mask=None):
     return e0.elapsed_time(e1) / steps, torch.cuda.max_memory_allocated() - base
 
 
+class Run:
+    """One workload set up on one device: plan, resident inputs, k_f buffer,
+    workspaces and the conv closure (fwd [+ bwd]) through the C ABI."""
+
+    def __init__(self, wl, dev, rank=0, h_range=None, seed_rank=0):
+        import torch
+
+        import synth
+        from paper_2311_05908_b200 import FFTConvPlan, _abi
+        from paper_2311_05908_b200.fftconv import _ptr, _stream
+        self.wl, self.dev = wl, dev
+        B, H, N, K, L = wl["B"], wl["H"], wl["N"], wl["K"], wl["fft"]
+        h0, h1 = h_range if h_range is not None else (0, H)
+        self.Hl = Hl = h1 - h0
+        self.tdt = tdt = {"f16": torch.float16, "bf16": torch.bfloat16}[wl["dtype"]]
+        self.plan = plan = FFTConvPlan(N, fft_size=L, dtype=tdt, causal=wl["causal"], device=dev,
+                                       sparsity=sparsity_spec(wl["sparse"], L))
+
+        def sig(name):
+            if h_range is None:  # this rank's own B x H rows (weak scaling)
+                return synth.signal_torch(0, name, B, H, N, dev, tdt, row0=rank * B * H)
+            # head shard of the global problem: rows b * H + h, h in [h0, h1)
+            return torch.cat([synth.signal_torch(0, name, 1, Hl, N, dev, tdt, row0=b * H + h0) for b in range(B)])
+
+        self.u = sig("u")
+        self.w = sig("w") if wl["gated"] else None
+        self.v = sig("v") if wl["gated"] else None
+        self.dy = sig("dy") if wl["bwd"] else None
+        kfull = synth.decay_filters_torch(seed_rank, H, K, dev)
+        self.k = kfull[h0:h1].contiguous()
+        self.y = torch.empty_like(self.u)
+        self.ws_f = plan.workspace(B, Hl, device=dev)
+        self.ws_b = plan.workspace(B, Hl, for_bwd=True, device=dev) if wl["bwd"] else None
+        self.grads = None
+        if wl["bwd"]:
+            u = self.u
+            self.grads = dict(du=torch.empty_like(u), dw=torch.empty_like(u) if self.w is not None else None,
+                              dv=torch.empty_like(u) if self.v is not None else None,
+                              dk=torch.empty(Hl, K, dtype=torch.float32, device=dev))
+        self.kfb = plan.kf_buffer(Hl, dev)  # reused every step (N = 4M: 64 MB of fp32 k_f per head)
+        self._abi, self._ptr, self._stream = _abi, _ptr, _stream
+
+    def kf(self, k=None):
+        return self.plan.precompute_kf(self.k if k is None else k, out=self.kfb)
+
+    def conv(self, kf, uu=None, ww=None, vv=None, out=None):
+        wl, plan, B, K = self.wl, self.plan, self.wl["B"], self.wl["K"]
+        uu = self.u if uu is None else uu
+        ww = self.w if ww is None else ww
+        vv = self.v if vv is None else vv
+        out = self.y if out is None else out
+        if wl["gated"]:
+            plan.gated_fwd(uu, ww, vv, kf, out=out, workspace=self.ws_f)
+        else:
+            plan.fwd(uu, kf, out=out, workspace=self.ws_f)
+        if wl["bwd"]:
+            g, p = self.grads, self._ptr
+            self._abi.check(self._abi.lib().fftconv_bwd(
+                plan._h, p(self.dy), p(uu), p(ww), p(vv), p(kf), p(g["du"]), p(g["dw"]), p(g["dv"]), p(g["dk"]),
+                B, self.Hl, K, p(self.ws_b), self._stream(self.dev)))
+
+    def time(self, steps, warmup, world=1, clock_index=0):
+        """W untimed steps, then S timed steps of precompute_kf + conv with
+        CUDA events on the launching stream; returns (step ms, conv ms,
+        launches, clocks), each the max over ranks."""
+        import torch
+        import torch.distributed as dist
+        from paper_2311_05908_b200 import launch_count_reset
+        for _ in range(warmup):
+            self.conv(self.kf())
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev_s = torch.cuda.Event(enable_timing=True)
+        ev_e = torch.cuda.Event(enable_timing=True)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        launch_count_reset()
+        with ClockSampler(clock_index) as clk:
+            torch.cuda.synchronize()
+            ev_s.record()
+            for i in range(steps):
+                kf = self.kf()
+                ev[i][0].record()
+                self.conv(kf)
+                ev[i][1].record()
+            ev_e.record()
+            torch.cuda.synchronize()
+        launches = launch_count_reset()
+        if world > 1:
+            dist.barrier()
+        total_ms = ev_s.elapsed_time(ev_e)
+        conv_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+        if world > 1:
+            t = torch.tensor([total_ms, conv_ms], device=self.dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total_ms, conv_ms = t.tolist()
+        return total_ms / steps, conv_ms, launches, clk.summary()
+
+    def release(self):
+        for name in ("u", "w", "v", "dy", "y", "ws_f", "ws_b", "grads", "kfb", "k", "plan"):
+            setattr(self, name, None)
+
+
+def roofline_of(wl, conv_ms, H_local, peaks, traffic=None):
+    """Algorithmic bytes of one conv call (16-bit I/O tensors +
+    fp32 k_f of the call's heads) over its measured time, and the governing
+    roofline (max of HBM bytes and the method's minimum tensor flops)."""
+    w2 = dict(wl)
+    w2["H"] = H_local
+    bytes_per_call = algorithmic_bytes(w2, H_local * wl["fft"] * 8)
+    achieved = bytes_per_call / (conv_ms * 1e-3) / 1e9
+    tflops = min_tensor_flops_per_row(wl) * wl["B"] * H_local
+    t_hbm = bytes_per_call / (peaks["hbm"] * 1e9)
+    t_tc = tflops / (peaks["tc"] * 1e12)
+    governing = {"bound": "hbm" if t_hbm >= t_tc else "tensor", "frac": max(t_hbm, t_tc) / (conv_ms * 1e-3),
+                 "min_tensor_flops_per_call": tflops, "tensor_peak_tflops": peaks["tc"]}
+    return {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm"], "traffic": traffic, "kernel_ms": conv_ms,
+            "algorithmic_bytes_per_launch": bytes_per_call, "peak_source": peaks["src"], "governing": governing}
+
+
+def _traffic(name):
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            return json.load(open(prof)).get(name, {}).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def run_sweep(names, dev, peaks, steps_small, steps_big, warmup):
+    """Every regime of the metric: per point seq/s of the step,
+    conv ms, roofline fraction on the same measured peak, clocks.  Launched
+    one after another on this GPU, each with its own inputs (> L2)."""
+    import torch
+    out = {}
+    for name in names:
+        wl = WORKLOADS[name]
+        try:
+            r = Run(wl, dev)
+            S = steps_small if wl["B"] * wl["H"] * wl["N"] <= (1 << 26) else steps_big
+            step_ms, conv_ms, launches, clocks = r.time(S, warmup, clock_index=dev.index or 0)
+            rf = roofline_of(wl, conv_ms, wl["H"], peaks, _traffic(name))
+            out[name] = {"workload": wl["name"], "seq_per_s": wl["B"] * wl["H"] / (step_ms * 1e-3),
+                         "ms_per_step": step_ms, "conv_ms": conv_ms, "frac": rf["frac"],
+                         "governing": rf["governing"]["bound"], "governing_frac": rf["governing"]["frac"],
+                         "algorithmic_bytes": rf["algorithmic_bytes_per_launch"], "traffic": rf["traffic"],
+                         "regime": {1: "fused", 2: "partial", 3: "multipass"}[r.plan.info.regime],
+                         "skip_fraction": r.plan.info.skip_fraction if wl["sparse"] else None,
+                         "steps": S, "gpu_launches": launches, "clocks": clocks}
+            if name in PAPER_SEQ_S:
+                out[name]["paper_h100_seq_per_s"] = PAPER_SEQ_S[name]
+            r.release()
+            del r
+        except torch.OutOfMemoryError as e:
+            out[name] = {"unavailable": f"out of memory: {e}"[:200]}
+        torch.cuda.empty_cache()
+    return out
+
+
+def run_shard(args, wl, dev, rank, world):
+    """one FIXED problem head-sharded over WORLD_SIZE ranks
+    (strong scaling; rows independent).  compute-only: every rank
+    convolves its resident shard; end-to-end: rank 0 holds the full (B, H,
+    N) tensors, NCCL scatters head shards (paper_2311_05908_b200.dist), each
+    rank convolves, NCCL gathers y back to rank 0.  Both timed on the device
+    with CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_05908_b200.dist import gather_heads, head_shard, scatter_heads
+    B, H, N = wl["B"], wl["H"], wl["N"]
+    h0, h1 = head_shard(H, rank, world)
+    r = Run(wl, dev, h_range=(h0, h1))
+    step_ms, conv_ms, launches, clocks = r.time(args.steps, args.warmup, world, dev.index or 0)
+    # end to end from rank 0's device tensors
+    full = {}
+    if rank == 0:
+        import synth
+        for name in ("u", "w", "v"):
+            if name == "u" or wl["gated"]:
+                full[name] = synth.signal_torch(0, name, B, H, N, dev, r.tdt)
+    def e2e_once():
+        parts = {name: scatter_heads(full.get(name), H, (B, N), r.tdt, dev) for name in ("u", "w", "v")
+                 if name == "u" or wl["gated"]}
+        kf = r.kf()
+        r.conv(kf, parts["u"], parts.get("w"), parts.get("v"), r.y)
+        return gather_heads(r.y, H)
+    for _ in range(2):
+        e2e_once()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    E = max(3, min(args.steps, 10))
+    e0.record()
+    for _ in range(E):
+        e2e_once()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / E], device=dev)
+    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = e2e_ms.item()
+    if rank == 0:
+        peaks = load_peaks()
+        rf = roofline_of(wl, conv_ms, h1 - h0, peaks)
+        moved = B * H * N * 2 * ((3 if wl["gated"] else 1) + 1)
+        out = {
+            "metric": METRIC, "value": B * H / (step_ms * 1e-3), "unit": "sequences/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic",
+            "config": {"workload": wl["name"] + f" -- fixed problem, heads sharded over {world} GPU(s)",
+                       "B": B, "H": H, "N": N, "K": wl["K"], "fft_size": wl["fft"],
+                       "heads_per_rank": [b - a for a, b in (head_shard(H, q, world) for q in range(world))],
+                       "parallelism": f"head-sharded x{world}, NCCL scatter/gather only outside the conv"},
+            "roofline": dict(rf, note="rank 0's shard (its heads, all B)"),
+            "compute_only": {"value": B * H / (step_ms * 1e-3), "ms_per_step": step_ms, "conv_ms": conv_ms,
+                             "note": "resident shards (inputs generated on each rank), precompute_kf + conv"},
+            "e2e": {"value": B * H / (e2e_ms * 1e-3), "unit": "sequences/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0, "nccl_bytes_per_step": moved,
+                    "path": "rank 0 device tensors -> NCCL scatter (u[, w, v]) -> conv -> NCCL gather (y)"},
+            "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -317,9 +554,13 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-torch-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the per-regime sweep object")
+    ap.add_argument("--sweep", default=None, help="comma-separated sweep workloads (default: SWEEP)")
+    ap.add_argument("--shard", default=None, choices=sorted(SHARD),
+                    help="fixed problem head-sharded over WORLD_SIZE ranks (strong scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    wl = WORKLOADS[args.workload]
+    wl = WORKLOADS[args.shard or args.workload]
     if args.steps is None:
         args.steps = 500 if wl["B"] * wl["H"] * wl["N"] <= (1 << 26) else 40
 
@@ -334,77 +575,23 @@ def main():
     import torch
     import torch.distributed as dist
 
-    import synth
-    from paper_2311_05908_b200 import FFTConvPlan, launch_count_reset
-
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 or args.shard:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    if args.shard:
+        run_shard(args, wl, dev, rank, world)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
 
     B, H, N, K, L = wl["B"], wl["H"], wl["N"], wl["K"], wl["fft"]
-    tdt = {"f16": torch.float16, "bf16": torch.bfloat16}[wl["dtype"]]
-    plan = FFTConvPlan(N, fft_size=L, dtype=tdt, causal=wl["causal"], device=dev,
-                       sparsity=sparsity_spec(wl["sparse"], L))
-    row0 = rank * B * H  # this rank's rows of the global problem (weak scaling)
-    u = synth.signal_torch(0, "u", B, H, N, dev, tdt, row0=row0)
-    w = synth.signal_torch(0, "w", B, H, N, dev, tdt, row0=row0) if wl["gated"] else None
-    v = synth.signal_torch(0, "v", B, H, N, dev, tdt, row0=row0) if wl["gated"] else None
-    dy = synth.signal_torch(0, "dy", B, H, N, dev, tdt, row0=row0) if wl["bwd"] else None
-    k = synth.decay_filters_torch(rank, H, K, dev)
-    y = torch.empty_like(u)
-    ws_f = plan.workspace(B, H, device=dev)
-    ws_b = plan.workspace(B, H, for_bwd=True, device=dev) if wl["bwd"] else None
-    grads = None
-    if wl["bwd"]:
-        grads = dict(du=torch.empty_like(u), dw=torch.empty_like(u) if w is not None else None,
-                     dv=torch.empty_like(u) if v is not None else None,
-                     dk=torch.empty(H, K, dtype=torch.float32, device=dev))
-
-    from paper_2311_05908_b200 import _abi
-    from paper_2311_05908_b200.fftconv import _ptr, _stream
-
-    def conv(kf, uu, ww, vv, out):
-        if wl["gated"]:
-            plan.gated_fwd(uu, ww, vv, kf, out=out, workspace=ws_f)
-        else:
-            plan.fwd(uu, kf, out=out, workspace=ws_f)
-        if wl["bwd"]:
-            _abi.check(_abi.lib().fftconv_bwd(
-                plan._h, _ptr(dy), _ptr(uu), _ptr(ww), _ptr(vv), _ptr(kf), _ptr(grads["du"]), _ptr(grads["dw"]),
-                _ptr(grads["dv"]), _ptr(grads["dk"]), B, H, K, _ptr(ws_b), _stream(dev)))
-
-    kfb = plan.kf_buffer(H, dev)  # reused every step (N = 4M: 64 MB of fp32 k_f per head)
-    for _ in range(args.warmup):
-        conv(plan.precompute_kf(k, out=kfb), u, w, v, y)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    run = Run(wl, dev, rank=rank, seed_rank=rank)
+    plan, u, w, v, dy, k, y = run.plan, run.u, run.w, run.v, run.dy, run.k, run.y
     S = args.steps
-    ev_s = torch.cuda.Event(enable_timing=True)
-    ev_e = torch.cuda.Event(enable_timing=True)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
-    launch_count_reset()
-    with ClockSampler(local_rank) as clk:
-        torch.cuda.synchronize()
-        ev_s.record()
-        for i in range(S):
-            kf = plan.precompute_kf(k, out=kfb)
-            ev[i][0].record()
-            conv(kf, u, w, v, y)
-            ev[i][1].record()
-        ev_e.record()
-        torch.cuda.synchronize()
-    launches = launch_count_reset()
-    if world > 1:
-        dist.barrier()
-    total_ms = ev_s.elapsed_time(ev_e)
-    conv_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
-    if world > 1:
-        t = torch.tensor([total_ms, conv_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, conv_ms = t.tolist()
-    step_ms = total_ms / S
+    step_ms, conv_ms, launches, clocks = run.time(S, args.warmup, world, local_rank)
     value = world * B * H / (step_ms * 1e-3)
 
     # ---------------- end-to-end through the public API with pinned host buffers
@@ -424,7 +611,7 @@ def main():
     d2h = hy.numel() * hy.element_size()
     if wl["bwd"]:
         hdu = torch.empty(u.shape, dtype=u.dtype, pin_memory=True)
-        d2h += hdu.numel() * hdu.element_size() + grads["dk"].numel() * 4
+        d2h += hdu.numel() * hdu.element_size() + run.grads["dk"].numel() * 4
 
     # forward workloads with B >= 2 go through fftconv_fwd_host: batch chunks
     # streamed through a device staging buffer, copies overlapping the conv
@@ -433,18 +620,18 @@ def main():
     def e2e_step():
         if use_host_api:
             dbuf["k"].copy_(hbuf["k"], non_blocking=True)
-            kf = plan.precompute_kf(dbuf["k"], out=kfb)
+            kf = run.kf(dbuf["k"])
             plan.fwd_host(hbuf["u"], kf, w=hbuf.get("w"), v=hbuf.get("v"), out=hy, rows_per_chunk=rpc, stage=stage)
             return
         for name, t in dbuf.items():
             t.copy_(hbuf[name], non_blocking=True)
         if dy is not None:
             dy.copy_(hbuf["dy"], non_blocking=True)
-        kf = plan.precompute_kf(dbuf["k"], out=kfb)
-        conv(kf, dbuf["u"], dbuf.get("w"), dbuf.get("v"), y)
+        kf = run.kf(dbuf["k"])
+        run.conv(kf, dbuf["u"], dbuf.get("w"), dbuf.get("v"), y)
         hy.copy_(y, non_blocking=True)
         if wl["bwd"]:
-            hdu.copy_(grads["du"], non_blocking=True)
+            hdu.copy_(run.grads["du"], non_blocking=True)
 
     E = max(3, args.e2e_steps) if args.e2e_steps > 0 else 0  # 0: no e2e leg (profiling runs)
     for _ in range(2 if E else 0):
@@ -467,32 +654,26 @@ def main():
 
     if rank == 0:
         peaks = load_peaks()
-        bytes_per_call = algorithmic_bytes(wl, H * L * 8)
-        achieved = bytes_per_call / (conv_ms * 1e-3) / 1e9
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(prof):
-            try:
-                traffic = json.load(open(prof)).get(args.workload, {}).get("dram_bytes_per_launch")
-            except Exception:
-                traffic = None
+        rf = roofline_of(wl, conv_ms, H, peaks, _traffic(args.workload))
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             rate, cores, sample, _, _, _ = oracle_rows_per_s(wl)
-            cpu = {"value": rate, "unit": "sequences/s", "cores": cores, "kind": "oracle", "sample": sample}
-        # governing roofline = max(bytes / BW, min tensor flops / peak)
-        tflops = min_tensor_flops_per_row(wl) * B * H
-        t_hbm = bytes_per_call / (peaks["hbm"] * 1e9)
-        t_tc = tflops / (peaks["tc"] * 1e12)
-        governing = {"bound": "hbm" if t_hbm >= t_tc else "tensor", "frac": max(t_hbm, t_tc) / (conv_ms * 1e-3),
-                     "min_tensor_flops_per_call": tflops, "tensor_peak_tflops": peaks["tc"],
-                     "note": "fraction of the governing roofline (HBM bytes vs the method's minimum Monarch "
-                             "tensor flops, p <= 4, SURVEY 8(d))"}
+            cpu = {"value": rate, "unit": "sequences/s", "cores": cores, "kind": "oracle", "sample": sample,
+                   "cpu_model": _cpu_model()}
+            try:  # the same oracle on one core
+                from oracle import oracle as orc
+                nt = orc.num_threads()
+                orc.set_num_threads(1)
+                r1, _, s1, _, _, _ = oracle_rows_per_s(wl, target_s=4.0)
+                orc.set_num_threads(nt)
+                cpu["one_core"] = {"value": r1, "unit": "sequences/s", "sample": s1}
+            except Exception as e:  # pragma: no cover
+                cpu["one_core"] = {"unavailable": str(e)[:200]}
         vs = PAPER_SEQ_S.get(args.workload)
         regime = {1: "fused", 2: "partial (overlap-save, multipass)", 3: "multipass"}[plan.info.regime]
         # device memory of this library for the step vs the cuFFT+PyTorch reference (NEXT-3)
-        lib_bytes = kfb.numel() + (ws_f.numel() if ws_f is not None else 0) + (ws_b.numel() if ws_b is not None else 0)
-        lib_bytes += plan.info.table_bytes
+        lib_bytes = run.kfb.numel() + (run.ws_f.numel() if run.ws_f is not None else 0) \
+            + (run.ws_b.numel() if run.ws_b is not None else 0) + plan.info.table_bytes
         tb = None
         if not args.no_torch_baseline:
             spec = B * H * (max(L, 2 * N) // 2 + 1) * 8  # one complex64 spectrum of the batch
@@ -508,6 +689,10 @@ def main():
                     tb = {"value": None, "unavailable": "out of memory"}
             else:
                 tb = {"value": None, "unavailable": "would not fit beside this run's buffers"}
+        rf["kernel"] = ("conv call (fftconv_fwd_o2_kernel" + (" + multipass outer passes" if plan.info.regime != 1 else "")
+                        + (" + bwd" if wl["bwd"] else "") + ")")
+        rf["governing"]["note"] = ("fraction of the governing roofline (HBM bytes vs the method's minimum Monarch "
+                                   "tensor flops, p <= 4, SURVEY 8(d))")
         out = {
             "metric": METRIC, "value": value, "unit": "sequences/s", "n_gpus": world, "steps": S,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
@@ -520,16 +705,9 @@ def main():
             "config": {"workload": wl["name"], "B": B, "H": H, "N": N, "K": K, "fft_size": L, "gated": wl["gated"],
                        "causal": wl["causal"], "backward": wl["bwd"], "regime": regime,
                        "step": "precompute_kf + conv" + (" fwd+bwd" if wl["bwd"] else " fwd"),
-                       "l2": f"inputs larger than L2 ({bytes_per_call / 1e6:.0f} MB per step)",
+                       "l2": f"inputs larger than L2 ({rf['algorithmic_bytes_per_launch'] / 1e6:.0f} MB per step)",
                        "parallelism": f"rows sharded, {world} GPU(s), no data-path collective"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm"], "traffic": traffic,
-                         "kernel": "conv call (fftconv_fwd_o2_kernel"
-                                   + (" + multipass outer passes" if plan.info.regime != 1 else "")
-                                   + (" + bwd" if wl["bwd"] else "") + ")",
-                         "kernel_ms": conv_ms, "algorithmic_bytes_per_launch": bytes_per_call,
-                         "peak_source": peaks["src"],
-                         "governing": governing},
+            "roofline": rf,
             "cpu_baseline": cpu,
             "cufft_baseline": tb,
             "memory": {"library_device_bytes": int(lib_bytes),
@@ -539,12 +717,30 @@ def main():
                     "path": (f"fftconv_fwd_host, {(B + rpc - 1) // rpc} chunks of {rpc} batch rows, copies overlapped"
                              if use_host_api else "device copies around fftconv calls")},
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
+    # ---------------- every regime of the metric, same run (rank 0's GPU; N=1 only)
+    if world == 1 and not args.no_sweep:
+        run.release()
+        del run, plan, u, w, v, dy, k, y, hbuf, dbuf, stage
+        torch.cuda.empty_cache()
+        names = args.sweep.split(",") if args.sweep else SWEEP
+        out["sweep"] = run_sweep(names, dev, load_peaks(), steps_small=30, steps_big=5, warmup=3)
+    if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 if __name__ == "__main__":

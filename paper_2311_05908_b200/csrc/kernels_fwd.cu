@@ -48,6 +48,10 @@ namespace fc {
 __device__ long long fc_trace_buf[8][64][24];
 #endif
 
+#ifndef FC_NEG_B
+#define FC_NEG_B 0
+#endif
+
 // Shared-memory plan of the forward kernel: tables | per-warpgroup (k_f,
 // operand buffer) | staging.  Causal tiles move their rows with bulk (TMA)
 // copies through two slots shared by the warpgroups in tile order: the
@@ -57,20 +61,51 @@ template <int L1, bool CAUSAL, bool GATED>
 struct FwdCfg {
   using C = O2Cfg<L1, CAUSAL>;
   static constexpr bool STG = CAUSAL;
+  // Stage B / B^-1 N: re | im only (the negated plane the complex multiply
+  // needs is a sign folded into the f32x2 multiplies); FC_NEG_B=1 has the
+  // tensor core emit it as a third block of the G_B table instead.
+  static constexpr int NBF = FC_NEG_B ? C::NB : (2 * L1 + 15) / 16 * 16;
+  // The forward's shared-memory table layout is a compacted copy of the
+  // plan image: G_A | G_B, G_B^-1 (only the NBF rows the forward reads) |
+  // G_A^-1 (causal: rows n2 < L2/2 only).  Twiddles are not stored: they
+  // are computed on the fly (MUFU sin/cos, fp32 recurrences).
+  static constexpr uint32_t GB_SM = uint32_t(NBF) * (2 * L1) * 2;
+  static constexpr uint32_t S_GA = 0;
+  static constexpr uint32_t S_GB = C::al(S_GA + C::GA_BYTES);
+  static constexpr uint32_t S_GBI = C::al(S_GB + GB_SM);
+  static constexpr uint32_t S_GAI = C::al(S_GBI + GB_SM);
+  static constexpr uint32_t TABLES = C::al(S_GAI + C::GAI_FWD_BYTES);
   static constexpr uint32_t ROW_BYTES = C::NOUT * 2;  // one 16-bit input row
   static constexpr uint32_t UW_BYTES = STG ? C::R * ROW_BYTES * (GATED ? 2 : 1) : 0;
   static constexpr uint32_t V_BYTES = STG ? C::R * ROW_BYTES : 0;
+  // circular plain tiles (the multipass inner pass): y staging shared by
+  // the warpgroups in tile order, leaving by one TMA tensor store each
+  static constexpr uint32_t YS_BYTES = (!CAUSAL && !GATED) ? C::R * C::NOUT * 2 : 0;
   static constexpr uint32_t bytes_for(int wg) {
-    return C::al(C::al(C::TABLES_FWD + wg * C::WG_BYTES) + UW_BYTES) + V_BYTES + 1024;  // + alignment slack
+    return C::al(C::al(C::al(TABLES + wg * C::WG_BYTES) + UW_BYTES) + V_BYTES) + YS_BYTES + 1024;  // + alignment slack
   }
   static constexpr int WG = bytes_for(2) <= 227 * 1024 ? 2 : 1;
   static constexpr int THREADS = WG * kWGThreads;
-  static constexpr uint32_t OFF_WG = C::TABLES_FWD;
+  static constexpr uint32_t OFF_WG = TABLES;
   static constexpr uint32_t OFF_UW = C::al(OFF_WG + WG * C::WG_BYTES);
   static constexpr uint32_t OFF_V = C::al(OFF_UW + UW_BYTES);
+  static constexpr uint32_t OFF_YS = C::al(OFF_V + V_BYTES);
   static constexpr uint32_t SMEM = bytes_for(WG);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert(GB_SM <= C::GB_BYTES, "G_B prefix");
 };
+
+// W_L^e = exp(-2 pi i e / L) (e reduced mod L to (-L/2, L/2]) with the
+// MUFU sin/cos: absolute error <= 2^-21.4 on [-pi, pi] (CUDA math API),
+// far below the fp16 operand rounding (2^-11) every stage applies.
+template <int L>
+FC_DEVICE float2 wroot(int e) {
+  e &= (L - 1);
+  if (e > L / 2) e -= L;
+  float sn, cs;
+  __sincosf(float(e) * (-6.28318530717958647692f / float(L)), &sn, &cs);
+  return make_float2(cs, sn);
+}
 
 // Each CTA runs kWG independent warpgroups; warpgroup g processes tiles
 // t0 + g, t0 + g + kWG, ... of the CTA's contiguous tile range, with its own
@@ -85,22 +120,17 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
   constexpr bool STG = F::STG;      // input staging by bulk copies
   constexpr int L2 = C::L2;
   constexpr bool TS = C::TS_BI;     // stage B^-1 data operand in TMEM
-#ifndef FC_NEG_B
-#define FC_NEG_B 0
-#endif
-  // Stage B / B^-1 N: re | im only (the negated plane the complex multiply
-  // needs is a sign folded into the f32x2 multiplies); FC_NEG_B=1 has the
-  // tensor core emit it as a third block of the G_B table instead.
-  constexpr int NBF = FC_NEG_B ? C::NB : (2 * L1 + 15) / 16 * 16;
+  constexpr int NBF = F::NBF;
   constexpr bool M64 = CAUSAL;      // stage A^-1 as M = 64 MMAs (rows n2 < L2/2 only)
 
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t mma_bar[kWG][2];  // completion of the first / second half of a stage
   __shared__ uint64_t stg_bar[2][2];   // [u|w slot, v slot][consuming warpgroup]: bulk copy landed
+  __shared__ uint64_t ys_bar;          // circular TMA-y staging: use j - 1 has been read (phase j - 1)
   __shared__ uint32_t tmem_slot;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;  // 1024-aligned
-  const uint32_t sGA = base + C::OFF_GA, sGB = base + C::OFF_GB, sGBI = base + C::OFF_GBI,
-                 sGAI = base + C::OFF_GAI, sTW = base + C::OFF_TW;
+  const uint32_t sGA = base + F::S_GA, sGB = base + F::S_GB, sGBI = base + F::S_GBI, sGAI = base + F::S_GAI;
+  const uint32_t sYS = base + F::OFF_YS;
   const uint32_t sUW = base + F::OFF_UW, sV = base + F::OFF_V;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -111,6 +141,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
   const int m = quad * 32 + lane;        // TMEM lane / MMA row owned by this thread
   const uint32_t sKF = base + F::OFF_WG + wg * C::WG_BYTES;
   const uint32_t bufX = sKF + C::al(C::KF_BYTES);
+  const uint32_t sY = bufX + C::BUFX_BYTES / 2;  // causal: y rows staged for the bulk stores
   const int64_t B = prm.B, H = prm.H, N = prm.N;
   const int64_t nbt = (B + C::R - 1) / C::R;
   const int64_t Hi = prm.row_map ? (H / prm.row_L0) * prm.nrow : H;  // heads iterated
@@ -130,7 +161,13 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
   // ---- one-time setup: tables -> smem, barriers, TMEM (both warpgroups)
   {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.tables);
-    for (uint32_t o = tid * 16; o < C::TABLES_FWD; o += kThreads * 16) cp_async16(base + o, src + o, true);
+    auto seg = [&](uint32_t dst, uint32_t img_off, uint32_t bytes) {
+      for (uint32_t o = tid * 16; o < bytes; o += kThreads * 16) cp_async16(base + dst + o, src + img_off + o, true);
+    };
+    seg(F::S_GA, C::OFF_GA, C::GA_BYTES);
+    seg(F::S_GB, C::OFF_GB, F::GB_SM);
+    seg(F::S_GBI, C::OFF_GBI, F::GB_SM);
+    seg(F::S_GAI, C::OFF_GAI, C::GAI_FWD_BYTES);
     cp_async_commit();
   }
   if (tid == 0) {
@@ -140,6 +177,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
       mbar_init(&stg_bar[0][g], 1);
       mbar_init(&stg_bar[1][g], 1);
     }
+    mbar_init(&ys_bar, 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<(kWG * C::TMEM_COLS > 512 ? 512 : kWG * C::TMEM_COLS)>(&tmem_slot);
@@ -250,10 +288,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
   // Twiddle-recurrence constants (tables are resident after the setup sync):
   // epilogue 1 steps k2 by 2 at fixed n1 (W^{2 n1}); epilogue 3 steps n1 at
   // fixed k2 (W^{k2}, W^{2 k2}) for the thread's two k2 (group parity).
-  auto tw_at = [&](int n1, int k2) {  // W_L^{n1 k2} from TW
-    const float4 a = ld_shared_f4(sTW + tab_off<L2 / 2>(n1, k2 >> 1));
-    return (k2 & 1) ? make_float2(a.y, a.w) : make_float2(a.x, a.z);
-  };
+  auto tw_at = [&](int n1, int k2) { return wroot<C::L>(n1 * k2); };  // W_L^{n1 k2}
   const float2 tw1_c2 = tw_at(n1A, 2);
   float4 tw3_c[2];
 #pragma unroll
@@ -367,6 +402,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
 
   int64_t hh = (t0 + wg) / nbt, bt = (t0 + wg) % nbt;
   bool loaded = false;  // the tile's operand was stored by the previous tile's epilogue 4
+  bool ys_pending = false;  // (wtid 0) a TMA store of y from sYS is in flight
   for (int64_t t = t0 + wg; t < t1; t += kWG, bt += kWG) {
     while (bt >= nbt) { bt -= nbt; ++hh; }
     stage_no = 0;
@@ -391,6 +427,17 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
     }
     stamp(1);
 
+    // the previous tile's y rows leave from bufX's second half by bulk
+    // stores; epilogue 1 rewrites it, so they must have been read by then
+    // (the stage-A barrier below publishes this wait to the warpgroup)
+    if (STG && filler()) bulk_wait_read0();
+    // circular TMA-y tiles: hand the shared y staging to the next user once
+    // this warpgroup's previous tensor store has read it
+    if (ys_pending) {
+      bulk_wait_read0();
+      mbar_arrive(&ys_bar);
+      ys_pending = false;
+    }
     // ---------------- stage A: D[(p,n1)][(re|im|-im, k2)] = X[(p,n1)][(c,n2)] * G_A
     // TMEM column of (block, k2): (k2 / 32) * NA/2 + 32 * block + k2 % 32
     sync_and_issue([&](int h2) {  // half h2: k2 in [32 h2, 32 h2 + 32) of every block, one MMA per K step
@@ -424,14 +471,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         // W^{n1 k2}, k2 = k20 .. k20 + 15: the table pair at k20, then fp32
         // steps by W^{2 n1} (register recurrence instead of 8 table loads)
         float4 w[8];
-#ifndef FC_TW1_TABLE
-#define FC_TW1_TABLE 0
-#endif
-        if constexpr (FC_TW1_TABLE) {  // 8 conflict-free table reads
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) w[jj] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1A, k20 / 2 + jj));
-        } else {
-          w[0] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1A, k20 / 2));
+        {
+          const float2 a = tw_at(n1A, k20), b = tw_at(n1A, k20 + 1);
+          w[0] = make_float4(a.x, b.x, a.y, b.y);
 #pragma unroll
           for (int jj = 1; jj < 8; ++jj) w[jj] = cstep(w[jj - 1], tw1_c2);
         }
@@ -542,8 +584,8 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         // by W^{2 k2}
         float4 w[4];
         {
-          const float4 a = ld_shared_f4(sTW + tab_off<L2 / 2>(n1c * 8, k2 >> 1));
-          const float br = (k2 & 1) ? a.y : a.x, bi = (k2 & 1) ? a.w : a.z;
+          const float2 a = tw_at(n1c * 8, k2);
+          const float br = a.x, bi = a.y;
           const float4 c = tw3_c[gi & 1];  // {Re W^{k2}, Im W^{k2}, Re W^{2k2}, Im W^{2k2}}
           w[0] = make_float4(br, br * c.x - bi * c.y, bi, br * c.y + bi * c.x);
 #pragma unroll
@@ -591,6 +633,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
       using S = typename std::conditional<GATED, __half, T>::type;
       constexpr int OCH = C::R * C::NOUT / 8 / kWGThreads;  // coalesced output chunks per thread
       static_assert(!STAGE || C::R * C::NOUT * sizeof(S) <= C::BUFX_BYTES, "y staging fits in bufX");
+      static_assert(!STG || (C::R * C::NOUT * sizeof(S) <= C::BUFX_BYTES / 2 && C::R * F::ROW_BYTES <= C::BUFX_BYTES / 2 &&
+                             128 * 2 * C::KA * 2 <= C::BUFX_BYTES / 2),
+                    "causal: staged conv output, next stage-A operand and y rows share bufX by halves");
       constexpr int PER = OUT_COLS / 8;  // transposed 8-column items per thread
       constexpr int NV = STAGE ? OCH : PER;
       const bool has_next = t + kWG < t1;
@@ -621,32 +666,43 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
       wait_half(M64 ? 1 : slice ^ 1);  // bufX is rewritten below: both halves done
       stamp(15);
       if constexpr (STAGE) {
+        // circular plain tiles (the multipass inner pass): the staged tile
+        // leaves by one TMA tensor store from the y staging the warpgroups
+        // share in tile order (the store's read of it is awaited only before
+        // this warpgroup's next stage A); the staging layout is the 128 B
+        // swizzle of the {64, Lp/64, 1, R} box
+        const bool tma_out = F::YS_BYTES > 0 && prm.tma_y;
+        const uint32_t sstg = tma_out ? sYS : bufX;
+        if (tma_out && t > t0) mbar_wait(&ys_bar, uint32_t((t - t0 - 1) & 1));
+        // all of this thread's TMEM loads in flight before one wait (PER <= 8)
+        float ob[PER][8];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) tmem_ld8(tq + o_tcol + 8 * i, ob[i]);
+        tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
-          float o[8];
-          tmem_ld8(tq + o_tcol + 8 * i, o);
-          tmem_ld_wait();
+          const float* o = ob[i];
           int r, n;
           item_rn(i, r, n);
           const uint32_t off = uint32_t(r * C::NOUT + n) * sizeof(S);
-          st_shared_v4(bufX + swz128(off), IO<S>::pack2(o[0], o[1]), IO<S>::pack2(o[2], o[3]),
+          st_shared_v4(sstg + swz128(off), IO<S>::pack2(o[0], o[1]), IO<S>::pack2(o[2], o[3]),
                        IO<S>::pack2(o[4], o[5]), IO<S>::pack2(o[6], o[7]));
         }
         stamp(16);
-        // circular plain tiles (the multipass inner pass): the staged tile
-        // leaves by one TMA tensor store; the staging layout is the 128 B
-        // swizzle of the {64, Lp/64, 1, R} box
-        const bool tma_out = (!CAUSAL && !GATED) && prm.tma_y;
         if (tma_out) {
           fence_async_smem();
           tc_fence_before();
           wg_sync();
           if (wtid == 0) {
-            tma_store_4d(&prm.tmap_y, bufX, 0, 0, int(h), int(bt * C::R));
+            tma_store_4d(&prm.tmap_y, sYS, 0, 0, int(h), int(bt * C::R));
             bulk_commit();
-            bulk_wait_read0();
+            ys_pending = true;
+            if (t + kWG >= t1) {  // no further tile of this warpgroup: hand over now
+              bulk_wait_read0();
+              mbar_arrive(&ys_bar);
+              ys_pending = false;
+            }
           }
-          wg_sync();  // the TMA has read the staging before bufX takes the next operand
         } else {
         tc_fence_before();
         if (STG) stg_wait(1);
@@ -677,16 +733,18 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
           } else {
             st = ld_shared_u4(bufX + swz128(off));
           }
-          if (STG) st_shared_v4(sV + r * F::ROW_BYTES + n * 2, st.x, st.y, st.z, st.w);  // y, natural order
+          // y in natural order in bufX's second half (the staged conv output
+          // and the next tile's stage-A operand use only the first half)
+          if (STG) st_shared_v4(sY + r * F::ROW_BYTES + n * 2, st.x, st.y, st.z, st.w);
           else if (r < rows_left) *reinterpret_cast<uint4*>(gy + tile_base + int64_t(r) * HN + n) = st;
         }
         stamp(19);
         if (STG) fence_async_smem();  // y rows -> bulk stores (async proxy)
         wg_sync();  // staging reads done before bufX takes the next tile's operand
         if (STG && filler()) {
-          for (int r = 0; r < rows_left; ++r) bulk_s2g(gy + tile_base + int64_t(r) * HN, sV + r * F::ROW_BYTES, F::ROW_BYTES);
+          for (int r = 0; r < rows_left; ++r) bulk_s2g(gy + tile_base + int64_t(r) * HN, sY + r * F::ROW_BYTES, F::ROW_BYTES);
           bulk_commit();
-          bulk_wait_read0();
+          // v has been read: the output slot goes to tile t + 1 at once
           if (t + 1 < t1) release_out(t + 1, bt + 1 < nbt ? hh : hh + 1, bt + 1 < nbt ? bt + 1 : 0);
         }
         }  // !tma_out

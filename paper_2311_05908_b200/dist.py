@@ -13,11 +13,18 @@ import torch
 import torch.distributed as dist
 
 
-def head_shard(H: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous, balanced head range of `rank` (sizes differ by at most 1)."""
-    base, extra = divmod(H, world)
-    h0 = rank * base + min(rank, extra)
-    return h0, h0 + base + (1 if rank < extra else 0)
+def head_shard(H: int, rank: int, world: int, align: int = 2) -> tuple[int, int]:
+    """Contiguous, balanced head range of `rank`, in units of `align` heads
+    (shard sizes differ by at most 2 * align - 1).  The default align = 2 keeps
+    the head pairs (2j, 2j + 1) the k_f precompute transforms together (two
+    real filters as one complex FFT) inside one shard, so a shard's k_f --
+    and hence its y, du, dw, dv and dk -- is bitwise the corresponding slice
+    of the unsharded call."""
+    G = (H + align - 1) // align  # groups of `align` heads (the last may be short)
+    base, extra = divmod(G, world)
+    g0 = rank * base + min(rank, extra)
+    g1 = g0 + base + (1 if rank < extra else 0)
+    return min(H, g0 * align), min(H, g1 * align)
 
 
 def scatter_heads(x: torch.Tensor | None, H: int, shape_bn, dtype, device, src: int = 0) -> torch.Tensor:
