@@ -125,6 +125,19 @@ cudaError_t make_tmap_rows(CUtensorMap* map, void* base, int64_t rows, int64_t h
                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
+cudaError_t make_tmap_sig(CUtensorMap* map, const void* base, int64_t B, int64_t H, int64_t N, int R) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc || N % 256 != 0) return cudaErrorNotSupported;
+  // dims by increasing stride: element in a 512 B segment, segment, head, batch row
+  const cuuint64_t dim[4] = {256, cuuint64_t(N / 256), cuuint64_t(H), cuuint64_t(B)};
+  const cuuint64_t stride[3] = {512, cuuint64_t(N) * 2, cuuint64_t(H) * cuuint64_t(N) * 2};
+  const cuuint32_t box[4] = {256, cuuint32_t(N / 256), 1, cuuint32_t(R)};
+  const cuuint32_t estride[4] = {1, 1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(base), dim, stride, box, estride,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
 }  // namespace fc
 
 extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float* d_k, int64_t H, int64_t K,
@@ -318,6 +331,15 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
   prm.dtype = p->dtype == FFTCONV_BF16 ? 1 : p->dtype == FFTCONV_F32 ? 2 : 0;
   prm.num_sms = num_sms_current();
   prm.wl = static_cast<const uint8_t*>(p->d_tables) + p->tl.wl;
+  if (p->causal && p->dtype != FFTCONV_F32 && tma_y_enabled()) {  // one tensor copy per tile and tensor
+    const int R = 2 * p->P;
+    bool ok = make_tmap_sig(&prm.tmap_u, u, B, H, p->N, R) == cudaSuccess &&
+              make_tmap_sig(&prm.tmap_yo, y, B, H, p->N, R) == cudaSuccess;
+    if (ok && gated)
+      ok = make_tmap_sig(&prm.tmap_w, w, B, H, p->N, R) == cudaSuccess &&
+           make_tmap_sig(&prm.tmap_v, v, B, H, p->N, R) == cudaSuccess;
+    prm.tma_io = ok ? 1 : 0;
+  }
   cudaError_t e = p->dtype == FFTCONV_F32 ? launch_fwd_f32(prm, st) : launch_fwd_fused(prm, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
   g_launches += 1;

@@ -34,7 +34,14 @@ struct FwdParams {
   // TMA tensor store (4-D box {64, Lp/64, 1 head, R rows}, 128 B swizzle)
   int32_t tma_y;
   CUtensorMap tmap_y;
+  // causal fused tiles: u, w, v rows of a tile arrive by one TMA tensor load
+  // per tensor and y leaves by one tensor store (4-D box {256, N/256, 1
+  // head, R rows}); 0 = per-row bulk copies
+  int32_t tma_io;
+  CUtensorMap tmap_u, tmap_w, tmap_v, tmap_yo;
 };
+// Encode a map of 16-bit signal rows (B, H, N), box of R rows of one head.
+cudaError_t make_tmap_sig(CUtensorMap* map, const void* base, int64_t B, int64_t H, int64_t N, int R);
 // Encode tmap_y for fp16 rows (rows, heads, n) of length n = Lp (in elements),
 // row stride heads * Lp; box of R rows of one head.
 cudaError_t make_tmap_rows(CUtensorMap* map, void* base, int64_t rows, int64_t heads, int64_t Lp, int R);

@@ -204,6 +204,17 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
     const int rows = int(B - tb * C::R < C::R ? B - tb * C::R : C::R);
     uint64_t* bar = &stg_bar[kind][(t - t0) % kWG];
     const int planes = (kind == 0 && GATED) ? 2 : 1;
+    if (prm.tma_io) {  // one tensor copy per plane; rows past B arrive as zeros (full box counted)
+      mbar_arrive_expect_tx(bar, uint32_t(C::R * planes) * F::ROW_BYTES);
+      const int hc = int(phys_head(th)), b0 = int(tb * C::R);
+      if (kind == 0) {
+        tma_load_4d(sUW, &prm.tmap_u, 0, 0, hc, b0, bar);
+        if (GATED) tma_load_4d(sUW + C::R * F::ROW_BYTES, &prm.tmap_w, 0, 0, hc, b0, bar);
+      } else {
+        tma_load_4d(sV, &prm.tmap_v, 0, 0, hc, b0, bar);
+      }
+      return;
+    }
     mbar_arrive_expect_tx(bar, uint32_t(rows * planes) * F::ROW_BYTES);
     for (int r = 0; r < rows; ++r) {
       const int64_t go = tbase + r * H * N;
@@ -742,7 +753,10 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         if (STG) fence_async_smem();  // y rows -> bulk stores (async proxy)
         wg_sync();  // staging reads done before bufX takes the next tile's operand
         if (STG && filler()) {
-          for (int r = 0; r < rows_left; ++r) bulk_s2g(gy + tile_base + int64_t(r) * HN, sY + r * F::ROW_BYTES, F::ROW_BYTES);
+          if (prm.tma_io)  // one tensor store (rows past B are clipped)
+            tma_store_4d(&prm.tmap_yo, sY, 0, 0, int(h), int(bt * C::R));
+          else
+            for (int r = 0; r < rows_left; ++r) bulk_s2g(gy + tile_base + int64_t(r) * HN, sY + r * F::ROW_BYTES, F::ROW_BYTES);
           bulk_commit();
           // v has been read: the output slot goes to tile t + 1 at once
           if (t + 1 < t1) release_out(t + 1, bt + 1 < nbt ? hh : hh + 1, bt + 1 < nbt ? bt + 1 : 0);
