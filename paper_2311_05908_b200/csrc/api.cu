@@ -161,7 +161,10 @@ extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float*
   prm.L1 = p->L1;
   prm.L2 = p->L2;
   cudaError_t e;
-  if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
+  if (p->dit > 1) {  // single-pass order 3: L0 blocks of K_f[f' + 2048 k0] per head
+    e = launch_precompute_kf_dit(prm, p->dit, reinterpret_cast<cudaStream_t>(stream));
+    g_launches += H > 0 ? 1 : 0;
+  } else if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
     const size_t block = size_t(p->L2) * tab_stride(uint32_t(p->L1 / 2));
     prm.L = p->Lp;
     if (p->sparse && p->row_map.size() < size_t(p->L0))
@@ -186,6 +189,27 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
   if (gated && !v) { set_last_error(std::string(fn) + ": v is NULL"); return FFTCONV_ERR_INVALID_ARG; }
   if (B * H == 0) return FFTCONV_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (p->dit > 1) {  // single-pass order 3: one fused launch, no workspace
+    FwdParams prm{};
+    prm.u = u; prm.w = w; prm.v = v; prm.y = y; prm.kf = kf;
+    prm.tables = static_cast<const uint8_t*>(p->d_tables) + p->dit_tab_off;
+    prm.B = B; prm.H = H; prm.N = p->N; prm.L1 = 32; prm.causal = 1;
+    prm.gated = gated ? 1 : 0;
+    prm.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
+    prm.num_sms = num_sms_current();
+    prm.L0I = p->dit;
+    const int R = 8 / p->dit;  // real rows per tile
+    bool ok = make_tmap_sig(&prm.tmap_u, u, B, H, p->N, R) == cudaSuccess &&
+              make_tmap_sig(&prm.tmap_yo, y, B, H, p->N, R) == cudaSuccess;
+    if (ok && gated)
+      ok = make_tmap_sig(&prm.tmap_w, w, B, H, p->N, R) == cudaSuccess &&
+           make_tmap_sig(&prm.tmap_v, v, B, H, p->N, R) == cudaSuccess;
+    prm.tma_io = ok ? 1 : 0;
+    cudaError_t e = launch_fwd_fused(prm, st);
+    if (e != cudaSuccess) return cuda_fail(fn, e);
+    g_launches += 1;
+    return FFTCONV_OK;
+  }
   if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
     if (!ws) { set_last_error(std::string(fn) + ": multipass regime needs a workspace"); return FFTCONV_ERR_INVALID_ARG; }
     if (!aligned16(ws)) { set_last_error(std::string(fn) + ": workspace not 16-byte aligned"); return FFTCONV_ERR_MISALIGNED; }
@@ -331,6 +355,7 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
   prm.dtype = p->dtype == FFTCONV_BF16 ? 1 : p->dtype == FFTCONV_F32 ? 2 : 0;
   prm.num_sms = num_sms_current();
   prm.wl = static_cast<const uint8_t*>(p->d_tables) + p->tl.wl;
+  prm.L0I = 1;
   if (p->causal && p->dtype != FFTCONV_F32 && tma_y_enabled()) {  // one tensor copy per tile and tensor
     const int R = 2 * p->P;
     bool ok = make_tmap_sig(&prm.tmap_u, u, B, H, p->N, R) == cudaSuccess &&
@@ -600,7 +625,9 @@ static size_t bwd_ws_bytes(const fftconv_plan_s* p, int64_t B, int64_t H) {
     const size_t t = size_t(rows) * size_t(H) * size_t(p->L) * t_elem_bytes(p);
     const int64_t units = p->dtype == FFTCONV_F32 ? bwd_f32_units_per_head(rows) : bwd_tiles_per_head(rows, p->L1);
     const size_t part = size_t(H) * p->L0 * size_t(units) * size_t(p->Lp) * 8;
-    return (p->nlev > 1 ? 4 : 2) * t + part + size_t(H) * size_t(p->L) * 8;
+    // order-3 plans: the multipass-layout copy of k_f at the end
+    const size_t kf_copy = p->dit > 1 ? size_t(H) * p->kf_bytes_per_head : 0;
+    return (p->nlev > 1 ? 4 : 2) * t + part + size_t(H) * size_t(p->L) * 8 + kf_copy;
   }
   const int64_t units = p->dtype == FFTCONV_F32 ? bwd_f32_units_per_head(B) : bwd_tiles_per_head(B, p->L1);
   return size_t(H) * size_t(units) * size_t(p->L) * 8;
@@ -666,6 +693,13 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   // window's correlation with k is block j's contribution to dg over both
   // halves (overlap-add in pass 3) and Sum_windows DC conj(G) is exactly
   // Sum_i dc[i] g[i - t] for t < K <= C (dk).
+  if (p->dit > 1) {  // order-3 k_f -> the multipass layout, in the workspace's tail
+    uint8_t* kf2 = static_cast<uint8_t*>(d_workspace) + bwd_ws_bytes(p, B, H) - size_t(H) * p->kf_bytes_per_head;
+    e = launch_kf_dit_to_dif(d_kf, kf2, H, p->dit, st);
+    if (e != cudaSuccess) return cuda_fail(fn, e);
+    g_launches += 1;
+    d_kf = kf2;
+  }
   const bool partial = p->regime == REGIME_PARTIAL;
   const int64_t NCw = partial ? p->N / (p->L / 2) : 1;
   const int64_t Bv = B * NCw;
@@ -768,7 +802,7 @@ extern "C" fftconv_status_t fftconv_workspace_size(fftconv_plan_t p, int64_t B, 
   if (!p || !bytes || B < 0 || H < 0) { set_last_error("fftconv_workspace_size: bad argument"); return FFTCONV_ERR_INVALID_ARG; }
   size_t n = 0;
   if (for_bwd) n = bwd_ws_bytes(p, B, H);
-  else if (p->regime == REGIME_MULTIPASS)
+  else if (p->regime == REGIME_MULTIPASS && p->dit == 1)  // (order-3 plans need none)
     n = size_t(p->nlev > 1 ? 2 : 1) * size_t(2 * ((B + 1) / 2)) * size_t(H) * size_t(p->L) * t_elem_bytes(p);
   else if (p->regime == REGIME_PARTIAL) {
     const int64_t Bv = B * (p->N / (p->L / 2));

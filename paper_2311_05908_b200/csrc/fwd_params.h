@@ -39,6 +39,9 @@ struct FwdParams {
   // head, R rows}); 0 = per-row bulk copies
   int32_t tma_io;
   CUtensorMap tmap_u, tmap_w, tmap_v, tmap_yo;
+  // single-pass order 3 (causal fft_size = L0I * 2048, L0I in {2, 4}): k_f
+  // holds L0I blocks per head, block k0 = K_f[f' + 2048 k0]; 1 = order 2
+  int32_t L0I;
 };
 // Encode a map of 16-bit signal rows (B, H, N), box of R rows of one head.
 cudaError_t make_tmap_sig(CUtensorMap* map, const void* base, int64_t B, int64_t H, int64_t N, int R);
@@ -74,6 +77,10 @@ FC_HD_PARAMS int32_t row_freq_digit(int32_t r, int32_t nlev, const int32_t* lev)
   return k;
 }
 cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s);
+// single-pass order-3 plans: k_f in L0 blocks per head, block k0 = K_f[f' + 2048 k0]
+cudaError_t launch_precompute_kf_dit(const KfParams& prm, int L0, cudaStream_t s);
+// ... and its multipass (DIF) layout for the backward
+cudaError_t launch_kf_dit_to_dif(const void* src, void* dst, int64_t H, int L0, cudaStream_t s);
 
 // multipass regime (kernels_mp.cu)
 struct MpParams {

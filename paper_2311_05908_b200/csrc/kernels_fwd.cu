@@ -57,10 +57,17 @@ __device__ long long fc_trace_buf[8][64][24];
 // copies through two slots shared by the warpgroups in tile order: the
 // input slot (u [| w], filled a tile ahead) and the output slot (v arrives
 // there for the gate; y leaves from it).
-template <int L1, bool CAUSAL, bool GATED>
+template <int L1, bool CAUSAL, bool GATED, int L0I = 1>
 struct FwdCfg {
   using C = O2Cfg<L1, CAUSAL>;
   static constexpr bool STG = CAUSAL;
+  // L0I > 1 (single-pass order 3, causal only): the tile's P complex rows
+  // are the L0I decimated inner rows z[n0 + L0I n'] of P / L0I row pairs;
+  // real rows of length NROW = L0I * NOUT, RR = R / L0I rows per tile
+  static constexpr bool DIT = L0I > 1;
+  static_assert(!DIT || (CAUSAL && L1 == 32 && C::P % L0I == 0 && (L0I == 2 || L0I == 4)), "single-pass order 3");
+  static constexpr int RR = C::R / L0I;
+  static constexpr int NROW = C::NOUT * L0I;
   // Stage B / B^-1 N: re | im only (the negated plane the complex multiply
   // needs is a sign folded into the f32x2 multiplies); FC_NEG_B=1 has the
   // tensor core emit it as a third block of the G_B table instead.
@@ -75,19 +82,23 @@ struct FwdCfg {
   static constexpr uint32_t S_GBI = C::al(S_GB + GB_SM);
   static constexpr uint32_t S_GAI = C::al(S_GBI + GB_SM);
   static constexpr uint32_t TABLES = C::al(S_GAI + C::GAI_FWD_BYTES);
-  static constexpr uint32_t ROW_BYTES = C::NOUT * 2;  // one 16-bit input row
-  static constexpr uint32_t UW_BYTES = STG ? C::R * ROW_BYTES * (GATED ? 2 : 1) : 0;
-  static constexpr uint32_t V_BYTES = STG ? C::R * ROW_BYTES : 0;
+  static constexpr uint32_t ROW_BYTES = NROW * 2;  // one 16-bit input row
+  static constexpr uint32_t UW_BYTES = STG ? RR * ROW_BYTES * (GATED ? 2 : 1) : 0;
+  static constexpr uint32_t V_BYTES = STG ? RR * ROW_BYTES : 0;
+  // per-warpgroup buffers: k_f copy (L0I = 1; the order-3 tiles read their
+  // L0I k_f blocks from global memory / L2) and the operand buffer
+  static constexpr uint32_t KF_SM = DIT ? 0 : C::al(C::KF_BYTES);
+  static constexpr uint32_t WG_BYTES = KF_SM + C::al(C::BUFX_BYTES);
   // circular plain tiles (the multipass inner pass): y staging shared by
   // the warpgroups in tile order, leaving by one TMA tensor store each
   static constexpr uint32_t YS_BYTES = (!CAUSAL && !GATED) ? C::R * C::NOUT * 2 : 0;
   static constexpr uint32_t bytes_for(int wg) {
-    return C::al(C::al(C::al(TABLES + wg * C::WG_BYTES) + UW_BYTES) + V_BYTES) + YS_BYTES + 1024;  // + alignment slack
+    return C::al(C::al(C::al(TABLES + wg * WG_BYTES) + UW_BYTES) + V_BYTES) + YS_BYTES + 1024;  // + alignment slack
   }
   static constexpr int WG = bytes_for(2) <= 227 * 1024 ? 2 : 1;
   static constexpr int THREADS = WG * kWGThreads;
   static constexpr uint32_t OFF_WG = TABLES;
-  static constexpr uint32_t OFF_UW = C::al(OFF_WG + WG * C::WG_BYTES);
+  static constexpr uint32_t OFF_UW = C::al(OFF_WG + WG * WG_BYTES);
   static constexpr uint32_t OFF_V = C::al(OFF_UW + UW_BYTES);
   static constexpr uint32_t OFF_YS = C::al(OFF_V + V_BYTES);
   static constexpr uint32_t SMEM = bytes_for(WG);
@@ -111,10 +122,14 @@ FC_DEVICE float2 wroot(int e) {
 // t0 + g, t0 + g + kWG, ... of the CTA's contiguous tile range, with its own
 // TMEM columns, mbarriers, named barrier, k_f copy and operand buffer, so one
 // warpgroup's MMAs, memory waits and barriers overlap the other's math.
-template <int L1, bool CAUSAL, bool GATED, typename T>
-__global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv_fwd_o2_kernel(const __grid_constant__ FwdParams prm) {
+template <int L1, bool CAUSAL, bool GATED, typename T, int L0I>
+__global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) fftconv_fwd_o2_kernel(const __grid_constant__ FwdParams prm) {
   using C = O2Cfg<L1, CAUSAL>;
-  using F = FwdCfg<L1, CAUSAL, GATED>;
+  using F = FwdCfg<L1, CAUSAL, GATED, L0I>;
+  constexpr bool DIT = F::DIT;
+  constexpr int RR = F::RR;        // real rows per tile
+  constexpr int NROW = F::NROW;    // real row length (N)
+  constexpr int LF = C::L * L0I;   // the whole transform (fft_size)
   constexpr int kWG = F::WG;
   constexpr int kThreads = F::THREADS;
   constexpr bool STG = F::STG;      // input staging by bulk copies
@@ -139,11 +154,11 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
   const int quad = warp & 3;             // TMEM lane quadrant this warp may access
   const int slice = (warp >> 2) & 1;     // column slice 0..1
   const int m = quad * 32 + lane;        // TMEM lane / MMA row owned by this thread
-  const uint32_t sKF = base + F::OFF_WG + wg * C::WG_BYTES;
-  const uint32_t bufX = sKF + C::al(C::KF_BYTES);
+  const uint32_t sKF = base + F::OFF_WG + wg * F::WG_BYTES;
+  const uint32_t bufX = sKF + F::KF_SM;
   const uint32_t sY = bufX + C::BUFX_BYTES / 2;  // causal: y rows staged for the bulk stores
   const int64_t B = prm.B, H = prm.H, N = prm.N;
-  const int64_t nbt = (B + C::R - 1) / C::R;
+  const int64_t nbt = (B + RR - 1) / RR;
   const int64_t Hi = prm.row_map ? (H / prm.row_L0) * prm.nrow : H;  // heads iterated
   auto phys_head = [&](int64_t hh) -> int64_t {
     return prm.row_map ? (hh / prm.nrow) * prm.row_L0 + prm.row_map[hh % prm.nrow] : hh;
@@ -200,16 +215,16 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
   // it, so fills (and reads) follow tile order and each slot's fill for the
   // next warpgroup's tile overlaps the rest of the current tile.
   auto fill = [&](int kind, int64_t t, int64_t th, int64_t tb) {  // tile t = th * nbt + tb
-    const int64_t tbase = (tb * C::R * H + phys_head(th)) * N;
-    const int rows = int(B - tb * C::R < C::R ? B - tb * C::R : C::R);
+    const int64_t tbase = (tb * RR * H + phys_head(th)) * N;
+    const int rows = int(B - tb * RR < RR ? B - tb * RR : RR);
     uint64_t* bar = &stg_bar[kind][(t - t0) % kWG];
     const int planes = (kind == 0 && GATED) ? 2 : 1;
     if (prm.tma_io) {  // one tensor copy per plane; rows past B arrive as zeros (full box counted)
-      mbar_arrive_expect_tx(bar, uint32_t(C::R * planes) * F::ROW_BYTES);
-      const int hc = int(phys_head(th)), b0 = int(tb * C::R);
+      mbar_arrive_expect_tx(bar, uint32_t(RR * planes) * F::ROW_BYTES);
+      const int hc = int(phys_head(th)), b0 = int(tb * RR);
       if (kind == 0) {
         tma_load_4d(sUW, &prm.tmap_u, 0, 0, hc, b0, bar);
-        if (GATED) tma_load_4d(sUW + C::R * F::ROW_BYTES, &prm.tmap_w, 0, 0, hc, b0, bar);
+        if (GATED) tma_load_4d(sUW + RR * F::ROW_BYTES, &prm.tmap_w, 0, 0, hc, b0, bar);
       } else {
         tma_load_4d(sV, &prm.tmap_v, 0, 0, hc, b0, bar);
       }
@@ -220,7 +235,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
       const int64_t go = tbase + r * H * N;
       if (kind == 0) {
         bulk_g2s(sUW + r * F::ROW_BYTES, gu + go, F::ROW_BYTES, bar);
-        if (GATED) bulk_g2s(sUW + (C::R + r) * F::ROW_BYTES, gw + go, F::ROW_BYTES, bar);
+        if (GATED) bulk_g2s(sUW + (RR + r) * F::ROW_BYTES, gw + go, F::ROW_BYTES, bar);
       } else {
         bulk_g2s(sV + r * F::ROW_BYTES, gv + go, F::ROW_BYTES, bar);
       }
@@ -294,22 +309,33 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
   // shared by 4 lanes (one shared-memory wavefront per 8 distinct words).
   constexpr int JC = L1 / 8;    // 8-element n1 chunks
   const int pA = ((m >> 5) / JC) * 4 + ((m >> 3) & 3), n1A = ((m >> 5) % JC) * 8 + (m & 7);
-  auto rowB_p = [&](int gi) { return (gi >> 1) * 4 + ((m >> 3) & 3); };
-  auto rowB_k2 = [&](int gi) { return (gi & 1) * 32 + (m >> 5) * 8 + (m & 7); };
-  // Twiddle-recurrence constants (tables are resident after the setup sync):
-  // epilogue 1 steps k2 by 2 at fixed n1 (W^{2 n1}); epilogue 3 steps n1 at
-  // fixed k2 (W^{k2}, W^{2 k2}) for the thread's two k2 (group parity).
-  auto tw_at = [&](int n1, int k2) { return wroot<C::L>(n1 * k2); };  // W_L^{n1 k2}
-  const float2 tw1_c2 = tw_at(n1A, 2);
+  // Order 3 (DIT): inner row p = q L0I + n0 holds z_q[n0 + L0I n'], so the
+  // transform index of stage-A row (p, n1) is n0 + L0I n1 and the stage-B /
+  // B^-1 rows put n0 where the outer DFT_L0I can reach it: its low bit in
+  // the group gi (both in this thread's TMEM columns), its high bit (L0I =
+  // 4; for L0I = 2 the pair q) in lane bit 3 (one shuffle away).
+  auto rowB_p = [&](int gi) { return DIT ? ((m >> 3) & 1) * 2 + gi : (gi >> 1) * 4 + ((m >> 3) & 3); };
+  auto rowB_k2 = [&](int gi) {
+    return DIT ? (m & 7) + 8 * (m >> 5) + 32 * ((m >> 4) & 1) : (gi & 1) * 32 + (m >> 5) * 8 + (m & 7);
+  };
+  // Twiddle-recurrence constants: epilogue 1 steps k2 by 2 at fixed
+  // transform index e1 = n0 + L0I n1 (W^{2 e1}); epilogue 3 steps n1 at
+  // fixed (n0, k2) (W^{L0I k2}, W^{2 L0I k2}) for the thread's two k2.
+  auto tw_at = [&](int e1, int k2) { return wroot<LF>(e1 * k2); };  // W_LF^{e1 k2}
+  const int e1A = (pA % L0I) + L0I * n1A;
+  const float2 tw1_c2 = tw_at(e1A, 2);
   float4 tw3_c[2];
 #pragma unroll
   for (int par = 0; par < 2; ++par) {
-    const int k2 = par * 32 + (m >> 5) * 8 + (m & 7);
-    const float2 w1 = tw_at(1, k2), w2 = tw_at(2, k2);
+    const int k2 = rowB_k2(par);
+    const float2 w1 = tw_at(L0I, k2), w2 = tw_at(2 * L0I, k2);
     tw3_c[par] = make_float4(w1.x, w1.y, w2.x, w2.y);
   }
   // 8-row group of stage-B row (p, k2) (k2 a multiple of 8)
-  auto grpB = [](int p, int k2) { return (((p >> 2) * 2 + (k2 >> 5)) * 16) + ((k2 & 31) >> 3) * 4 + (p & 3); };
+  auto grpB = [](int p, int k2) {
+    return DIT ? (p & 1) * 16 + ((k2 >> 3) & 3) * 4 + ((k2 >> 5) & 1) * 2 + (p >> 1)
+               : (((p >> 2) * 2 + (k2 >> 5)) * 16) + ((k2 & 31) >> 3) * 4 + (p & 3);
+  };
 
   // Input loader: each warp instruction reads 32 consecutive 16 B chunks of
   // one row (memory chunk cm = n2 * JC + j); lanes are permuted so that each
@@ -318,7 +344,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
   constexpr int KROWS = C::KA;  // n2 rows per row
   constexpr int WPR = KROWS * JC / 32;  // warp instructions per row
   constexpr int RSTEP = 8 / WPR;
-  constexpr int NCH = C::R * C::CH;
+  constexpr int NCH = RR * (NROW / 8);
   constexpr int PER_ALL = NCH / kWGThreads;  // chunks per thread and tile
   static_assert(WPR >= 1 && 8 % WPR == 0 && NCH % kWGThreads == 0, "loader mapping");
   const int64_t HN = H * N;
@@ -387,10 +413,47 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
       uint4 uv = make_uint4(0, 0, 0, 0), wv = make_uint4(0, 0, 0, 0);
       if (r < left) {
         uv = ld_shared_u4(sUW + r * F::ROW_BYTES + ld_cm * 16);
-        if (GATED) wv = ld_shared_u4(sUW + (C::R + r) * F::ROW_BYTES + ld_cm * 16);
+        if (GATED) wv = ld_shared_u4(sUW + (RR + r) * F::ROW_BYTES + ld_cm * 16);
       }
       const uint4 g = gate8(uv, wv);
       st_shared_v4(chunk_dst(i), g.x, g.y, g.z, g.w);
+    }
+  };
+  // Order 3 (DIT): a thread's super-chunk (row r, n2, j) is the 8 L0I
+  // samples [8 L0I (n2 JC + j), +8 L0I) of real row r = 2q + c; gated, then
+  // de-interleaved into the L0I operand chunks of inner rows p = q L0I + n0
+  // (samples n0 + L0I (8 j + e + 32 n2), e < 8).
+  constexpr int PER_SC = DIT ? RR * (NROW / (8 * L0I)) / kWGThreads : 1;
+  auto build_dit = [&](int left) {
+#pragma unroll
+    for (int i = 0; i < PER_SC; ++i) {
+      const int r = ld_r0 + i * RSTEP;
+      uint32_t wd[4 * L0I];
+#pragma unroll
+      for (int sc = 0; sc < L0I; ++sc) {
+        uint4 uv = make_uint4(0, 0, 0, 0), wv = make_uint4(0, 0, 0, 0);
+        if (r < left) {
+          const uint32_t o = (ld_cm * L0I + sc) * 16;
+          uv = ld_shared_u4(sUW + r * F::ROW_BYTES + o);
+          if (GATED) wv = ld_shared_u4(sUW + (RR + r) * F::ROW_BYTES + o);
+        }
+        const uint4 g = gate8(uv, wv);
+        wd[4 * sc + 0] = g.x; wd[4 * sc + 1] = g.y; wd[4 * sc + 2] = g.z; wd[4 * sc + 3] = g.w;
+      }
+      const int q = r >> 1, c = r & 1, k = c * C::KA + ld_n2;
+#pragma unroll
+      for (int n0 = 0; n0 < L0I; ++n0) {
+        // output word t = samples (n0 + L0I (2t), n0 + L0I (2t + 1)) of the super-chunk
+        uint32_t o[4];
+#pragma unroll
+        for (int t2 = 0; t2 < 4; ++t2) {
+          const int a = n0 + L0I * 2 * t2, b = a + L0I;  // half indices
+          o[t2] = __byte_perm(wd[a >> 1], wd[b >> 1], ((a & 1) ? 0x32u : 0x10u) | ((b & 1) ? 0x7600u : 0x5400u));
+        }
+        const int p = q * L0I + n0;
+        const int g8 = ((p >> 2) * JC + ld_j) * 4 + (p & 3);
+        st_shared_v4(bufX + g8 * C::SBO_A + (k >> 3) * 128 + (k & 7) * 16, o[0], o[1], o[2], o[3]);
+      }
     }
   };
   auto store_chunks = [&](const uint4* uv, const uint4* wv) {
@@ -419,16 +482,19 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
     stage_no = 0;
     stamp(0);
     const int64_t h = phys_head(hh);
-    const int64_t tile_base = (bt * C::R * H + h) * N;  // element offset of row (bt*R, h)
-    const int rows_left = int(B - bt * C::R < C::R ? B - bt * C::R : C::R);
-    const bool new_h = h != cur_h;
+    const int64_t tile_base = (bt * RR * H + h) * N;  // element offset of row (bt*R, h)
+    const int rows_left = int(B - bt * RR < RR ? B - bt * RR : RR);
+    const bool new_h = !DIT && h != cur_h;
     if (new_h) {  // refresh this warpgroup's k_f copy (previous tile's epi2 is long done)
       const uint8_t* src = gkf + h * int64_t(C::KF_BYTES);
       for (uint32_t o = wtid * 16; o < C::KF_BYTES; o += kWGThreads * 16) cp_async16(sKF + o, src + o, true);
       cp_async_commit();
       cur_h = h;
     }
-    if constexpr (STG) {
+    if constexpr (DIT) {
+      stg_wait(0);
+      build_dit(rows_left);
+    } else if constexpr (STG) {
       stg_wait(0);
       build_from_staging(rows_left);
     } else if (!loaded) {
@@ -483,7 +549,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         // steps by W^{2 n1} (register recurrence instead of 8 table loads)
         float4 w[8];
         {
-          const float2 a = tw_at(n1A, k20), b = tw_at(n1A, k20 + 1);
+          const float2 a = tw_at(e1A, k20), b = tw_at(e1A, k20 + 1);
           w[0] = make_float4(a.x, b.x, a.y, b.y);
 #pragma unroll
           for (int jj = 1; jj < 8; ++jj) w[jj] = cstep(w[jj - 1], tw1_c2);
@@ -521,7 +587,133 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
     });
 
     // ---------------- epilogue 2: pointwise * k_f -> stage B^-1 operand (own row: TMEM, else K-major smem)
-    {
+    if constexpr (DIT) {
+      // Order 3: for each f' = k2 + 64 k1 the L0I inner rows n0 hold
+      // Y_n0[f']; X[f' + 2048 k0] = sum_n0 W_L0I^{n0 k0} W_{32 L0I}^{n0 k1}
+      // Y_n0[f'] (the W_LF^{n0 k2} part of the twiddle was applied in
+      // epilogue 1), * k_f, the inverse DFT_L0I back to n0, conj twiddle,
+      // 1 / L0I.  n0 low bit = group (this thread's two TMEM column blocks),
+      // n0 high bit (L0I = 4) = lane bit 3 (shuffles).  k_f blocks are read
+      // from global memory (L2-resident, 16 B per load).
+      static_assert(TS && !FC_NEG_B, "order-3 epilogue 2");
+      const int k2 = rowB_k2(0);
+      const int xb = (m >> 3) & 1;
+      const uint8_t* kfh = gkf + h * int64_t(L0I) * C::KF_BYTES;
+      auto k0_of = [&](int slot) { return L0I == 2 ? slot : xb + 2 * slot; };
+      auto n0_of = [&](int slot) { return L0I == 2 ? slot : 2 * xb + slot; };
+      auto load_kf = [&](int k1c, float4 (&dst)[2][4]) {
+#pragma unroll
+        for (int slot = 0; slot < 2; ++slot)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            dst[slot][jj] = __ldg(reinterpret_cast<const float4*>(kfh + k0_of(slot) * C::KF_BYTES +
+                                                                  tab_off<L1 / 2>(k2, k1c * 4 + jj)));
+      };
+      auto process = [&](int k1c, const float4 (&kf)[2][4]) {
+        float re[2][8], im[2][8];
+#pragma unroll
+        for (int slot = 0; slot < 2; ++slot) {
+          tmem_ld8(tq + slot * NBF + k1c * 8, re[slot]);
+          tmem_ld8(tq + slot * NBF + k1c * 8 + L1, im[slot]);
+        }
+        // W_{32 L0I}^{n0 k1}, k1 = 8 k1c + e, per slot (n0)
+        float wr[2][8], wi[2][8];
+#pragma unroll
+        for (int slot = 0; slot < 2; ++slot) {
+          const int n0 = n0_of(slot);
+          float2 b = wroot<32 * L0I>(n0 * 8 * k1c);
+          const float2 st = wroot<32 * L0I>(n0);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            wr[slot][e] = b.x; wi[slot][e] = b.y;
+            b = make_float2(b.x * st.x - b.y * st.y, b.x * st.y + b.y * st.x);
+          }
+        }
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float xr[2], xi[2];
+#pragma unroll
+          for (int slot = 0; slot < 2; ++slot) {  // T = W^{n0 k1} Y
+            xr[slot] = re[slot][e] * wr[slot][e] - im[slot][e] * wi[slot][e];
+            xi[slot] = re[slot][e] * wi[slot][e] + im[slot][e] * wr[slot][e];
+          }
+          float sr[2], si[2];
+          if constexpr (L0I == 2) {
+            sr[0] = xr[0] + xr[1]; si[0] = xi[0] + xi[1];
+            sr[1] = xr[0] - xr[1]; si[1] = xi[0] - xi[1];
+          } else {
+            float pr[2], pi[2];
+#pragma unroll
+            for (int slot = 0; slot < 2; ++slot) {
+              pr[slot] = __shfl_xor_sync(0xffffffffu, xr[slot], 8);
+              pi[slot] = __shfl_xor_sync(0xffffffffu, xi[slot], 8);
+            }
+            float tr[2], ti[2];  // S_b[n0lo] = T[0][n0lo] + (-1)^b T[1][n0lo]
+#pragma unroll
+            for (int slot = 0; slot < 2; ++slot) {
+              tr[slot] = xb ? pr[slot] - xr[slot] : xr[slot] + pr[slot];
+              ti[slot] = xb ? pi[slot] - xi[slot] : xi[slot] + pi[slot];
+            }
+            // X[b + 2 kk] = S0 +- W_4^b S1, W_4^1 = -i
+            const float ur = xb ? ti[1] : tr[1], ui = xb ? -tr[1] : ti[1];
+            sr[0] = tr[0] + ur; si[0] = ti[0] + ui;
+            sr[1] = tr[0] - ur; si[1] = ti[0] - ui;
+          }
+          // * k_f[f' + 2048 k0]: kf[slot][e/2] = {kr_e, kr_e+1, ki_e, ki_e+1}
+#pragma unroll
+          for (int slot = 0; slot < 2; ++slot) {
+            const float4 q = kf[slot][e >> 1];
+            const float kr = (e & 1) ? q.y : q.x, ki = (e & 1) ? q.w : q.z;
+            const float zr = sr[slot] * kr - si[slot] * ki, zi = sr[slot] * ki + si[slot] * kr;
+            sr[slot] = zr; si[slot] = zi;
+          }
+          float ar[2], ai[2];
+          if constexpr (L0I == 2) {
+            ar[0] = sr[0] + sr[1]; ai[0] = si[0] + si[1];
+            ar[1] = sr[0] - sr[1]; ai[1] = si[0] - si[1];
+          } else {
+            // R[0] = Z0 + Z1, R[1] = W_4^{-b} (Z0 - Z1), W_4^{-1} = +i
+            const float dr = sr[0] - sr[1], di = si[0] - si[1];
+            float rr[2], ri[2];
+            rr[0] = sr[0] + sr[1]; ri[0] = si[0] + si[1];
+            rr[1] = xb ? -di : dr; ri[1] = xb ? dr : di;
+#pragma unroll
+            for (int slot = 0; slot < 2; ++slot) {
+              const float qr = __shfl_xor_sync(0xffffffffu, rr[slot], 8);
+              const float qi = __shfl_xor_sync(0xffffffffu, ri[slot], 8);
+              ar[slot] = xb ? qr - rr[slot] : rr[slot] + qr;
+              ai[slot] = xb ? qi - ri[slot] : ri[slot] + qi;
+            }
+          }
+          constexpr float sc = 1.0f / float(L0I);
+#pragma unroll
+          for (int slot = 0; slot < 2; ++slot) {  // conj twiddle, 1 / L0I
+            re[slot][e] = sc * (ar[slot] * wr[slot][e] + ai[slot] * wi[slot][e]);
+            im[slot][e] = sc * (ai[slot] * wr[slot][e] - ar[slot] * wi[slot][e]);
+          }
+        }
+#pragma unroll
+        for (int slot = 0; slot < 2; ++slot) {  // K index c*L1 + k1 -> column (c*L1 + k1) / 2
+          const uint32_t ca = tq + C::CA + slot * L1 + k1c * 4;
+          tmem_st4(ca, pack_half2(re[slot][0], re[slot][1]), pack_half2(re[slot][2], re[slot][3]),
+                   pack_half2(re[slot][4], re[slot][5]), pack_half2(re[slot][6], re[slot][7]));
+          tmem_st4(ca + L1 / 2, pack_half2(im[slot][0], im[slot][1]), pack_half2(im[slot][2], im[slot][3]),
+                   pack_half2(im[slot][4], im[slot][5]), pack_half2(im[slot][6], im[slot][7]));
+        }
+      };
+      float4 kfa[2][4];
+      load_kf(slice, kfa);
+      wait_half(0);
+      wait_half(1);
+      {
+        float4 kfb[2][4];
+        load_kf(slice + 2, kfb);
+        process(slice, kfa);
+        process(slice + 2, kfb);
+      }
+      tmem_st_wait();
+    } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int it = slice + 2 * i;  // items 0..3 in half 0, 4..7 in half 1
@@ -595,7 +787,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         // by W^{2 k2}
         float4 w[4];
         {
-          const float2 a = tw_at(n1c * 8, k2);
+          const float2 a = tw_at((p % L0I) + L0I * 8 * n1c, k2);
           const float br = a.x, bi = a.y;
           const float4 c = tw3_c[gi & 1];  // {Re W^{k2}, Im W^{k2}, Re W^{2k2}, Im W^{2k2}}
           w[0] = make_float4(br, br * c.x - bi * c.y, bi, br * c.y + bi * c.x);
@@ -609,7 +801,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         }
         cmulc8(re, im, nr, w);
         if (!TS && i == 0) wait_half(1);  // stores may overwrite operands of the second half
-        const int ng = (p * L1) / 8 + n1c;
+        // A^-1 output column groups: (p, n1c) in natural order; order 3:
+        // (n1c, p) so that epilogue 4 finds every n0 of 8 samples together
+        const int ng = DIT ? n1c * C::P + p : (p * L1) / 8 + n1c;
         st_half8(bufX + ng * C::SBO_XA + (k2 >> 3) * 128 + (k2 & 7) * 16, re);
         st_half8(bufX + ng * C::SBO_XA + ((L2 + k2) >> 3) * 128 + (k2 & 7) * 16, im);
       }
@@ -642,17 +836,17 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
       // staging through bufX for fully coalesced rows (FC_CIRC_DIRECT)
       constexpr bool STAGE = CAUSAL || (!GATED && !FC_CIRC_DIRECT);
       using S = typename std::conditional<GATED, __half, T>::type;
-      constexpr int OCH = C::R * C::NOUT / 8 / kWGThreads;  // coalesced output chunks per thread
-      static_assert(!STAGE || C::R * C::NOUT * sizeof(S) <= C::BUFX_BYTES, "y staging fits in bufX");
-      static_assert(!STG || (C::R * C::NOUT * sizeof(S) <= C::BUFX_BYTES / 2 && C::R * F::ROW_BYTES <= C::BUFX_BYTES / 2 &&
+      constexpr int OCH = RR * NROW / 8 / kWGThreads;  // coalesced output chunks per thread
+      static_assert(!STAGE || RR * NROW * sizeof(S) <= C::BUFX_BYTES, "y staging fits in bufX");
+      static_assert(!STG || (RR * NROW * sizeof(S) <= C::BUFX_BYTES / 2 && RR * F::ROW_BYTES <= C::BUFX_BYTES / 2 &&
                              128 * 2 * C::KA * 2 <= C::BUFX_BYTES / 2),
                     "causal: staged conv output, next stage-A operand and y rows share bufX by halves");
       constexpr int PER = OUT_COLS / 8;  // transposed 8-column items per thread
       constexpr int NV = STAGE ? OCH : PER;
       const bool has_next = t + kWG < t1;
       uint4 nu[PER_ALL], nw[PER_ALL], vv[NV];
-      auto och_r = [&](int i) { return (i * kWGThreads + wtid) / (C::NOUT / 8); };
-      auto och_n = [&](int i) { return ((i * kWGThreads + wtid) % (C::NOUT / 8)) * 8; };
+      auto och_r = [&](int i) { return (i * kWGThreads + wtid) / (NROW / 8); };
+      auto och_n = [&](int i) { return ((i * kWGThreads + wtid) % (NROW / 8)) * 8; };
       auto item_rn = [&](int i, int& r, int& n) {  // transposed item -> (tile row, position)
         const int gc = o_col0 + 8 * i;
         r = 2 * (gc / L1) + o_cp;
@@ -669,8 +863,8 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
       if (!STG && has_next && (STAGE || !GATED)) {
         int64_t hh2 = hh, bt2 = bt + kWG;
         while (bt2 >= nbt) { bt2 -= nbt; ++hh2; }
-        const int64_t base2 = (bt2 * C::R * H + phys_head(hh2)) * N;
-        const int left2 = int(B - bt2 * C::R < C::R ? B - bt2 * C::R : C::R);
+        const int64_t base2 = (bt2 * RR * H + phys_head(hh2)) * N;
+        const int left2 = int(B - bt2 * RR < RR ? B - bt2 * RR : RR);
         load_chunks(base2, left2, nu, nw);
       }
       wait_half(M64 ? 0 : slice);
@@ -690,14 +884,37 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
 #pragma unroll
         for (int i = 0; i < PER; ++i) tmem_ld8(tq + o_tcol + 8 * i, ob[i]);
         tmem_ld_wait();
+        if constexpr (DIT) {
+          // items i = inner rows p = q L0I + n0 at 8 n1 of column group n1c:
+          // samples n0 + L0I (n1 + 32 n2) of real row 2q + c', interleaved
+          const int n1c = 2 * o_hh + slice;
+          static_assert(PER == C::P, "order-3 epilogue 4 items");
+#pragma unroll
+          for (int q = 0; q < C::P / L0I; ++q) {
+            const int r = 2 * q + o_cp;
+            const int nb = L0I * (8 * n1c + 32 * o_n2);
+            uint32_t wd[4 * L0I];
+#pragma unroll
+            for (int t2 = 0; t2 < 4 * L0I; ++t2) {
+              const int a = 2 * t2, b = 2 * t2 + 1;  // samples nb + a, nb + b
+              wd[t2] = IO<S>::pack2(ob[q * L0I + a % L0I][a / L0I], ob[q * L0I + b % L0I][b / L0I]);
+            }
+#pragma unroll
+            for (int v4 = 0; v4 < L0I; ++v4) {
+              const uint32_t off = uint32_t(r * NROW + nb + 8 * v4) * sizeof(S);
+              st_shared_v4(sstg + swz128(off), wd[4 * v4], wd[4 * v4 + 1], wd[4 * v4 + 2], wd[4 * v4 + 3]);
+            }
+          }
+        } else {
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
           const float* o = ob[i];
           int r, n;
           item_rn(i, r, n);
-          const uint32_t off = uint32_t(r * C::NOUT + n) * sizeof(S);
+          const uint32_t off = uint32_t(r * NROW + n) * sizeof(S);
           st_shared_v4(sstg + swz128(off), IO<S>::pack2(o[0], o[1]), IO<S>::pack2(o[2], o[3]),
                        IO<S>::pack2(o[4], o[5]), IO<S>::pack2(o[6], o[7]));
+        }
         }
         stamp(16);
         if (tma_out) {
@@ -705,7 +922,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
           tc_fence_before();
           wg_sync();
           if (wtid == 0) {
-            tma_store_4d(&prm.tmap_y, sYS, 0, 0, int(h), int(bt * C::R));
+            tma_store_4d(&prm.tmap_y, sYS, 0, 0, int(h), int(bt * RR));
             bulk_commit();
             ys_pending = true;
             if (t + kWG >= t1) {  // no further tile of this warpgroup: hand over now
@@ -723,7 +940,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
 #pragma unroll
         for (int i = 0; i < OCH; ++i) {
           const int r = och_r(i), n = och_n(i);
-          const uint32_t off = uint32_t(r * C::NOUT + n) * sizeof(S);
+          const uint32_t off = uint32_t(r * NROW + n) * sizeof(S);
           uint4 st;
           if constexpr (GATED && std::is_same<T, __half>::value) {
             // fp16 y * fp16 v: HMUL2 rounds the exact product once, the same
@@ -754,7 +971,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         wg_sync();  // staging reads done before bufX takes the next tile's operand
         if (STG && filler()) {
           if (prm.tma_io)  // one tensor store (rows past B are clipped)
-            tma_store_4d(&prm.tmap_yo, sY, 0, 0, int(h), int(bt * C::R));
+            tma_store_4d(&prm.tmap_yo, sY, 0, 0, int(h), int(bt * RR));
           else
             for (int r = 0; r < rows_left; ++r) bulk_s2g(gy + tile_base + int64_t(r) * HN, sY + r * F::ROW_BYTES, F::ROW_BYTES);
           bulk_commit();
@@ -784,8 +1001,8 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
         if (GATED && has_next) {  // (plain tiles prefetched these before the wait)
           int64_t hh2 = hh, bt2 = bt + kWG;
           while (bt2 >= nbt) { bt2 -= nbt; ++hh2; }
-          const int64_t base2 = (bt2 * C::R * H + phys_head(hh2)) * N;
-          const int left2 = int(B - bt2 * C::R < C::R ? B - bt2 * C::R : C::R);
+          const int64_t base2 = (bt2 * RR * H + phys_head(hh2)) * N;
+          const int left2 = int(B - bt2 * RR < RR ? B - bt2 * RR : RR);
           load_chunks(base2, left2, nu, nw);
         }
         tc_fence_before();
@@ -804,14 +1021,13 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED>::THREADS, 1) fftconv
 }
 
 // ------------------------------------------------------------------ launch
-template <int L1, bool CAUSAL, bool GATED, typename T>
+template <int L1, bool CAUSAL, bool GATED, typename T, int L0I = 1>
 static cudaError_t launch_o2(const FwdParams& prm, cudaStream_t stream) {
-  using C = O2Cfg<L1, CAUSAL>;
-  using F = FwdCfg<L1, CAUSAL, GATED>;
-  auto kern = fftconv_fwd_o2_kernel<L1, CAUSAL, GATED, T>;
+  using F = FwdCfg<L1, CAUSAL, GATED, L0I>;
+  auto kern = fftconv_fwd_o2_kernel<L1, CAUSAL, GATED, T, L0I>;
   static int attr[64] = {0};
   if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(F::SMEM), attr)) return e;
-  const int64_t nbt = (prm.B + C::R - 1) / C::R;
+  const int64_t nbt = (prm.B + F::RR - 1) / F::RR;
   const int64_t tiles = (prm.row_map ? (prm.H / prm.row_L0) * prm.nrow : prm.H) * nbt;
   int grid = int(tiles < prm.num_sms ? tiles : prm.num_sms);
   if (grid < 1) return cudaSuccess;
@@ -821,6 +1037,11 @@ static cudaError_t launch_o2(const FwdParams& prm, cudaStream_t stream) {
 
 template <bool CAUSAL, bool GATED, typename T>
 static cudaError_t dispatch_l1(const FwdParams& prm, cudaStream_t s) {
+  if constexpr (CAUSAL) {  // single-pass order 3 (fft_size 4096 / 8192)
+    if (prm.L0I == 2) return prm.L1 == 32 ? launch_o2<32, true, GATED, T, 2>(prm, s) : cudaErrorInvalidValue;
+    if (prm.L0I == 4) return prm.L1 == 32 ? launch_o2<32, true, GATED, T, 4>(prm, s) : cudaErrorInvalidValue;
+  }
+  if (prm.L0I > 1) return cudaErrorInvalidValue;
   switch (prm.L1) {
     case 8: return launch_o2<8, CAUSAL, GATED, T>(prm, s);
     case 16: return launch_o2<16, CAUSAL, GATED, T>(prm, s);

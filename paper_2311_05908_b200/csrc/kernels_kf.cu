@@ -115,8 +115,19 @@ FC_DEVICE void stockham_pass_ct(float2* x, const float2* __restrict__ tw) {
 }
 template <int L>
 FC_DEVICE void fft_inplace_ct(float2* xs, const float2* tws) {
-  static_assert(L == 512 || L == 1024 || L == 2048, "compile-time FFT sizes");
-  if constexpr (L == 512) {  // 8 * 8 * 8
+  static_assert(L == 512 || L == 1024 || L == 2048 || L == 4096 || L == 8192, "compile-time FFT sizes");
+  if constexpr (L == 8192) {  // 2 * 8 * 8 * 8 * 8
+    stockham_pass_ct<2, L, 1>(xs, tws);
+    stockham_pass_ct<8, L, 2>(xs, tws);
+    stockham_pass_ct<8, L, 16>(xs, tws);
+    stockham_pass_ct<8, L, 128>(xs, tws);
+    stockham_pass_ct<8, L, 1024>(xs, tws);
+  } else if constexpr (L == 4096) {  // 8 * 8 * 8 * 8
+    stockham_pass_ct<8, L, 1>(xs, tws);
+    stockham_pass_ct<8, L, 8>(xs, tws);
+    stockham_pass_ct<8, L, 64>(xs, tws);
+    stockham_pass_ct<8, L, 512>(xs, tws);
+  } else if constexpr (L == 512) {  // 8 * 8 * 8
     stockham_pass_ct<8, L, 1>(xs, tws);
     stockham_pass_ct<8, L, 8>(xs, tws);
     stockham_pass_ct<8, L, 64>(xs, tws);
@@ -397,6 +408,110 @@ cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
     case 16: dk_cols_kernel<16><<<grid, 256, 0, s>>>(c); break;
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+// Single-pass order-3 plans (fft_size LF = L0 * 2048, L0 in {2, 4}): two
+// heads per CTA as above, the LF-point transform in shared memory with
+// twiddles W_LF^e from sincospif of the exact dyadic argument -2e/LF (this
+// precompute is not the hot path), written as L0 blocks per head: block k0
+// holds K_f[f' + 2048 k0], f' = k2 + 64 k1, in the fused kernel's [k2][k1/2]
+// padded layout (DIT order: the forward kernel's outer DFT produces the
+// frequency digit k0 = f / 2048).
+template <int LF>
+__global__ void __launch_bounds__(256) precompute_kf_dit_kernel(const KfParams prm) {
+  extern __shared__ float2 sm[];  // padded LF data + LF twiddles
+  constexpr int PL = LF + LF / 8;
+  float2* tws = sm + PL;
+  const int64_t h0 = 2 * int64_t(blockIdx.x);
+  const bool has1 = h0 + 1 < prm.H;
+  const int K = int(prm.K);
+  for (int e = threadIdx.x; e < LF; e += 256) {
+    float sn, cs;
+    sincospif(-2.0f * float(e) / float(LF), &sn, &cs);
+    tws[pd(e)] = make_float2(cs, sn);
+  }
+  const float* k0row = prm.k + h0 * K;
+  const float* k1row = k0row + K;
+  for (int n = threadIdx.x; n < LF; n += 256)
+    sm[pd(n)] = n < K ? make_float2(k0row[n], has1 ? k1row[n] : 0.f) : make_float2(0.f, 0.f);
+  __syncthreads();
+  fft_inplace_ct<LF>(sm, tws);
+  const float2* xs = sm;
+  constexpr int L0 = LF / 2048, CPR = 16;  // L1 = 32: 16 pairs per k2 row
+  const size_t hbytes = size_t(64) * tab_stride(CPR);  // one block
+  uint8_t* out0 = reinterpret_cast<uint8_t*>(prm.kf) + h0 * int64_t(L0 * hbytes);
+  uint8_t* out1 = out0 + L0 * hbytes;
+  for (int q = threadIdx.x; q < L0 * 64 * CPR; q += blockDim.x) {
+    const int k0 = q / (64 * CPR), qr = q % (64 * CPR);
+    const int w = qr >> 5, lane = qr & 31;
+    const int k2 = (w % 8) * 8 + (lane & 7);
+    const int k1 = 2 * ((w / 8) * 4 + (lane >> 3));
+    const int f0 = k2 + 64 * k1 + 2048 * k0, f1 = f0 + 64;
+    const float2 z0 = xs[pd(f0)], z1 = xs[pd(f1)], m0 = xs[pd((LF - f0) & (LF - 1))], m1 = xs[pd((LF - f1) & (LF - 1))];
+    const float2 a0 = make_float2(0.5f * (z0.x + m0.x), 0.5f * (z0.y - m0.y));
+    const float2 a1 = make_float2(0.5f * (z1.x + m1.x), 0.5f * (z1.y - m1.y));
+    const float2 b0 = make_float2(0.5f * (z0.y + m0.y), -0.5f * (z0.x - m0.x));
+    const float2 b1 = make_float2(0.5f * (z1.y + m1.y), -0.5f * (z1.x - m1.x));
+    const uint32_t off = uint32_t(k0 * hbytes) + tab_off_rt(CPR, uint32_t(k2), uint32_t(k1 / 2));
+    *reinterpret_cast<float4*>(out0 + off) = make_float4(a0.x, a1.x, a0.y, a1.y);
+    if (has1) *reinterpret_cast<float4*>(out1 + off) = make_float4(b0.x, b1.x, b0.y, b1.y);
+  }
+}
+
+cudaError_t launch_precompute_kf_dit(const KfParams& prm, int L0, cudaStream_t s) {
+  if (prm.H <= 0) return cudaSuccess;
+  const unsigned grid = unsigned((prm.H + 1) / 2);
+  if (L0 == 2) {
+    const size_t smem = size_t(2 * (4096 + 512)) * sizeof(float2);
+    static int attr[64] = {0};
+    if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_dit_kernel<4096>), int(smem), attr))
+      return e;
+    precompute_kf_dit_kernel<4096><<<grid, 256, smem, s>>>(prm);
+  } else if (L0 == 4) {
+    const size_t smem = size_t(2 * (8192 + 1024)) * sizeof(float2);
+    static int attr[64] = {0};
+    if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_dit_kernel<8192>), int(smem), attr))
+      return e;
+    precompute_kf_dit_kernel<8192><<<grid, 256, smem, s>>>(prm);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// The backward of an order-3 plan runs the multipass path, whose k_f layout
+// is L0 blocks per head with block k0 = K_f[k0 + L0 f']: gather it from the
+// order-3 layout (block f / 2048 at f % 2048), one float4 {re, re', im, im'}
+// of the destination per thread.
+__global__ void kf_dit_to_dif_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t H, int L0) {
+  constexpr int CPR = 16;
+  const size_t hb = size_t(64) * tab_stride(CPR);
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t per_head = int64_t(L0) * 64 * CPR;
+  if (idx >= H * per_head) return;
+  const int64_t h = idx / per_head;
+  const int rem = int(idx % per_head);
+  const int k0 = rem / (64 * CPR), k2 = (rem % (64 * CPR)) / CPR, kp = rem % CPR;
+  float v[4];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int f = k0 + L0 * (k2 + 64 * (2 * kp + s));
+    const int b = f / 2048, g = f % 2048;
+    const int k2s = g % 64, k1s = g / 64;
+    const float4 q = *reinterpret_cast<const float4*>(src + (h * L0 + b) * hb + tab_off_rt(CPR, uint32_t(k2s), uint32_t(k1s / 2)));
+    v[s] = (k1s & 1) ? q.y : q.x;
+    v[2 + s] = (k1s & 1) ? q.w : q.z;
+  }
+  *reinterpret_cast<float4*>(dst + (h * L0 + k0) * hb + tab_off_rt(CPR, uint32_t(k2), uint32_t(kp))) =
+      make_float4(v[0], v[1], v[2], v[3]);
+}
+
+cudaError_t launch_kf_dit_to_dif(const void* src, void* dst, int64_t H, int L0, cudaStream_t s) {
+  const int64_t n = H * int64_t(L0) * 64 * 16;
+  if (n == 0) return cudaSuccess;
+  kf_dit_to_dif_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(static_cast<const uint8_t*>(src),
+                                                                 static_cast<uint8_t*>(dst), H, L0);
   return cudaGetLastError();
 }
 

@@ -390,6 +390,28 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
     p->KA = 64;  // the inner transform is circular over complex rows
     p->P = 4;
     build_fused_tables(p, p->Lp);
+    // single-pass order 3 for causal fft_size 4096 / 8192 (N = 2K, 4K): the
+    // whole row pair stays on chip (decimated inner rows z[n0 + L0 n'] are
+    // the tile's complex rows, the outer DFT_L0 runs in the fused kernel's
+    // pointwise step).  Not for partial, sparse (row skipping stays with the
+    // multipass passes) or fp32 validation plans; FFTCONV_DIT=0 disables it.
+    const char* dit_env = getenv("FFTCONV_DIT");
+    if (p->regime == REGIME_MULTIPASS && causal && fft_size == 2 * N && (L == 4096 || L == 8192) &&
+        dtype != FFTCONV_F32 && !sparsity && !(dit_env && dit_env[0] == '0')) {
+      fftconv_plan_s t;
+      t.L = 2048;
+      t.causal = 1;
+      t.L2 = 64;
+      t.L1 = 32;
+      t.KA = 32;
+      t.P = 4;
+      build_fused_tables(&t, 2048);
+      p->dit = int32_t(L / 2048);
+      p->dit_tab_off = align_up(p->image.size(), 1024);
+      p->image.resize(p->dit_tab_off, 0);
+      p->image.insert(p->image.end(), t.image.begin(), t.image.end());
+      p->order = 3;
+    }
     if (dtype == FFTCONV_F32 && p->nlev > 1) {
       delete p;
       set_last_error("fftconv_plan: the fp32 validation build supports fft_size <= 32768");
@@ -443,7 +465,12 @@ extern "C" fftconv_status_t fftconv_plan_info(fftconv_plan_t p, fftconv_plan_inf
   info->dtype = p->dtype;
   info->regime = p->regime;
   info->order = p->order;
-  if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
+  if (p->dit > 1) {  // order 3: L0 (outer, in the pointwise step) * L1 * L2
+    info->regime = REGIME_FUSED;
+    info->factors[0] = p->dit;
+    info->factors[1] = p->L1;
+    info->factors[2] = p->L2;
+  } else if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
     int i = 0;
     for (int l = 0; l < p->nlev && i < FFTCONV_MAX_ORDER - 2; ++l) info->factors[i++] = p->lev_L0[l];
     info->factors[i++] = p->L1;
@@ -452,7 +479,7 @@ extern "C" fftconv_status_t fftconv_plan_info(fftconv_plan_t p, fftconv_plan_inf
     info->factors[0] = p->L1;
     info->factors[1] = p->L2;
   }
-  info->rows_per_tile = 2 * p->P;
+  info->rows_per_tile = 2 * p->P / p->dit;
   info->max_kernel_len = p->causal ? p->L / 2 : p->L;
   info->table_bytes = p->image.size();
   info->kf_bytes_per_head = p->kf_bytes_per_head;

@@ -53,7 +53,8 @@ def test_plan_validation(lib):
     assert lib.fftconv_last_error() is not None
 
 
-@pytest.mark.parametrize("N,fft,causal", [(1024, 2048, 1), (8192, 16384, 1), (1 << 15, 1 << 16, 1),
+@pytest.mark.parametrize("N,fft,causal", [(1024, 2048, 1), (2048, 4096, 1), (4096, 8192, 1), (8192, 16384, 1),
+                                          (1 << 15, 1 << 16, 1),
                                           (1 << 20, 1 << 21, 1), (1 << 22, 1 << 23, 1), (1 << 23, 1 << 23, 0),
                                           (1 << 20, 16384, 1)])
 def test_plan_info_factors_cover_L(lib, N, fft, causal):

@@ -36,7 +36,7 @@ def _run(N, dtype, gated, B, H, seed=0):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("N", [256, 1024, 2048, 8192])
+@pytest.mark.parametrize("N", [256, 1024, 2048, 4096, 8192])
 @pytest.mark.parametrize("dtype,gated", [("f16", False), ("f16", True), ("bf16", True)])
 def test_bwd_parity(N, dtype, gated):
     got, ref = _run(N, dtype, gated, B=5, H=3)

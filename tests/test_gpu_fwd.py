@@ -162,6 +162,24 @@ def test_fwd_multipass_cfg3_shape_sampled():
     assert_parity(got, ref)
 
 
+# ---------------------------------------------------------------- single-pass order 3 (N = 2048, 4096)
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [2048, 4096])
+@pytest.mark.parametrize("dtype,gated", [("f16", False), ("f16", True), ("bf16", False), ("bf16", True)])
+def test_fwd_order3_single_pass(N, dtype, gated):
+    """fft_size 4096 / 8192 in ONE fused launch (plan order 3: the DFT over
+    the L0 = fft_size / 2048 decimated inner rows z[n0 + L0 n'] runs in the
+    pointwise step); B = 37 leaves a ragged last tile (2 or 4 rows per tile)."""
+    from paper_2311_05908_b200 import FFTConvPlan, launch_count_reset
+    plan = FFTConvPlan(N, dtype=TDT[dtype])
+    assert plan.info.order == 3 and plan.info.regime == 1
+    assert plan.info.factors == (N // 1024, 32, 64)
+    launch_count_reset()
+    got, ref = _run(N, True, dtype, gated, B=37, H=3, seed=31)
+    assert launch_count_reset() == 2  # precompute_kf + one convolution
+    _assert_close(got, ref)
+
+
 # ---------------------------------------------------------------- recursive multipass (N >= 32768)
 @pytest.mark.gpu
 @pytest.mark.parametrize("N", [32768, 262144])
@@ -213,7 +231,7 @@ def test_fwd_range_stress(N):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("N,K", [(1024, 300), (512, 17), (8192, 1000), (32768, 4097)])
+@pytest.mark.parametrize("N,K", [(1024, 300), (512, 17), (2048, 999), (4096, 33), (8192, 1000), (32768, 4097)])
 def test_fwd_full_causal_short_filter(N, K):
     """Full causal plans (fft_size = 2N) with a filter shorter than the
     input (Hyena-style K < N): k is zero-padded to fft_size in k_f, the
