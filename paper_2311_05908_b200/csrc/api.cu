@@ -214,6 +214,7 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     if (!ws) { set_last_error(std::string(fn) + ": multipass regime needs a workspace"); return FFTCONV_ERR_INVALID_ARG; }
     if (!aligned16(ws)) { set_last_error(std::string(fn) + ": workspace not 16-byte aligned"); return FFTCONV_ERR_MISALIGNED; }
     MpParams mp{};
+    mp.shift = p->headroom_shift;  // fp16 headroom pre-scale (top-level passes only)
     mp.u = u; mp.w = w; mp.v = v; mp.y = y; mp.ws = ws;
     mp.L0 = p->lev_L0[0];
     mp.wbase = reinterpret_cast<const float2*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.wbase);
@@ -658,6 +659,7 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   const uint8_t* tab = static_cast<const uint8_t*>(p->d_tables);
   DkParams dk{};
   dk.dk = d_dk;
+  dk.shift2 = 2 * p->headroom_shift;  // G and DC both carry 2^-shift
   dk.mask = p->sparse ? reinterpret_cast<const float*>(tab + p->tl.total) : nullptr;
   dk.twiddle = reinterpret_cast<const float2*>(tab + p->tl.wl);
   dk.H = H;
@@ -717,6 +719,7 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   const int64_t nbt_in = f32 ? bwd_f32_units_per_head(rows) : bwd_tiles_per_head(rows, p->L1);
   void* scratch = static_cast<uint8_t*>(part) + size_t(H) * p->L0 * size_t(nbt_in) * size_t(p->Lp) * 8;
   MpParams mp{};
+  mp.shift = p->headroom_shift;  // fp16 headroom pre-scale (top-level passes only)
   mp.wbase = reinterpret_cast<const float2*>(tab + p->tl.wbase);
   mp.wtab = reinterpret_cast<const float2*>(tab + p->tl.wtab);
   mp.B = Bv; mp.H = H; mp.N = p->N; mp.L0 = p->lev_L0[0]; mp.Lp = int32_t(p->L / p->lev_L0[0]);

@@ -118,6 +118,9 @@ struct MpParams {
   // backward of the partial conv: pass 1 loads only the second half of each
   // window (dc blocks); pass 3 overlap-adds neighbouring windows (dg)
   int32_t win_hi_only, ola;
+  // fp16 headroom of the intermediates (top level only): pass 1 scales its
+  // output by 2^-shift, pass 3 its result by 2^+shift (exact; 0 = none)
+  int32_t shift;
 };
 cudaError_t launch_mp_pass(const MpParams& prm, int pass, cudaStream_t s);
 
@@ -165,6 +168,7 @@ struct DkParams {
   int32_t nlev;
   int64_t Lfull;
   int32_t lev[4];  // device copy of lev_L0 (mask digit mapping)
+  int32_t shift2;  // dk *= 2^shift2 (undoes the headroom pre-scale of G and DC)
 };
 cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s);
 cudaError_t launch_mp_precompute_kf(const KfParams& prm, const int32_t* lev_L0, int nlev, int64_t Lfull,

@@ -36,6 +36,7 @@
 
 #include <type_traits>
 
+#include "dft_vec.cuh"
 #include "fused_common.cuh"
 #include "fwd_params.h"
 #include "launch_util.h"
@@ -609,6 +610,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
             dst[slot][jj] = __ldg(reinterpret_cast<const float4*>(kfh + k0_of(slot) * C::KF_BYTES +
                                                                   tab_off<L1 / 2>(k2, k1c * 4 + jj)));
       };
+      // all complex math on f32x2 pairs of consecutive k1 (FMUL2/FFMA2/FADD2)
       auto process = [&](int k1c, const float4 (&kf)[2][4]) {
         float re[2][8], im[2][8];
 #pragma unroll
@@ -616,81 +618,90 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
           tmem_ld8(tq + slot * NBF + k1c * 8, re[slot]);
           tmem_ld8(tq + slot * NBF + k1c * 8 + L1, im[slot]);
         }
-        // W_{32 L0I}^{n0 k1}, k1 = 8 k1c + e, per slot (n0)
-        float wr[2][8], wi[2][8];
+        // W_{32 L0I}^{n0 k1}, k1 = 8 k1c + e, per slot (n0), as pairs (e, e+1)
+        float2 wr[2][4], wi[2][4];
 #pragma unroll
         for (int slot = 0; slot < 2; ++slot) {
           const int n0 = n0_of(slot);
-          float2 b = wroot<32 * L0I>(n0 * 8 * k1c);
-          const float2 st = wroot<32 * L0I>(n0);
+          const float2 b0 = wroot<32 * L0I>(n0 * 8 * k1c), b1 = wroot<32 * L0I>(n0 * (8 * k1c + 1));
+          const float2 st2 = wroot<32 * L0I>(2 * n0);
+          float2 pr = make_float2(b0.x, b1.x), pi = make_float2(b0.y, b1.y);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            wr[slot][e] = b.x; wi[slot][e] = b.y;
-            b = make_float2(b.x * st.x - b.y * st.y, b.x * st.y + b.y * st.x);
+          for (int ee = 0; ee < 4; ++ee) {
+            wr[slot][ee] = pr; wi[slot][ee] = pi;
+            const float2 nr = fma2(pr, make_float2(st2.x, st2.x), mul2(pi, make_float2(-st2.y, -st2.y)));
+            pi = fma2(pr, make_float2(st2.y, st2.y), mul2(pi, make_float2(st2.x, st2.x)));
+            pr = nr;
           }
         }
         tmem_ld_wait();
+        constexpr float sc = 1.0f / float(L0I);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          float xr[2], xi[2];
+        for (int ee = 0; ee < 4; ++ee) {
+          const int e = 2 * ee;
+          float2 xr[2], xi[2];
 #pragma unroll
           for (int slot = 0; slot < 2; ++slot) {  // T = W^{n0 k1} Y
-            xr[slot] = re[slot][e] * wr[slot][e] - im[slot][e] * wi[slot][e];
-            xi[slot] = re[slot][e] * wi[slot][e] + im[slot][e] * wr[slot][e];
+            const float2 r2 = make_float2(re[slot][e], re[slot][e + 1]), i2 = make_float2(im[slot][e], im[slot][e + 1]);
+            xr[slot] = sub2(mul2(r2, wr[slot][ee]), mul2(i2, wi[slot][ee]));
+            xi[slot] = fma2(i2, wr[slot][ee], mul2(r2, wi[slot][ee]));
           }
-          float sr[2], si[2];
+          float2 sr[2], si[2];
           if constexpr (L0I == 2) {
-            sr[0] = xr[0] + xr[1]; si[0] = xi[0] + xi[1];
-            sr[1] = xr[0] - xr[1]; si[1] = xi[0] - xi[1];
+            sr[0] = add2(xr[0], xr[1]); si[0] = add2(xi[0], xi[1]);
+            sr[1] = sub2(xr[0], xr[1]); si[1] = sub2(xi[0], xi[1]);
           } else {
-            float pr[2], pi[2];
+            float2 tr[2], ti[2];  // S_b[n0lo] = T[0][n0lo] + (-1)^b T[1][n0lo]
 #pragma unroll
             for (int slot = 0; slot < 2; ++slot) {
-              pr[slot] = __shfl_xor_sync(0xffffffffu, xr[slot], 8);
-              pi[slot] = __shfl_xor_sync(0xffffffffu, xi[slot], 8);
-            }
-            float tr[2], ti[2];  // S_b[n0lo] = T[0][n0lo] + (-1)^b T[1][n0lo]
-#pragma unroll
-            for (int slot = 0; slot < 2; ++slot) {
-              tr[slot] = xb ? pr[slot] - xr[slot] : xr[slot] + pr[slot];
-              ti[slot] = xb ? pi[slot] - xi[slot] : xi[slot] + pi[slot];
+              const float2 pr = make_float2(__shfl_xor_sync(0xffffffffu, xr[slot].x, 8),
+                                            __shfl_xor_sync(0xffffffffu, xr[slot].y, 8));
+              const float2 pi = make_float2(__shfl_xor_sync(0xffffffffu, xi[slot].x, 8),
+                                            __shfl_xor_sync(0xffffffffu, xi[slot].y, 8));
+              tr[slot] = xb ? sub2(pr, xr[slot]) : add2(xr[slot], pr);
+              ti[slot] = xb ? sub2(pi, xi[slot]) : add2(xi[slot], pi);
             }
             // X[b + 2 kk] = S0 +- W_4^b S1, W_4^1 = -i
-            const float ur = xb ? ti[1] : tr[1], ui = xb ? -tr[1] : ti[1];
-            sr[0] = tr[0] + ur; si[0] = ti[0] + ui;
-            sr[1] = tr[0] - ur; si[1] = ti[0] - ui;
+            const float2 ur = xb ? ti[1] : tr[1], ui = xb ? make_float2(-tr[1].x, -tr[1].y) : ti[1];
+            sr[0] = add2(tr[0], ur); si[0] = add2(ti[0], ui);
+            sr[1] = sub2(tr[0], ur); si[1] = sub2(ti[0], ui);
           }
-          // * k_f[f' + 2048 k0]: kf[slot][e/2] = {kr_e, kr_e+1, ki_e, ki_e+1}
+          // * k_f[f' + 2048 k0] / L0I: kf[slot][ee] = {kr_e, kr_e+1, ki_e, ki_e+1}
 #pragma unroll
           for (int slot = 0; slot < 2; ++slot) {
-            const float4 q = kf[slot][e >> 1];
-            const float kr = (e & 1) ? q.y : q.x, ki = (e & 1) ? q.w : q.z;
-            const float zr = sr[slot] * kr - si[slot] * ki, zi = sr[slot] * ki + si[slot] * kr;
+            const float4 q = kf[slot][ee];
+            const float2 kr = make_float2(sc * q.x, sc * q.y), ki = make_float2(sc * q.z, sc * q.w);
+            const float2 nki = make_float2(-ki.x, -ki.y);
+            const float2 zr = fma2(si[slot], nki, mul2(sr[slot], kr));
+            const float2 zi = fma2(si[slot], kr, mul2(sr[slot], ki));
             sr[slot] = zr; si[slot] = zi;
           }
-          float ar[2], ai[2];
+          float2 ar[2], ai[2];
           if constexpr (L0I == 2) {
-            ar[0] = sr[0] + sr[1]; ai[0] = si[0] + si[1];
-            ar[1] = sr[0] - sr[1]; ai[1] = si[0] - si[1];
+            ar[0] = add2(sr[0], sr[1]); ai[0] = add2(si[0], si[1]);
+            ar[1] = sub2(sr[0], sr[1]); ai[1] = sub2(si[0], si[1]);
           } else {
             // R[0] = Z0 + Z1, R[1] = W_4^{-b} (Z0 - Z1), W_4^{-1} = +i
-            const float dr = sr[0] - sr[1], di = si[0] - si[1];
-            float rr[2], ri[2];
-            rr[0] = sr[0] + sr[1]; ri[0] = si[0] + si[1];
-            rr[1] = xb ? -di : dr; ri[1] = xb ? dr : di;
+            const float2 dr = sub2(sr[0], sr[1]), di = sub2(si[0], si[1]);
+            float2 rr[2], ri[2];
+            rr[0] = add2(sr[0], sr[1]); ri[0] = add2(si[0], si[1]);
+            rr[1] = xb ? make_float2(-di.x, -di.y) : dr; ri[1] = xb ? dr : di;
 #pragma unroll
             for (int slot = 0; slot < 2; ++slot) {
-              const float qr = __shfl_xor_sync(0xffffffffu, rr[slot], 8);
-              const float qi = __shfl_xor_sync(0xffffffffu, ri[slot], 8);
-              ar[slot] = xb ? qr - rr[slot] : rr[slot] + qr;
-              ai[slot] = xb ? qi - ri[slot] : ri[slot] + qi;
+              const float2 qr = make_float2(__shfl_xor_sync(0xffffffffu, rr[slot].x, 8),
+                                            __shfl_xor_sync(0xffffffffu, rr[slot].y, 8));
+              const float2 qi = make_float2(__shfl_xor_sync(0xffffffffu, ri[slot].x, 8),
+                                            __shfl_xor_sync(0xffffffffu, ri[slot].y, 8));
+              ar[slot] = xb ? sub2(qr, rr[slot]) : add2(rr[slot], qr);
+              ai[slot] = xb ? sub2(qi, ri[slot]) : add2(ri[slot], qi);
             }
           }
-          constexpr float sc = 1.0f / float(L0I);
 #pragma unroll
-          for (int slot = 0; slot < 2; ++slot) {  // conj twiddle, 1 / L0I
-            re[slot][e] = sc * (ar[slot] * wr[slot][e] + ai[slot] * wi[slot][e]);
-            im[slot][e] = sc * (ai[slot] * wr[slot][e] - ar[slot] * wi[slot][e]);
+          for (int slot = 0; slot < 2; ++slot) {  // conj twiddle
+            const float2 o_r = fma2(ai[slot], wi[slot][ee], mul2(ar[slot], wr[slot][ee]));
+            const float2 o_i = sub2(mul2(ai[slot], wr[slot][ee]), mul2(ar[slot], wi[slot][ee]));
+            re[slot][e] = o_r.x; re[slot][e + 1] = o_r.y;
+            im[slot][e] = o_i.x; im[slot][e + 1] = o_i.y;
           }
         }
 #pragma unroll

@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(256) dk_cols_kernel(const DkParams prm) {
 #pragma unroll
   for (int n0 = 0; n0 < L0; ++n0) {
     const int64_t t = int64_t(n) + int64_t(n0) * prm.Lp;
-    if (t < prm.K) prm.dk[h * prm.K + t] = x[n0].x;
+    if (t < prm.K) prm.dk[h * prm.K + t] = ldexpf(x[n0].x, prm.shift2);
   }
 }
 

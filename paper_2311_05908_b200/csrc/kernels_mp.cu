@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256, FC_PASS_MINB) mp_pass1_kernel(const MpPar
   }
   // twiddle W_L^{n' k0} (recurrence over k0 from W_L^{n'}), scale 1/sqrt(L0)
   const CV<C2> bw = twiddle_base<C2>(prm, n);
-  const float s = rsqrtf(float(L0));
+  const float s = ldexpf(rsqrtf(float(L0)), -prm.shift);  // (headroom pre-scale)
   CV<C2> tw;
 #pragma unroll
   for (int cc = 0; cc < C2; ++cc) {
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(256, FC_PASS_MINB) mp_pass3_kernel(const MpPar
       reinterpret_cast<const TT*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
   const TT* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
   const CV<C2> bw = twiddle_base<C2>(prm, n);
-  const float s = rsqrtf(float(L0));
+  const float s = ldexpf(rsqrtf(float(L0)), prm.shift);  // (undo the headroom pre-scale)
   CV<C2> tw;
 #pragma unroll
   for (int cc = 0; cc < C2; ++cc) {
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(256, 2) mp_pass1_sparse_kernel(const MpParams 
 #pragma unroll
       for (int cc = 0; cc < C2; ++cc) z[n0].i[cc] = z[n0 + L0 / 2].r[cc];
   }
-  const float s = rsqrtf(float(L0));
+  const float s = ldexpf(rsqrtf(float(L0)), -prm.shift);  // (headroom pre-scale)
   TT* __restrict__ Tre = reinterpret_cast<TT*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
   TT* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
   for (int q = 0; q < prm.nrow; ++q) {
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(256, 2) mp_pass3_sparse_kernel(const MpParams 
   const TT* __restrict__ Tre =
       reinterpret_cast<const TT*>(prm.ws) + ((2 * p) * prm.H * L0 + h * L0) * int64_t(prm.Lp) + n;
   const TT* __restrict__ Tim = Tre + prm.H * L0 * int64_t(prm.Lp);
-  const float s = rsqrtf(float(L0));
+  const float s = ldexpf(rsqrtf(float(L0)), prm.shift);  // (undo the headroom pre-scale)
   CV<C2> x[NOUT];
 #pragma unroll
   for (int m = 0; m < NOUT; ++m)
@@ -627,7 +627,7 @@ FC_DEVICE void pair_idft(const MpParams& prm, int64_t p, int64_t h, int n, const
     rr[k0] = *reinterpret_cast<const RawT*>(Tre + int64_t(k0) * prm.Lp);
     ri[k0] = *reinterpret_cast<const RawT*>(Tim + int64_t(k0) * prm.Lp);
   }
-  const float s = rsqrtf(float(L0));
+  const float s = ldexpf(rsqrtf(float(L0)), prm.shift);  // (undo the headroom pre-scale)
   CV<C2> tw;
 #pragma unroll
   for (int cc = 0; cc < C2; ++cc) {

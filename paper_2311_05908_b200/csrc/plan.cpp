@@ -448,6 +448,18 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
       std::memcpy(p->image.data() + p->row_map_off, p->row_map.data(), bytes);
     }
   }
+  // fp16 headroom: with unitary stages the largest intermediate of a row
+  // pair z = g_b + i g_{b+1} with |g| <= A is its DC bin, |Z_0| <= |z|_1 /
+  // sqrt(L) = A sqrt(L/2) (causal, N = L/2 nonzero samples) or A sqrt(2L)
+  // (circular).  Keep it <= 2^15 (half of fp16's range, margin for the
+  // k_f product) for A = 256 by an exact power-of-two pre-scale.
+  if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
+    const double amp = 256.0;
+    const double peak = amp * std::sqrt((causal ? 0.5 : 2.0) * double(L));
+    int sh = 0;
+    while (peak / std::ldexp(1.0, sh) > 32768.0) ++sh;
+    p->headroom_shift = p->dit > 1 ? 0 : sh;
+  }
   // complex fp32 [k2][k1/2] pairs with padded rows, one block per outer index k0
   p->kf_bytes_per_head = size_t(p->L0) * size_t(p->L2) * tab_stride(uint32_t(p->L1 / 2));
   p->ws_bytes_per_head = size_t(L) * 8;  // fp32 spectral accumulator for dk

@@ -52,6 +52,10 @@ struct fftconv_plan_s {
   // dit blocks per head, block k0 = K_f[f' + 2048 k0]; the backward runs the
   // multipass path on k_f re-laid out in its workspace.  1 = not used.
   int32_t dit = 1;
+  // fp16 headroom: multipass / partial plans pre-scale the first
+  // outer pass's output by 2^-headroom_shift (undone exactly by the last), so
+  // every fp16 intermediate stays finite for rows with max|g| <= 256
+  int32_t headroom_shift = 0;
   size_t dit_tab_off = 0;
   fc::TableLayout tl;
   std::vector<uint8_t> image;  // host copy of the table image

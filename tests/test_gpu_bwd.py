@@ -117,3 +117,26 @@ def test_bwd_circular_multipass(N):
         got = g[key].float().cpu().numpy().astype(np.float64)
         assert np.all(np.isfinite(got)), key
         assert_parity(got, ref[key], str(key))
+
+
+@pytest.mark.gpu
+def test_bwd_range_stress_headroom():
+    """Backward at N = 1M with u = const 64 (the g chain's DC bin, 64 *
+    sqrt(fft_size / 2) = 65536, exceeds fp16 without the plan's headroom
+    pre-scale) and k = delta + noise: du and dk against the oracle."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    N, B, H = 1 << 20, 2, 1
+    plan = FFTConvPlan(N, dtype=torch.float16, causal=True)
+    u = synth.quantize(np.full((B, H, N), 64.0), "f16")
+    dy = synth.quantize(synth.signal(14, "dy", B, H, N), "f16")
+    k = np.zeros((H, N))
+    k[0, 0] = 1.0
+    k[0, 1:] = 1e-2 * synth.normal(14, 9, np.arange(1), N - 1)[0] / np.sqrt(N)
+    k = k.astype(np.float32)
+    t = lambda a: torch.tensor(a, dtype=torch.float16, device="cuda")
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    g = plan.bwd(t(dy), t(u), kf, N)
+    torch.cuda.synchronize()
+    ref = orc.conv_bwd(dy, u, k.astype(np.float64))
+    assert_parity(g["du"].float().cpu().numpy(), ref["du"], "du")
+    assert_parity(g["dk"].cpu().numpy(), ref["dk"], "dk")
