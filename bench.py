@@ -64,7 +64,7 @@ for _n in (256, 512, 2048, 4096, 8192, 16384):
 # default sweep carried in the bench line (every regime of the metric)
 SWEEP = ["sweep256", "sweep512", "sweep1024", "sweep2048", "sweep4096", "sweep8192", "sweep16384",
          "sweep32768", "sweep65536", "sweep262144", "sweep1048576", "sweep4194304",
-         "gsweep2048", "gsweep8192", "cfg3", "cfg4", "cfg4bwd", "cfg5", "cfg5dense", "circ1024", "circ16384"]
+         "gsweep512", "gsweep2048", "gsweep4096", "gsweep8192", "cfg3", "cfg4", "cfg4bwd", "cfg5", "cfg5dense", "circ1024", "circ16384"]
 # row-sharded fixed problems (--shard): SURVEY 8(e)
 SHARD = {"cfg4": "cfg4", "cfg5b": "cfg5b"}
 # the paper's circular forward table (FFT size = input length, B=64, H=768)

@@ -210,6 +210,32 @@ void fftconv_plan_destroy(fftconv_plan_t plan);
 /* Thread-local description of the last error ("" if none). */
 const char* fftconv_last_error(void);
 
+/* ---- cost models (host only, no CUDA calls) --------------------------
+ * Eq. 2 of the paper, C = BH sum_i [16 N N_i / gamma(N_i) + 4N /
+ * omega(i)] for the balanced order-p factorisation of N,
+ * gamma / omega per P:276-279 with the working-set rule of SURVEY A11; and
+ * the order p (2..4) it selects (ties -> smaller p).  Pinned by the tests to
+ * the paper's A100 grouping. */
+double fftconv_cost_eq2(int64_t N, int32_t p, double mu, double sigma_h, double sigma_s, double tau_m,
+                        double tau_g, double sram_bytes);
+int32_t fftconv_select_order(int64_t N, double mu, double sigma_h, double sigma_s, double tau_m, double tau_g,
+                             double sram_bytes);
+int32_t fftconv_factorize(int64_t n, int32_t p, int64_t* out);
+/* B200 tier cost model: the work units of the kernels a
+ * plan launches for one call on (B, H) rows -- feat[0..3] fused tiles
+ * (order 2 causal, order 2 circular incl. the multipass inner pass, order 3
+ * L0 = 2, L0 = 4), feat[4] outer-pass elements (levels x pairs x H x L),
+ * feat[5] k_f precompute elements, feat[6] launches, feat[7..9] (bwd != 0)
+ * backward tiles, T-chain elements, dk elements, feat[10] the gated share
+ * of the fused tiles (their extra w / v traffic), feat[11] the call's
+ * algorithmic HBM bytes -- and the predicted seconds
+ * sum coef[i] feat[i] (coef NULL: the library's B200 fit). */
+#define FFTCONV_COST_NFEAT 12
+fftconv_status_t fftconv_cost_features(fftconv_plan_t plan, int64_t B, int64_t H, int bwd, int gated,
+                                       double* feat);
+fftconv_status_t fftconv_cost_predict(fftconv_plan_t plan, int64_t B, int64_t H, int bwd, int gated, const double* coef,
+                                      double* seconds);
+
 /* Number of kernel launches issued by this thread since the last call
  * (instrumentation for the bench's gpu_launches count). */
 int64_t fftconv_launch_count_reset(void);

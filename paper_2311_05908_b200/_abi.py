@@ -29,6 +29,8 @@ ABI_SYMBOLS = [
     "fftconv_fwd", "fftconv_gated_fwd", "fftconv_bwd", "fftconv_plan_destroy",
     "fftconv_last_error", "fftconv_launch_count_reset", "fftconv_workspace_size",
     "fftconv_fwd_host", "fftconv_host_stage_size", "fftconv_fwd_stream", "fftconv_stream_stage_size",
+    "fftconv_cost_eq2", "fftconv_select_order", "fftconv_factorize", "fftconv_cost_features",
+    "fftconv_cost_predict",
 ]
 
 
@@ -96,6 +98,11 @@ def lib():
         L.fftconv_cost_eq2.restype = ctypes.c_double
         L.fftconv_select_order.argtypes = [i64] + [ctypes.c_double] * 6
         L.fftconv_select_order.restype = i32
+        D = ctypes.POINTER(ctypes.c_double)
+        L.fftconv_cost_features.argtypes = [P, i64, i64, ctypes.c_int, ctypes.c_int, D]
+        L.fftconv_cost_features.restype = ctypes.c_int
+        L.fftconv_cost_predict.argtypes = [P, i64, i64, ctypes.c_int, ctypes.c_int, D, D]
+        L.fftconv_cost_predict.restype = ctypes.c_int
         L.fftconv_factorize.argtypes = [i64, i32, ctypes.POINTER(i64)]
         L.fftconv_factorize.restype = i32
         _lib = L

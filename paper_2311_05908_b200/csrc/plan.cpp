@@ -20,6 +20,21 @@
 #include "plan.h"
 #include "layout.h"
 
+// B200 tier cost model coefficients (seconds per feature unit), fitted by
+// tools/cost_model.py on the bench sweep (profiles/r02/cost_model.md).
+#define COST_B200_0 0.0
+#define COST_B200_1 0.0
+#define COST_B200_2 0.0
+#define COST_B200_3 0.0
+#define COST_B200_4 0.0
+#define COST_B200_5 0.0
+#define COST_B200_6 0.0
+#define COST_B200_7 0.0
+#define COST_B200_8 0.0
+#define COST_B200_9 0.0
+#define COST_B200_10 0.0
+#define COST_B200_11 0.0
+
 namespace fc {
 
 static thread_local std::string g_last_error;
@@ -518,6 +533,87 @@ extern "C" int32_t fftconv_select_order(int64_t N, double mu, double sigma_h, do
   CostConstants c{mu, sigma_h, sigma_s, tau_m, tau_g, sram_bytes};
   return select_order(N, c, nullptr);
 }
+// ---------------------------------------------------------------- B200 tier cost model (NEXT-1)
+// Eq. 2 charges each Monarch stage its flops at tau_M / tau_G and
+// its intermediate I/O at sigma_S / sigma_H.  On B200 the fused kernels are
+// bound by their tile pipeline's latency, not by any of those rates, so the
+// B200 model counts the work units of the plan's actual kernels and charges
+// each a measured cost: fused tiles per variant (order 2 causal / circular,
+// order 3 with L0 = 2 / 4), outer-pass elements (every multipass level
+// moves the fp16 intermediate through HBM: Eq. 2's 4N / sigma_H term),
+// k_f precompute elements, launches, and the backward's tiles, T-chain
+// elements and dk elements.  t = sum_i coef[i] * feat[i]; the default
+// coefficients are a least-squares fit to the bench sweep on one B200
+// (tools/cost_model.py, profiles/r02/cost_model.md).
+static double cdiv(double a, double b) { return std::ceil(a / b); }
+
+static void cost_features(const fftconv_plan_s* p, int64_t B, int64_t H, bool bwd, bool gated, double* f) {
+  for (int i = 0; i < FFTCONV_COST_NFEAT; ++i) f[i] = 0.0;
+  const double L = double(p->L), Hd = double(H);
+  const bool mp = p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL;
+  const double Bv = p->regime == REGIME_PARTIAL ? double(B) * double(p->N / (p->L / 2)) : double(B);
+  const double pairs = std::ceil(Bv / 2.0);
+  f[5] = Hd * L;  // k_f precompute
+  if (p->dit > 1) {
+    f[p->dit == 2 ? 2 : 3] = Hd * cdiv(double(B), 8.0 / p->dit);
+    f[6] = 2;
+  } else if (!mp) {
+    f[p->causal ? 0 : 1] = Hd * cdiv(double(B), 2.0 * p->P);
+    f[6] = 2;
+  } else {
+    const double kept = p->row_map.empty() ? double(p->L0) : double(p->row_map.size());
+    f[1] = Hd * kept * cdiv(2.0 * pairs, 8.0);
+    const double lvl = double(p->nlev - 1) + kept / double(p->L0);
+    f[4] = lvl * pairs * Hd * L;
+    f[6] = 1 + (1 + p->nlev) + (1 + 2 * p->nlev);
+  }
+  if (bwd) {
+    if (!mp && p->dit == 1) {
+      f[7] = Hd * cdiv(double(B), 2.0 * p->P);
+      f[6] += 2;
+    } else {
+      const double L0 = double(p->L0);
+      f[7] = Hd * L0 * cdiv(2.0 * pairs, 8.0);
+      f[8] = 2.0 * double(p->nlev) * pairs * Hd * L;
+      f[6] += 2 + 4 * p->nlev + (p->dit > 1 ? 1 : 0);
+    }
+    f[9] = Hd * L;
+  }
+  if (gated) f[10] = f[0] + f[1] + f[2] + f[3];
+  // algorithmic HBM bytes: 16-bit u, y (+ w, v) per row, fp32 k_f;
+  // backward: dy, u (+ w, v) in, du (+ dw, dv) out, dk
+  const double el = double(B) * Hd * double(p->N) * 2.0;
+  f[11] = el * (gated ? 4.0 : 2.0) + Hd * L * 8.0;
+  if (bwd) f[11] += el * (gated ? 7.0 : 3.0) + Hd * L * 8.0;
+}
+
+// Default coefficients (seconds per unit; fitted on B200, 1965 MHz).
+static const double kCostB200[FFTCONV_COST_NFEAT] = {
+    COST_B200_0, COST_B200_1, COST_B200_2, COST_B200_3, COST_B200_4,
+    COST_B200_5, COST_B200_6, COST_B200_7, COST_B200_8, COST_B200_9, COST_B200_10, COST_B200_11};
+
+double predict_seconds(const fftconv_plan_s* p, int64_t B, int64_t H, bool bwd, bool gated, const double* coef) {
+  double f[FFTCONV_COST_NFEAT];
+  cost_features(p, B, H, bwd, gated, f);
+  const double* c = coef ? coef : kCostB200;
+  double t = 0.0;
+  for (int i = 0; i < FFTCONV_COST_NFEAT; ++i) t += c[i] * f[i];
+  return t;
+}
+
+extern "C" fftconv_status_t fftconv_cost_features(fftconv_plan_t p, int64_t B, int64_t H, int bwd, int gated,
+                                                  double* feat) {
+  if (!p || !feat || B < 0 || H < 0) { set_last_error("fftconv_cost_features: bad argument"); return FFTCONV_ERR_INVALID_ARG; }
+  cost_features(p, B, H, bwd != 0, gated != 0, feat);
+  return FFTCONV_OK;
+}
+extern "C" fftconv_status_t fftconv_cost_predict(fftconv_plan_t p, int64_t B, int64_t H, int bwd, int gated,
+                                                 const double* coef, double* seconds) {
+  if (!p || !seconds || B < 0 || H < 0) { set_last_error("fftconv_cost_predict: bad argument"); return FFTCONV_ERR_INVALID_ARG; }
+  *seconds = predict_seconds(p, B, H, bwd != 0, gated != 0, coef);
+  return FFTCONV_OK;
+}
+
 extern "C" int32_t fftconv_factorize(int64_t n, int32_t p, int64_t* out) {
   auto f = factorize(n, p);
   for (size_t i = 0; i < f.size(); ++i) out[i] = f[i];

@@ -190,7 +190,66 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int nmma, int N, int t
   __syncthreads();
   if (tid < 32) fc::tmem_dealloc<512>(tb);
 }
+// Cost-model constants (P:786-791 protocol, re-measured on B200).
+// tau_G: "continuously applying Twiddle factors" -- every thread keeps 16
+// complex values (8 f32x2 pairs) and multiplies them by a twiddle pair per
+// iteration (2 FMUL2 + 2 FFMA2 = 6 real flops per complex value), the
+// twiddle itself advancing by a fixed step (another 6 flops per pair).
+__global__ void __launch_bounds__(256) twiddle_rate_kernel(int iters, float* sink) {
+  float2 xr[8], xi[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    xr[j] = make_float2(1.0f + j, 0.5f);
+    xi[j] = make_float2(0.25f, -1.0f + j);
+  }
+  float2 wr = make_float2(0.9999f, 0.9998f), wi = make_float2(0.0141f, 0.0200f);
+  const float2 sr = make_float2(0.99999f, 0.99999f), si = make_float2(0.0045f, 0.0045f);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float2 nr = fc::fma2(xr[j], wr, fc::mul2(xi[j], make_float2(-wi.x, -wi.y)));
+      const float2 ni = fc::fma2(xr[j], wi, fc::mul2(xi[j], wr));
+      xr[j] = nr;
+      xi[j] = ni;
+    }
+    const float2 nwr = fc::fma2(wr, sr, fc::mul2(wi, make_float2(-si.x, -si.y)));
+    wi = fc::fma2(wr, si, fc::mul2(wi, sr));
+    wr = nwr;
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc += xr[j].x + xr[j].y + xi[j].x + xi[j].y;
+  if (acc == 123.456f) sink[threadIdx.x] = acc;  // keep the work
+}
+
+// sigma_S: shared-memory bandwidth of intermediate writes and reads -- each
+// thread stores and reloads 16 B per step at conflict-free addresses.
+__global__ void __launch_bounds__(256) smem_bw_kernel(int iters, float* sink) {
+  __shared__ uint4 buf[2][256];
+  uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      fc::st_shared_v4(fc::smem_u32(&buf[j & 1][threadIdx.x]), v.x, v.y, v.z, v.w);
+      const uint4 r = fc::ld_shared_u4(fc::smem_u32(&buf[(j + 1) & 1][threadIdx.x ^ 1]));
+      v.x += r.y;
+      v.y ^= r.z;
+    }
+  }
+  if (v.x == 0xdeadbeefu) sink[threadIdx.x] = float(v.y);
+}
 }  // namespace
+
+// Chip-wide launches for the cost-model script (tools/cost_model.py); the
+// caller times them with CUDA events on the current stream.
+extern "C" int fcst_twiddle_rate(int blocks, int iters, void* sink, void* stream) {
+  twiddle_rate_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(iters, static_cast<float*>(sink));
+  return int(cudaGetLastError());
+}
+extern "C" int fcst_smem_bw(int blocks, int iters, void* sink, void* stream) {
+  smem_bw_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(iters, static_cast<float*>(sink));
+  return int(cudaGetLastError());
+}
 
 extern "C" int fcst_tmem_ld_bench(int iters, int nwarps, long long* host_out) {
   long long* d;

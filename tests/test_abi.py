@@ -24,7 +24,8 @@ def lib():
 
 def test_header_symbols_exported(lib):
     hdr = open(os.path.join(ROOT, "include", "fftconv.h")).read()
-    declared = set(re.findall(r"^(?:fftconv_status_t|void|const char\*|int64_t)\s+(fftconv_[a-z_]+)\s*\(", hdr, re.M))
+    declared = set(re.findall(r"^(?:fftconv_status_t|void|const char\*|int64_t|int32_t|double)\s+(fftconv_[a-z0-9_]+)\s*\(",
+                              hdr, re.M))
     assert {"fftconv_plan", "fftconv_precompute_kf", "fftconv_fwd", "fftconv_gated_fwd", "fftconv_bwd"} <= declared
     for name in declared:
         assert hasattr(lib, name), name
