@@ -22,18 +22,18 @@
 
 // B200 tier cost model coefficients (seconds per feature unit), fitted by
 // tools/cost_model.py on the bench sweep (profiles/r02/cost_model.md).
-#define COST_B200_0 0.0
-#define COST_B200_1 0.0
-#define COST_B200_2 0.0
-#define COST_B200_3 0.0
-#define COST_B200_4 0.0
-#define COST_B200_5 0.0
-#define COST_B200_6 0.0
-#define COST_B200_7 0.0
-#define COST_B200_8 0.0
-#define COST_B200_9 0.0
-#define COST_B200_10 0.0
-#define COST_B200_11 0.0
+#define COST_B200_0 1.438129e-08
+#define COST_B200_1 1.608477e-08
+#define COST_B200_2 1.932282e-08
+#define COST_B200_3 3.031798e-08
+#define COST_B200_4 3.096212e-12
+#define COST_B200_5 1.213060e-11
+#define COST_B200_6 1.121617e-05
+#define COST_B200_7 6.189846e-08
+#define COST_B200_8 3.296687e-12
+#define COST_B200_9 4.139593e-11
+#define COST_B200_10 0.000000e+00
+#define COST_B200_11 7.246451e-14
 
 namespace fc {
 
@@ -326,6 +326,8 @@ static fftconv_status_t build_mask(fftconv_plan_s* p, const fftconv_sparsity_t* 
 
 using namespace fc;
 
+double predict_seconds(const fftconv_plan_s* p, int64_t B, int64_t H, bool bwd, bool gated, const double* coef);
+
 extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t fft_size, fftconv_dtype_t dtype,
                                          int causal, const fftconv_sparsity_t* sparsity) {
   if (!out) { set_last_error("fftconv_plan: out is NULL"); return FFTCONV_ERR_INVALID_ARG; }
@@ -420,12 +422,21 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
       t.L1 = 32;
       t.KA = 32;
       t.P = 4;
-      build_fused_tables(&t, 2048);
+      // NEXT-1: the B200 tier cost model picks order 3 vs multipass for the
+      // paper's benchmark shape (B = 64, H = 768; the choice does not depend
+      // on B H beyond tile rounding)
+      const double t_mp = predict_seconds(p, 64, 768, false, false, nullptr);
       p->dit = int32_t(L / 2048);
-      p->dit_tab_off = align_up(p->image.size(), 1024);
-      p->image.resize(p->dit_tab_off, 0);
-      p->image.insert(p->image.end(), t.image.begin(), t.image.end());
-      p->order = 3;
+      const double t_dit = predict_seconds(p, 64, 768, false, false, nullptr);
+      if (t_dit < t_mp) {
+        build_fused_tables(&t, 2048);
+        p->dit_tab_off = align_up(p->image.size(), 1024);
+        p->image.resize(p->dit_tab_off, 0);
+        p->image.insert(p->image.end(), t.image.begin(), t.image.end());
+        p->order = 3;
+      } else {
+        p->dit = 1;
+      }
     }
     if (dtype == FFTCONV_F32 && p->nlev > 1) {
       delete p;

@@ -158,3 +158,42 @@ def test_f32_validation_plans(lib):
         assert rc == 0, (N, L)
         lib.fftconv_plan_destroy(h)
     assert _plan(lib, 32768, 65536, dtype=2)[0] == 5
+
+
+def test_b200_cost_model_predicts_sweep(lib):
+    """NEXT-1: the library's B200 tier cost model (default coefficients,
+    fitted by tools/cost_model.py) predicts every measured bench step within
+    +-20 % (tests/golden/b200_step_times.json: the sweep of one B200 run,
+    k_f precompute + convolution), and the planner uses it to choose the
+    single-pass order-3 regime at fft_size 4096 / 8192."""
+    import bench
+    from paper_2311_05908_b200 import _abi
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "b200_step_times.json")))
+    assert len(g["ms_per_step"]) >= 20
+    for name, ms in g["ms_per_step"].items():
+        wl = bench.WORKLOADS[name]
+        dt = {"f16": 0, "bf16": 1}[wl["dtype"]]
+        sp = None
+        if wl["sparse"]:
+            dims, keeps = bench.sparsity_spec(wl["sparse"], wl["fft"])
+            sp = _abi.Sparsity()
+            sp.ndims = len(dims)
+            bufs = []
+            for j, (d, kp) in enumerate(zip(dims, keeps)):
+                sp.dims[j] = int(d)
+                bufs.append((ctypes.c_uint8 * int(d))(*[1 if q else 0 for q in kp]))
+                sp.keep[j] = ctypes.cast(bufs[-1], ctypes.POINTER(ctypes.c_uint8))
+        h = ctypes.c_void_p()
+        assert lib.fftconv_plan(ctypes.byref(h), wl["N"], wl["fft"], dt, int(wl["causal"]),
+                                ctypes.byref(sp) if sp is not None else None) == 0
+        t = ctypes.c_double()
+        assert lib.fftconv_cost_predict(h, wl["B"], wl["H"], int(wl["bwd"]), int(wl["gated"]), None,
+                                        ctypes.byref(t)) == 0
+        lib.fftconv_plan_destroy(h)
+        assert abs(t.value * 1e3 / ms - 1) <= 0.20, (name, t.value * 1e3, ms)
+    for N in (2048, 4096):
+        rc, h = _plan(lib, N, 2 * N)
+        info = _abi.PlanInfo()
+        assert lib.fftconv_plan_info(h, ctypes.byref(info)) == 0
+        assert info.order == 3 and info.regime == 1
+        lib.fftconv_plan_destroy(h)
