@@ -245,3 +245,64 @@ def frequency_mask(dims, keeps) -> np.ndarray:
     L = k.size
     m = k | k[(L - np.arange(L)) % L]
     return m.astype(np.float64)
+
+
+# --------------------------------------------------------------------------
+# bidirectional (two-sided) long convolution -- SURVEY 8(f) NEXT-4, reading
+# B1 in DESIGN.md (the paper names M2-BERT, whose long
+# convolutions are bidirectional, but prints no formula for them)
+# --------------------------------------------------------------------------
+def conv_fwd_bidir(u, k_fwd, k_bwd, *, w=None, v=None):
+    """Bidirectional convolution, reading B1:
+
+        c[i] = sum_{j<=i} g[j] k_fwd[i-j]  +  sum_{j>=i} g[j] k_bwd[j-i]
+
+    (lag 0 carries k_fwd[0] + k_bwd[0]), g = u [* w], y = [v *] c.  Written
+    out as its two halves: the causal convolution of g with k_fwd (the
+    pinned conv_fwd) plus the time reverse of the causal convolution of the
+    reversed g with k_bwd.  u, w, v: (B, H, N); k_fwd, k_bwd: (H, K), K <= N.
+    Returns fp64 (B, H, N)."""
+    u = _f64(u)
+    g = u * _f64(w) if w is not None else u
+    c = conv_fwd(g, k_fwd) + conv_fwd(g[..., ::-1], k_bwd)[..., ::-1]
+    return c * _f64(v) if v is not None else c
+
+
+def conv_bwd_bidir(dy, u, k_fwd, k_bwd, *, w=None, v=None):
+    """Gradients of <y, dy> for conv_fwd_bidir: dc = dy [* v]; dg = the
+    adjoint of each half (conv_bwd of the causal half, time-reversed conv_bwd
+    of the anti-causal half); du = dg [* w]; dw = dg * u; dv = dy * c;
+    dk_fwd[t] = sum_b sum_i dc[i] g[i-t], dk_bwd[t] = sum_b sum_i dc[i]
+    g[i+t] (t < K).  Returns dict du, dw, dv, dk_fwd, dk_bwd."""
+    dy, u = _f64(dy), _f64(u)
+    g = u * _f64(w) if w is not None else u
+    dc = dy * _f64(v) if v is not None else dy
+    a = conv_bwd(dc, g, k_fwd)
+    b = conv_bwd(np.ascontiguousarray(dc[..., ::-1]), np.ascontiguousarray(g[..., ::-1]), k_bwd)
+    dg = a["du"] + b["du"][..., ::-1]
+    out = {"dk_fwd": a["dk"], "dk_bwd": b["dk"], "dw": None, "dv": None}
+    out["du"] = dg * _f64(w) if w is not None else dg
+    if w is not None:
+        out["dw"] = dg * u
+    if v is not None:
+        out["dv"] = dy * conv_fwd_bidir(u, k_fwd, k_bwd, w=w)
+    return out
+
+
+def direct_conv_bidir_py(g, k_fwd, k_bwd) -> np.ndarray:
+    """Pure-Python loops of the B1 definition (both sums written out), for
+    tiny inputs: an implementation independent of the FFT path."""
+    g = [float(x) for x in np.ravel(g)]
+    kf = [float(x) for x in np.ravel(k_fwd)]
+    kb = [float(x) for x in np.ravel(k_bwd)]
+    N = len(g)
+    out = []
+    for i in range(N):
+        s = 0.0
+        for j in range(N):
+            if 0 <= i - j < len(kf):
+                s += g[j] * kf[i - j]
+            if 0 <= j - i < len(kb):
+                s += g[j] * kb[j - i]
+        out.append(s)
+    return np.array(out)
