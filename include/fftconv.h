@@ -136,6 +136,21 @@ fftconv_status_t fftconv_plan_upload(fftconv_plan_t plan, void* d_tables, fftcon
 fftconv_status_t fftconv_precompute_kf(fftconv_plan_t plan, const float* d_k, int64_t H, int64_t K, void* d_kf,
                                        fftconv_stream_t stream);
 
+/* Bidirectional (two-sided) filters (the M2-BERT-style
+ * long convolution; the paper names M2-BERT, but prints no
+ * formula, so DESIGN.md reading B1 fixes it):
+ *     c[i] = sum_{j<=i} g[j] k_fwd[h, i-j] + sum_{j>=i} g[j] k_bwd[h, j-i]
+ * (lag 0 carries k_fwd[0] + k_bwd[0]).  With fft_size L = 2N and K <= N the
+ * two-sided filter k_fwd[t] + k_bwd[L - t] (t > L - K) is exactly the
+ * circular filter whose first N outputs are c, so k_f of it feeds the
+ * unchanged fftconv_fwd / fftconv_gated_fwd / fftconv_fwd_host calls.
+ * d_k_fwd, d_k_bwd: (H, K) fp32 device; d_kf: H * kf_bytes_per_head bytes.
+ * FFTCONV_ERR_UNSUPPORTED unless the plan is dense, causal and full
+ * (fft_size == 2N; partial and circular plans have no anti-causal room);
+ * other errors as fftconv_precompute_kf. */
+fftconv_status_t fftconv_precompute_kf_bidir(fftconv_plan_t plan, const float* d_k_fwd, const float* d_k_bwd,
+                                             int64_t H, int64_t K, void* d_kf, fftconv_stream_t stream);
+
 /* Device workspace the forward (for_bwd = 0) or backward (for_bwd = 1) call
  * needs for a (B, H) problem.  The fused regime's forward needs none; the
  * multipass and partial regimes (Alg. 4) keep their fp16
@@ -204,6 +219,16 @@ fftconv_status_t fftconv_stream_stage_size(fftconv_plan_t plan, int64_t B, int64
 fftconv_status_t fftconv_bwd(fftconv_plan_t plan, const void* d_dy, const void* d_u, const void* d_w,
                              const void* d_v, const void* d_kf, void* d_du, void* d_dw, void* d_dv, float* d_dk,
                              int64_t B, int64_t H, int64_t K, void* d_workspace, fftconv_stream_t stream);
+
+/* Backward of the bidirectional convolution (d_kf from
+ * fftconv_precompute_kf_bidir): as fftconv_bwd, with dk split into
+ * d_dk_fwd[h, t] = sum_b sum_i dc[i] g[i - t] and d_dk_bwd[h, t] =
+ * sum_b sum_i dc[i] g[i + t] (both (H, K) fp32, overwritten; lag 0 appears
+ * in both).  Same plans as fftconv_precompute_kf_bidir. */
+fftconv_status_t fftconv_bwd_bidir(fftconv_plan_t plan, const void* d_dy, const void* d_u, const void* d_w,
+                                   const void* d_v, const void* d_kf, void* d_du, void* d_dw, void* d_dv,
+                                   float* d_dk_fwd, float* d_dk_bwd, int64_t B, int64_t H, int64_t K,
+                                   void* d_workspace, fftconv_stream_t stream);
 
 void fftconv_plan_destroy(fftconv_plan_t plan);
 

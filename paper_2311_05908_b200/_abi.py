@@ -30,7 +30,7 @@ ABI_SYMBOLS = [
     "fftconv_last_error", "fftconv_launch_count_reset", "fftconv_workspace_size",
     "fftconv_fwd_host", "fftconv_host_stage_size", "fftconv_fwd_stream", "fftconv_stream_stage_size",
     "fftconv_cost_eq2", "fftconv_select_order", "fftconv_factorize", "fftconv_cost_features",
-    "fftconv_cost_predict",
+    "fftconv_cost_predict", "fftconv_precompute_kf_bidir", "fftconv_bwd_bidir",
 ]
 
 
@@ -77,6 +77,8 @@ def lib():
         L.fftconv_fwd.argtypes = [P, P, P, P, i64, i64, P, P]
         L.fftconv_gated_fwd.argtypes = [P, P, P, P, P, P, i64, i64, P, P]
         L.fftconv_bwd.argtypes = [P, P, P, P, P, P, P, P, P, P, i64, i64, i64, P, P]
+        L.fftconv_precompute_kf_bidir.argtypes = [P, P, P, i64, i64, P, P]
+        L.fftconv_bwd_bidir.argtypes = [P, P, P, P, P, P, P, P, P, P, P, i64, i64, i64, P, P]
         L.fftconv_workspace_size.argtypes = [P, i64, i64, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]
         L.fftconv_fwd_host.argtypes = [P, P, P, P, P, P, i64, i64, i64, P, ctypes.c_size_t, P]
         L.fftconv_fwd_host.restype = ctypes.c_int
@@ -88,7 +90,8 @@ def lib():
         L.fftconv_stream_stage_size.restype = ctypes.c_int
         L.fftconv_workspace_size.restype = ctypes.c_int
         for f in ("fftconv_plan", "fftconv_plan_info", "fftconv_plan_upload", "fftconv_precompute_kf",
-                  "fftconv_fwd", "fftconv_gated_fwd", "fftconv_bwd"):
+                  "fftconv_fwd", "fftconv_gated_fwd", "fftconv_bwd", "fftconv_precompute_kf_bidir",
+                  "fftconv_bwd_bidir"):
             getattr(L, f).restype = ctypes.c_int
         L.fftconv_plan_destroy.argtypes = [P]
         L.fftconv_plan_destroy.restype = None

@@ -140,8 +140,8 @@ cudaError_t make_tmap_sig(CUtensorMap* map, const void* base, int64_t B, int64_t
 }
 }  // namespace fc
 
-extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float* d_k, int64_t H, int64_t K,
-                                                  void* d_kf, fftconv_stream_t stream) {
+static fftconv_status_t run_precompute(fftconv_plan_t p, const float* d_k, const float* d_kb, int64_t H, int64_t K,
+                                       void* d_kf, fftconv_stream_t stream, bool bidir) {
   if (!p) { set_last_error("fftconv_precompute_kf: plan is NULL"); return FFTCONV_ERR_INVALID_ARG; }
   if (!p->d_tables) { set_last_error("fftconv_precompute_kf: plan tables not uploaded"); return FFTCONV_ERR_INVALID_ARG; }
   if (H < 0 || K < 1) { set_last_error("fftconv_precompute_kf: need H >= 0 and K >= 1"); return FFTCONV_ERR_INVALID_ARG; }
@@ -149,8 +149,17 @@ extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float*
   if (K > kmax) { set_last_error("fftconv_precompute_kf: kernel exceeds causal budget"); return FFTCONV_ERR_KERNEL_TOO_LONG; }
   if (H > 0 && (!d_k || !d_kf)) { set_last_error("fftconv_precompute_kf: NULL device pointer"); return FFTCONV_ERR_INVALID_ARG; }
   if (d_kf && !aligned16(d_kf)) { set_last_error("fftconv_precompute_kf: k_f not 16-byte aligned"); return FFTCONV_ERR_MISALIGNED; }
+  if (bidir) {  // bidirectional: full causal plans (fft_size = 2N), dense
+    if (H > 0 && !d_kb) { set_last_error("fftconv_precompute_kf_bidir: NULL device pointer"); return FFTCONV_ERR_INVALID_ARG; }
+    if (!p->causal || p->regime == REGIME_PARTIAL || p->L != 2 * p->N || p->sparse) {
+      set_last_error("fftconv_precompute_kf_bidir: needs a dense full causal plan (fft_size == 2N)");
+      return FFTCONV_ERR_UNSUPPORTED;
+    }
+  }
   KfParams prm{};
   prm.k = d_k;
+  prm.kb = d_kb;
+  prm.Lk = p->L;
   prm.kf = d_kf;
   prm.mask = p->sparse ? reinterpret_cast<const float*>(static_cast<const uint8_t*>(p->d_tables) + p->tl.total)
                        : nullptr;
@@ -179,6 +188,16 @@ extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float*
   }
   if (e != cudaSuccess) return cuda_fail("fftconv_precompute_kf", e);
   return FFTCONV_OK;
+}
+
+extern "C" fftconv_status_t fftconv_precompute_kf(fftconv_plan_t p, const float* d_k, int64_t H, int64_t K,
+                                                  void* d_kf, fftconv_stream_t stream) {
+  return run_precompute(p, d_k, nullptr, H, K, d_kf, stream, false);
+}
+
+extern "C" fftconv_status_t fftconv_precompute_kf_bidir(fftconv_plan_t p, const float* d_k_fwd, const float* d_k_bwd,
+                                                        int64_t H, int64_t K, void* d_kf, fftconv_stream_t stream) {
+  return run_precompute(p, d_k_fwd, d_k_bwd, H, K, d_kf, stream, true);
 }
 
 static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, const void* v, const void* kf,
@@ -634,11 +653,11 @@ static size_t bwd_ws_bytes(const fftconv_plan_s* p, int64_t B, int64_t H) {
   return size_t(H) * size_t(units) * size_t(p->L) * 8;
 }
 
-extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, const void* d_u, const void* d_w,
-                                        const void* d_v, const void* d_kf, void* d_du, void* d_dw, void* d_dv,
-                                        float* d_dk, int64_t B, int64_t H, int64_t K, void* d_workspace,
-                                        fftconv_stream_t stream) {
-  const char* fn = "fftconv_bwd";
+static fftconv_status_t run_bwd(fftconv_plan_t p, const void* d_dy, const void* d_u, const void* d_w,
+                                const void* d_v, const void* d_kf, void* d_du, void* d_dw, void* d_dv,
+                                float* d_dk, float* d_dkb, int64_t B, int64_t H, int64_t K, void* d_workspace,
+                                fftconv_stream_t stream, bool bidir) {
+  const char* fn = bidir ? "fftconv_bwd_bidir" : "fftconv_bwd";
   const bool gated = d_w != nullptr || d_v != nullptr;
   if (gated && !(d_w && d_v && d_dw && d_dv)) {
     set_last_error("fftconv_bwd: gated backward needs w, v, dw and dv");
@@ -650,15 +669,24 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   const int64_t kmax = p->causal ? p->L / 2 : p->L;
   if (K < 1 || K > kmax) { set_last_error("fftconv_bwd: K out of range"); return FFTCONV_ERR_KERNEL_TOO_LONG; }
   if (!d_dk && H > 0) { set_last_error("fftconv_bwd: dk is NULL"); return FFTCONV_ERR_INVALID_ARG; }
+  if (bidir) {
+    if (!d_dkb && H > 0) { set_last_error("fftconv_bwd_bidir: dk_bwd is NULL"); return FFTCONV_ERR_INVALID_ARG; }
+    if (!p->causal || p->regime == REGIME_PARTIAL || p->L != 2 * p->N || p->sparse) {
+      set_last_error("fftconv_bwd_bidir: needs a dense full causal plan (fft_size == 2N)");
+      return FFTCONV_ERR_UNSUPPORTED;
+    }
+  }
   if (H == 0) return FFTCONV_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (B == 0) {
     cudaError_t e = cudaMemsetAsync(d_dk, 0, size_t(H) * size_t(K) * sizeof(float), st);
+    if (e == cudaSuccess && d_dkb) e = cudaMemsetAsync(d_dkb, 0, size_t(H) * size_t(K) * sizeof(float), st);
     return e == cudaSuccess ? FFTCONV_OK : cuda_fail(fn, e);
   }
   const uint8_t* tab = static_cast<const uint8_t*>(p->d_tables);
   DkParams dk{};
   dk.dk = d_dk;
+  dk.dkb = d_dkb;
   dk.shift2 = 2 * p->headroom_shift;  // G and DC both carry 2^-shift
   dk.mask = p->sparse ? reinterpret_cast<const float*>(tab + p->tl.total) : nullptr;
   dk.twiddle = reinterpret_cast<const float2*>(tab + p->tl.wl);
@@ -799,6 +827,21 @@ extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, cons
   if (e != cudaSuccess) return cuda_fail(fn, e);
   g_launches += launches + 1 + nlev;
   return FFTCONV_OK;
+}
+
+extern "C" fftconv_status_t fftconv_bwd(fftconv_plan_t p, const void* d_dy, const void* d_u, const void* d_w,
+                                        const void* d_v, const void* d_kf, void* d_du, void* d_dw, void* d_dv,
+                                        float* d_dk, int64_t B, int64_t H, int64_t K, void* d_workspace,
+                                        fftconv_stream_t stream) {
+  return run_bwd(p, d_dy, d_u, d_w, d_v, d_kf, d_du, d_dw, d_dv, d_dk, nullptr, B, H, K, d_workspace, stream, false);
+}
+
+extern "C" fftconv_status_t fftconv_bwd_bidir(fftconv_plan_t p, const void* d_dy, const void* d_u, const void* d_w,
+                                              const void* d_v, const void* d_kf, void* d_du, void* d_dw, void* d_dv,
+                                              float* d_dk_fwd, float* d_dk_bwd, int64_t B, int64_t H, int64_t K,
+                                              void* d_workspace, fftconv_stream_t stream) {
+  return run_bwd(p, d_dy, d_u, d_w, d_v, d_kf, d_du, d_dw, d_dv, d_dk_fwd, d_dk_bwd, B, H, K, d_workspace, stream,
+                 true);
 }
 
 extern "C" fftconv_status_t fftconv_workspace_size(fftconv_plan_t p, int64_t B, int64_t H, int for_bwd, size_t* bytes) {

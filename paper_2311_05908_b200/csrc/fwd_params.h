@@ -65,7 +65,21 @@ struct KfParams {
   // recursive plans: outer level sizes (inner row r -> frequency digit k0(r))
   int32_t nlev;
   int32_t lev[4];
+  // bidirectional filters (reading B1): k_bwd (H, K) acts at lags -t; the
+  // two-sided filter of the length-Lk transform is k[t] + k_bwd[Lk - t]
+  // (t > Lk - K) with lag 0 = k[0] + k_bwd[0]; nullptr = causal filter only
+  const float* kb;
+  int64_t Lk;
 };
+// tap t (0 <= t < Lk) of head h's (two-sided) filter, zero-padded
+FC_HD_PARAMS float filter_tap(const KfParams& p, int64_t h, int64_t t) {
+  float v = t < p.K ? p.k[h * p.K + t] : 0.f;
+  if (p.kb) {
+    if (t == 0) v += p.kb[h * p.K];
+    else if (t > p.Lk - p.K) v = p.kb[h * p.K + (p.Lk - t)];
+  }
+  return v;
+}
 // frequency digit k0 + L0 f' of inner row r of a recursive plan: rows nest
 // level 0 outermost, frequencies have level 0 fastest
 FC_HD_PARAMS int32_t row_freq_digit(int32_t r, int32_t nlev, const int32_t* lev) {
@@ -169,7 +183,18 @@ struct DkParams {
   int64_t Lfull;
   int32_t lev[4];  // device copy of lev_L0 (mask digit mapping)
   int32_t shift2;  // dk *= 2^shift2 (undoes the headroom pre-scale of G and DC)
+  // bidirectional backward (reading B1): dk_bwd[t] = lag -t of the inverse
+  // transform, i.e. index (Lfull - t) mod Lfull; nullptr = not written
+  float* dkb;
 };
+// lag index t (0 <= t < Lfull) of the inverse transform of head h -> dk / dkb
+FC_HD_PARAMS void dk_emit(const DkParams& p, int64_t h, int64_t t, int64_t Lfull, float x) {
+  if (t < p.K) p.dk[h * p.K + t] = x;
+  if (p.dkb) {
+    if (t == 0) p.dkb[h * p.K] = x;
+    else if (t > Lfull - p.K) p.dkb[h * p.K + (Lfull - t)] = x;
+  }
+}
 cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s);
 cudaError_t launch_mp_precompute_kf(const KfParams& prm, const int32_t* lev_L0, int nlev, int64_t Lfull,
                                     size_t block_bytes, cudaStream_t s);

@@ -196,7 +196,11 @@ __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) 
     for (int i = 0; i < 8; ++i) {
       const int n = threadIdx.x + i * 256;
       kv[i] = make_float2(0.f, 0.f);
-      if (n < L && n < K) kv[i] = make_float2(k0row[n], has1 ? k1row[n] : 0.f);
+      if (prm.kb) {  // bidirectional: two-sided taps (reading B1)
+        if (n < L) kv[i] = make_float2(filter_tap(prm, h0, n), has1 ? filter_tap(prm, h0 + 1, n) : 0.f);
+      } else if (n < L && n < K) {
+        kv[i] = make_float2(k0row[n], has1 ? k1row[n] : 0.f);
+      }
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -340,6 +344,8 @@ __global__ void __launch_bounds__(256) dk_rows_kernel(const DkParams prm) {
   if (prm.L0 == 1) {
     float* dk = prm.dk + row * prm.K;
     for (int t = threadIdx.x; t < prm.K; t += blockDim.x) dk[t] = xs[pd(t)].x;
+    if (prm.dkb)  // bidirectional: lags -t at index L - t (t = 0 shared)
+      for (int t = threadIdx.x; t < prm.K; t += blockDim.x) prm.dkb[row * prm.K + t] = xs[pd((L - t) & (L - 1))].x;
   } else {
     float2* a = prm.scratch + row * L;
     for (int t = threadIdx.x; t < L; t += blockDim.x) a[t] = make_float2(xs[pd(t)].x, -xs[pd(t)].y);  // undo conj
@@ -376,7 +382,7 @@ __global__ void __launch_bounds__(256) dk_cols_kernel(const DkParams prm) {
 #pragma unroll
   for (int n0 = 0; n0 < L0; ++n0) {
     const int64_t t = int64_t(n) + int64_t(n0) * prm.Lp;
-    if (t < prm.K) prm.dk[h * prm.K + t] = ldexpf(x[n0].x, prm.shift2);
+    dk_emit(prm, h, t, int64_t(prm.L0) * prm.Lp, ldexpf(x[n0].x, prm.shift2));
   }
 }
 
@@ -434,7 +440,9 @@ __global__ void __launch_bounds__(256) precompute_kf_dit_kernel(const KfParams p
   const float* k0row = prm.k + h0 * K;
   const float* k1row = k0row + K;
   for (int n = threadIdx.x; n < LF; n += 256)
-    sm[pd(n)] = n < K ? make_float2(k0row[n], has1 ? k1row[n] : 0.f) : make_float2(0.f, 0.f);
+    sm[pd(n)] = prm.kb ? make_float2(filter_tap(prm, h0, n), has1 ? filter_tap(prm, h0 + 1, n) : 0.f)
+              : n < K  ? make_float2(k0row[n], has1 ? k1row[n] : 0.f)
+                       : make_float2(0.f, 0.f);
   __syncthreads();
   fft_inplace_ct<LF>(sm, tws);
   const float2* xs = sm;

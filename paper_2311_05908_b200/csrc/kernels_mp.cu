@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(256) mp_kf_cols_kernel(const KfParams prm, int
 #pragma unroll
   for (int n0 = 0; n0 < L0; ++n0) {
     const int64_t t = n + int64_t(n0) * Lrow;
-    z[n0] = make_float2(t < prm.K ? prm.k[h * prm.K + t] : 0.f, 0.f);
+    z[n0] = make_float2(prm.kb ? filter_tap(prm, h, t) : t < prm.K ? prm.k[h * prm.K + t] : 0.f, 0.f);
   }
   DftReg<L0, false>::run(z);
   float sn, cs;

@@ -117,6 +117,22 @@ class FFTConvPlan:
         _abi.check(_abi.lib().fftconv_precompute_kf(self._h, _ptr(k), H, K, _ptr(kf), _stream(k.device)))
         return kf
 
+    def precompute_kf_bidir(self, k_fwd: torch.Tensor, k_bwd: torch.Tensor, out: torch.Tensor | None = None):
+        """Bidirectional filters (reading B1): k_fwd, k_bwd (H, K) fp32 on
+        device -> opaque k_f of the two-sided filter, for fwd / gated_fwd."""
+        for k in (k_fwd, k_bwd):
+            if not (isinstance(k, torch.Tensor) and k.dtype == torch.float32 and k.is_cuda and k.dim() == 2):
+                raise ValueError("k_fwd and k_bwd must be (H, K) float32 CUDA tensors")
+        if k_fwd.shape != k_bwd.shape or k_fwd.device != k_bwd.device:
+            raise ValueError("k_fwd and k_bwd must have one shape and device")
+        k_fwd, k_bwd = k_fwd.contiguous(), k_bwd.contiguous()
+        H, K = k_fwd.shape
+        kf = out if out is not None else _aligned_empty(max(H, 1) * self.info.kf_bytes_per_head, k_fwd.device, 16)
+        self._check_kf(kf, H, k_fwd.device)
+        _abi.check(_abi.lib().fftconv_precompute_kf_bidir(self._h, _ptr(k_fwd), _ptr(k_bwd), H, K, _ptr(kf),
+                                                          _stream(k_fwd.device)))
+        return kf
+
     def _check_sig(self, *ts):
         """Signal tensors (B, H, N): plan dtype, contiguous, on one CUDA
         device, all the same shape (the C ABI takes raw pointers: a mismatch
@@ -263,6 +279,24 @@ class FFTConvPlan:
         _abi.check(_abi.lib().fftconv_bwd(self._h, _ptr(dy), _ptr(u), _ptr(w), _ptr(v), _ptr(kf), _ptr(du),
                                           _ptr(dw), _ptr(dv), _ptr(dk), B, H, K, _ptr(ws), _stream(u.device)))
         return {"du": du, "dw": dw, "dv": dv, "dk": dk}
+
+    def bwd_bidir(self, dy, u, kf, K, w=None, v=None):
+        """Gradients of <y, dy> for a bidirectional k_f: du, dw, dv, dk_fwd, dk_bwd."""
+        if (w is None) != (v is None):
+            raise ValueError("bwd_bidir: the gated backward needs both w and v")
+        self._check_sig(dy, u, w, v)
+        B, H, _ = u.shape
+        self._check_kf(kf, H, u.device)
+        du = torch.empty_like(u)
+        dw = torch.empty_like(u) if w is not None else None
+        dv = torch.empty_like(u) if v is not None else None
+        dkf = torch.empty(H, K, dtype=torch.float32, device=u.device)
+        dkb = torch.empty(H, K, dtype=torch.float32, device=u.device)
+        ws = self.workspace(B, H, for_bwd=True, device=u.device)
+        _abi.check(_abi.lib().fftconv_bwd_bidir(self._h, _ptr(dy), _ptr(u), _ptr(w), _ptr(v), _ptr(kf), _ptr(du),
+                                                _ptr(dw), _ptr(dv), _ptr(dkf), _ptr(dkb), B, H, K, _ptr(ws),
+                                                _stream(u.device)))
+        return {"du": du, "dw": dw, "dv": dv, "dk_fwd": dkf, "dk_bwd": dkb}
 
 
 def launch_count_reset() -> int:
