@@ -50,6 +50,12 @@ WORKLOADS = {
     "cfg5": _wl("cfg5: frequency-sparse causal conv B=8 H=768 N=16384 fp16, 75% of inner Monarch rows skipped",
                 8, 768, 16384, sparse="rows75"),
     "cfg5dense": _wl("cfg5 dense reference: causal conv B=8 H=768 N=16384 fp16", 8, 768, 16384),
+    "cfg5a": _wl("cfg5a: frequency-sparse causal conv B=8 H=768 N=16384 fp16, symmetric low-pass |f| < L/8 "
+                 "(mask 75%), 2 of 4 stage-B column chunks skipped", 8, 768, 16384, sparse="lowpass8"),
+    "sp1m91": _wl("frequency-sparse causal conv B=8 H=96 N=1048576 fp16, tab:sparsity_fraction a=b=c=d=16 "
+                  "on the 32x32x32x64 grid (P:1035, P:1053-1058)", 8, 96, 1 << 20, sparse="paper:16,16,16,16"),
+    "sp1m_lp": _wl("frequency-sparse causal conv B=8 H=96 N=1048576 fp16, symmetric low-pass |f| < L/8",
+                   8, 96, 1 << 20, sparse="lowpass8"),
     "cfg5b": _wl("cfg5b: causal conv B=8 H=96 N=4194304 fp16 (fft_size 8M, three outer levels)", 8, 96, 1 << 22),
 }
 for _n in (256, 512, 1024, 2048, 4096, 8192, 16384, 32768, 65536):
@@ -64,7 +70,7 @@ for _n in (256, 512, 2048, 4096, 8192, 16384):
 # default sweep carried in the bench line (every regime of the metric)
 SWEEP = ["sweep256", "sweep512", "sweep1024", "sweep2048", "sweep4096", "sweep8192", "sweep16384",
          "sweep32768", "sweep65536", "sweep262144", "sweep1048576", "sweep4194304",
-         "gsweep512", "gsweep2048", "gsweep4096", "gsweep8192", "cfg3", "cfg4", "cfg4bwd", "cfg5", "cfg5dense", "circ1024", "circ16384"]
+         "gsweep512", "gsweep2048", "gsweep4096", "gsweep8192", "cfg3", "cfg4", "cfg4bwd", "cfg5", "cfg5a", "cfg5dense", "sp1m_lp", "circ1024", "circ16384"]
 # row-sharded fixed problems (--shard): SURVEY 8(e)
 SHARD = {"cfg4": "cfg4", "cfg5b": "cfg5b"}
 # the paper's circular forward table (FFT size = input length, B=64, H=768)
@@ -91,6 +97,14 @@ def sparsity_spec(kind, fft):
         keep = np.zeros(L0, bool)
         keep[[0, 1, L0 // 2, L0 - 1]] = True
         return ([2048, L0], [np.ones(2048, bool), keep])
+    if kind == "lowpass8":  # keep f < L/8 (slowest digit of [16, L/16] < 2); Hermitian closure adds f > 7L/8
+        dims = [16, fft // 16]
+        return (dims, [np.arange(16) < 2, np.ones(fft // 16, bool)])
+    if kind.startswith("paper:"):  # tab:sparsity_fraction pattern: trailing a,b,c,d zeroed on 32x32x32x64
+        z = [int(x) for x in kind[6:].split(",")]
+        dims = [32, 32, 32, 64]
+        assert fft == int(np.prod(dims))
+        return (dims, [np.arange(d) < d - a for d, a in zip(dims, z)])
     raise ValueError(kind)
 
 

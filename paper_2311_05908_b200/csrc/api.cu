@@ -200,6 +200,15 @@ extern "C" fftconv_status_t fftconv_precompute_kf_bidir(fftconv_plan_t p, const 
   return run_precompute(p, d_k_fwd, d_k_bwd, H, K, d_kf, stream, true);
 }
 
+// frequency-sparse slow-digit skip of the fused kernel (plan.cpp build_mask)
+static void set_k1_skip(fftconv_plan_t p, FwdParams& prm) {
+  if (p->k1_chunks <= 0) return;
+  prm.kcn = p->k1_chunks;
+  prm.k1map = p->k1_map;
+  prm.off_gb = uint32_t(p->gb_sp);
+  prm.off_gbi = uint32_t(p->gbi_sp);
+}
+
 static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, const void* v, const void* kf,
                                 void* y, int64_t B, int64_t H, void* ws, fftconv_stream_t stream, const char* fn) {
   const bool gated = (w != nullptr);
@@ -289,6 +298,8 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
           if (tma_y_enabled() && p->dtype != FFTCONV_F32 &&
               make_tmap_rows(&in.tmap_y, ws, 2 * ((rows_c + 1) / 2), hc * p->L0, p->Lp, 8) == cudaSuccess)
             in.tma_y = 1;
+          // the inner tiles' input rows arrive by one TMA tensor load each
+          in.tma_io = make_tmap_sig(&in.tmap_u, ws, 2 * ((rows_c + 1) / 2), hc * p->L0, p->Lp, 8) == cudaSuccess;
           in.kf = static_cast<const uint8_t*>(kf) + size_t(h0) * p->kf_bytes_per_head;
           in.B = 2 * ((rows_c + 1) / 2); in.H = hc * p->L0; in.N = p->Lp;
           in.L1 = p->L1; in.causal = 0; in.gated = 0; in.dtype = 0;
@@ -303,6 +314,7 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
               in.nrow = int32_t(p->row_map.size());
               in.row_L0 = p->L0;
             }
+            set_k1_skip(p, in);
             e = launch_fwd_fused(in, st);
           }
           if (e != cudaSuccess) return cuda_fail(fn, e);
@@ -338,6 +350,7 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     FwdParams in{};
     in.u = Tin; in.y = Tin; in.kf = kf; in.tables = p->d_tables;
     if (tma_y_enabled() && make_tmap_rows(&in.tmap_y, Tin, rows, H * p->L0, p->Lp, 8) == cudaSuccess) in.tma_y = 1;
+    in.tma_io = make_tmap_sig(&in.tmap_u, Tin, rows, H * p->L0, p->Lp, 8) == cudaSuccess;
     in.B = rows; in.H = H * p->L0; in.N = p->Lp;
     in.L1 = p->L1; in.causal = 0; in.gated = 0; in.dtype = 0;
     in.num_sms = num_sms_current();
@@ -346,6 +359,7 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
       in.nrow = int32_t(p->row_map.size());
       in.row_L0 = p->L0;
     }
+    set_k1_skip(p, in);
     e = launch_fwd_fused(in, st);
     if (e != cudaSuccess) return cuda_fail(fn, e);
     for (int l = p->nlev - 1; l >= 1; --l) {
@@ -384,7 +398,10 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
       ok = make_tmap_sig(&prm.tmap_w, w, B, H, p->N, R) == cudaSuccess &&
            make_tmap_sig(&prm.tmap_v, v, B, H, p->N, R) == cudaSuccess;
     prm.tma_io = ok ? 1 : 0;
+  } else if (!p->causal && !gated && p->dtype != FFTCONV_F32) {  // circular plain: input rows by TMA
+    prm.tma_io = make_tmap_sig(&prm.tmap_u, u, B, H, p->N, 2 * p->P) == cudaSuccess;
   }
+  set_k1_skip(p, prm);
   cudaError_t e = p->dtype == FFTCONV_F32 ? launch_fwd_f32(prm, st) : launch_fwd_fused(prm, st);
   if (e != cudaSuccess) return cuda_fail(fn, e);
   g_launches += 1;

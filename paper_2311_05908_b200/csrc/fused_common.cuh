@@ -104,6 +104,18 @@ struct O2Cfg {
   static_assert(128 * 2 * KA * 2 <= BUFX_BYTES, "stage A operand fits in bufX");
 };
 
+// W_L^e = exp(-2 pi i e / L) (e reduced mod L to (-L/2, L/2]) with the
+// MUFU sin/cos: absolute error <= 2^-21.4 on [-pi, pi] (CUDA math API),
+// far below the fp16 operand rounding (2^-11) every stage applies.
+template <int L>
+FC_DEVICE float2 wroot(int e) {
+  e &= (L - 1);
+  if (e > L / 2) e -= L;
+  float sn, cs;
+  __sincosf(float(e) * (-6.28318530717958647692f / float(L)), &sn, &cs);
+  return make_float2(cs, sn);
+}
+
 FC_DEVICE void st_half8(uint32_t addr, const float* v) {
   st_shared_v4(addr, pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
                pack_half2(v[6], v[7]));

@@ -42,6 +42,13 @@ struct FwdParams {
   // single-pass order 3 (causal fft_size = L0I * 2048, L0I in {2, 4}): k_f
   // holds L0I blocks per head, block k0 = K_f[f' + 2048 k0]; 1 = order 2
   int32_t L0I;
+  // frequency-sparse slow-digit skip: only kcn chunks of 8 k1 columns
+  // (original chunk of kept chunk j = (k1map >> 2 j) & 3) run through stage
+  // B, the pointwise step and stage B^-1, with the compacted G_B / G_B^-1 at
+  // image offsets off_gb / off_gbi; kcn = 0: dense
+  int32_t kcn;
+  uint32_t k1map;
+  uint32_t off_gb, off_gbi;
 };
 // Encode a map of 16-bit signal rows (B, H, N), box of R rows of one head.
 cudaError_t make_tmap_sig(CUtensorMap* map, const void* base, int64_t B, int64_t H, int64_t N, int R);

@@ -27,34 +27,57 @@
 
 namespace fc {
 
+// Two independent warpgroups per CTA (as the forward kernel): each owns 256
+// TMEM columns (G spectrum in [0, 128), DC in [128, 256): stage B / B^-1 emit
+// re | im only, the negated plane a complex multiply needs is a register
+// negation) and its own k_f copy, operand buffer and reduction buffer; the
+// DFT tables are shared (G_B / G_B^-1 only their re | im rows; twiddles from
+// MUFU sin/cos and fp32 recurrences instead of tables).
 template <int L1, bool CAUSAL>
 struct BwdCfg {
   using C = O2Cfg<L1, CAUSAL>;
+  static constexpr int NBF = 2 * L1;                          // stage B / B^-1 N: re | im
+  static constexpr uint32_t GB_SM = uint32_t(NBF) * (2 * L1) * 2;
+  static constexpr uint32_t S_GA = 0;
+  static constexpr uint32_t S_GB = C::al(S_GA + C::GA_BYTES);
+  static constexpr uint32_t S_GBI = C::al(S_GB + GB_SM);
+  static constexpr uint32_t S_GAI = C::al(S_GBI + GB_SM);
+  static constexpr uint32_t TABLES = C::al(S_GAI + C::GAI_BYTES);  // full G_A^-1 (M = 128)
   static constexpr uint32_t RED_BYTES = 64 * (L1 * 8 + 16);  // tile partial spectrum, padded rows
-  static constexpr uint32_t OFF_KF = C::TABLES;
-  static constexpr uint32_t OFF_BUFX = C::al(OFF_KF + C::KF_BYTES);
-  static constexpr uint32_t OFF_RED = C::al(OFF_BUFX + C::BUFX_BYTES);
-  static constexpr uint32_t SMEM = C::al(OFF_RED + RED_BYTES) + 1024;
-  static constexpr uint32_t RD = 256;  // TMEM column base of the DC spectrum (G uses [0, 256))
+  static constexpr uint32_t WG_BYTES = C::al(C::KF_BYTES) + C::al(C::BUFX_BYTES) + C::al(RED_BYTES);
+  static constexpr uint32_t bytes_for(int wg) { return TABLES + wg * WG_BYTES + 1024; }  // + alignment slack
+  static constexpr int WG = bytes_for(2) <= 227 * 1024 ? 2 : 1;
+  static constexpr int THREADS = WG * kWGThreads;
+  static constexpr uint32_t SMEM = bytes_for(WG);
+  static constexpr uint32_t TMEM_COLS = 256;  // per warpgroup
+  static constexpr uint32_t RD = 128;         // TMEM column base of the DC spectrum (G uses [0, 128))
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert((C::P / 2) * NBF <= 128 && C::NA <= 128, "G and DC spectra in 128 TMEM columns each");
 };
 
 template <int L1, bool CAUSAL, bool GATE_IO, bool NEED_C, typename T>
-__global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const BwdParams prm) {
+__global__ void __launch_bounds__(BwdCfg<L1, CAUSAL>::THREADS, 1) fftconv_bwd_o2_kernel(const BwdParams prm) {
   using C = O2Cfg<L1, CAUSAL>;
   using BC = BwdCfg<L1, CAUSAL>;
   constexpr int L2 = C::L2;
+  constexpr int NBF = BC::NBF;
+  constexpr int kWG = BC::WG;
+  constexpr int kThreads = BC::THREADS;
   extern __shared__ uint8_t smem_raw[];
-  __shared__ uint64_t mma_bar[2];
+  __shared__ uint64_t mma_bars[kWG][2];
   __shared__ uint32_t tmem_slot;
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t sGA = base + C::OFF_GA, sGB = base + C::OFF_GB, sGBI = base + C::OFF_GBI,
-                 sGAI = base + C::OFF_GAI, sTW = base + C::OFF_TW, sTWT = base + C::OFF_TWT;
-  const uint32_t sKF = base + BC::OFF_KF, bufX = base + BC::OFF_BUFX, sRED = base + BC::OFF_RED;
+  const uint32_t sGA = base + BC::S_GA, sGB = base + BC::S_GB, sGBI = base + BC::S_GBI, sGAI = base + BC::S_GAI;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wg = int(warp_uniform(warp >> 3));
+  const int wtid = tid & (kWGThreads - 1);
   const int quad = warp & 3, slice = (warp >> 2) & 1;
   const int m = quad * 32 + lane;
+  const uint32_t sKF = base + BC::TABLES + wg * BC::WG_BYTES;
+  const uint32_t bufX = sKF + C::al(C::KF_BYTES), sRED = bufX + C::al(C::BUFX_BYTES);
+  uint64_t* mma_bar = mma_bars[wg];
+  const uint32_t bar_id = 1 + wg;
   const int64_t B = prm.B, H = prm.H, N = prm.N;
   const int64_t nbt = (B + C::R - 1) / C::R;
   const int64_t tiles = H * nbt;
@@ -72,21 +95,29 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
 
   {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.tables);
-    for (uint32_t o = tid * 16; o < C::TABLES; o += kWGThreads * 16) cp_async16(base + o, src + o, true);
+    auto seg = [&](uint32_t dst, uint32_t img_off, uint32_t bytes) {
+      for (uint32_t o = tid * 16; o < bytes; o += kThreads * 16) cp_async16(base + dst + o, src + img_off + o, true);
+    };
+    seg(BC::S_GA, C::OFF_GA, C::GA_BYTES);
+    seg(BC::S_GB, C::OFF_GB, BC::GB_SM);   // rows re | im (the first NBF rows)
+    seg(BC::S_GBI, C::OFF_GBI, BC::GB_SM);
+    seg(BC::S_GAI, C::OFF_GAI, C::GAI_BYTES);
     cp_async_commit();
   }
   if (tid == 0) {
-    mbar_init(&mma_bar[0], 1);
-    mbar_init(&mma_bar[1], 1);
+    for (int g = 0; g < kWG; ++g) {
+      mbar_init(&mma_bars[g][0], 1);
+      mbar_init(&mma_bars[g][1], 1);
+    }
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc<512>(&tmem_slot);
+  if (warp == 0) tmem_alloc<kWG * BC::TMEM_COLS>(&tmem_slot);
   cp_async_wait_all();
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = warp_uniform(tmem_slot);
+  const uint32_t tmem = warp_uniform(tmem_slot) + wg * BC::TMEM_COLS;
   const uint32_t tq = tmem + (uint32_t(quad * 32) << 16);
   uint32_t phase = 0;
   int64_t cur_h = -1;
@@ -101,11 +132,12 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
   const uint64_t dXAI = smem_desc(bufX, 128, C::SBO_XA);
   auto dadd = [](uint64_t d, uint32_t off) { return d + uint64_t(off >> 4); };
 
+  auto wg_sync = [&] { named_sync(bar_id, kWGThreads); };
   auto sync_and_issue = [&](auto&& issue_half) {
     fence_async_smem();
     tc_fence_before();
-    __syncthreads();
-    if (tid < 32 && elect_one()) {
+    wg_sync();
+    if (wtid < 32 && elect_one()) {
       tc_fence_after();
       issue_half(0);
       mma_commit(&mma_bar[0]);
@@ -127,7 +159,7 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
   constexpr int JC = L1 / 8;
   constexpr int RSTEP = kWGThreads / (KROWS * JC);
   const int64_t HN = H * N;
-  const int ld_n2 = tid % KROWS, ld_j = (tid / KROWS) % JC, ld_r0 = tid / (KROWS * JC);
+  const int ld_n2 = wtid % KROWS, ld_j = (wtid / KROWS) % JC, ld_r0 = wtid / (KROWS * JC);
   const int64_t ld_off0 = int64_t(ld_r0) * HN + int64_t(ld_n2 * JC + ld_j) * 8;
   // stage A^-1 output lane m = G_AI row (n2 half, c', n2 mod 32), see plan.cpp
   const int64_t st_off0 = int64_t((m >> 5) & 1) * HN + int64_t(L1) * ((m >> 6) * 32 + (m & 31));
@@ -203,9 +235,15 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
         tmem_ld16(tq + c0, re);
         tmem_ld16(tq + c0 + 32, im);
         if constexpr (C::NEG_A) tmem_ld16(tq + c0 + 64, ni);
+        // W_L^{n1 k2}, k2 = k20 .. k20 + 15: MUFU pair at k20, fp32 steps by W^{2 n1}
         float4 w[8];
+        {
+          const float2 a = wroot<C::L>(n1 * k20), b = wroot<C::L>(n1 * (k20 + 1));
+          w[0] = make_float4(a.x, b.x, a.y, b.y);
+          const float2 st = wroot<C::L>(2 * n1);
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) w[jj] = ld_shared_f4(sTW + tab_off<L2 / 2>(n1, k20 / 2 + jj));
+          for (int jj = 1; jj < 8; ++jj) w[jj] = cstep(w[jj - 1], st);
+        }
         tmem_ld_wait();
         if constexpr (!C::NEG_A) {
 #pragma unroll
@@ -223,12 +261,12 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
       }
     }
     sync_and_issue([&](int hh) {
-      constexpr uint32_t idesc = idesc_f16(128, C::NB, true, false);
+      constexpr uint32_t idesc = idesc_f16(128, NBF, true, false);
 #pragma unroll
       for (int gi = hh * (C::P / 4); gi < (hh + 1) * (C::P / 4); ++gi) {
 #pragma unroll
         for (int s = 0; s < 2 * L1 / 16; ++s)
-          mma_f16_ss(tmem + rb + gi * C::NB, dadd(dXB, gi * 2048 + 2 * s * C::LBO_B), dadd(dGB, 256 * s), idesc,
+          mma_f16_ss(tmem + rb + gi * NBF, dadd(dXB, gi * 2048 + 2 * s * C::LBO_B), dadd(dGB, 256 * s), idesc,
                      s > 0);
       }
     });
@@ -237,12 +275,12 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
   // ---- inverse stages B^-1, conj twiddle, A^-1 of the operand in bufX (TMEM [0, 256))
   auto inverse_BA = [&] {
     sync_and_issue([&](int hh) {
-      constexpr uint32_t idesc = idesc_f16(128, C::NB, false, false);
+      constexpr uint32_t idesc = idesc_f16(128, NBF, false, false);
 #pragma unroll
       for (int gi = hh * (C::P / 4); gi < (hh + 1) * (C::P / 4); ++gi) {
 #pragma unroll
         for (int s = 0; s < 2 * L1 / 16; ++s)
-          mma_f16_ss(tmem + gi * C::NB, dadd(dXBP, gi * 16 * C::SBO_BP + 256 * s), dadd(dGBI, 256 * s), idesc,
+          mma_f16_ss(tmem + gi * NBF, dadd(dXBP, gi * 16 * C::SBO_BP + 256 * s), dadd(dGBI, 256 * s), idesc,
                      s > 0);
       }
     });
@@ -254,15 +292,21 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
         const int gi = it / (L1 / 8), n1c = it % (L1 / 8);
         const int p = gi * 2 + (m >> 6);
         if (i == 0) wait_half(0);
-        const uint32_t col = gi * C::NB + n1c * 8;
+        const uint32_t col = gi * NBF + n1c * 8;
         float re[8], im[8], nr[8];
         tmem_ld8(tq + col, re);
         tmem_ld8(tq + col + L1, im);
-        tmem_ld8(tq + col + 2 * L1, nr);
+        // W^{n1 k2}, n1 = 8 n1c .. 8 n1c + 7: MUFU pair, fp32 steps by W^{2 k2}
         float4 w[4];
+        {
+          const float2 a = wroot<C::L>(8 * n1c * k2), c1 = wroot<C::L>(k2), c2 = wroot<C::L>(2 * k2);
+          w[0] = make_float4(a.x, a.x * c1.x - a.y * c1.y, a.y, a.x * c1.y + a.y * c1.x);
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) w[jj] = ld_shared_f4(sTWT + tab_off<L1 / 2>(k2, n1c * 4 + jj));
+          for (int jj = 1; jj < 4; ++jj) w[jj] = cstep(w[jj - 1], c2);
+        }
         tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) nr[e] = -re[e];
         cmulc8(re, im, nr, w);
         if (i == 0) wait_half(1);
         const int ng = (p * L1) / 8 + n1c;
@@ -324,22 +368,23 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
   };
 
   constexpr int NK1C = (L1 / 8) / 2 > 0 ? (L1 / 8) / 2 : 1;  // distinct k1 chunks per thread
-  int64_t h = t0 / nbt, bt = t0 % nbt;
+  // warpgroup wg processes tiles t0 + wg, t0 + wg + kWG, ...
+  int64_t h = (t0 + wg) / nbt, bt = (t0 + wg) % nbt;
   uint4 nxa[PER_ALL], nya[PER_ALL];  // g rows of the next tile (prefetched)
-  for (int64_t t = t0; t < t1; ++t, ++bt) {
+  for (int64_t t = t0 + wg; t < t1; t += kWG, bt += kWG) {
     while (bt >= nbt) { bt -= nbt; ++h; }
     const int64_t tile_base = (bt * C::R * H + h) * N;
     const int rows_left = int(B - bt * C::R < C::R ? B - bt * C::R : C::R);
     if (h != cur_h) {
       const uint8_t* src = gkf + h * int64_t(C::KF_BYTES);
-      for (uint32_t o = tid * 16; o < C::KF_BYTES; o += kWGThreads * 16) cp_async16(sKF + o, src + o, true);
+      for (uint32_t o = wtid * 16; o < C::KF_BYTES; o += kWGThreads * 16) cp_async16(sKF + o, src + o, true);
       cp_async_commit();
       cur_h = h;
     }
     uint4 xa[PER_ALL], ya[PER_ALL];
     // 1. G = FFT(g) (its rows were prefetched during the previous tile's
     // last epilogue)
-    if (t == t0) load_rows(gu, gw, GATE_IO, tile_base, rows_left, nxa, nya);
+    if (t == t0 + wg) load_rows(gu, gw, GATE_IO, tile_base, rows_left, nxa, nya);
     store_rows(nxa, nya, GATE_IO);
     cp_async_wait_all();
     forward_AB(0);
@@ -364,17 +409,18 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
         const int gi = it / (L1 / 8), k1c = it % (L1 / 8);
         const int ai = (k1c >> 1) % NK1C;  // k1c = slice + 2 * ai for L1 = 32
         const int row = gi * 128 + m;
-        const uint32_t col = gi * C::NB + k1c * 8;
+        const uint32_t col = gi * NBF + k1c * 8;
         float gr[8], gim[8], gni[8], dr[8], di[8];
         tmem_ld8(tq + col, gr);
         tmem_ld8(tq + col + L1, gim);
-        tmem_ld8(tq + col + 2 * L1, gni);
         tmem_ld8(tq + BC::RD + col, dr);
         tmem_ld8(tq + BC::RD + col + L1, di);
         float4 kf[4];
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) kf[jj] = ld_shared_f4(sKF + tab_off<L1 / 2>(k2, k1c * 4 + jj));
         tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) gni[e] = -gim[e];
         // acc += DC * conj(G): re = dr gr + di gi, im = di gr - dr gi (= di gr + dr (-gi))
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -423,10 +469,10 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
             }
           }
         }
-        __syncthreads();
+        wg_sync();
       }
       float2* part = reinterpret_cast<float2*>(prm.acc) + t * int64_t(C::L);
-      for (int q = tid; q < C::L; q += kWGThreads) part[q] = ld_shared_f2(sRED + (q % L2) * RS + (q / L2) * 8);
+      for (int q = wtid; q < C::L; q += kWGThreads) part[q] = ld_shared_f2(sRED + (q % L2) * RS + (q / L2) * 8);
     }
 
     // 4. (gated / inner) c = IFFT(X1)
@@ -443,11 +489,10 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
         const int it = slice + 2 * i;
         const int gi = it / (L1 / 8), k1c = it % (L1 / 8);
         const int row = gi * 128 + m;
-        const uint32_t col = BC::RD + gi * C::NB + k1c * 8;
-        float dr[8], di[8], dn[8];
+        const uint32_t col = BC::RD + gi * NBF + k1c * 8;
+        float dr[8], di[8];
         tmem_ld8(tq + col, dr);
         tmem_ld8(tq + col + L1, di);
-        tmem_ld8(tq + col + 2 * L1, dn);
         float4 kf[4];
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) kf[jj] = ld_shared_f4(sKF + tab_off<L1 / 2>(k2, k1c * 4 + jj));
@@ -459,23 +504,23 @@ __global__ void __launch_bounds__(kWGThreads, 1) fftconv_bwd_o2_kernel(const Bwd
         cmulc8(dr, di, nr, kf);
         st_half8(bufX + (row >> 3) * C::SBO_BP + k1c * 128 + (row & 7) * 16, dr);
         st_half8(bufX + (row >> 3) * C::SBO_BP + (L1 / 8 + k1c) * 128 + (row & 7) * 16, di);
-        (void)dn;
       }
     }
     inverse_BA();
-    if (t + 1 < t1) {  // prefetch the next tile's g rows behind the last epilogue
-      int64_t h2 = h, bt2 = bt + 1;
-      if (bt2 >= nbt) { bt2 = 0; ++h2; }
+    if (t + kWG < t1) {  // prefetch the next tile's g rows behind the last epilogue
+      int64_t h2 = h, bt2 = bt + kWG;
+      while (bt2 >= nbt) { bt2 -= nbt; ++h2; }
       const int64_t base2 = (bt2 * C::R * H + h2) * N;
       load_rows(gu, gw, GATE_IO, base2, int(B - bt2 * C::R < C::R ? B - bt2 * C::R : C::R), nxa, nya);
     }
     if (GATE_IO) epi_out(tile_base, rows_left, gw, gdu, gu, gdw, true);
     else epi_out(tile_base, rows_left, nullptr, gdu, nullptr, nullptr, false);
     tc_fence_before();
-    __syncthreads();
+    wg_sync();
   }
+  tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<512>(tmem);
+  if (warp == 0) tmem_dealloc<kWG * BC::TMEM_COLS>(warp_uniform(tmem_slot));
 }
 
 int64_t bwd_tiles_per_head(int64_t B, int L1) {
@@ -492,7 +537,7 @@ static cudaError_t launch_bwd_t(const BwdParams& prm, cudaStream_t s) {
   const int64_t tiles = prm.H * bwd_tiles_per_head(prm.B, L1);
   const int grid = int(tiles < prm.num_sms ? tiles : prm.num_sms);
   if (grid < 1) return cudaSuccess;
-  kern<<<grid, kWGThreads, BC::SMEM, s>>>(prm);
+  kern<<<grid, BC::THREADS, BC::SMEM, s>>>(prm);
   return cudaGetLastError();
 }
 

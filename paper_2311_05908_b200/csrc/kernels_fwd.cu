@@ -52,6 +52,24 @@ __device__ long long fc_trace_buf[8][64][24];
 #ifndef FC_NEG_B
 #define FC_NEG_B 0
 #endif
+#ifndef FC_A_FULL
+#define FC_A_FULL 1
+#endif
+#ifndef FC_EPI_PIPE
+#define FC_EPI_PIPE 0
+#endif
+#ifndef FC_EPI1_PIPE
+#define FC_EPI1_PIPE 0
+#endif
+#ifndef FC_CIRC_STG
+#define FC_CIRC_STG 1
+#endif
+#ifndef FC_CIRC_TS
+#define FC_CIRC_TS 1
+#endif
+#ifndef FC_AI_TS
+#define FC_AI_TS 0
+#endif
 
 // Shared-memory plan of the forward kernel: tables | per-warpgroup (k_f,
 // operand buffer) | staging.  Causal tiles move their rows with bulk (TMA)
@@ -62,6 +80,12 @@ template <int L1, bool CAUSAL, bool GATED, int L0I = 1>
 struct FwdCfg {
   using C = O2Cfg<L1, CAUSAL>;
   static constexpr bool STG = CAUSAL;
+  // circular plain tiles (the multipass inner pass) stage their input rows
+  // the same way (one TMA tensor load per tile into a slot shared in tile
+  // order, filled a tile ahead) instead of register loads issued in the
+  // previous tile's last epilogue
+  static constexpr bool CIN = !CAUSAL && !GATED && FC_CIRC_STG;
+  static constexpr bool STG_IN = STG || CIN;
   // L0I > 1 (single-pass order 3, causal only): the tile's P complex rows
   // are the L0I decimated inner rows z[n0 + L0I n'] of P / L0I row pairs;
   // real rows of length NROW = L0I * NOUT, RR = R / L0I rows per tile
@@ -82,48 +106,53 @@ struct FwdCfg {
   static constexpr uint32_t S_GB = C::al(S_GA + C::GA_BYTES);
   static constexpr uint32_t S_GBI = C::al(S_GB + GB_SM);
   static constexpr uint32_t S_GAI = C::al(S_GBI + GB_SM);
-  static constexpr uint32_t TABLES = C::al(S_GAI + C::GAI_FWD_BYTES);
+  // circular tiles keep G_A^-1 in TMEM (stage A^-1 reads its A operand
+  // there), not in shared memory
+  static constexpr bool GAI_TMEM = !CAUSAL && FC_CIRC_TS;
+  static constexpr uint32_t TABLES = C::al(S_GAI + (GAI_TMEM ? 0 : C::GAI_FWD_BYTES));
   static constexpr uint32_t ROW_BYTES = NROW * 2;  // one 16-bit input row
-  static constexpr uint32_t UW_BYTES = STG ? RR * ROW_BYTES * (GATED ? 2 : 1) : 0;
+  // one u [| w] input slot per warpgroup: a warpgroup refills its own slot
+  // for its next tile right after reading it (a whole tile of prefetch
+  // distance, past the HBM latency); v arrives in one slot shared in tile order
+  static constexpr uint32_t UW_BYTES = STG_IN ? RR * ROW_BYTES * (GATED ? 2 : 1) : 0;
   static constexpr uint32_t V_BYTES = STG ? RR * ROW_BYTES : 0;
+  // mbarriers + TMEM slot live at the end of the dynamic buffer (no static
+  // shared memory: the dynamic base is 1024-aligned, no alignment slack)
+  static constexpr uint32_t BAR_BYTES = 128;
   // per-warpgroup buffers: k_f copy (L0I = 1; the order-3 tiles read their
   // L0I k_f blocks from global memory / L2) and the operand buffer
   static constexpr uint32_t KF_SM = DIT ? 0 : C::al(C::KF_BYTES);
-  static constexpr uint32_t WG_BYTES = KF_SM + C::al(C::BUFX_BYTES);
+  // per warpgroup: [k_f | operand buffer bufX | u [| w] input slot]; the
+  // order-3 tiles keep one slot shared in tile order (measured: per-warpgroup
+  // slots made the gated order-3 kernel 20 % slower, the order-2 ones 2 %
+  // faster)
+  static constexpr bool SLOT_WG = !DIT && !CIN;
+  static constexpr uint32_t WG_BYTES = KF_SM + C::al(C::BUFX_BYTES) + (SLOT_WG ? C::al(UW_BYTES) : 0);
   // circular plain tiles (the multipass inner pass): y staging shared by
   // the warpgroups in tile order, leaving by one TMA tensor store each
   static constexpr uint32_t YS_BYTES = (!CAUSAL && !GATED) ? C::R * C::NOUT * 2 : 0;
   static constexpr uint32_t bytes_for(int wg) {
-    return C::al(C::al(C::al(TABLES + wg * WG_BYTES) + UW_BYTES) + V_BYTES) + YS_BYTES + 1024;  // + alignment slack
+    return C::al(C::al(C::al(TABLES + wg * WG_BYTES) + (SLOT_WG ? 0 : UW_BYTES)) + V_BYTES) + YS_BYTES + BAR_BYTES;
   }
   static constexpr int WG = bytes_for(2) <= 227 * 1024 ? 2 : 1;
   static constexpr int THREADS = WG * kWGThreads;
   static constexpr uint32_t OFF_WG = TABLES;
-  static constexpr uint32_t OFF_UW = C::al(OFF_WG + WG * WG_BYTES);
-  static constexpr uint32_t OFF_V = C::al(OFF_UW + UW_BYTES);
+  static constexpr uint32_t UW_IN_WG = KF_SM + C::al(C::BUFX_BYTES);  // the slot's offset in its warpgroup's block
+  static constexpr uint32_t OFF_UW = C::al(OFF_WG + WG * WG_BYTES);    // (shared slot, !SLOT_WG)
+  static constexpr uint32_t OFF_V = C::al(OFF_UW + (SLOT_WG ? 0 : UW_BYTES));
   static constexpr uint32_t OFF_YS = C::al(OFF_V + V_BYTES);
+  static constexpr uint32_t OFF_BAR = OFF_YS + YS_BYTES;
   static constexpr uint32_t SMEM = bytes_for(WG);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(GB_SM <= C::GB_BYTES, "G_B prefix");
 };
 
-// W_L^e = exp(-2 pi i e / L) (e reduced mod L to (-L/2, L/2]) with the
-// MUFU sin/cos: absolute error <= 2^-21.4 on [-pi, pi] (CUDA math API),
-// far below the fp16 operand rounding (2^-11) every stage applies.
-template <int L>
-FC_DEVICE float2 wroot(int e) {
-  e &= (L - 1);
-  if (e > L / 2) e -= L;
-  float sn, cs;
-  __sincosf(float(e) * (-6.28318530717958647692f / float(L)), &sn, &cs);
-  return make_float2(cs, sn);
-}
 
 // Each CTA runs kWG independent warpgroups; warpgroup g processes tiles
 // t0 + g, t0 + g + kWG, ... of the CTA's contiguous tile range, with its own
 // TMEM columns, mbarriers, named barrier, k_f copy and operand buffer, so one
 // warpgroup's MMAs, memory waits and barriers overlap the other's math.
-template <int L1, bool CAUSAL, bool GATED, typename T, int L0I>
+template <int L1, bool CAUSAL, bool GATED, typename T, int L0I, bool SKP>
 __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) fftconv_fwd_o2_kernel(const __grid_constant__ FwdParams prm) {
   using C = O2Cfg<L1, CAUSAL>;
   using F = FwdCfg<L1, CAUSAL, GATED, L0I>;
@@ -133,21 +162,53 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   constexpr int LF = C::L * L0I;   // the whole transform (fft_size)
   constexpr int kWG = F::WG;
   constexpr int kThreads = F::THREADS;
-  constexpr bool STG = F::STG;      // input staging by bulk copies
+  constexpr bool STG = F::STG;      // input staging by bulk copies (causal: + v slot, y by bulk stores)
+  constexpr bool STG_IN = F::STG_IN;  // input staging (causal or circular plain)
   constexpr int L2 = C::L2;
   constexpr bool TS = C::TS_BI;     // stage B^-1 data operand in TMEM
   constexpr int NBF = F::NBF;
   constexpr bool M64 = CAUSAL;      // stage A^-1 as M = 64 MMAs (rows n2 < L2/2 only)
+  // epilogues 2/3 prefetch the next item's TMEM load (experiment, off:
+  // within 0.5 % on causal tiles, 1-3 % slower on circular ones -- the extra
+  // live registers spill; the same for epilogue 1, FC_EPI1_PIPE: 1-9 % slower)
+  constexpr bool EPI_PIPE = FC_EPI_PIPE && !FC_NEG_B;
+  constexpr bool EPI1_PIPE = FC_EPI1_PIPE && !C::NEG_A && !DIT;  // epilogue 1 likewise
+  constexpr bool A_FULL = FC_A_FULL && !DIT;  // stage A as one MMA chain (measured: o2 -1.3 %, order 3 +2 %)
+  // circular tiles: stage A^-1 reads G_A^-1 from TMEM (loaded once per CTA
+  // into warpgroup 0's free columns [128, 192)) as one N = 128 MMA chain:
+  // a shared-memory A operand costs ~32 extra cycles per K = 16 MMA
+  // (tools/microbench.py) and both halves re-read it
+  // (Experiment, off: FC_AI_TS=1.  Measured on B200: circular tiles 4.5 %
+  // slower -- the single chain loses the half overlap of epilogue 4 --,
+  // causal order 2 within 0.5 %, and the order-3 L0I = 4 instance failed
+  // parity.)
+  // Causal tiles keep only rows n2 < L2/2 (64 of 128): two N = 64 chains,
+  // column half h against a copy of G_A^-1 rotated by 64 h rows (copy 1 in
+  // warpgroup 1's free columns), so the useful rows of half h land in lane
+  // quadrants 2h, 2h + 1 and every epilogue-4 thread keeps 32 columns
+  constexpr bool AI_TS = (FC_AI_TS && kWG == 2) || F::GAI_TMEM;
+  constexpr uint32_t GAI_COL = 128;
+  static_assert(!AI_TS || (C::TMEM_COLS == 256 && C::NA <= 128 && (C::P / 2) * NBF <= 128 && C::CA >= 192),
+                "TMEM columns [128, 192) of each warpgroup hold a G_A^-1 copy");
 
-  extern __shared__ uint8_t smem_raw[];
-  __shared__ uint64_t mma_bar[kWG][2];  // completion of the first / second half of a stage
-  __shared__ uint64_t stg_bar[2][2];   // [u|w slot, v slot][consuming warpgroup]: bulk copy landed
-  __shared__ uint64_t ys_bar;          // circular TMA-y staging: use j - 1 has been read (phase j - 1)
-  __shared__ uint32_t tmem_slot;
-  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;  // 1024-aligned
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  struct Bars {
+    uint64_t mma[2][2];  // [warpgroup]: completion of the first / second half of a stage
+    uint64_t stg[2][2];  // [u|w slot, v slot][consuming warpgroup]: bulk copy landed
+    uint64_t ys;         // circular TMA-y staging: use j - 1 has been read (phase j - 1)
+    uint32_t tmem_slot;
+  };
+  static_assert(sizeof(Bars) <= F::BAR_BYTES, "barrier block");
+  Bars& bb = *reinterpret_cast<Bars*>(smem_raw + F::OFF_BAR);
+  auto& mma_bar = bb.mma;
+  auto& stg_bar = bb.stg;
+  auto& ys_bar = bb.ys;
+  auto& tmem_slot = bb.tmem_slot;
+  const uint32_t base = smem_u32(smem_raw);
+  if (base & 1023u) __trap();  // operand layouts and the 128 B swizzle need 1024-byte alignment
   const uint32_t sGA = base + F::S_GA, sGB = base + F::S_GB, sGBI = base + F::S_GBI, sGAI = base + F::S_GAI;
   const uint32_t sYS = base + F::OFF_YS;
-  const uint32_t sUW = base + F::OFF_UW, sV = base + F::OFF_V;
+  const uint32_t sV = base + F::OFF_V;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wg = int(warp_uniform(warp >> 3));  // warpgroup
@@ -181,9 +242,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
       for (uint32_t o = tid * 16; o < bytes; o += kThreads * 16) cp_async16(base + dst + o, src + img_off + o, true);
     };
     seg(F::S_GA, C::OFF_GA, C::GA_BYTES);
-    seg(F::S_GB, C::OFF_GB, F::GB_SM);
-    seg(F::S_GBI, C::OFF_GBI, F::GB_SM);
-    seg(F::S_GAI, C::OFF_GAI, C::GAI_FWD_BYTES);
+    seg(F::S_GB, prm.kcn ? prm.off_gb : C::OFF_GB, F::GB_SM);  // (compacted copies: slow-digit skip)
+    seg(F::S_GBI, prm.kcn ? prm.off_gbi : C::OFF_GBI, F::GB_SM);
+    if (!F::GAI_TMEM) seg(F::S_GAI, C::OFF_GAI, C::GAI_FWD_BYTES);
     cp_async_commit();
   }
   if (tid == 0) {
@@ -202,6 +263,28 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (AI_TS) {
+    // G_A^-1 (128 rows (n2 half, c', n2 mod 32) x K = 2 L2 fp16, K-major
+    // canonical in the table image) -> TMEM lane = row, column j = K pair
+    // (2j, 2j + 1); warp w writes lanes of quadrant w & 3, K range quarter w >> 2
+    constexpr int KQ = 2 * L2 / (kThreads / 128);  // K elements per thread
+    const int k0 = (warp >> 2) * KQ;
+    const uint8_t* g = reinterpret_cast<const uint8_t*>(prm.tables) + C::OFF_GAI;
+#pragma unroll
+    for (int cp = 0; cp < (M64 ? 2 : 1); ++cp) {
+      const int r = ((warp & 3) * 32 + lane + 64 * cp) & 127;  // table row held by this lane in copy cp
+      const uint32_t tg = warp_uniform(tmem_slot) + cp * C::TMEM_COLS + GAI_COL + (uint32_t((warp & 3) * 32) << 16);
+#pragma unroll
+      for (int k = k0; k < k0 + KQ; k += 8) {
+        const uint4 v = *reinterpret_cast<const uint4*>(g + (r >> 3) * C::SBO_GAI + (k >> 3) * 128 + (r & 7) * 16);
+        tmem_st4(tg + k / 2, v.x, v.y, v.z, v.w);
+      }
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   const uint32_t tmem = warp_uniform(tmem_slot) + wg * C::TMEM_COLS;
   const uint32_t tq = tmem + (uint32_t(quad * 32) << 16);  // this warp's lane quadrant
   uint64_t* bars = mma_bar[wg];
@@ -219,6 +302,8 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
     const int64_t tbase = (tb * RR * H + phys_head(th)) * N;
     const int rows = int(B - tb * RR < RR ? B - tb * RR : RR);
     uint64_t* bar = &stg_bar[kind][(t - t0) % kWG];
+    const uint32_t sUW = F::SLOT_WG ? base + F::OFF_WG + uint32_t((t - t0) % kWG) * F::WG_BYTES + F::UW_IN_WG
+                                    : base + F::OFF_UW;  // the consumer's slot
     const int planes = (kind == 0 && GATED) ? 2 : 1;
     if (prm.tma_io) {  // one tensor copy per plane; rows past B arrive as zeros (full box counted)
       mbar_arrive_expect_tx(bar, uint32_t(RR * planes) * F::ROW_BYTES);
@@ -253,9 +338,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
     if (GATED) fill(1, t, th, tb);
     else mbar_arrive(&stg_bar[1][(t - t0) % kWG]);
   };
-  if (STG && tid == 0) {
-    fill(0, t0, t0 / nbt, t0 % nbt);
-    release_out(t0, t0 / nbt, t0 % nbt);
+  if (STG_IN && tid == 0) {
+    for (int64_t t = t0; t < t0 + (F::SLOT_WG ? kWG : 1) && t < t1; ++t) fill(0, t, t / nbt, t % nbt);
+    if (STG) release_out(t0, t0 / nbt, t0 % nbt);
   }
   // a thread other than the MMA issuer (warp 1 of the warpgroup) refills the slots
   auto filler = [&]() { return (wtid >> 5) == 1 && elect_one(); };
@@ -309,6 +394,14 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   // (k2) in each warp, so every twiddle / k_f table word a warp reads is
   // shared by 4 lanes (one shared-memory wavefront per 8 distinct words).
   constexpr int JC = L1 / 8;    // 8-element n1 chunks
+  // frequency-sparse slow-digit skip: stage B / pointwise / B^-1 run over
+  // kc of the JC chunks of 8 k1 (kept chunk j = original chunk k1c_of(j));
+  // stage-B columns re | im of the kept k1, B^-1 contracts 2 * kk of them
+  static_assert(!SKP || (!DIT && TS && !FC_NEG_B && L1 == 32), "slow-digit skip variant");
+  const int kc = SKP ? prm.kcn : JC;
+  const int kk = 8 * kc;
+  const uint32_t k1map = kc < JC ? prm.k1map : 0xE4u;  // identity 0, 1, 2, 3
+  auto k1c_of = [&](int j) { return int((k1map >> (2 * j)) & 3u); };
   const int pA = ((m >> 5) / JC) * 4 + ((m >> 3) & 3), n1A = ((m >> 5) % JC) * 8 + (m & 7);
   // Order 3 (DIT): inner row p = q L0I + n0 holds z_q[n0 + L0I n'], so the
   // transform index of stage-A row (p, n1) is n0 + L0I n1 and the stage-B /
@@ -349,13 +442,14 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   constexpr int PER_ALL = NCH / kWGThreads;  // chunks per thread and tile
   static_assert(WPR >= 1 && 8 % WPR == 0 && NCH % kWGThreads == 0, "loader mapping");
   const int64_t HN = H * N;
+  const uint32_t sUW = F::SLOT_WG ? bufX + C::al(C::BUFX_BYTES) : base + F::OFF_UW;  // this warpgroup's input slot
   // From staging (STG) the lanes of each 8-lane phase take 8 consecutive n2
   // and n1 chunks j rotated so that both the staging read (chunk cm mod 8)
   // and the operand write (n2 mod 8) are bank-conflict-free.
   constexpr int LJC = JC == 4 ? 2 : JC == 2 ? 1 : 0;
-  const int ld_n2 = STG ? ((wtid >> 5) % WPR) * (32 / JC) + ((lane >> 3) >> LJC) * 8 + (lane & 7)
+  const int ld_n2 = STG_IN ? ((wtid >> 5) % WPR) * (32 / JC) + ((lane >> 3) >> LJC) * 8 + (lane & 7)
                         : (((wtid >> 5) % WPR) * 32 + (lane % (32 / JC)) * JC + lane / (32 / JC)) / JC;
-  const int ld_j = STG ? (((lane & 7) >> (3 - LJC)) + (lane >> 3)) & (JC - 1)
+  const int ld_j = STG_IN ? (((lane & 7) >> (3 - LJC)) + (lane >> 3)) & (JC - 1)
                        : (((wtid >> 5) % WPR) * 32 + (lane % (32 / JC)) * JC + lane / (32 / JC)) % JC;
   const int ld_r0 = (wtid >> 5) / WPR;
   const int ld_cm = ld_n2 * JC + ld_j;
@@ -468,12 +562,14 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   // Epilogue-4 geometry.  Output lane m holds G_AI row (n2 half, c', n2 mod
   // 32) (plan.cpp).  Causal: two M = 64 MMAs put column half hh in lanes
   // 16 hh .. 16 hh + 15 of every quadrant, rows q*16 + lane%16 (n2 < 32).
+  // (TMEM stage A^-1, causal: half h in lane quadrants 2h, 2h + 1, row
+  // (c' = quad & 1, n2 = lane), columns [64 h, 64 h + 64))
   constexpr int OUT_COLS = M64 ? 32 : 64;  // output columns per thread (this slice)
-  const int o_hh = M64 ? (lane >> 4) : slice;
-  const int o_row = M64 ? quad * 16 + (lane & 15) : m;
+  const int o_hh = M64 ? (AI_TS ? quad >> 1 : lane >> 4) : slice;
+  const int o_row = M64 ? (AI_TS ? (quad & 1) * 32 + lane : quad * 16 + (lane & 15)) : m;
   const int o_cp = (o_row >> 5) & 1, o_n2 = (o_row >> 6) * 32 + (o_row & 31);
   const int o_col0 = M64 ? o_hh * 64 + slice * 32 : slice * 64;  // first (p, n1) column of this thread
-  const uint32_t o_tcol = M64 ? slice * 32 : slice * 64;          // its TMEM column
+  const uint32_t o_tcol = M64 ? (AI_TS ? o_hh * 64 : 0) + slice * 32 : slice * 64;  // its TMEM column
 
   int64_t hh = (t0 + wg) / nbt, bt = (t0 + wg) % nbt;
   bool loaded = false;  // the tile's operand was stored by the previous tile's epilogue 4
@@ -495,7 +591,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
     if constexpr (DIT) {
       stg_wait(0);
       build_dit(rows_left);
-    } else if constexpr (STG) {
+    } else if constexpr (STG_IN) {
       stg_wait(0);
       build_from_staging(rows_left);
     } else if (!loaded) {
@@ -519,20 +615,75 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
     // ---------------- stage A: D[(p,n1)][(re|im|-im, k2)] = X[(p,n1)][(c,n2)] * G_A
     // TMEM column of (block, k2): (k2 / 32) * NA/2 + 32 * block + k2 % 32
     sync_and_issue([&](int h2) {  // half h2: k2 in [32 h2, 32 h2 + 32) of every block, one MMA per K step
-      constexpr uint32_t idesc = idesc_f16(128, C::NA / 2, true, false);
+      if constexpr (A_FULL) {
+        // one N = NA MMA per K step (the G_A rows of both halves are
+        // contiguous): the data operand is read from shared memory once
+        // instead of once per half (a K = 16 MMA costs ~47 + N/2 cycles,
+        // tools/microbench.py); half 1 commits nothing new
+        if (h2 == 0) {
+          constexpr uint32_t idesc = idesc_f16(128, C::NA, true, false);
 #pragma unroll
-      for (int s = 0; s < 2 * C::KA / 16; ++s)
-        mma_f16_ss(tmem + h2 * (C::NA / 2), dadd(dXA, 256 * s),
-                   dadd(dGA, h2 * (C::NA / 16) * C::SBO_GA + 256 * s), idesc, s > 0);
+          for (int s = 0; s < 2 * C::KA / 16; ++s)
+            mma_f16_ss(tmem, dadd(dXA, 256 * s), dadd(dGA, 256 * s), idesc, s > 0);
+        }
+      } else {
+        constexpr uint32_t idesc = idesc_f16(128, C::NA / 2, true, false);
+#pragma unroll
+        for (int s = 0; s < 2 * C::KA / 16; ++s)
+          mma_f16_ss(tmem + h2 * (C::NA / 2), dadd(dXA, 256 * s),
+                     dadd(dGA, h2 * (C::NA / 16) * C::SBO_GA + 256 * s), idesc, s > 0);
+      }
     });
-    // the u|w slot has been read by the whole warpgroup: stage tile t + 1
-    if (STG && t + 1 < t1 && filler()) fill(0, t + 1, bt + 1 < nbt ? hh : hh + 1, bt + 1 < nbt ? bt + 1 : 0);
+    // this warpgroup's u|w slot has been read by all of it: stage its next tile
+    if constexpr (F::SLOT_WG) {
+      if (STG_IN && t + kWG < t1 && filler()) fill(0, t + kWG, (t + kWG) / nbt, (t + kWG) % nbt);
+    } else {  // the shared slot goes to tile t + 1 (the other warpgroup's)
+      if (STG_IN && t + 1 < t1 && filler()) fill(0, t + 1, bt + 1 < nbt ? hh : hh + 1, bt + 1 < nbt ? bt + 1 : 0);
+    }
 
     // ---------------- epilogue 1: twiddle W^{n1 k2}, transpose -> stage B operand (MN-major)
     // Every stage's operand aliases bufX, so stores wait for BOTH halves of
     // the stage (the other half's MMAs may still read bufX); math on the
     // first item only needs this warp's half.
-    {
+    if constexpr (EPI1_PIPE) {
+      // the second 16-k2 item's TMEM loads are issued right after the first
+      // item's wait, so they overlap its math
+      wait_half(slice);
+      float bre[2][16], bim[2][16];
+      const uint32_t cb = slice * (C::NA / 2);
+      tmem_ld16(tq + cb, bre[0]);
+      tmem_ld16(tq + cb + 32, bim[0]);
+#pragma unroll
+      for (int sub = 0; sub < 2; ++sub) {
+        const int k20 = slice * 32 + sub * 16;
+        float4 w[8];
+        {
+          const float2 a = tw_at(e1A, k20), b = tw_at(e1A, k20 + 1);
+          w[0] = make_float4(a.x, b.x, a.y, b.y);
+#pragma unroll
+          for (int jj = 1; jj < 8; ++jj) w[jj] = cstep(w[jj - 1], tw1_c2);
+        }
+        tmem_ld_wait();
+        if (sub == 0) {
+          tmem_ld16(tq + cb + 16, bre[1]);
+          tmem_ld16(tq + cb + 16 + 32, bim[1]);
+        }
+        float* re = bre[sub];
+        float* im = bim[sub];
+        float ni[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) ni[e] = -im[e];
+        cmul8(re, im, ni, w);
+        cmul8(re + 8, im + 8, ni + 8, w + 4);
+        if (sub == 0) wait_half(slice ^ 1);
+#pragma unroll
+        for (int hh2 = 0; hh2 < 2; ++hh2) {
+          const int mg = grpB(pA, k20 + 8 * hh2);
+          st_half8(bufX + mg * 128 + (n1A >> 3) * C::LBO_B + (n1A & 7) * 16, re + 8 * hh2);
+          st_half8(bufX + mg * 128 + ((L1 + n1A) >> 3) * C::LBO_B + (n1A & 7) * 16, im + 8 * hh2);
+        }
+      }
+    } else {
       wait_half(slice);
       // both 16-k2 items unrolled (more ILP, 122 registers) measured 1-2 %
       // faster for gated causal and circular tiles and ~1 % slower for plain
@@ -578,7 +729,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
     if (new_h) cp_async_wait_all();
     // ---------------- stage B: per group of 128 rows (p,k2), contract n1 -> k1
     sync_and_issue([&](int h2) {
-      constexpr uint32_t idesc = idesc_f16(128, NBF, true, false);
+      const uint32_t idesc = kc == JC ? idesc_f16(128, NBF, true, false) : idesc_f16(128, 2 * kk, true, false);
 #pragma unroll
       for (int gi = h2 * (C::P / 4); gi < (h2 + 1) * (C::P / 4); ++gi) {
 #pragma unroll
@@ -724,18 +875,72 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         process(slice + 2, kfb);
       }
       tmem_st_wait();
-    } else {
+    } else if constexpr (EPI_PIPE) {
+      // items it = slice + 2 i < (P/2) kc: group gi = it / kc, kept chunk
+      // j = it % kc (half 0: groups < P/4).  The TMEM load of item i + 1 is
+      // issued right after item i's wait, so its latency overlaps item i's
+      // math (tcgen05.wait::ld waits for every earlier load).
+      const int nit = (C::P / 2) * kc, it_h1 = (C::P / 4) * kc;
+      auto col_of = [&](int i) { const int it = slice + 2 * i; return uint32_t((it / kc) * NBF + (it % kc) * 8); };
+      float buf[2][16];  // re[8] | im[8], double-buffered
+      bool h1 = false;
+      wait_half(0);
+      if (slice >= it_h1) { wait_half(1); h1 = true; }
+      tmem_ld8(tq + col_of(0), buf[0]);
+      tmem_ld8(tq + col_of(0) + kk, buf[0] + 8);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int it = slice + 2 * i;  // items 0..3 in half 0, 4..7 in half 1
-        const int gi = it / JC, k1c = it % JC;
+        const int it = slice + 2 * i;
+        if (it >= nit) break;
+        const int gi = it / kc, j = it % kc, k1c = k1c_of(j);
+        const int k2 = rowB_k2(gi);
+        float4 kf[4];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) kf[jj] = ld_shared_f4(sKF + tab_off<L1 / 2>(k2, k1c * 4 + jj));
+        tmem_ld_wait();
+        if (it + 2 < nit) {
+          if (TS && !h1 && it + 2 >= it_h1) { wait_half(1); h1 = true; }
+          tmem_ld8(tq + col_of(i + 1), buf[(i + 1) & 1]);
+          tmem_ld8(tq + col_of(i + 1) + kk, buf[(i + 1) & 1] + 8);
+        }
+        float* re = buf[i & 1];
+        float* im = buf[i & 1] + 8;
+        float ni[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ni[e] = -im[e];
+        cmul8(re, im, ni, kf);
+        if constexpr (TS) {  // K index c*kk + k1' -> column (c*kk + k1') / 2
+          const uint32_t ca = tq + C::CA + gi * L1 + j * 4;
+          tmem_st4(ca, pack_half2(re[0], re[1]), pack_half2(re[2], re[3]), pack_half2(re[4], re[5]),
+                   pack_half2(re[6], re[7]));
+          tmem_st4(ca + kk / 2, pack_half2(im[0], im[1]), pack_half2(im[2], im[3]), pack_half2(im[4], im[5]),
+                   pack_half2(im[6], im[7]));
+        } else {
+          if (!h1) { wait_half(1); h1 = true; }  // stores may overwrite operands of the second half
+          const int row = gi * 128 + m;
+          st_half8(bufX + (row >> 3) * C::SBO_BP + k1c * 128 + (row & 7) * 16, re);
+          st_half8(bufX + (row >> 3) * C::SBO_BP + (L1 / 8 + k1c) * 128 + (row & 7) * 16, im);
+        }
+      }
+      if (!h1) wait_half(1);  // (the stage-B barrier phase is tracked per stage)
+    } else {
+      // items it = slice + 2 i (dense: 0..3 in half 0, 4..7 in half 1; the
+      // slow-digit-skip variant: (P/2) kc items, group it / kc, kept chunk
+      // it % kc, half 1 from item (P/4) kc)
+      const int nit = (C::P / 2) * kc, it_h1 = (C::P / 4) * kc;
+      bool h1 = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int it = slice + 2 * i;
+        if (SKP && it >= nit) break;
+        const int gi = it / kc, j = it % kc, k1c = SKP ? k1c_of(j) : j;
         const int k2 = rowB_k2(gi);
         if (i == 0) wait_half(0);
-        if (TS && i == 2) wait_half(1);
-        const uint32_t col = gi * NBF + k1c * 8;
+        if (TS && (SKP ? (!h1 && it >= it_h1) : i == 2)) { wait_half(1); h1 = true; }
+        const uint32_t col = gi * NBF + j * 8;
         float re[8], im[8], ni[8];
         tmem_ld8(tq + col, re);
-        tmem_ld8(tq + col + L1, im);
+        tmem_ld8(tq + col + kk, im);
         if constexpr (FC_NEG_B) tmem_ld8(tq + col + 2 * L1, ni);
         float4 kf[4];
 #pragma unroll
@@ -746,11 +951,11 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
           for (int e = 0; e < 8; ++e) ni[e] = -im[e];
         }
         cmul8(re, im, ni, kf);
-        if constexpr (TS) {  // K index c*L1 + k1 -> column (c*L1 + k1) / 2
-          const uint32_t ca = tq + C::CA + gi * L1 + k1c * 4;
+        if constexpr (TS) {  // K index c*kk + k1' -> column (c*kk + k1') / 2
+          const uint32_t ca = tq + C::CA + gi * L1 + j * 4;
           tmem_st4(ca, pack_half2(re[0], re[1]), pack_half2(re[2], re[3]), pack_half2(re[4], re[5]),
                    pack_half2(re[6], re[7]));
-          tmem_st4(ca + L1 / 2, pack_half2(im[0], im[1]), pack_half2(im[2], im[3]), pack_half2(im[4], im[5]),
+          tmem_st4(ca + kk / 2, pack_half2(im[0], im[1]), pack_half2(im[2], im[3]), pack_half2(im[4], im[5]),
                    pack_half2(im[6], im[7]));
         } else {
           if (i == 0) wait_half(1);  // stores may overwrite operands of the second half
@@ -759,6 +964,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
           st_half8(bufX + (row >> 3) * C::SBO_BP + (L1 / 8 + k1c) * 128 + (row & 7) * 16, im);
         }
       }
+      if (SKP && TS && !h1) wait_half(1);  // every thread waits each stage's barriers (phase tracking)
       if constexpr (TS) tmem_st_wait();
     }
     stamp(7);
@@ -770,6 +976,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
       for (int gi = h2 * (C::P / 4); gi < (h2 + 1) * (C::P / 4); ++gi) {
 #pragma unroll
         for (int s = 0; s < 2 * L1 / 16; ++s) {
+          if (TS && s >= kc) break;  // slow-digit skip: K = 2 kk
           if constexpr (TS)
             mma_f16_ts(tmem + gi * NBF, tmem + C::CA + gi * L1 + 8 * s, dadd(dGBI, 256 * s), idesc, s > 0);
           else
@@ -780,7 +987,44 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
     });
 
     // ---------------- epilogue 3: conj twiddle, transpose -> stage A^-1 operand (MN-major B)
-    {
+    if constexpr (EPI_PIPE) {  // item i + 1's TMEM load overlaps item i's math (as epilogue 2)
+      auto col_of = [&](int i) { const int it = slice + 2 * i; return uint32_t((it / JC) * NBF + (it % JC) * 8); };
+      float buf[2][16];
+      wait_half(0);
+      tmem_ld8(tq + col_of(0), buf[0]);
+      tmem_ld8(tq + col_of(0) + L1, buf[0] + 8);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int it = slice + 2 * i;
+        const int gi = it / JC, n1c = it % JC;
+        const int p = rowB_p(gi), k2 = rowB_k2(gi);
+        float4 w[4];
+        {
+          const float2 a = tw_at((p % L0I) + L0I * 8 * n1c, k2);
+          const float br = a.x, bi = a.y;
+          const float4 c = tw3_c[gi & 1];  // {Re W^{k2}, Im W^{k2}, Re W^{2k2}, Im W^{2k2}}
+          w[0] = make_float4(br, br * c.x - bi * c.y, bi, br * c.y + bi * c.x);
+#pragma unroll
+          for (int jj = 1; jj < 4; ++jj) w[jj] = cstep(w[jj - 1], make_float2(c.z, c.w));
+        }
+        tmem_ld_wait();
+        if (i + 1 < 4) {
+          if (TS && i + 1 == 2) wait_half(1);  // bufX is not an operand of stage B^-1 here
+          tmem_ld8(tq + col_of(i + 1), buf[(i + 1) & 1]);
+          tmem_ld8(tq + col_of(i + 1) + L1, buf[(i + 1) & 1] + 8);
+        }
+        float* re = buf[i & 1];
+        float* im = buf[i & 1] + 8;
+        float nr[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) nr[e] = -re[e];
+        cmulc8(re, im, nr, w);
+        if (!TS && i == 0) wait_half(1);  // stores may overwrite operands of the second half
+        const int ng = DIT ? n1c * C::P + p : (p * L1) / 8 + n1c;
+        st_half8(bufX + ng * C::SBO_XA + (k2 >> 3) * 128 + (k2 & 7) * 16, re);
+        st_half8(bufX + ng * C::SBO_XA + ((L2 + k2) >> 3) * 128 + (k2 & 7) * 16, im);
+      }
+    } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int it = slice + 2 * i;
@@ -823,11 +1067,19 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
 
     // ---------------- stage A^-1: D[(c',n2)][(p,n1)] = G_A^-1 * X[(c,k2)][(p,n1)]
     sync_and_issue([&](int h2) {  // half h2: output columns (p, n1) in [64 h2, 64 h2 + 64)
-      constexpr uint32_t idesc = idesc_f16(M64 ? 64 : 128, 64, false, true);
-      const uint32_t dcol = M64 ? tmem + (uint32_t(16 * h2) << 16) : tmem + h2 * 64;
+      if constexpr (AI_TS) {  // half h2 against the G_A^-1 copy in TMEM (causal: copy h2), N = 64
+        constexpr uint32_t idesc = idesc_f16(128, 64, false, true);
+        const uint32_t ga = tmem - wg * C::TMEM_COLS + (M64 ? h2 * C::TMEM_COLS : 0) + GAI_COL;
 #pragma unroll
-      for (int s = 0; s < 2 * L2 / 16; ++s)
-        mma_f16_ss(dcol, dadd(dGAI, 256 * s), dadd(dXAI, h2 * 8 * C::SBO_XA + 256 * s), idesc, s > 0);
+        for (int s = 0; s < 2 * L2 / 16; ++s)
+          mma_f16_ts(tmem + h2 * 64, ga + 8 * s, dadd(dXAI, h2 * 8 * C::SBO_XA + 256 * s), idesc, s > 0);
+      } else {
+        constexpr uint32_t idesc = idesc_f16(M64 ? 64 : 128, 64, false, true);
+        const uint32_t dcol = M64 ? tmem + (uint32_t(16 * h2) << 16) : tmem + h2 * 64;
+#pragma unroll
+        for (int s = 0; s < 2 * L2 / 16; ++s)
+          mma_f16_ss(dcol, dadd(dGAI, 256 * s), dadd(dXAI, h2 * 8 * C::SBO_XA + 256 * s), idesc, s > 0);
+      }
     });
 
     // ---------------- epilogue 4: (gate), convert, store y; load the next tile
@@ -871,7 +1123,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
           if (r < rows_left) vv[i] = *reinterpret_cast<const uint4*>(gv + tile_base + int64_t(r) * HN + n);
         }
       }
-      if (!STG && has_next && (STAGE || !GATED)) {
+      if (!STG_IN && has_next && (STAGE || !GATED)) {
         int64_t hh2 = hh, bt2 = bt + kWG;
         while (bt2 >= nbt) { bt2 -= nbt; ++hh2; }
         const int64_t base2 = (bt2 * RR * H + phys_head(hh2)) * N;
@@ -1019,8 +1271,8 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         tc_fence_before();
         wg_sync();
       }
-      if (!STG && has_next) store_chunks(nu, nw);
-      loaded = !STG && has_next;
+      if (!STG_IN && has_next) store_chunks(nu, nw);
+      loaded = !STG_IN && has_next;
     }
     stamp(13);
     stamp(14);
@@ -1032,10 +1284,10 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
 }
 
 // ------------------------------------------------------------------ launch
-template <int L1, bool CAUSAL, bool GATED, typename T, int L0I = 1>
+template <int L1, bool CAUSAL, bool GATED, typename T, int L0I = 1, bool SKP = false>
 static cudaError_t launch_o2(const FwdParams& prm, cudaStream_t stream) {
   using F = FwdCfg<L1, CAUSAL, GATED, L0I>;
-  auto kern = fftconv_fwd_o2_kernel<L1, CAUSAL, GATED, T, L0I>;
+  auto kern = fftconv_fwd_o2_kernel<L1, CAUSAL, GATED, T, L0I, SKP>;
   static int attr[64] = {0};
   if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(F::SMEM), attr)) return e;
   const int64_t nbt = (prm.B + F::RR - 1) / F::RR;
@@ -1053,6 +1305,8 @@ static cudaError_t dispatch_l1(const FwdParams& prm, cudaStream_t s) {
     if (prm.L0I == 4) return prm.L1 == 32 ? launch_o2<32, true, GATED, T, 4>(prm, s) : cudaErrorInvalidValue;
   }
   if (prm.L0I > 1) return cudaErrorInvalidValue;
+  if (prm.kcn > 0)  // frequency-sparse slow-digit skip (kept k1 chunks only)
+    return prm.L1 == 32 && prm.kcn < 4 ? launch_o2<32, CAUSAL, GATED, T, 1, true>(prm, s) : cudaErrorInvalidValue;
   switch (prm.L1) {
     case 8: return launch_o2<8, CAUSAL, GATED, T>(prm, s);
     case 16: return launch_o2<16, CAUSAL, GATED, T>(prm, s);

@@ -319,7 +319,59 @@ static fftconv_status_t build_mask(fftconv_plan_s* p, const fftconv_sparsity_t* 
   } else {
     p->skip_fraction = 0.0;
   }
+  // Slow-digit skip ("sparsity in the first dimension allows us
+  // to skip computation in B"): the inner transform's frequency is
+  // f = k0 + L0 (k2 + L2 k1) (L0 = 1 fused), so stage-B output column chunk
+  // c (k1 in [8c, 8c + 8)) holds exactly the frequencies f in
+  // [c L / (L1/8), (c + 1) L / (L1/8)); a chunk masked there for every f is
+  // never computed.  Inner transforms with L1 = 32 (fused fft_size 2048 and
+  // every multipass inner pass; chunks of 8 = one K = 16 step of re | im).
+  p->k1_chunks = 0;
+  p->k1_map = 0;
+  const int nch = p->L1 / 8;
+  if (p->L1 == 32 && p->dit == 1) {
+    int kept = 0;
+    uint32_t map = 0;
+    const int64_t span = L / nch;
+    for (int c = 0; c < nch; ++c) {
+      bool any = false;
+      for (int64_t f = c * span; f < (c + 1) * span && !any; ++f) any = p->mask[size_t(f)] != 0.0f;
+      if (any) map |= uint32_t(c) << (2 * kept++);
+    }
+    if (kept > 0 && kept < nch) {
+      p->k1_chunks = kept;
+      p->k1_map = map;
+      const double rows_kept = p->L0 > 1 ? double(p->row_map.size()) / double(p->L0) : 1.0;
+      p->skip_fraction = 1.0 - rows_kept * double(kept) / double(nch);
+    }
+  }
   return FFTCONV_OK;
+}
+
+// Compacted copies of the forward's G_B (output rows re | im, only the kept
+// k1 chunks) and G_B^-1 (contraction index (c, k1) -> (c, kept k1)) for the
+// slow-digit skip; same K-major canonical layout and strides as the dense
+// tables, unused rows / K columns zero.
+static void build_k1_compact(fftconv_plan_s* p) {
+  if (p->k1_chunks == 0) return;
+  const int L1 = p->L1, kk = 8 * p->k1_chunks, Kt = 2 * L1;
+  auto k1_of = [&](int k1c) {  // compacted k1 -> original
+    return int((p->k1_map >> (2 * (k1c / 8))) & 3u) * 8 + k1c % 8;
+  };
+  std::vector<uint8_t>& img = p->image;
+  p->gb_sp = align_up(img.size(), 1024);
+  p->gbi_sp = align_up(p->gb_sp + p->tl.gb_bytes, 1024);
+  img.resize(align_up(p->gbi_sp + p->tl.gbi_bytes, 1024), 0);
+  for (int blk = 0; blk < 2; ++blk)
+    for (int j = 0; j < kk; ++j)
+      for (int k = 0; k < Kt; ++k)
+        std::memcpy(img.data() + p->gb_sp + kmajor_off(blk * kk + j, k, Kt),
+                    img.data() + p->tl.gb + kmajor_off(blk * L1 + k1_of(j), k, Kt), 2);
+  for (int row = 0; row < 2 * L1; ++row)  // forward rows re | im (n1)
+    for (int c = 0; c < 2; ++c)
+      for (int j = 0; j < kk; ++j)
+        std::memcpy(img.data() + p->gbi_sp + kmajor_off(row, c * kk + j, Kt),
+                    img.data() + p->tl.gbi + kmajor_off(row, c * L1 + k1_of(j), Kt), 2);
 }
 
 }  // namespace fc
@@ -458,7 +510,8 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
       return s;
     }
     // the mask rides at the end of the table image (read by precompute_kf),
-    // followed by the row keep flags and the list of kept rows
+    // followed by the row keep flags and the list of kept rows, then the
+    // compacted stage-B tables of the slow-digit skip
     const size_t mo = p->image.size();
     p->image.resize(mo + p->mask.size() * sizeof(float));
     std::memcpy(p->image.data() + mo, p->mask.data(), p->mask.size() * sizeof(float));
@@ -473,6 +526,8 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
       p->image.resize(p->image.size() + align_up(bytes, 16), 0);
       std::memcpy(p->image.data() + p->row_map_off, p->row_map.data(), bytes);
     }
+    if (dtype != FFTCONV_F32) build_k1_compact(p);
+    else { p->k1_chunks = 0; p->skip_fraction = p->L0 > 1 ? 1.0 - double(p->row_map.size()) / double(p->L0) : 0.0; }
   }
   // fp16 headroom: with unitary stages the largest intermediate of a row
   // pair z = g_b + i g_{b+1} with |g| <= A is its DC bin, |Z_0| <= |z|_1 /

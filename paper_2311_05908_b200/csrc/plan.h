@@ -67,6 +67,13 @@ struct fftconv_plan_s {
   size_t row_keep_off = 0, row_map_off = 0;  // image offsets (sparse multipass)
   double mask_fraction = 0.0;
   double skip_fraction = 0.0;
+  // slow-digit skip: chunks of 8 stage-B output columns k1
+  // whose frequencies are masked for every k2 and every inner row are left
+  // out of stage B, the pointwise step and stage B^-1 (0 = dense); the
+  // forward reads compacted G_B / G_B^-1 copies at gb_sp / gbi_sp
+  int32_t k1_chunks = 0;
+  uint32_t k1_map = 0;   // 2 bits per kept chunk: its original chunk index
+  size_t gb_sp = 0, gbi_sp = 0;
   size_t kf_bytes_per_head = 0;
   size_t ws_bytes_per_head = 0;
   int32_t sram_smem_bytes = 0;  // dynamic shared memory of the fused kernel

@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(512, 1) tmem_ld_bench_kernel(int iters, int nw
   if (warp == 0) fc::tmem_dealloc<512>(tmem_base);
 }
 
-__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int nmma, int N, int ts, long long* out) {
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int nmma, int N, int ts, long long* out, int M = 128) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int nmma, int N, int t
     for (int r = 0; r < 2; ++r) {
       if (r == 1) c0 = clock64();
       for (int s = 0; s < nmma; ++s) {
-        const uint32_t idesc = fc::idesc_f16(128, N, false, false);
+        const uint32_t idesc = fc::idesc_f16(M, N, false, false);
         if (ts) fc::mma_f16_ts(tb, tb + 256, bd, idesc, s > 0);
         else fc::mma_f16_ss(tb, ad, bd, idesc, s > 0);
       }
@@ -269,3 +269,16 @@ extern "C" int fcst_mma_rate(int nmma, int N, int ts, long long* host_out) {
   cudaFree(d);
   return e == cudaSuccess ? 0 : 100 + (int)e;
 }
+
+// tcgen05.mma issue/completion cost for an M x N x 16 fp16 MMA chain
+// (M = 64 or 128; ts: A from TMEM, M = 128 only)
+extern "C" int fcst_mma_rate_m(int nmma, int M, int N, int ts, long long* host_out) {
+  long long* d;
+  cudaMalloc(&d, 32);
+  cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  mma_rate_kernel<<<1, 128, 65536>>>(nmma, N, ts, d, M);
+  cudaError_t e = cudaMemcpy(host_out, d, 32, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return int(e);
+}
+

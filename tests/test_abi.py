@@ -139,6 +139,55 @@ def test_sparsity_mask_matches_oracle_reading(lib):
     assert lib.fftconv_plan(ctypes.byref(h), 1024, L, 0, 1, ctypes.byref(sp)) == 4
 
 
+def _sparse_plan(lib, N, dims, keeps, dtype=0):
+    from paper_2311_05908_b200 import _abi
+    sp = _abi.Sparsity()
+    sp.ndims = len(dims)
+    bufs = []
+    for j, (d, kp) in enumerate(zip(dims, keeps)):
+        sp.dims[j] = d
+        b = (ctypes.c_uint8 * d)(*[int(x) for x in kp])
+        bufs.append(b)
+        sp.keep[j] = ctypes.cast(b, ctypes.POINTER(ctypes.c_uint8))
+    h = ctypes.c_void_p()
+    assert lib.fftconv_plan(ctypes.byref(h), N, 2 * N, dtype, 1, ctypes.byref(sp)) == 0
+    info = _abi.PlanInfo()
+    lib.fftconv_plan_info(h, ctypes.byref(info))
+    lib.fftconv_plan_destroy(h)
+    return info
+
+
+@pytest.mark.parametrize("N", [1024, 8192, 16384, 32768, 1 << 20])
+def test_slow_digit_skip_fraction(lib, N):
+    """A symmetric low-pass mask (keep |f| < L/8, A13) zeroes the middle two
+    of the four chunks of 8 stage-B columns k1 of the inner transform
+    (f = k0 + L0 (k2 + 64 k1)): the planner skips them and
+    reports skip_fraction 0.5; the oracle's mask confirms which chunks are
+    all-zero.  A dense-chunk mask (trailing zeros of the FAST digit) skips
+    no chunk."""
+    L = 2 * N
+    dims = [16, L // 16]
+    keeps = orc.keep_masks_from_zero_counts(dims, [14, 0])
+    m = orc.frequency_mask(dims, keeps)
+    span = L // 4
+    assert [bool(m[c * span:(c + 1) * span].any()) for c in range(4)] == [True, False, False, True]
+    info = _sparse_plan(lib, N, dims, keeps)
+    assert abs(info.skip_fraction - 0.5) < 1e-12
+    assert abs(info.mask_fraction - (1 - m.mean())) < 1e-12
+    # fp32 validation plans never skip stage-B chunks
+    if N <= 16384:
+        assert _sparse_plan(lib, N, dims, keeps, dtype=2).skip_fraction == 0.0
+    # a fast-digit mask (keep f mod 16 < 2) leaves every chunk live; one-level
+    # multipass plans skip its all-zero outer rows k0 = f mod L0 instead
+    dims2 = [L // 16, 16]
+    keeps2 = orc.keep_masks_from_zero_counts(dims2, [0, 14])
+    m2 = orc.frequency_mask(dims2, keeps2)
+    L0 = L // 2048
+    rows = 1.0 if L0 == 1 else np.mean([m2[k0::L0].any() for k0 in range(L0)])
+    expect = 1.0 - rows if 1 < L0 <= 16 else 0.0
+    assert abs(_sparse_plan(lib, N, dims2, keeps2).skip_fraction - expect) < 1e-12
+
+
 def test_no_cpu_fallback_in_product():
     """The product package never imports the oracle."""
     pkg = os.path.join(ROOT, "paper_2311_05908_b200")

@@ -206,3 +206,49 @@ def test_sparse_partial_plan(dims, keep_fn):
     ref_dk = gb["dk"].reshape(H, NC, L).sum(axis=1)[:, :K]
     assert_parity(g["du"].float().cpu().numpy(), ref_du, "du")
     assert_parity(g["dk"].cpu().numpy(), ref_dk, "dk")
+
+
+def _lowpass(L, keep_frac_inv=8):
+    """Symmetric low-pass (A13): digit grid [keep_frac_inv * 2, L / (2 keep_frac_inv)]
+    (slowest first) with all but the first two slow digits zeroed keeps
+    f < L / keep_frac_inv, and the Hermitian closure adds f > L - L / keep_frac_inv."""
+    d0 = 2 * keep_frac_inv
+    dims = [d0, L // d0]
+    return dims, orc.keep_masks_from_zero_counts(dims, [d0 - 2, 0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [1024, 8192, 16384, 32768])
+@pytest.mark.parametrize("gated", [False, True])
+def test_sparse_lowpass_slow_digit_skip(N, gated):
+    """A genuine symmetric low-pass mask skips the slow digit:
+    stage-B column chunks whose frequencies are all masked are left out of
+    stage B, the pointwise step and stage B^-1 (here 2 of 4 chunks), in the
+    fused (N = 1024), one-level (8192, 16384) and recursive (32768) plans."""
+    dims, keeps = _lowpass(2 * N)
+    plan, got, ref, m = _run(N, dims, keeps, gated=gated)
+    assert abs(plan.info.mask_fraction - (1 - m.mean())) < 1e-12
+    assert abs(plan.info.skip_fraction - 0.5) < 1e-12
+    assert_parity(got, ref, f"low-pass N={N}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [1024, 8192])
+def test_sparse_lowpass_backward(N):
+    """The backward of a slow-digit-skipping plan (dense kernels on the
+    masked k_f) against the oracle's masked gradients."""
+    from paper_2311_05908_b200 import FFTConvPlan
+    dims, keeps = _lowpass(2 * N, 16)
+    B, H, seed = 3, 2, 9
+    plan = FFTConvPlan(N, dtype=torch.float16, causal=True, sparsity=(dims, keeps))
+    q = lambda name: synth.quantize(synth.signal(seed, name, B, H, N), "f16")
+    u, w, v, dy = q("u"), q("w"), q("v"), q("dy")
+    k = synth.decay_filters(seed, H, N).astype(np.float32)
+    t = lambda a: torch.tensor(a, dtype=torch.float16, device="cuda")
+    kf = plan.precompute_kf(torch.tensor(k, device="cuda"))
+    g = plan.bwd(t(dy), t(u), kf, N, w=t(w), v=t(v))
+    torch.cuda.synchronize()
+    m = orc.frequency_mask(dims, keeps)
+    ref = orc.conv_bwd(dy, u, k.astype(np.float64), w=w, v=v, mask=m)
+    for key in ("du", "dw", "dv", "dk"):
+        assert_parity(g[key].float().cpu().numpy(), ref[key], f"low-pass bwd {key}")

@@ -17,3 +17,7 @@ for ts in (0, 1):
         for n in (8, 64):
             lib.fcst_mma_rate(n, N, ts, out.ctypes.data_as(ctypes.c_void_p))
             print(f"mma {'ts' if ts else 'ss'} N={N:3d} n={n:3d}: issue {out[2]:6d} done {out[3]:6d} cyc/mma {out[3]/n:6.1f}")
+for M in (64, 128):
+    for N in (64, 128, 256):
+        lib.fcst_mma_rate_m(64, M, N, 0, out.ctypes.data_as(ctypes.c_void_p))
+        print(f"mma ss M={M} N={N:3d} n= 64: issue {out[2]:6d} done {out[3]:6d} cyc/mma {out[3]/64:6.1f}")
