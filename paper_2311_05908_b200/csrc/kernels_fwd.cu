@@ -58,6 +58,9 @@ __device__ long long fc_trace_buf[8][64][24];
 #ifndef FC_EPI_PIPE
 #define FC_EPI_PIPE 0
 #endif
+#ifndef FC_SPLIT_ISSUE
+#define FC_SPLIT_ISSUE 0
+#endif
 #ifndef FC_EPI1_PIPE
 #define FC_EPI1_PIPE 0
 #endif
@@ -123,9 +126,10 @@ struct FwdCfg {
   // L0I k_f blocks from global memory / L2) and the operand buffer
   static constexpr uint32_t KF_SM = DIT ? 0 : C::al(C::KF_BYTES);
   // per warpgroup: [k_f | operand buffer bufX | u [| w] input slot]; the
-  // order-3 tiles keep one slot shared in tile order (measured: per-warpgroup
-  // slots made the gated order-3 kernel 20 % slower, the order-2 ones 2 %
-  // faster)
+  // order-3 tiles and circular tiles keep one slot shared in tile order
+  // (measured: per-warpgroup slots made the order-2 kernels 2 % faster, the
+  // gated order-3 kernel 20 % and plain L0 = 4 4 % slower -- register
+  // spills --, plain L0 = 2 0.7 % faster; circular tiles have no SMEM for two)
   static constexpr bool SLOT_WG = !DIT && !CIN;
   static constexpr uint32_t WG_BYTES = KF_SM + C::al(C::BUFX_BYTES) + (SLOT_WG ? C::al(UW_BYTES) : 0);
   // circular plain tiles (the multipass inner pass): y staging shared by
@@ -368,12 +372,27 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   // Operands written -> warpgroup barrier -> one elected thread issues the
   // stage as two halves, each committed to its own mbarrier so the epilogue
   // of the first half overlaps the MMAs of the second.
-  auto sync_and_issue = [&](auto&& issue_half) {
+  // split = true (experiment, FC_SPLIT_ISSUE=1, off): the halves are
+  // independent MMA chains issued by two threads (warps 0 and 4), so no warp
+  // blocks on the tensor queue for a whole stage (a half with no MMAs must
+  // not be split: its commit would complete at once).  Measured 2-8 %
+  // slower on every workload.
+  auto sync_and_issue = [&](auto&& issue_half, bool split = false) {
     fence_async_smem();
     tc_fence_before();
     wg_sync();
     stamp(2 + 3 * stage_no);
-    if (wtid < 32 && elect_one()) {
+    if (FC_SPLIT_ISSUE && split) {
+      if (wtid < 32 && elect_one()) {
+        tc_fence_after();
+        issue_half(0);
+        mma_commit(&bars[0]);
+      } else if ((wtid >> 5) == 4 && elect_one()) {
+        tc_fence_after();
+        issue_half(1);
+        mma_commit(&bars[1]);
+      }
+    } else if (wtid < 32 && elect_one()) {
       tc_fence_after();
       issue_half(0);
       mma_commit(&bars[0]);
@@ -736,7 +755,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         for (int s = 0; s < 2 * L1 / 16; ++s)
           mma_f16_ss(tmem + gi * NBF, dadd(dXB, gi * 2048 + 2 * s * C::LBO_B), dadd(dGB, 256 * s), idesc, s > 0);
       }
-    });
+    }, true);
 
     // ---------------- epilogue 2: pointwise * k_f -> stage B^-1 operand (own row: TMEM, else K-major smem)
     if constexpr (DIT) {
@@ -984,7 +1003,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
                        s > 0);
         }
       }
-    });
+    }, true);
 
     // ---------------- epilogue 3: conj twiddle, transpose -> stage A^-1 operand (MN-major B)
     if constexpr (EPI_PIPE) {  // item i + 1's TMEM load overlaps item i's math (as epilogue 2)
@@ -1080,7 +1099,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         for (int s = 0; s < 2 * L2 / 16; ++s)
           mma_f16_ss(dcol, dadd(dGAI, 256 * s), dadd(dXAI, h2 * 8 * C::SBO_XA + 256 * s), idesc, s > 0);
       }
-    });
+    }, true);
 
     // ---------------- epilogue 4: (gate), convert, store y; load the next tile
     // v (output gate) and the next tile's input are read with coalesced 16 B
@@ -1140,13 +1159,46 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         // this warpgroup's next stage A); the staging layout is the 128 B
         // swizzle of the {64, Lp/64, 1, R} box
         const bool tma_out = F::YS_BYTES > 0 && prm.tma_y;
-        const uint32_t sstg = tma_out ? sYS : bufX;
+        // causal tiles with TMA I/O: v arrives and y leaves in the 128 B
+        // swizzled layout of a {64, N/64, 1, R} box, so each thread gates
+        // its own 16-byte units in place (v and y at swz128(offset): no bank
+        // conflicts) and writes y straight into the store staging -- no
+        // intermediate copy of the conv output, no second pass, one barrier
+        // (not for gated order-3 tiles: the extra registers spill there, 14 %
+        // slower at L0 = 4; their v / y maps stay natural-order, api.cu)
+        constexpr bool Y_DIRECT = STG && !(DIT && GATED);
+        const bool direct = Y_DIRECT && prm.tma_io;
+        const uint32_t sstg = tma_out ? sYS : direct ? sY : bufX;
         if (tma_out && t > t0) mbar_wait(&ys_bar, uint32_t((t - t0 - 1) & 1));
         // all of this thread's TMEM loads in flight before one wait (PER <= 8)
         float ob[PER][8];
 #pragma unroll
         for (int i = 0; i < PER; ++i) tmem_ld8(tq + o_tcol + 8 * i, ob[i]);
+        if (STG && direct) stg_wait(1);  // v has landed in the output slot
         tmem_ld_wait();
+        // one 16-byte unit of y (8 samples at byte offset off of the tile's
+        // natural layout, conv output already packed in S): gate, store
+        auto put16 = [&](uint32_t off, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3) {
+          if (!direct || !GATED) {
+            st_shared_v4(sstg + swz128(off), w0, w1, w2, w3);
+            return;
+          }
+          uint4 st = make_uint4(w0, w1, w2, w3);
+          const uint4 vq = ld_shared_u4(sV + swz128(off));
+          if constexpr (std::is_same<T, __half>::value) {
+            __half2* a2 = reinterpret_cast<__half2*>(&st);
+            const __half2* v2 = reinterpret_cast<const __half2*>(&vq);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) a2[e] = __hmul2(a2[e], v2[e]);
+          } else {
+            float a[8], v8[8];
+            IO<__half>::to_f32x8(st, a);
+            IO<T>::to_f32x8(vq, v8);
+            st = make_uint4(IO<T>::pack2(a[0] * v8[0], a[1] * v8[1]), IO<T>::pack2(a[2] * v8[2], a[3] * v8[3]),
+                            IO<T>::pack2(a[4] * v8[4], a[5] * v8[5]), IO<T>::pack2(a[6] * v8[6], a[7] * v8[7]));
+          }
+          st_shared_v4(sstg + swz128(off), st.x, st.y, st.z, st.w);
+        };
         if constexpr (DIT) {
           // items i = inner rows p = q L0I + n0 at 8 n1 of column group n1c:
           // samples n0 + L0I (n1 + 32 n2) of real row 2q + c', interleaved
@@ -1163,10 +1215,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
               wd[t2] = IO<S>::pack2(ob[q * L0I + a % L0I][a / L0I], ob[q * L0I + b % L0I][b / L0I]);
             }
 #pragma unroll
-            for (int v4 = 0; v4 < L0I; ++v4) {
-              const uint32_t off = uint32_t(r * NROW + nb + 8 * v4) * sizeof(S);
-              st_shared_v4(sstg + swz128(off), wd[4 * v4], wd[4 * v4 + 1], wd[4 * v4 + 2], wd[4 * v4 + 3]);
-            }
+            for (int v4 = 0; v4 < L0I; ++v4)
+              put16(uint32_t(r * NROW + nb + 8 * v4) * sizeof(S), wd[4 * v4], wd[4 * v4 + 1], wd[4 * v4 + 2],
+                    wd[4 * v4 + 3]);
           }
         } else {
 #pragma unroll
@@ -1174,13 +1225,21 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
           const float* o = ob[i];
           int r, n;
           item_rn(i, r, n);
-          const uint32_t off = uint32_t(r * NROW + n) * sizeof(S);
-          st_shared_v4(sstg + swz128(off), IO<S>::pack2(o[0], o[1]), IO<S>::pack2(o[2], o[3]),
-                       IO<S>::pack2(o[4], o[5]), IO<S>::pack2(o[6], o[7]));
+          put16(uint32_t(r * NROW + n) * sizeof(S), IO<S>::pack2(o[0], o[1]), IO<S>::pack2(o[2], o[3]),
+                IO<S>::pack2(o[4], o[5]), IO<S>::pack2(o[6], o[7]));
         }
         }
         stamp(16);
-        if (tma_out) {
+        if (STG && direct) {
+          fence_async_smem();  // y -> the tensor store (async proxy)
+          wg_sync();           // all of y written, all of v read
+          if (filler()) {
+            tma_store_4d(&prm.tmap_yo, sY, 0, 0, int(h), int(bt * RR));  // rows past B are clipped
+            bulk_commit();
+            // v has been read: the output slot goes to tile t + 1 at once
+            if (t + 1 < t1) release_out(t + 1, bt + 1 < nbt ? hh : hh + 1, bt + 1 < nbt ? bt + 1 : 0);
+          }
+        } else if (tma_out) {
           fence_async_smem();
           tc_fence_before();
           wg_sync();

@@ -89,10 +89,20 @@ FC_DEVICE void named_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// One lane polls, the rest of the warp waits at the warp barrier.
+// Warp-wide wait for an mbarrier phase.  FC_WAIT_LANE0=1: one lane polls,
+// the rest of the warp waits at the warp barrier (divergent branch +
+// convergence barrier); default: every lane waits (converged, the suspend
+// hint parks the warp).
+#ifndef FC_WAIT_LANE0
+#define FC_WAIT_LANE0 0
+#endif
 FC_DEVICE void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+#if FC_WAIT_LANE0
   if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
   __syncwarp();
+#else
+  mbar_wait(bar, parity);
+#endif
 }
 
 // ---------------------------------------------------------------- fences
