@@ -21,19 +21,19 @@
 #include "layout.h"
 
 // B200 tier cost model coefficients (seconds per feature unit), fitted by
-// tools/cost_model.py on the bench sweep (profiles/r02/cost_model.md).
-#define COST_B200_0 1.438129e-08
-#define COST_B200_1 1.608477e-08
-#define COST_B200_2 1.932282e-08
-#define COST_B200_3 3.031798e-08
-#define COST_B200_4 3.096212e-12
-#define COST_B200_5 1.213060e-11
-#define COST_B200_6 1.121617e-05
-#define COST_B200_7 6.189846e-08
-#define COST_B200_8 3.296687e-12
-#define COST_B200_9 4.139593e-11
+// tools/cost_model.py on the bench sweep (profiles/r02b/cost_model.md).
+#define COST_B200_0 9.260535e-09
+#define COST_B200_1 6.101121e-09
+#define COST_B200_2 1.626946e-08
+#define COST_B200_3 2.661771e-08
+#define COST_B200_4 3.456787e-12
+#define COST_B200_5 1.048704e-11
+#define COST_B200_6 1.231446e-05
+#define COST_B200_7 0.000000e+00
+#define COST_B200_8 5.072926e-12
+#define COST_B200_9 3.132192e-11
 #define COST_B200_10 0.000000e+00
-#define COST_B200_11 7.246451e-14
+#define COST_B200_11 1.170779e-13
 
 namespace fc {
 
@@ -610,7 +610,7 @@ extern "C" int32_t fftconv_select_order(int64_t N, double mu, double sigma_h, do
 // k_f precompute elements, launches, and the backward's tiles, T-chain
 // elements and dk elements.  t = sum_i coef[i] * feat[i]; the default
 // coefficients are a least-squares fit to the bench sweep on one B200
-// (tools/cost_model.py, profiles/r02/cost_model.md).
+// (tools/cost_model.py, profiles/r02b/cost_model.md).
 static double cdiv(double a, double b) { return std::ceil(a / b); }
 
 static void cost_features(const fftconv_plan_s* p, int64_t B, int64_t H, bool bwd, bool gated, double* f) {
