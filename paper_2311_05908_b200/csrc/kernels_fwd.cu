@@ -172,10 +172,12 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   constexpr bool TS = C::TS_BI;     // stage B^-1 data operand in TMEM
   constexpr int NBF = F::NBF;
   constexpr bool M64 = CAUSAL;      // stage A^-1 as M = 64 MMAs (rows n2 < L2/2 only)
-  // epilogues 2/3 prefetch the next item's TMEM load (experiment, off:
-  // within 0.5 % on causal tiles, 1-3 % slower on circular ones -- the extra
-  // live registers spill; the same for epilogue 1, FC_EPI1_PIPE: 1-9 % slower)
-  constexpr bool EPI_PIPE = FC_EPI_PIPE && !FC_NEG_B;
+  // epilogues 2/3 prefetch the next item's TMEM load: on for gated order-2
+  // tiles (measured with the converged waits: cfg2 -1.4 %, gated N = 512
+  // -4 %); plain causal +0.5 %, circular 0 %, and before the converged
+  // waits 1-3 % slower on circular tiles (spills), so off there
+  // (FC_EPI_PIPE=1 forces it); epilogue 1 likewise (FC_EPI1_PIPE): 1-9 % slower
+  constexpr bool EPI_PIPE = (FC_EPI_PIPE || (GATED && !DIT)) && !FC_NEG_B;
   constexpr bool EPI1_PIPE = FC_EPI1_PIPE && !C::NEG_A && !DIT;  // epilogue 1 likewise
   constexpr bool A_FULL = FC_A_FULL && !DIT;  // stage A as one MMA chain (measured: o2 -1.3 %, order 3 +2 %)
   // circular tiles: stage A^-1 reads G_A^-1 from TMEM (loaded once per CTA
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   // column half h against a copy of G_A^-1 rotated by 64 h rows (copy 1 in
   // warpgroup 1's free columns), so the useful rows of half h land in lane
   // quadrants 2h, 2h + 1 and every epilogue-4 thread keeps 32 columns
-  constexpr bool AI_TS = (FC_AI_TS && kWG == 2) || F::GAI_TMEM;
+  constexpr bool AI_TS = (FC_AI_TS && kWG == 2 && !DIT) || F::GAI_TMEM;  // (causal: measured +-1 %, off)
   constexpr uint32_t GAI_COL = 128;
   static_assert(!AI_TS || (C::TMEM_COLS == 256 && C::NA <= 128 && (C::P / 2) * NBF <= 128 && C::CA >= 192),
                 "TMEM columns [128, 192) of each warpgroup hold a G_A^-1 copy");
