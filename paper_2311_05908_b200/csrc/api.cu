@@ -227,15 +227,17 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     prm.num_sms = num_sms_current();
     prm.L0I = p->dit;
     const int R = 8 / p->dit;  // real rows per tile
-    // u, w: natural-order boxes; y: 128 B swizzled box (epilogue 4 stages
-    // 16-byte units in place) -- gated order-3 tiles keep natural-order v
-    // and y (their epilogue 4 gates in a second pass, kernels_fwd.cu)
+    // u, w: natural-order boxes; v, y: 128 B swizzled boxes (epilogue 4
+    // gates and stages 16-byte units in place) -- gated L0 = 4 tiles keep
+    // natural-order v and y (their epilogue 4 gates in a second pass)
+    const bool natural = gated && p->dit == 4;  // (kernels_fwd.cu: Y_DIRECT)
     bool ok = make_tmap_sig(&prm.tmap_u, u, B, H, p->N, R) == cudaSuccess &&
-              (gated ? make_tmap_sig(&prm.tmap_yo, y, B, H, p->N, R)
-                     : make_tmap_rows(&prm.tmap_yo, y, B, H, p->N, R)) == cudaSuccess;
+              (natural ? make_tmap_sig(&prm.tmap_yo, y, B, H, p->N, R)
+                       : make_tmap_rows(&prm.tmap_yo, y, B, H, p->N, R)) == cudaSuccess;
     if (ok && gated)
       ok = make_tmap_sig(&prm.tmap_w, w, B, H, p->N, R) == cudaSuccess &&
-           make_tmap_sig(&prm.tmap_v, v, B, H, p->N, R) == cudaSuccess;
+           (natural ? make_tmap_sig(&prm.tmap_v, v, B, H, p->N, R)
+                    : make_tmap_rows(&prm.tmap_v, const_cast<void*>(v), B, H, p->N, R)) == cudaSuccess;
     prm.tma_io = ok ? 1 : 0;
     cudaError_t e = launch_fwd_fused(prm, st);
     if (e != cudaSuccess) return cuda_fail(fn, e);

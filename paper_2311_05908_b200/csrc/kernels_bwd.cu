@@ -328,6 +328,21 @@ __global__ void __launch_bounds__(BwdCfg<L1, CAUSAL>::THREADS, 1) fftconv_bwd_o2
     if (!CAUSAL || m < 64) {  // warp-uniform
       constexpr int NIT = C::P * (L1 / 8);
       constexpr int PER = NIT / 2;
+      // the gate vectors of item i + 1 are loaded while item i is processed
+      // (the first before the MMA wait): their global latency is hidden
+      uint4 ga[2], gb[2];
+      auto ld_gate = [&](int i, uint4& a, uint4& b) {
+        const int it = slice * PER + i;
+        const int p = it / (L1 / 8), n1c = it % (L1 / 8);
+        const int64_t goff = tile_base + st_off0 + int64_t(2 * p) * HN + n1c * 8;
+        a = make_uint4(0, 0, 0, 0);
+        b = make_uint4(0, 0, 0, 0);
+        if (gate && 2 * p + cp < rows_left) {
+          a = *reinterpret_cast<const uint4*>(a1 + goff);
+          if (out2) b = *reinterpret_cast<const uint4*>(a2 + goff);
+        }
+      };
+      ld_gate(0, ga[0], gb[0]);
       wait_half(slice);
 #pragma unroll 2
       for (int i = 0; i < PER; ++i) {
@@ -335,11 +350,8 @@ __global__ void __launch_bounds__(BwdCfg<L1, CAUSAL>::THREADS, 1) fftconv_bwd_o2
         const int p = it / (L1 / 8), n1c = it % (L1 / 8);
         const bool ok = 2 * p + cp < rows_left;
         const int64_t goff = tile_base + st_off0 + int64_t(2 * p) * HN + n1c * 8;
-        uint4 va = make_uint4(0, 0, 0, 0), vb = make_uint4(0, 0, 0, 0);
-        if (gate && ok) {
-          va = *reinterpret_cast<const uint4*>(a1 + goff);
-          if (out2) vb = *reinterpret_cast<const uint4*>(a2 + goff);
-        }
+        if (i + 1 < PER) ld_gate(i + 1, ga[(i + 1) & 1], gb[(i + 1) & 1]);
+        const uint4 va = ga[i & 1], vb = gb[i & 1];
         float o[8];
         tmem_ld8(tq + p * L1 + n1c * 8, o);
         tmem_ld_wait();
@@ -449,13 +461,17 @@ __global__ void __launch_bounds__(BwdCfg<L1, CAUSAL>::THREADS, 1) fftconv_bwd_o2
       constexpr uint32_t RS = L1 * 8 + 16;  // padded row stride of red[k2][k1]
       const int k2 = m & 63;
       const int cls = (m >= 64 ? 2 : 0) + slice;
+      // L1 >= 16: the two column slices hold disjoint k1 chunks, so classes
+      // 0 and 1 store in one step and classes 2 and 3 add in the next (the
+      // same per-element order as four steps: class 0 (1), then + class 2 (3))
+      constexpr bool TWO = L1 / 8 >= 2;
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        if (cls == c) {
+      for (int c = 0; c < (TWO ? 2 : 4); ++c) {
+        if ((TWO ? (cls >> 1) : cls) == c) {
 #pragma unroll
           for (int a = 0; a < NK1C; ++a) {
-            const int k1c = (L1 / 8 >= 2) ? slice + 2 * a : 0;
-            const bool add = (c >= 2) || (L1 / 8 < 2 && c == 1);
+            const int k1c = TWO ? slice + 2 * a : 0;
+            const bool add = TWO ? c == 1 : c >= 1;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const uint32_t o = sRED + k2 * RS + (k1c * 8 + e) * 8;

@@ -709,7 +709,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
       // both 16-k2 items unrolled (more ILP, 122 registers) measured 1-2 %
       // faster for gated causal and circular tiles and ~1 % slower for plain
       // causal ones on B200
-      constexpr int kEpi1Unroll = (GATED || !CAUSAL) ? 2 : 1;
+      // (gated order 3 with L0 = 2: 1 -- with the in-place epilogue 4 below
+      // 9 % faster; L0 = 4 keeps 2 and the two-pass epilogue 4: 4-7 % faster)
+      constexpr int kEpi1Unroll = ((GATED && L0I != 2) || !CAUSAL) ? 2 : 1;
 #pragma unroll kEpi1Unroll
       for (int sub = 0; sub < 2; ++sub) {
         const int k20 = slice * 32 + sub * 16;  // 16 k2 per item
@@ -1166,9 +1168,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         // its own 16-byte units in place (v and y at swz128(offset): no bank
         // conflicts) and writes y straight into the store staging -- no
         // intermediate copy of the conv output, no second pass, one barrier
-        // (not for gated order-3 tiles: the extra registers spill there, 14 %
-        // slower at L0 = 4; their v / y maps stay natural-order, api.cu)
-        constexpr bool Y_DIRECT = STG && !(DIT && GATED);
+        // (not for gated order-3 tiles with L0 = 4: the extra registers spill
+        // there, 14 % slower; their v / y maps stay natural-order, api.cu)
+        constexpr bool Y_DIRECT = STG && !(GATED && L0I == 4);
         const bool direct = Y_DIRECT && prm.tma_io;
         const uint32_t sstg = tma_out ? sYS : direct ? sY : bufX;
         if (tma_out && t > t0) mbar_wait(&ys_bar, uint32_t((t - t0 - 1) & 1));
