@@ -73,6 +73,12 @@ __device__ long long fc_trace_buf[8][64][24];
 #ifndef FC_AI_TS
 #define FC_AI_TS 0
 #endif
+#ifndef FC_DIT_KFS
+#define FC_DIT_KFS 1
+#endif
+#ifndef FC_O3_FRAG
+#define FC_O3_FRAG 1
+#endif
 
 // Shared-memory plan of the forward kernel: tables | per-warpgroup (k_f,
 // operand buffer) | staging.  Causal tiles move their rows with bulk (TMA)
@@ -125,6 +131,13 @@ struct FwdCfg {
   // per-warpgroup buffers: k_f copy (L0I = 1; the order-3 tiles read their
   // L0I k_f blocks from global memory / L2) and the operand buffer
   static constexpr uint32_t KF_SM = DIT ? 0 : C::al(C::KF_BYTES);
+  // order 3: the L0I k_f blocks of the current head (16 KB each, layout.h
+  // dit_kf_off) in one buffer both warpgroups read, refilled by bulk copies
+  // when the head changes (FC_DIT_KFS=0: epilogue 2 reads them from L2)
+  // (measured: L0I = 4 4 % faster, L0I = 2 1 % slower -> L0I = 4 only)
+  static constexpr bool KFS = DIT && FC_DIT_KFS && L0I >= 4;
+  static constexpr uint32_t KFD_BLOCK = 16384;
+  static constexpr uint32_t KFD_SM = KFS ? L0I * KFD_BLOCK : 0;
   // per warpgroup: [k_f | operand buffer bufX | u [| w] input slot]; the
   // order-3 tiles and circular tiles keep one slot shared in tile order
   // (measured: per-warpgroup slots made the order-2 kernels 2 % faster, the
@@ -136,7 +149,8 @@ struct FwdCfg {
   // the warpgroups in tile order, leaving by one TMA tensor store each
   static constexpr uint32_t YS_BYTES = (!CAUSAL && !GATED) ? C::R * C::NOUT * 2 : 0;
   static constexpr uint32_t bytes_for(int wg) {
-    return C::al(C::al(C::al(TABLES + wg * WG_BYTES) + (SLOT_WG ? 0 : UW_BYTES)) + V_BYTES) + YS_BYTES + BAR_BYTES;
+    return C::al(C::al(C::al(C::al(TABLES + wg * WG_BYTES) + (SLOT_WG ? 0 : UW_BYTES)) + V_BYTES) + KFD_SM) + YS_BYTES +
+           BAR_BYTES;
   }
   static constexpr int WG = bytes_for(2) <= 227 * 1024 ? 2 : 1;
   static constexpr int THREADS = WG * kWGThreads;
@@ -144,7 +158,8 @@ struct FwdCfg {
   static constexpr uint32_t UW_IN_WG = KF_SM + C::al(C::BUFX_BYTES);  // the slot's offset in its warpgroup's block
   static constexpr uint32_t OFF_UW = C::al(OFF_WG + WG * WG_BYTES);    // (shared slot, !SLOT_WG)
   static constexpr uint32_t OFF_V = C::al(OFF_UW + (SLOT_WG ? 0 : UW_BYTES));
-  static constexpr uint32_t OFF_YS = C::al(OFF_V + V_BYTES);
+  static constexpr uint32_t OFF_KFD = C::al(OFF_V + V_BYTES);
+  static constexpr uint32_t OFF_YS = C::al(OFF_KFD + KFD_SM);
   static constexpr uint32_t OFF_BAR = OFF_YS + YS_BYTES;
   static constexpr uint32_t SMEM = bytes_for(WG);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
@@ -202,6 +217,8 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
     uint64_t mma[2][2];  // [warpgroup]: completion of the first / second half of a stage
     uint64_t stg[2][2];  // [u|w slot, v slot][consuming warpgroup]: bulk copy landed
     uint64_t ys;         // circular TMA-y staging: use j - 1 has been read (phase j - 1)
+    uint64_t kff;        // order 3: k_f buffer refill r landed (phase r)
+    uint64_t e2d[2];     // order 3: [warpgroup] epilogue 2 of its j-th tile done (phase j)
     uint32_t tmem_slot;
   };
   static_assert(sizeof(Bars) <= F::BAR_BYTES, "barrier block");
@@ -261,6 +278,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
       mbar_init(&stg_bar[1][g], 1);
     }
     mbar_init(&ys_bar, 1);
+    mbar_init(&bb.kff, 1);
+    mbar_init(&bb.e2d[0], 1);
+    mbar_init(&bb.e2d[1], 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<(kWG * C::TMEM_COLS > 512 ? 512 : kWG * C::TMEM_COLS)>(&tmem_slot);
@@ -344,6 +364,19 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
     if (GATED) fill(1, t, th, tb);
     else mbar_arrive(&stg_bar[1][(t - t0) % kWG]);
   };
+  // PDL: everything above (tables, barriers, TMEM) overlapped the previous
+  // kernel (the k_f precompute); u, w, v and k_f are read only below
+  griddep_wait();
+  griddep_launch();
+  // order 3: head hh's L0I k_f blocks -> the shared buffer (one elected thread)
+  const uint32_t sKFD = base + F::OFF_KFD;
+  auto kf_fill = [&](int64_t hh_) {
+    const uint8_t* src = gkf + phys_head(hh_) * int64_t(L0I) * C::KF_BYTES;
+    mbar_arrive_expect_tx(&bb.kff, F::KFD_SM);
+#pragma unroll
+    for (int k0 = 0; k0 < L0I; ++k0) bulk_g2s(sKFD + k0 * F::KFD_BLOCK, src + k0 * C::KF_BYTES, F::KFD_BLOCK, &bb.kff);
+  };
+  if (F::KFS && tid == 0) kf_fill(t0 / nbt);
   if (STG_IN && tid == 0) {
     for (int64_t t = t0; t < t0 + (F::SLOT_WG ? kWG : 1) && t < t1; ++t) fill(0, t, t / nbt, t % nbt);
     if (STG) release_out(t0, t0 / nbt, t0 % nbt);
@@ -762,7 +795,169 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
     }, true);
 
     // ---------------- epilogue 2: pointwise * k_f -> stage B^-1 operand (own row: TMEM, else K-major smem)
-    if constexpr (DIT) {
+    if constexpr (DIT && FC_O3_FRAG) {
+      // Order 3 with no lane shuffles: a 16x256b TMEM fragment gives a
+      // thread rows r and r + 8 of its 16-lane block (lane bit 3 = xb: n0's
+      // high bit for L0 = 4, the row pair q for L0 = 2) at one (k2, k1 pair),
+      // and the two column blocks hold n0's low bit, so every n0 of X[f' +
+      // 2048 k0] = sum_n0 W_L0^{n0 k0} W_{32 L0}^{n0 k1} Y_n0[f'] is in the
+      // thread: the outer DFT_L0, * k_f / L0, the inverse DFT_L0 and the
+      // conjugate twiddle run in registers on f32x2 pairs (k1, k1 + 1), and
+      // (L0 = 2) the two rows share each k_f load.  Thread: 16-lane block =
+      // slice, r = lane / 4 (k2 = r + 8 quad + 32 slice), kp % 4 = lane % 4
+      // (k1 = 8 k1c + 2 (lane % 4) + e, k1c = 0..3, e = 0, 1).
+      // (Round 2 before: one row per thread, n0's high bit by shuffles, k_f
+      // by 16 B loads from 32 lines per instruction; epilogue 2 took 8.5k of
+      // a 17k-cycle L0 = 4 tile, now ~3k.)
+      static_assert(TS && !FC_NEG_B && L1 == 32, "order-3 epilogue 2");
+      const int fr = lane >> 2, fq = lane & 3;
+      const int k2 = fr + 8 * quad + 32 * slice;
+      const uint32_t tl = tq + (uint32_t(16 * slice) << 16);  // lane base of the 16-lane block
+      const uint8_t* kfh = gkf + h * int64_t(L0I) * C::KF_BYTES;
+      auto kf_at = [&](int k0, int k1c) -> float4 {
+        const uint32_t off = dit_kf_off(uint32_t(k2), uint32_t(4 * k1c + fq));
+        if constexpr (F::KFS) {
+          const uint4 v4 = ld_shared_u4(sKFD + k0 * F::KFD_BLOCK + off);
+          return make_float4(__uint_as_float(v4.x), __uint_as_float(v4.y), __uint_as_float(v4.z), __uint_as_float(v4.w));
+        } else {
+          return __ldg(reinterpret_cast<const float4*>(kfh + k0 * C::KF_BYTES + off));
+        }
+      };
+      if constexpr (F::KFS) mbar_wait(&bb.kff, uint32_t(hh - t0 / nbt) & 1u);  // this head's refill landed
+      wait_half(0);
+      wait_half(1);
+#pragma unroll
+      for (int bh = 0; bh < 2; ++bh) {  // two k1 chunks per batch of TMEM loads
+        // yv[c][slot][re|im] = {(xb 0, k1), (xb 0, k1 + 1), (xb 1, k1), (xb 1, k1 + 1)}
+        float yv[2][2][2][4];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int slot = 0; slot < 2; ++slot) {
+            const uint32_t col = slot * NBF + 8 * (2 * bh + c);
+            tmem_ld_16x256b(tl + col, yv[c][slot][0]);
+            tmem_ld_16x256b(tl + col + L1, yv[c][slot][1]);
+          }
+        float4 kf[2][4];
+        float2 wb[2][2];  // W_128^{k1 + e}
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+          for (int k0 = 0; k0 < L0I; ++k0) kf[c][k0] = kf_at(k0, 2 * bh + c);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) wb[c][e] = wroot<32 * L0I>(8 * (2 * bh + c) + 2 * fq + e);
+        }
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int k1c = 2 * bh + c;
+          if constexpr (L0I == 4) {
+            float2 xr[4], xi[4];  // Y_n0, n0 = 2 xb + slot
+#pragma unroll
+            for (int slot = 0; slot < 2; ++slot)
+#pragma unroll
+              for (int xb = 0; xb < 2; ++xb) {
+                xr[2 * xb + slot] = make_float2(yv[c][slot][0][2 * xb], yv[c][slot][0][2 * xb + 1]);
+                xi[2 * xb + slot] = make_float2(yv[c][slot][1][2 * xb], yv[c][slot][1][2 * xb + 1]);
+              }
+            // W_128^{n0 k1}: n0 = 1 from MUFU, 2 = its square, 3 = 1 * 2
+            float2 wr[4], wi[4];
+            wr[1] = make_float2(wb[c][0].x, wb[c][1].x);
+            wi[1] = make_float2(wb[c][0].y, wb[c][1].y);
+            wr[2] = fma2(wr[1], wr[1], mul2(wi[1], make_float2(-wi[1].x, -wi[1].y)));
+            wi[2] = mul2(make_float2(2.f * wr[1].x, 2.f * wr[1].y), wi[1]);
+            wr[3] = fma2(wr[1], wr[2], mul2(wi[1], make_float2(-wi[2].x, -wi[2].y)));
+            wi[3] = fma2(wr[1], wi[2], mul2(wi[1], wr[2]));
+            float2 tr[4], ti[4];
+            tr[0] = xr[0]; ti[0] = xi[0];
+#pragma unroll
+            for (int n0 = 1; n0 < 4; ++n0) {  // T = W Y
+              tr[n0] = fma2(xr[n0], wr[n0], mul2(xi[n0], make_float2(-wi[n0].x, -wi[n0].y)));
+              ti[n0] = fma2(xr[n0], wi[n0], mul2(xi[n0], wr[n0]));
+            }
+            // S[k0] = sum_n0 W_4^{n0 k0} T[n0], W_4 = -i
+            const float2 ar = add2(tr[0], tr[2]), ai = add2(ti[0], ti[2]);
+            const float2 br = sub2(tr[0], tr[2]), bi = sub2(ti[0], ti[2]);
+            const float2 cr = add2(tr[1], tr[3]), ci = add2(ti[1], ti[3]);
+            const float2 dr = sub2(tr[1], tr[3]), di = sub2(ti[1], ti[3]);
+            float2 sr[4], si[4];
+            sr[0] = add2(ar, cr); si[0] = add2(ai, ci);
+            sr[2] = sub2(ar, cr); si[2] = sub2(ai, ci);
+            sr[1] = add2(br, di); si[1] = sub2(bi, dr);  // B - i D
+            sr[3] = sub2(br, di); si[3] = add2(bi, dr);  // B + i D
+            // * k_f[f' + 2048 k0] / 4: kf = {kr_e0, kr_e1, ki_e0, ki_e1}
+#pragma unroll
+            for (int k0 = 0; k0 < 4; ++k0) {
+              const float4 qv = kf[c][k0];
+              const float2 kr = make_float2(0.25f * qv.x, 0.25f * qv.y), ki = make_float2(0.25f * qv.z, 0.25f * qv.w);
+              const float2 zr = fma2(sr[k0], kr, mul2(si[k0], make_float2(-ki.x, -ki.y)));
+              const float2 zi = fma2(sr[k0], ki, mul2(si[k0], kr));
+              sr[k0] = zr; si[k0] = zi;
+            }
+            // R[n0] = sum_k0 W_4^{-n0 k0} Z[k0]
+            const float2 a2r = add2(sr[0], sr[2]), a2i = add2(si[0], si[2]);
+            const float2 b2r = sub2(sr[0], sr[2]), b2i = sub2(si[0], si[2]);
+            const float2 c2r = add2(sr[1], sr[3]), c2i = add2(si[1], si[3]);
+            const float2 d2r = sub2(sr[1], sr[3]), d2i = sub2(si[1], si[3]);
+            float2 rr[4], ri[4];
+            rr[0] = add2(a2r, c2r); ri[0] = add2(a2i, c2i);
+            rr[2] = sub2(a2r, c2r); ri[2] = sub2(a2i, c2i);
+            rr[1] = sub2(b2r, d2i); ri[1] = add2(b2i, d2r);  // B' + i D'
+            rr[3] = add2(b2r, d2i); ri[3] = sub2(b2i, d2r);  // B' - i D'
+#pragma unroll
+            for (int n0 = 1; n0 < 4; ++n0) {  // conj twiddle
+              const float2 o_r = fma2(rr[n0], wr[n0], mul2(ri[n0], wi[n0]));
+              const float2 o_i = fma2(ri[n0], wr[n0], mul2(rr[n0], make_float2(-wi[n0].x, -wi[n0].y)));
+              rr[n0] = o_r; ri[n0] = o_i;
+            }
+            // B^-1 operand (K index c*L1 + k1 -> column (c*L1 + k1) / 2): rows
+            // r (xb 0: n0 = slot) and r + 8 (xb 1: n0 = 2 + slot), column kp
+#pragma unroll
+            for (int slot = 0; slot < 2; ++slot) {
+              const uint32_t ca = tl + C::CA + slot * L1 + 4 * k1c;
+              tmem_st_16x128b(ca, pack_half2(rr[slot].x, rr[slot].y), pack_half2(rr[2 + slot].x, rr[2 + slot].y));
+              tmem_st_16x128b(ca + L1 / 2, pack_half2(ri[slot].x, ri[slot].y), pack_half2(ri[2 + slot].x, ri[2 + slot].y));
+            }
+          } else {
+          // L0 = 2: per row pair xb, n0 = slot; X[k0] = Y_0 + (-1)^k0 W_64^{k1} Y_1
+          const float2 wr = make_float2(wb[c][0].x, wb[c][1].x), wi = make_float2(wb[c][0].y, wb[c][1].y);
+          const float2 nwi = make_float2(-wi.x, -wi.y);
+          float2 orr[2][2], oii[2][2];  // [xb][n0]
+#pragma unroll
+          for (int xb = 0; xb < 2; ++xb) {
+            const float2 y0r = make_float2(yv[c][0][0][2 * xb], yv[c][0][0][2 * xb + 1]);
+            const float2 y0i = make_float2(yv[c][0][1][2 * xb], yv[c][0][1][2 * xb + 1]);
+            const float2 y1r = make_float2(yv[c][1][0][2 * xb], yv[c][1][0][2 * xb + 1]);
+            const float2 y1i = make_float2(yv[c][1][1][2 * xb], yv[c][1][1][2 * xb + 1]);
+            const float2 t1r = fma2(y1r, wr, mul2(y1i, nwi)), t1i = fma2(y1r, wi, mul2(y1i, wr));
+            float2 sr[2], si[2];
+            sr[0] = add2(y0r, t1r); si[0] = add2(y0i, t1i);
+            sr[1] = sub2(y0r, t1r); si[1] = sub2(y0i, t1i);
+#pragma unroll
+            for (int k0 = 0; k0 < 2; ++k0) {  // * k_f / 2
+              const float4 qv = kf[c][k0];
+              const float2 kr = make_float2(0.5f * qv.x, 0.5f * qv.y), ki = make_float2(0.5f * qv.z, 0.5f * qv.w);
+              const float2 zr = fma2(sr[k0], kr, mul2(si[k0], make_float2(-ki.x, -ki.y)));
+              const float2 zi = fma2(sr[k0], ki, mul2(si[k0], kr));
+              sr[k0] = zr; si[k0] = zi;
+            }
+            orr[xb][0] = add2(sr[0], sr[1]); oii[xb][0] = add2(si[0], si[1]);
+            const float2 r1r = sub2(sr[0], sr[1]), r1i = sub2(si[0], si[1]);
+            orr[xb][1] = fma2(r1r, wr, mul2(r1i, wi));  // * conj W
+            oii[xb][1] = fma2(r1i, wr, mul2(r1r, nwi));
+          }
+#pragma unroll
+          for (int slot = 0; slot < 2; ++slot) {  // rows r (xb 0), r + 8 (xb 1); n0 = slot
+            const uint32_t ca = tl + C::CA + slot * L1 + 4 * k1c;
+            tmem_st_16x128b(ca, pack_half2(orr[0][slot].x, orr[0][slot].y), pack_half2(orr[1][slot].x, orr[1][slot].y));
+            tmem_st_16x128b(ca + L1 / 2, pack_half2(oii[0][slot].x, oii[0][slot].y),
+                            pack_half2(oii[1][slot].x, oii[1][slot].y));
+          }
+          }
+        }
+      }
+      tmem_st_wait();
+    } else if constexpr (DIT) {
       // Order 3: for each f' = k2 + 64 k1 the L0I inner rows n0 hold
       // Y_n0[f']; X[f' + 2048 k0] = sum_n0 W_L0I^{n0 k0} W_{32 L0I}^{n0 k1}
       // Y_n0[f'] (the W_LF^{n0 k2} part of the twiddle was applied in
@@ -780,9 +975,16 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
 #pragma unroll
         for (int slot = 0; slot < 2; ++slot)
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj)
-            dst[slot][jj] = __ldg(reinterpret_cast<const float4*>(kfh + k0_of(slot) * C::KF_BYTES +
-                                                                  tab_off<L1 / 2>(k2, k1c * 4 + jj)));
+          for (int jj = 0; jj < 4; ++jj) {
+            if constexpr (F::KFS) {  // shared buffer: 8 lanes read 128 contiguous bytes per phase
+              const uint4 q = ld_shared_u4(sKFD + k0_of(slot) * F::KFD_BLOCK + dit_kf_off(k2, k1c * 4 + jj));
+              dst[slot][jj] = make_float4(__uint_as_float(q.x), __uint_as_float(q.y), __uint_as_float(q.z),
+                                          __uint_as_float(q.w));
+            } else {
+              dst[slot][jj] = __ldg(reinterpret_cast<const float4*>(kfh + k0_of(slot) * C::KF_BYTES +
+                                                                    dit_kf_off(k2, k1c * 4 + jj)));
+            }
+          }
       };
       // all complex math on f32x2 pairs of consecutive k1 (FMUL2/FFMA2/FADD2)
       auto process = [&](int k1c, const float4 (&kf)[2][4]) {
@@ -888,6 +1090,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         }
       };
       float4 kfa[2][4];
+      if constexpr (F::KFS) mbar_wait(&bb.kff, uint32_t(hh - t0 / nbt) & 1u);  // this head's refill landed
       load_kf(slice, kfa);
       wait_half(0);
       wait_half(1);
@@ -1008,6 +1211,19 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         }
       }
     }, true);
+    // order 3: the whole warpgroup is past epilogue 2 of tile t (the barrier
+    // above): signal it, and when the next tile starts a new head, refill
+    // the shared k_f buffer once the other warpgroup's tile t - 1 (the last
+    // other reader of the old head) is past its epilogue 2 as well
+    if constexpr (F::KFS) {
+      if (filler()) {
+        mbar_arrive(&bb.e2d[wg]);
+        if (t + 1 < t1 && (t + 1) / nbt != hh) {
+          if (kWG == 2 && t - 1 >= t0) mbar_wait(&bb.e2d[wg ^ 1], uint32_t((t - 1 - t0) / 2) & 1u);
+          kf_fill((t + 1) / nbt);
+        }
+      }
+    }
 
     // ---------------- epilogue 3: conj twiddle, transpose -> stage A^-1 operand (MN-major B)
     if constexpr (EPI_PIPE) {  // item i + 1's TMEM load overlaps item i's math (as epilogue 2)
@@ -1357,8 +1573,7 @@ static cudaError_t launch_o2(const FwdParams& prm, cudaStream_t stream) {
   const int64_t tiles = (prm.row_map ? (prm.H / prm.row_L0) * prm.nrow : prm.H) * nbt;
   int grid = int(tiles < prm.num_sms ? tiles : prm.num_sms);
   if (grid < 1) return cudaSuccess;
-  kern<<<grid, F::THREADS, F::SMEM, stream>>>(prm);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(F::THREADS), F::SMEM, stream, prm);
 }
 
 template <bool CAUSAL, bool GATED, typename T>

@@ -183,9 +183,11 @@ __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) 
   const bool has1 = h0 + 1 < prm.H;
   const int L = int(prm.L), K = int(prm.K);
   float2* tws = sm + L + L / 8;
+  griddep_launch();
   {
-    load_padded(tws, prm.twiddle, L);
+    load_padded(tws, prm.twiddle, L);  // plan-owned table
   }
+  griddep_wait();  // PDL: k is read and k_f written only after the previous kernel
   const float* k0row = prm.k + h0 * K;
   const float* k1row = k0row + K;
   // all of this thread's filter loads are issued before any is stored
@@ -421,8 +423,8 @@ cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
 // heads per CTA as above, the LF-point transform in shared memory with
 // twiddles W_LF^e from sincospif of the exact dyadic argument -2e/LF (this
 // precompute is not the hot path), written as L0 blocks per head: block k0
-// holds K_f[f' + 2048 k0], f' = k2 + 64 k1, in the fused kernel's [k2][k1/2]
-// padded layout (DIT order: the forward kernel's outer DFT produces the
+// holds K_f[f' + 2048 k0], f' = k2 + 64 k1, in the [k1/2][k2] layout of
+// layout.h dit_kf_off (DIT order: the forward kernel's outer DFT produces the
 // frequency digit k0 = f / 2048).
 template <int LF>
 __global__ void __launch_bounds__(256) precompute_kf_dit_kernel(const KfParams prm) {
@@ -437,6 +439,8 @@ __global__ void __launch_bounds__(256) precompute_kf_dit_kernel(const KfParams p
     sincospif(-2.0f * float(e) / float(LF), &sn, &cs);
     tws[pd(e)] = make_float2(cs, sn);
   }
+  griddep_launch();
+  griddep_wait();  // PDL: k is read and k_f written only after the previous kernel
   const float* k0row = prm.k + h0 * K;
   const float* k1row = k0row + K;
   for (int n = threadIdx.x; n < LF; n += 256)
@@ -461,7 +465,7 @@ __global__ void __launch_bounds__(256) precompute_kf_dit_kernel(const KfParams p
     const float2 a1 = make_float2(0.5f * (z1.x + m1.x), 0.5f * (z1.y - m1.y));
     const float2 b0 = make_float2(0.5f * (z0.y + m0.y), -0.5f * (z0.x - m0.x));
     const float2 b1 = make_float2(0.5f * (z1.y + m1.y), -0.5f * (z1.x - m1.x));
-    const uint32_t off = uint32_t(k0 * hbytes) + tab_off_rt(CPR, uint32_t(k2), uint32_t(k1 / 2));
+    const uint32_t off = uint32_t(k0 * hbytes) + dit_kf_off(uint32_t(k2), uint32_t(k1 / 2));
     *reinterpret_cast<float4*>(out0 + off) = make_float4(a0.x, a1.x, a0.y, a1.y);
     if (has1) *reinterpret_cast<float4*>(out1 + off) = make_float4(b0.x, b1.x, b0.y, b1.y);
   }
@@ -475,13 +479,13 @@ cudaError_t launch_precompute_kf_dit(const KfParams& prm, int L0, cudaStream_t s
     static int attr[64] = {0};
     if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_dit_kernel<4096>), int(smem), attr))
       return e;
-    precompute_kf_dit_kernel<4096><<<grid, 256, smem, s>>>(prm);
+    return launch_pdl(precompute_kf_dit_kernel<4096>, dim3(grid), dim3(256), smem, s, prm);
   } else if (L0 == 4) {
     const size_t smem = size_t(2 * (8192 + 1024)) * sizeof(float2);
     static int attr[64] = {0};
     if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_dit_kernel<8192>), int(smem), attr))
       return e;
-    precompute_kf_dit_kernel<8192><<<grid, 256, smem, s>>>(prm);
+    return launch_pdl(precompute_kf_dit_kernel<8192>, dim3(grid), dim3(256), smem, s, prm);
   } else {
     return cudaErrorInvalidValue;
   }
@@ -507,7 +511,7 @@ __global__ void kf_dit_to_dif_kernel(const uint8_t* __restrict__ src, uint8_t* _
     const int f = k0 + L0 * (k2 + 64 * (2 * kp + s));
     const int b = f / 2048, g = f % 2048;
     const int k2s = g % 64, k1s = g / 64;
-    const float4 q = *reinterpret_cast<const float4*>(src + (h * L0 + b) * hb + tab_off_rt(CPR, uint32_t(k2s), uint32_t(k1s / 2)));
+    const float4 q = *reinterpret_cast<const float4*>(src + (h * L0 + b) * hb + dit_kf_off(uint32_t(k2s), uint32_t(k1s / 2)));
     v[s] = (k1s & 1) ? q.y : q.x;
     v[2 + s] = (k1s & 1) ? q.w : q.z;
   }
@@ -528,8 +532,7 @@ cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s) {
   const size_t smem = fft_smem_bytes(prm.L);
   static int attr[64] = {0};
   if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_kernel), int(smem), attr)) return e;
-  precompute_kf_kernel<<<unsigned((prm.H + 1) / 2), 256, smem, s>>>(prm);
-  return cudaGetLastError();
+  return launch_pdl(precompute_kf_kernel, dim3(unsigned((prm.H + 1) / 2)), dim3(256), smem, s, prm);
 }
 
 }  // namespace fc

@@ -20,4 +20,13 @@ FC_HD uint32_t tab_off_rt(uint32_t cpr, uint32_t row, uint32_t j) { return row *
 template <int CPR>
 FC_HD uint32_t tab_off(uint32_t row, uint32_t j) { return row * (CPR * 16u + 16u) + j * 16u; }
 
+// k_f block of a single-pass order-3 plan (K_f[f' + 2048 k0], f' = k2 + 64 k1,
+// one block per (head, k0)): float4 {kr(k1), kr(k1+1), ki(k1), ki(k1+1)} of
+// k1 pair kp = k1 / 2 at index ((kp / 4) * 64 + k2) * 4 + kp % 4.  The
+// L0 = 4 epilogue-2 thread (k2 = lane / 4 + ..., kp % 4 = lane % 4, one
+// 16x256b TMEM fragment) reads one float4 per k0 and 4 k1 pairs: 8 lanes
+// cover 128 contiguous bytes (conflict-free from shared memory, full lines
+// from L2).  16 KB per block; blocks are tab_stride(16) * 64 bytes apart.
+FC_HD uint32_t dit_kf_off(uint32_t k2, uint32_t kp) { return (((kp >> 2) * 64u + k2) * 4u + (kp & 3u)) * 16u; }
+
 }  // namespace fc

@@ -30,6 +30,12 @@ FC_DEVICE uint32_t smem_u32(const void* p) {
 FC_DEVICE void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
+// Programmatic dependent launch (PDL).  griddep_wait(): block until every
+// prerequisite grid of this launch has completed and its memory is visible
+// (returns at once for a normal launch).  griddep_launch(): allow the next
+// PDL-launched grid in the stream to start its pre-wait prologue.
+FC_DEVICE void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+FC_DEVICE void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 FC_DEVICE void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -221,6 +227,19 @@ FC_DEVICE void tmem_st8(uint32_t taddr, const uint32_t* r) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
+}
+// 16-lane shapes (lanes base .. base + 15 of the warp's quadrant): thread t
+// holds rows t/4 and t/4 + 8.  16x256b: columns 2(t%4), 2(t%4)+1 of each row
+// -> v = {row r col c, row r col c+1, row r+8 col c, row r+8 col c+1};
+// 16x128b: column t%4 -> {row r, row r+8}
+FC_DEVICE void tmem_ld_16x256b(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+FC_DEVICE void tmem_st_16x128b(uint32_t taddr, uint32_t a, uint32_t b) {
+  asm volatile("tcgen05.st.sync.aligned.16x128b.x1.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(a), "r"(b) : "memory");
 }
 FC_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 FC_DEVICE void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
