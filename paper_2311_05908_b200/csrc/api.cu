@@ -170,7 +170,7 @@ static fftconv_status_t run_precompute(fftconv_plan_t p, const float* d_k, const
   prm.L1 = p->L1;
   prm.L2 = p->L2;
   cudaError_t e;
-  if (p->dit > 1) {  // single-pass order 3: L0 blocks of K_f[f' + 2048 k0] per head
+  if (p->dit > 1 && p->dit < 8) {  // single-pass order 3: L0 blocks of K_f[f' + 2048 k0] per head
     e = launch_precompute_kf_dit(prm, p->dit, reinterpret_cast<cudaStream_t>(stream));
     g_launches += H > 0 ? 1 : 0;
   } else if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
@@ -182,6 +182,10 @@ static fftconv_status_t run_precompute(fftconv_plan_t p, const float* d_k, const
     for (int l = 0; l < 4; ++l) prm.lev[l] = p->lev_L0[l];
     e = launch_mp_precompute_kf(prm, p->lev_L0, p->nlev, p->L, block, reinterpret_cast<cudaStream_t>(stream));
     g_launches += H > 0 ? 2 + p->nlev - 1 : 0;
+    if (e == cudaSuccess && p->dit == 8) {  // order 3, L0 = 8: the multipass k_f re-laid out per head
+      e = launch_kf_dif_to_dit(d_kf, H, p->dit, reinterpret_cast<cudaStream_t>(stream));
+      g_launches += H > 0 ? 1 : 0;
+    }
   } else {
     e = launch_precompute_kf(prm, reinterpret_cast<cudaStream_t>(stream));
     g_launches += H > 0 ? 1 : 0;
@@ -226,16 +230,21 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     prm.dtype = p->dtype == FFTCONV_BF16 ? 1 : 0;
     prm.num_sms = num_sms_current();
     prm.L0I = p->dit;
-    const int R = 8 / p->dit;  // real rows per tile
+    const int R = p->dit == 8 ? 2 : 8 / p->dit;  // real rows per tile (L0 = 8: one pair, coupled warpgroups)
     // u, w: natural-order boxes; v, y: 128 B swizzled boxes (epilogue 4
     // gates and stages 16-byte units in place) -- gated L0 = 4 tiles keep
     // natural-order v and y (their epilogue 4 gates in a second pass)
     const bool natural = gated && p->dit == 4;  // (kernels_fwd.cu: Y_DIRECT)
-    bool ok = make_tmap_sig(&prm.tmap_u, u, B, H, p->N, R) == cudaSuccess &&
+    // (L0 = 8: u, w arrive 128 B swizzled too -- each thread reads one 128 B
+    // line of a row, the swizzle spreads 8 lanes' lines over all banks)
+    const bool swz_in = p->dit == 8;
+    bool ok = (swz_in ? make_tmap_rows(&prm.tmap_u, const_cast<void*>(u), B, H, p->N, R)
+                      : make_tmap_sig(&prm.tmap_u, u, B, H, p->N, R)) == cudaSuccess &&
               (natural ? make_tmap_sig(&prm.tmap_yo, y, B, H, p->N, R)
                        : make_tmap_rows(&prm.tmap_yo, y, B, H, p->N, R)) == cudaSuccess;
     if (ok && gated)
-      ok = make_tmap_sig(&prm.tmap_w, w, B, H, p->N, R) == cudaSuccess &&
+      ok = (swz_in ? make_tmap_rows(&prm.tmap_w, const_cast<void*>(w), B, H, p->N, R)
+                   : make_tmap_sig(&prm.tmap_w, w, B, H, p->N, R)) == cudaSuccess &&
            (natural ? make_tmap_sig(&prm.tmap_v, v, B, H, p->N, R)
                     : make_tmap_rows(&prm.tmap_v, const_cast<void*>(v), B, H, p->N, R)) == cudaSuccess;
     prm.tma_io = ok ? 1 : 0;

@@ -99,8 +99,15 @@ struct FwdCfg {
   // are the L0I decimated inner rows z[n0 + L0I n'] of P / L0I row pairs;
   // real rows of length NROW = L0I * NOUT, RR = R / L0I rows per tile
   static constexpr bool DIT = L0I > 1;
-  static_assert(!DIT || (CAUSAL && L1 == 32 && C::P % L0I == 0 && (L0I == 2 || L0I == 4)), "single-pass order 3");
-  static constexpr int RR = C::R / L0I;
+  // L0I = 8 (fft_size 16384): one row pair's 8 inner rows are 256 stage-A
+  // rows, two warpgroup tiles -- the warpgroups work on the same pair
+  // ("coupled"), warpgroup g holding inner rows n0 = 4 g + p, and meet in
+  // epilogue 2 (the outer DFT_8 reads both warpgroups' TMEM) and epilogue 4
+  // (each writes 4 of every 8 output samples)
+  static constexpr bool CPL = L0I == 8;
+  static_assert(!DIT || (CAUSAL && L1 == 32 && (C::P % L0I == 0 || CPL) && (L0I == 2 || L0I == 4 || CPL)),
+                "single-pass order 3");
+  static constexpr int RR = CPL ? 2 : C::R / L0I;
   static constexpr int NROW = C::NOUT * L0I;
   // Stage B / B^-1 N: re | im only (the negated plane the complex multiply
   // needs is a sign folded into the f32x2 multiplies); FC_NEG_B=1 has the
@@ -135,7 +142,7 @@ struct FwdCfg {
   // dit_kf_off) in one buffer both warpgroups read, refilled by bulk copies
   // when the head changes (FC_DIT_KFS=0: epilogue 2 reads them from L2)
   // (measured: L0I = 4 4 % faster, L0I = 2 1 % slower -> L0I = 4 only)
-  static constexpr bool KFS = DIT && FC_DIT_KFS && L0I >= 4;
+  static constexpr bool KFS = DIT && FC_DIT_KFS && L0I == 4;
   static constexpr uint32_t KFD_BLOCK = 16384;
   static constexpr uint32_t KFD_SM = KFS ? L0I * KFD_BLOCK : 0;
   // per warpgroup: [k_f | operand buffer bufX | u [| w] input slot]; the
@@ -181,6 +188,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   constexpr int LF = C::L * L0I;   // the whole transform (fft_size)
   constexpr int kWG = F::WG;
   constexpr int kThreads = F::THREADS;
+  constexpr bool CPL = F::CPL;            // coupled warpgroups (order 3, L0I = 8)
+  constexpr int TSTEP = CPL ? 1 : kWG;     // tile stride of a warpgroup
+  static_assert(!CPL || kWG == 2, "coupled tiles need both warpgroups");
   constexpr bool STG = F::STG;      // input staging by bulk copies (causal: + v slot, y by bulk stores)
   constexpr bool STG_IN = F::STG_IN;  // input staging (causal or circular plain)
   constexpr int L2 = C::L2;
@@ -219,7 +229,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
     uint64_t ys;         // circular TMA-y staging: use j - 1 has been read (phase j - 1)
     uint64_t kff;        // order 3: k_f buffer refill r landed (phase r)
     uint64_t e2d[2];     // order 3: [warpgroup] epilogue 2 of its j-th tile done (phase j)
+    uint64_t bdone[2];   // coupled tiles: [warpgroup] stage B of its j-th tile complete (phase j)
     uint32_t tmem_slot;
+    uint32_t uw_cnt;     // coupled tiles: warpgroups past stage A (the second refills the input slot)
   };
   static_assert(sizeof(Bars) <= F::BAR_BYTES, "barrier block");
   Bars& bb = *reinterpret_cast<Bars*>(smem_raw + F::OFF_BAR);
@@ -281,6 +293,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
     mbar_init(&bb.kff, 1);
     mbar_init(&bb.e2d[0], 1);
     mbar_init(&bb.e2d[1], 1);
+    bb.uw_cnt = 0;
+    mbar_init(&bb.bdone[0], 1);
+    mbar_init(&bb.bdone[1], 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<(kWG * C::TMEM_COLS > 512 ? 512 : kWG * C::TMEM_COLS)>(&tmem_slot);
@@ -327,7 +342,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   auto fill = [&](int kind, int64_t t, int64_t th, int64_t tb) {  // tile t = th * nbt + tb
     const int64_t tbase = (tb * RR * H + phys_head(th)) * N;
     const int rows = int(B - tb * RR < RR ? B - tb * RR : RR);
-    uint64_t* bar = &stg_bar[kind][(t - t0) % kWG];
+    uint64_t* bar = &stg_bar[kind][CPL ? 0 : (t - t0) % kWG];
     const uint32_t sUW = F::SLOT_WG ? base + F::OFF_WG + uint32_t((t - t0) % kWG) * F::WG_BYTES + F::UW_IN_WG
                                     : base + F::OFF_UW;  // the consumer's slot
     const int planes = (kind == 0 && GATED) ? 2 : 1;
@@ -355,15 +370,18 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   };
   uint32_t stg_phase[2] = {0, 0};
   auto stg_wait = [&](int kind) {  // every thread waits (bulk-copied data)
-    mbar_wait(&stg_bar[kind][wg], stg_phase[kind]);
+    mbar_wait(&stg_bar[kind][CPL ? 0 : wg], stg_phase[kind]);
     stg_phase[kind] ^= 1;
   };
   // output slot hand-over for tile t: v landed (gated) or the previous
   // tile's y stores have read the slot (plain)
   auto release_out = [&](int64_t t, int64_t th, int64_t tb) {
     if (GATED) fill(1, t, th, tb);
-    else mbar_arrive(&stg_bar[1][(t - t0) % kWG]);
+    else mbar_arrive(&stg_bar[1][CPL ? 0 : (t - t0) % kWG]);
   };
+#ifdef FC_HANG_DEBUG
+  if (tid == 0 && blockIdx.x == 0) printf("smem base %u bars %u (mma, stg, ys, kff, e2d)\n", base, base + F::OFF_BAR);
+#endif
   // PDL: everything above (tables, barriers, TMEM) overlapped the previous
   // kernel (the k_f precompute); u, w, v and k_f are read only below
   griddep_wait();
@@ -412,10 +430,11 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   // blocks on the tensor queue for a whole stage (a half with no MMAs must
   // not be split: its commit would complete at once).  Measured 2-8 %
   // slower on every workload.
-  auto sync_and_issue = [&](auto&& issue_half, bool split = false) {
+  auto sync_and_issue = [&](auto&& issue_half, bool split = false, bool cta = false, uint64_t* extra = nullptr) {
     fence_async_smem();
     tc_fence_before();
-    wg_sync();
+    if (cta) named_sync(3, kThreads);  // coupled tiles: both warpgroups wrote this stage's operands
+    else wg_sync();
     stamp(2 + 3 * stage_no);
     if (FC_SPLIT_ISSUE && split) {
       if (wtid < 32 && elect_one()) {
@@ -433,6 +452,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
       mma_commit(&bars[0]);
       issue_half(1);
       mma_commit(&bars[1]);
+      if (extra) mma_commit(extra);  // a once-per-tile completion signal (coupled tiles)
     }
     stamp(3 + 3 * stage_no);
     ++stage_no;
@@ -470,7 +490,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   // transform index e1 = n0 + L0I n1 (W^{2 e1}); epilogue 3 steps n1 at
   // fixed (n0, k2) (W^{L0I k2}, W^{2 L0I k2}) for the thread's two k2.
   auto tw_at = [&](int e1, int k2) { return wroot<LF>(e1 * k2); };  // W_LF^{e1 k2}
-  const int e1A = (pA % L0I) + L0I * n1A;
+  // inner row p of this warpgroup's tile -> n0 (coupled tiles: n0 = 4 wg + p)
+  auto n0_of_p = [&](int p) { return CPL ? 4 * wg + p : p % L0I; };
+  const int e1A = n0_of_p(pA) + L0I * n1A;
   const float2 tw1_c2 = tw_at(e1A, 2);
   float4 tw3_c[2];
 #pragma unroll
@@ -574,6 +596,44 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   // (samples n0 + L0I (8 j + e + 32 n2), e < 8).
   constexpr int PER_SC = DIT ? RR * (NROW / (8 * L0I)) / kWGThreads : 1;
   auto build_dit = [&](int left) {
+    if constexpr (CPL) {
+      // coupled tiles: this warpgroup's inner rows n0 = 4 wg + p are the 8
+      // bytes at 8 wg of every 16 B chunk (chunk sc = sample n' = 8 (n2 JC +
+      // j) + sc of the row, its 8 n0; the thread's 8 chunks are one 128 B
+      // line, staged 128 B swizzled so 8 lanes' lines hit distinct banks):
+      // 16 B loads, this warpgroup's halves gated on pairs of chunks, then
+      // transposed into the 4 operand chunks (p, j)
+      static_assert(PER_SC == 1, "coupled build");
+      const int r = ld_r0;
+      uint32_t wd[16];  // [sc][2]: halves (p 0, 1), (p 2, 3) of chunk sc
+      auto half8 = [&](uint4 q) { return wg ? make_uint2(q.z, q.w) : make_uint2(q.x, q.y); };
+#pragma unroll
+      for (int sp = 0; sp < 4; ++sp) {
+        uint4 uv = make_uint4(0, 0, 0, 0), wv = make_uint4(0, 0, 0, 0);
+        if (r < left) {
+          const uint32_t o = r * F::ROW_BYTES + (ld_cm * L0I + 2 * sp) * 16;
+          const uint2 a = half8(ld_shared_u4(sUW + swz128(o))), b = half8(ld_shared_u4(sUW + swz128(o + 16)));
+          uv = make_uint4(a.x, a.y, b.x, b.y);
+          if (GATED) {
+            const uint32_t ow = RR * F::ROW_BYTES + o;
+            const uint2 c = half8(ld_shared_u4(sUW + swz128(ow))), d = half8(ld_shared_u4(sUW + swz128(ow + 16)));
+            wv = make_uint4(c.x, c.y, d.x, d.y);
+          }
+        }
+        const uint4 g = gate8(uv, wv);
+        wd[4 * sp + 0] = g.x; wd[4 * sp + 1] = g.y; wd[4 * sp + 2] = g.z; wd[4 * sp + 3] = g.w;
+      }
+      const int c = r & 1, k = c * C::KA + ld_n2;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        uint32_t o[4];
+#pragma unroll
+        for (int t2 = 0; t2 < 4; ++t2)  // samples n' = 2 t2, 2 t2 + 1 of inner row p
+          o[t2] = __byte_perm(wd[2 * (2 * t2) + (p >> 1)], wd[2 * (2 * t2 + 1) + (p >> 1)], (p & 1) ? 0x7632u : 0x5410u);
+        const int g8 = ld_j * 4 + p;
+        st_shared_v4(bufX + g8 * C::SBO_A + (k >> 3) * 128 + (k & 7) * 16, o[0], o[1], o[2], o[3]);
+      }
+    } else {
 #pragma unroll
     for (int i = 0; i < PER_SC; ++i) {
       const int r = ld_r0 + i * RSTEP;
@@ -604,6 +664,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         st_shared_v4(bufX + g8 * C::SBO_A + (k >> 3) * 128 + (k & 7) * 16, o[0], o[1], o[2], o[3]);
       }
     }
+    }
   };
   auto store_chunks = [&](const uint4* uv, const uint4* wv) {
 #pragma unroll
@@ -625,10 +686,10 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
   const int o_col0 = M64 ? o_hh * 64 + slice * 32 : slice * 64;  // first (p, n1) column of this thread
   const uint32_t o_tcol = M64 ? (AI_TS ? o_hh * 64 : 0) + slice * 32 : slice * 64;  // its TMEM column
 
-  int64_t hh = (t0 + wg) / nbt, bt = (t0 + wg) % nbt;
+  int64_t hh = (t0 + (CPL ? 0 : wg)) / nbt, bt = (t0 + (CPL ? 0 : wg)) % nbt;
   bool loaded = false;  // the tile's operand was stored by the previous tile's epilogue 4
   bool ys_pending = false;  // (wtid 0) a TMA store of y from sYS is in flight
-  for (int64_t t = t0 + wg; t < t1; t += kWG, bt += kWG) {
+  for (int64_t t = t0 + (CPL ? 0 : wg); t < t1; t += TSTEP, bt += TSTEP) {
     while (bt >= nbt) { bt -= nbt; ++hh; }
     stage_no = 0;
     stamp(0);
@@ -691,6 +752,11 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
     // this warpgroup's u|w slot has been read by all of it: stage its next tile
     if constexpr (F::SLOT_WG) {
       if (STG_IN && t + kWG < t1 && filler()) fill(0, t + kWG, (t + kWG) / nbt, (t + kWG) % nbt);
+    } else if constexpr (CPL) {  // both warpgroups read the slot: the second one past stage A refills it
+      if (STG_IN && t + 1 < t1 && filler()) {
+        __threadfence_block();
+        if (atomicAdd(&bb.uw_cnt, 1u) & 1u) fill(0, t + 1, bt + 1 < nbt ? hh : hh + 1, bt + 1 < nbt ? bt + 1 : 0);
+      }
     } else {  // the shared slot goes to tile t + 1 (the other warpgroup's)
       if (STG_IN && t + 1 < t1 && filler()) fill(0, t + 1, bt + 1 < nbt ? hh : hh + 1, bt + 1 < nbt ? bt + 1 : 0);
     }
@@ -792,10 +858,153 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         for (int s = 0; s < 2 * L1 / 16; ++s)
           mma_f16_ss(tmem + gi * NBF, dadd(dXB, gi * 2048 + 2 * s * C::LBO_B), dadd(dGB, 256 * s), idesc, s > 0);
       }
-    }, true);
+    }, true, false, CPL ? &bb.bdone[wg] : nullptr);
 
     // ---------------- epilogue 2: pointwise * k_f -> stage B^-1 operand (own row: TMEM, else K-major smem)
-    if constexpr (DIT && FC_O3_FRAG) {
+    if constexpr (CPL) {
+      // Coupled tiles (L0 = 8): X[f' + 2048 k0] = sum_n0 W_8^{n0 k0}
+      // W_256^{n0 k1} Y_n0[f'], n0 = slot + 2 xb + 4 g: the thread reads its
+      // (k2, k1 pair) fragment (rows r, r + 8 = xb) from both column blocks
+      // (slot) of BOTH warpgroups' TMEM (g) and writes the B^-1 operand of
+      // both; warpgroup wg handles k1 chunks 2 wg, 2 wg + 1.  The other
+      // warpgroup's stage B is awaited on its once-per-tile barrier (its
+      // per-stage barriers may be a stage behind or ahead: parity aliases).
+      static_assert(TS && !FC_NEG_B && L1 == 32, "coupled epilogue 2");
+      const int fr = lane >> 2, fq = lane & 3;
+      const int k2 = fr + 8 * quad + 32 * slice;
+      const uint32_t tl0 = tq - uint32_t(wg * C::TMEM_COLS) + (uint32_t(16 * slice) << 16);
+      const uint8_t* kfh = gkf + h * int64_t(L0I) * C::KF_BYTES;
+      // k_f of the first k1 chunk from L2 before the waits; the second
+      // chunk's loads are issued once the first's have been used
+      float4 kf[8];
+      auto load_kf8 = [&](int k1c) {
+#pragma unroll
+        for (int k0 = 0; k0 < 8; ++k0)
+          kf[k0] = __ldg(reinterpret_cast<const float4*>(kfh + k0 * C::KF_BYTES + dit_kf_off(k2, 4 * k1c + fq)));
+      };
+      load_kf8(2 * wg);
+      mbar_wait_warp(&bb.bdone[wg ^ 1], uint32_t(t - t0) & 1u);
+      wait_half(0);
+      wait_half(1);
+      constexpr float R2 = 0.70710678118654752f;
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        const int k1c = 2 * wg + c;
+        float yv[2][2][2][4];  // [g][slot][re|im]: {(xb 0, k1), (xb 0, k1 + 1), (xb 1, k1), (xb 1, k1 + 1)}
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int slot = 0; slot < 2; ++slot) {
+            const uint32_t col = g * C::TMEM_COLS + slot * NBF + 8 * k1c;
+            tmem_ld_16x256b(tl0 + col, yv[g][slot][0]);
+            tmem_ld_16x256b(tl0 + col + L1, yv[g][slot][1]);
+          }
+        // W_256^{n0 k1}, k1 = 8 k1c + 2 fq + e, as f32x2 pairs over e: n0 = 1
+        // from MUFU, the others as products W^{i1 k1} W^{i2 k1}, i1 + i2 = n0
+        float2 wr[8], wi[8];
+        {
+          const float2 a = wroot<256>(8 * k1c + 2 * fq), b = wroot<256>(8 * k1c + 2 * fq + 1);
+          wr[1] = make_float2(a.x, b.x);
+          wi[1] = make_float2(a.y, b.y);
+#pragma unroll
+          for (int n0 = 2; n0 < 8; ++n0) {
+            const int i1 = n0 / 2, i2 = n0 - n0 / 2;
+            wr[n0] = fma2(wr[i1], wr[i2], mul2(wi[i1], make_float2(-wi[i2].x, -wi[i2].y)));
+            wi[n0] = fma2(wr[i1], wi[i2], mul2(wi[i1], wr[i2]));
+          }
+        }
+        tmem_ld_wait();
+        float2 xr[8], xi[8];
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int xb = 0; xb < 2; ++xb)
+#pragma unroll
+            for (int slot = 0; slot < 2; ++slot) {
+              const int n0 = slot + 2 * xb + 4 * g;
+              const float2 yr = make_float2(yv[g][slot][0][2 * xb], yv[g][slot][0][2 * xb + 1]);
+              const float2 yi = make_float2(yv[g][slot][1][2 * xb], yv[g][slot][1][2 * xb + 1]);
+              if (n0 == 0) {
+                xr[0] = yr; xi[0] = yi;
+              } else {  // T = W Y
+                xr[n0] = fma2(yr, wr[n0], mul2(yi, make_float2(-wi[n0].x, -wi[n0].y)));
+                xi[n0] = fma2(yr, wi[n0], mul2(yi, wr[n0]));
+              }
+            }
+        // DFT_8 (W_8 = e^{-i pi / 4}): radix-2 over n0's high bit, DFT_4 of
+        // the even / odd n0, X[k] = E[k] + W_8^k O[k], X[k + 4] = E[k] - W_8^k O[k]
+        auto dft4 = [](float2* r, float2* i, int a0, int a1, int a2, int a3, bool inv, float2* orr, float2* oi) {
+          const float2 Ar = add2(r[a0], r[a2]), Ai = add2(i[a0], i[a2]);
+          const float2 Br = sub2(r[a0], r[a2]), Bi = sub2(i[a0], i[a2]);
+          const float2 Cr = add2(r[a1], r[a3]), Ci = add2(i[a1], i[a3]);
+          const float2 Dr = sub2(r[a1], r[a3]), Di = sub2(i[a1], i[a3]);
+          orr[0] = add2(Ar, Cr); oi[0] = add2(Ai, Ci);
+          orr[2] = sub2(Ar, Cr); oi[2] = sub2(Ai, Ci);
+          if (!inv) {  // B -+ i D
+            orr[1] = add2(Br, Di); oi[1] = sub2(Bi, Dr);
+            orr[3] = sub2(Br, Di); oi[3] = add2(Bi, Dr);
+          } else {     // B +- i D
+            orr[1] = sub2(Br, Di); oi[1] = add2(Bi, Dr);
+            orr[3] = add2(Br, Di); oi[3] = sub2(Bi, Dr);
+          }
+        };
+        auto dft8 = [&](float2* r, float2* i, bool inv) {
+          float2 er[4], ei[4], odr[4], odi[4];
+          dft4(r, i, 0, 2, 4, 6, inv, er, ei);
+          dft4(r, i, 1, 3, 5, 7, inv, odr, odi);
+          // odd * W_8^{+-k}: k = 1: (1 -+ i) R2, k = 2: -+ i, k = 3: (-1 -+ i) R2
+          const float s = inv ? 1.f : -1.f;
+          {
+            const float2 a = odr[1], b = odi[1];  // (a + i b)(1 + i s) R2
+            odr[1] = make_float2(R2 * (a.x - s * b.x), R2 * (a.y - s * b.y));
+            odi[1] = make_float2(R2 * (b.x + s * a.x), R2 * (b.y + s * a.y));
+          }
+          {
+            const float2 a = odr[2], b = odi[2];  // (a + i b)(i s)
+            odr[2] = make_float2(-s * b.x, -s * b.y);
+            odi[2] = make_float2(s * a.x, s * a.y);
+          }
+          {
+            const float2 a = odr[3], b = odi[3];  // (a + i b)(-1 + i s) R2
+            odr[3] = make_float2(R2 * (-a.x - s * b.x), R2 * (-a.y - s * b.y));
+            odi[3] = make_float2(R2 * (-b.x + s * a.x), R2 * (-b.y + s * a.y));
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            r[k] = add2(er[k], odr[k]); i[k] = add2(ei[k], odi[k]);
+            r[k + 4] = sub2(er[k], odr[k]); i[k + 4] = sub2(ei[k], odi[k]);
+          }
+        };
+        dft8(xr, xi, false);
+#pragma unroll
+        for (int k0 = 0; k0 < 8; ++k0) {  // * k_f[f' + 2048 k0] / 8: kf = {kr_e0, kr_e1, ki_e0, ki_e1}
+          const float4 qv = kf[k0];
+          const float2 kr = make_float2(0.125f * qv.x, 0.125f * qv.y), ki = make_float2(0.125f * qv.z, 0.125f * qv.w);
+          const float2 zr = fma2(xr[k0], kr, mul2(xi[k0], make_float2(-ki.x, -ki.y)));
+          const float2 zi = fma2(xr[k0], ki, mul2(xi[k0], kr));
+          xr[k0] = zr; xi[k0] = zi;
+        }
+        if (c == 0) load_kf8(2 * wg + 1);  // the next chunk's k_f (L2 latency under the rest of this one)
+        dft8(xr, xi, true);
+#pragma unroll
+        for (int n0 = 1; n0 < 8; ++n0) {  // conj twiddle
+          const float2 o_r = fma2(xr[n0], wr[n0], mul2(xi[n0], wi[n0]));
+          const float2 o_i = fma2(xi[n0], wr[n0], mul2(xr[n0], make_float2(-wi[n0].x, -wi[n0].y)));
+          xr[n0] = o_r; xi[n0] = o_i;
+        }
+        // B^-1 operands of both warpgroups: rows r (xb 0) and r + 8 (xb 1), column kp
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int slot = 0; slot < 2; ++slot) {
+            const int na = slot + 4 * g, nb2 = na + 2;
+            const uint32_t ca = tl0 + g * C::TMEM_COLS + C::CA + slot * L1 + 4 * k1c;
+            tmem_st_16x128b(ca, pack_half2(xr[na].x, xr[na].y), pack_half2(xr[nb2].x, xr[nb2].y));
+            tmem_st_16x128b(ca + L1 / 2, pack_half2(xi[na].x, xi[na].y), pack_half2(xi[nb2].x, xi[nb2].y));
+          }
+      }
+      tmem_st_wait();
+    } else if constexpr (DIT && FC_O3_FRAG) {
       // Order 3 with no lane shuffles: a 16x256b TMEM fragment gives a
       // thread rows r and r + 8 of its 16-lane block (lane bit 3 = xb: n0's
       // high bit for L0 = 4, the row pair q for L0 = 2) at one (k2, k1 pair),
@@ -1210,7 +1419,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
                        s > 0);
         }
       }
-    }, true);
+    }, true, CPL);
     // order 3: the whole warpgroup is past epilogue 2 of tile t (the barrier
     // above): signal it, and when the next tile starts a new head, refill
     // the shared k_f buffer once the other warpgroup's tile t - 1 (the last
@@ -1239,7 +1448,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         const int p = rowB_p(gi), k2 = rowB_k2(gi);
         float4 w[4];
         {
-          const float2 a = tw_at((p % L0I) + L0I * 8 * n1c, k2);
+          const float2 a = tw_at(n0_of_p(p) + L0I * 8 * n1c, k2);
           const float br = a.x, bi = a.y;
           const float4 c = tw3_c[gi & 1];  // {Re W^{k2}, Im W^{k2}, Re W^{2k2}, Im W^{2k2}}
           w[0] = make_float4(br, br * c.x - bi * c.y, bi, br * c.y + bi * c.x);
@@ -1281,7 +1490,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         // by W^{2 k2}
         float4 w[4];
         {
-          const float2 a = tw_at((p % L0I) + L0I * 8 * n1c, k2);
+          const float2 a = tw_at(n0_of_p(p) + L0I * 8 * n1c, k2);
           const float br = a.x, bi = a.y;
           const float4 c = tw3_c[gi & 1];  // {Re W^{k2}, Im W^{k2}, Re W^{2k2}, Im W^{2k2}}
           w[0] = make_float4(br, br * c.x - bi * c.y, bi, br * c.y + bi * c.x);
@@ -1340,7 +1549,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
       using S = typename std::conditional<GATED, __half, T>::type;
       constexpr int OCH = RR * NROW / 8 / kWGThreads;  // coalesced output chunks per thread
       static_assert(!STAGE || RR * NROW * sizeof(S) <= C::BUFX_BYTES, "y staging fits in bufX");
-      static_assert(!STG || (RR * NROW * sizeof(S) <= C::BUFX_BYTES / 2 && RR * F::ROW_BYTES <= C::BUFX_BYTES / 2 &&
+      static_assert(!STG || CPL || (RR * NROW * sizeof(S) <= C::BUFX_BYTES / 2 && RR * F::ROW_BYTES <= C::BUFX_BYTES / 2 &&
                              128 * 2 * C::KA * 2 <= C::BUFX_BYTES / 2),
                     "causal: staged conv output, next stage-A operand and y rows share bufX by halves");
       constexpr int PER = OUT_COLS / 8;  // transposed 8-column items per thread
@@ -1388,7 +1597,8 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         // there, 14 % slower; their v / y maps stay natural-order, api.cu)
         constexpr bool Y_DIRECT = STG && !(GATED && L0I == 4);
         const bool direct = Y_DIRECT && prm.tma_io;
-        const uint32_t sstg = tma_out ? sYS : direct ? sY : bufX;
+        // (coupled tiles: y is staged -- gated: gated in place -- in the v slot)
+        const uint32_t sstg = tma_out ? sYS : CPL ? sV : direct ? sY : bufX;
         if (tma_out && t > t0) mbar_wait(&ys_bar, uint32_t((t - t0 - 1) & 1));
         // all of this thread's TMEM loads in flight before one wait (PER <= 8)
         float ob[PER][8];
@@ -1419,7 +1629,40 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
           }
           st_shared_v4(sstg + swz128(off), st.x, st.y, st.z, st.w);
         };
-        if constexpr (DIT) {
+        // 8 bytes (4 samples) of y at byte offset off: gate, store (coupled tiles)
+        auto put8 = [&](uint32_t off, uint32_t w0, uint32_t w1) {
+          const uint32_t a = sstg + swz128(off);
+          if constexpr (!GATED) {
+            st_shared_v2(a, w0, w1);
+          } else {
+            uint2 st = make_uint2(w0, w1);
+            const uint2 vq = ld_shared_u2(sV + swz128(off));
+            if constexpr (std::is_same<T, __half>::value) {
+              __half2* a2 = reinterpret_cast<__half2*>(&st);
+              const __half2* v2 = reinterpret_cast<const __half2*>(&vq);
+              a2[0] = __hmul2(a2[0], v2[0]);
+              a2[1] = __hmul2(a2[1], v2[1]);
+            } else {
+              const __half2* a2 = reinterpret_cast<const __half2*>(&st);
+              const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vq);
+              const float2 a0 = __half22float2(a2[0]), a1 = __half22float2(a2[1]);
+              const float2 v0 = __bfloat1622float2(v2[0]), v1 = __bfloat1622float2(v2[1]);
+              st = make_uint2(IO<T>::pack2(a0.x * v0.x, a0.y * v0.y), IO<T>::pack2(a1.x * v1.x, a1.y * v1.y));
+            }
+            st_shared_v2(a, st.x, st.y);
+          }
+        };
+        if constexpr (CPL) {
+          // coupled tiles: inner rows n0 = 4 wg + p (items p) at n1 = 8 n1c + e:
+          // samples 4 wg + p + 8 (n1 + 32 n2) of real row c' -- 4 consecutive
+          // samples per e, the other warpgroup's 4 beside them
+          const int n1c = 2 * o_hh + slice;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int n = 4 * wg + 8 * (8 * n1c + e + 32 * o_n2);
+            put8(uint32_t(o_cp * NROW + n) * sizeof(S), IO<S>::pack2(ob[0][e], ob[1][e]), IO<S>::pack2(ob[2][e], ob[3][e]));
+          }
+        } else if constexpr (DIT) {
           // items i = inner rows p = q L0I + n0 at 8 n1 of column group n1c:
           // samples n0 + L0I (n1 + 32 n2) of real row 2q + c', interleaved
           const int n1c = 2 * o_hh + slice;
@@ -1452,10 +1695,12 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         stamp(16);
         if (STG && direct) {
           fence_async_smem();  // y -> the tensor store (async proxy)
-          wg_sync();           // all of y written, all of v read
-          if (filler()) {
-            tma_store_4d(&prm.tmap_yo, sY, 0, 0, int(h), int(bt * RR));  // rows past B are clipped
+          if (CPL) named_sync(3, kThreads);  // both warpgroups' samples written
+          else wg_sync();      // all of y written, all of v read
+          if ((!CPL || wg == 0) && filler()) {
+            tma_store_4d(&prm.tmap_yo, CPL ? sV : sY, 0, 0, int(h), int(bt * RR));  // rows past B are clipped
             bulk_commit();
+            if (CPL) bulk_wait_read0();  // the v slot (y staging) is refilled next
             // v has been read: the output slot goes to tile t + 1 at once
             if (t + 1 < t1) release_out(t + 1, bt + 1 < nbt ? hh : hh + 1, bt + 1 < nbt ? bt + 1 : 0);
           }
@@ -1578,9 +1823,11 @@ static cudaError_t launch_o2(const FwdParams& prm, cudaStream_t stream) {
 
 template <bool CAUSAL, bool GATED, typename T>
 static cudaError_t dispatch_l1(const FwdParams& prm, cudaStream_t s) {
-  if constexpr (CAUSAL) {  // single-pass order 3 (fft_size 4096 / 8192)
+  if constexpr (CAUSAL) {  // single-pass order 3 (fft_size 4096 / 8192 / 16384)
     if (prm.L0I == 2) return prm.L1 == 32 ? launch_o2<32, true, GATED, T, 2>(prm, s) : cudaErrorInvalidValue;
     if (prm.L0I == 4) return prm.L1 == 32 ? launch_o2<32, true, GATED, T, 4>(prm, s) : cudaErrorInvalidValue;
+    if (prm.L0I == 8)  // coupled warpgroups: tensor-map I/O only
+      return prm.L1 == 32 && prm.tma_io ? launch_o2<32, true, GATED, T, 8>(prm, s) : cudaErrorInvalidValue;
   }
   if (prm.L0I > 1) return cudaErrorInvalidValue;
   if (prm.kcn > 0)  // frequency-sparse slow-digit skip (kept k1 chunks only)

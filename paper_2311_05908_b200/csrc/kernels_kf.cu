@@ -519,6 +519,48 @@ __global__ void kf_dit_to_dif_kernel(const uint8_t* __restrict__ src, uint8_t* _
       make_float4(v[0], v[1], v[2], v[3]);
 }
 
+// Order-3 plans with L0 = 8 (fft_size 16384) build k_f with the multipass
+// precompute (block k0 = K_f[k0 + L0 f'], [k2][k1/2] table layout) and
+// re-lay it out in place, one CTA per head (all L0 blocks in shared memory),
+// into the order-3 blocks (block b = K_f[f' + 2048 b], dit_kf_off); each
+// thread writes one destination float4 {re, re', im, im'} (consecutive
+// threads: consecutive 16 B).
+__global__ void __launch_bounds__(512) kf_dif_to_dit_kernel(uint8_t* __restrict__ kf, int L0) {
+  extern __shared__ __align__(16) uint8_t smk[];
+  constexpr int CPR = 16;
+  const uint32_t hb = 64 * tab_stride(CPR);
+  uint8_t* head = kf + int64_t(blockIdx.x) * L0 * hb;
+  const uint32_t sbase = smem_u32(smk);
+  for (uint32_t o = threadIdx.x * 16; o < uint32_t(L0) * hb; o += blockDim.x * 16) cp_async16(sbase + o, head + o, true);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < L0 * 1024; idx += blockDim.x) {
+    const int b = idx >> 10, d = idx & 1023;
+    const int kp = (d >> 8) * 4 + (d & 3), k2 = (d >> 2) & 63;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int f = k2 + 64 * (2 * kp + e) + 2048 * b;
+      const int k0 = f % L0, fp = f / L0;
+      const int k2d = fp % 64, k1d = fp / 64;
+      const float4 q = *reinterpret_cast<const float4*>(smk + k0 * hb + tab_off_rt(CPR, uint32_t(k2d), uint32_t(k1d / 2)));
+      v[e] = (k1d & 1) ? q.y : q.x;
+      v[2 + e] = (k1d & 1) ? q.w : q.z;
+    }
+    *reinterpret_cast<float4*>(head + b * hb + dit_kf_off(uint32_t(k2), uint32_t(kp))) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+cudaError_t launch_kf_dif_to_dit(void* kf, int64_t H, int L0, cudaStream_t s) {
+  if (H <= 0) return cudaSuccess;
+  const size_t smem = size_t(L0) * 64 * tab_stride(16);
+  static int attr[64] = {0};
+  if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kf_dif_to_dit_kernel), int(smem), attr)) return e;
+  kf_dif_to_dit_kernel<<<unsigned(H), 512, smem, s>>>(static_cast<uint8_t*>(kf), L0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_kf_dit_to_dif(const void* src, void* dst, int64_t H, int L0, cudaStream_t s) {
   const int64_t n = H * int64_t(L0) * 64 * 16;
   if (n == 0) return cudaSuccess;

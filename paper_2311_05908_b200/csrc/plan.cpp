@@ -459,13 +459,14 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
     p->KA = 64;  // the inner transform is circular over complex rows
     p->P = 4;
     build_fused_tables(p, p->Lp);
-    // single-pass order 3 for causal fft_size 4096 / 8192 (N = 2K, 4K): the
+    // single-pass order 3 for causal fft_size 4096 / 8192 / 16384 (N = 2K, 4K,
+    // 8K; 8K: the two warpgroups share each row pair, kernels_fwd.cu): the
     // whole row pair stays on chip (decimated inner rows z[n0 + L0 n'] are
     // the tile's complex rows, the outer DFT_L0 runs in the fused kernel's
     // pointwise step).  Not for partial, sparse (row skipping stays with the
     // multipass passes) or fp32 validation plans; FFTCONV_DIT=0 disables it.
     const char* dit_env = getenv("FFTCONV_DIT");
-    if (p->regime == REGIME_MULTIPASS && causal && fft_size == 2 * N && (L == 4096 || L == 8192) &&
+    if (p->regime == REGIME_MULTIPASS && causal && fft_size == 2 * N && (L == 4096 || L == 8192 || L == 16384) &&
         dtype != FFTCONV_F32 && !sparsity && !(dit_env && dit_env[0] == '0')) {
       fftconv_plan_s t;
       t.L = 2048;

@@ -13,6 +13,7 @@
 //              LBO = byte distance between 8-row K groups.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
 
@@ -41,6 +42,19 @@ FC_DEVICE void fence_barrier_init() {
 }
 FC_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
+#ifdef FC_HANG_DEBUG  // experiment: report and trap a wait that never completes
+  {
+    uint32_t done = 0;
+    for (long long it = 0; it < (1ll << 22) && !done; ++it)
+      asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.b32 %0, 1, 0, P1;\n}"
+                   : "=r"(done) : "r"(addr), "r"(parity) : "memory");
+    if (!done) {
+      printf("HANG block %d thread %d bar smem+%u parity %u\n", blockIdx.x, threadIdx.x, addr, parity);
+      __trap();
+    }
+    return;
+  }
+#endif
   // suspend-time hint: the waiting thread sleeps until the phase completes
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -265,6 +279,14 @@ FC_DEVICE float2 ld_shared_f2(uint32_t addr) {
   float2 v;
   asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
   return v;
+}
+FC_DEVICE uint2 ld_shared_u2(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+FC_DEVICE void st_shared_v2(uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
 FC_DEVICE uint4 ld_shared_u4(uint32_t addr) {
   uint4 v;

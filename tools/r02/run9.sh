@@ -1,0 +1,6 @@
+timeout 200 python -u tools/r02/cpl_check.py 8192 2>&1 | grep rel
+timeout 900 python -m pytest tests/test_gpu_fwd.py -q -x -k "order3 or multipass or cfg3" 2>&1 | tail -3
+for w in sweep8192 gsweep8192; do
+echo -n "$w "; timeout 300 python bench.py --workload $w --steps 100 --no-cpu-baseline --e2e-steps 2 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('step_ms %.4f conv_ms %.4f frac %.3f' % (d['ms_per_step'], d['roofline']['kernel_ms'], d['roofline']['frac']))"
+done
+bash tools/trace_fwd.sh 8192 causal-plain 2>&1 | tail -20
