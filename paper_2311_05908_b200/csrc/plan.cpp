@@ -21,19 +21,19 @@
 #include "layout.h"
 
 // B200 tier cost model coefficients (seconds per feature unit), fitted by
-// tools/cost_model.py on the bench sweep (profiles/r02b/cost_model.md).
-#define COST_B200_0 9.260535e-09
-#define COST_B200_1 6.101121e-09
-#define COST_B200_2 1.626946e-08
-#define COST_B200_3 2.661771e-08
-#define COST_B200_4 3.456787e-12
-#define COST_B200_5 1.048704e-11
-#define COST_B200_6 1.231446e-05
+// tools/cost_model.py on the bench sweep (profiles/r02c/cost_model.md).
+#define COST_B200_0 1.178744e-08
+#define COST_B200_1 1.097990e-08
+#define COST_B200_2 1.577693e-08
+#define COST_B200_3 1.918414e-08
+#define COST_B200_4 3.198669e-12
+#define COST_B200_5 1.063888e-11
+#define COST_B200_6 1.153109e-05
 #define COST_B200_7 0.000000e+00
-#define COST_B200_8 5.072926e-12
-#define COST_B200_9 3.132192e-11
+#define COST_B200_8 5.093123e-12
+#define COST_B200_9 5.162027e-11
 #define COST_B200_10 0.000000e+00
-#define COST_B200_11 1.170779e-13
+#define COST_B200_11 6.556603e-14
 
 namespace fc {
 
@@ -464,7 +464,8 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
     // whole row pair stays on chip (decimated inner rows z[n0 + L0 n'] are
     // the tile's complex rows, the outer DFT_L0 runs in the fused kernel's
     // pointwise step).  Not for partial, sparse (row skipping stays with the
-    // multipass passes) or fp32 validation plans; FFTCONV_DIT=0 disables it.
+    // multipass passes) or fp32 validation plans; FFTCONV_DIT=0 disables it,
+    // FFTCONV_DIT=1 takes it wherever it applies (cost-model measurements).
     const char* dit_env = getenv("FFTCONV_DIT");
     if (p->regime == REGIME_MULTIPASS && causal && fft_size == 2 * N && (L == 4096 || L == 8192 || L == 16384) &&
         dtype != FFTCONV_F32 && !sparsity && !(dit_env && dit_env[0] == '0')) {
@@ -481,7 +482,7 @@ extern "C" fftconv_status_t fftconv_plan(fftconv_plan_t* out, int64_t N, int64_t
       const double t_mp = predict_seconds(p, 64, 768, false, false, nullptr);
       p->dit = int32_t(L / 2048);
       const double t_dit = predict_seconds(p, 64, 768, false, false, nullptr);
-      if (t_dit < t_mp) {
+      if (t_dit < t_mp || (dit_env && dit_env[0] == '1')) {  // (FFTCONV_DIT=1: always, for measurements)
         build_fused_tables(&t, 2048);
         p->dit_tab_off = align_up(p->image.size(), 1024);
         p->image.resize(p->dit_tab_off, 0);
@@ -611,7 +612,7 @@ extern "C" int32_t fftconv_select_order(int64_t N, double mu, double sigma_h, do
 // k_f precompute elements, launches, and the backward's tiles, T-chain
 // elements and dk elements.  t = sum_i coef[i] * feat[i]; the default
 // coefficients are a least-squares fit to the bench sweep on one B200
-// (tools/cost_model.py, profiles/r02b/cost_model.md).
+// (tools/cost_model.py, profiles/r02c/cost_model.md).
 static double cdiv(double a, double b) { return std::ceil(a / b); }
 
 static void cost_features(const fftconv_plan_s* p, int64_t B, int64_t H, bool bwd, bool gated, double* f) {
@@ -621,7 +622,10 @@ static void cost_features(const fftconv_plan_s* p, int64_t B, int64_t H, bool bw
   const double Bv = p->regime == REGIME_PARTIAL ? double(B) * double(p->N / (p->L / 2)) : double(B);
   const double pairs = std::ceil(Bv / 2.0);
   f[5] = Hd * L;  // k_f precompute
-  if (p->dit > 1) {
+  if (p->dit == 8) {  // coupled row-pair tiles: ~3 L0 = 4 tiles each (16.2k vs 5.4k cycles per pair, traced)
+    f[3] = 3.0 * Hd * cdiv(double(B), 2.0);
+    f[6] = 4;
+  } else if (p->dit > 1) {
     f[p->dit == 2 ? 2 : 3] = Hd * cdiv(double(B), 8.0 / p->dit);
     f[6] = 2;
   } else if (!mp) {
