@@ -1818,7 +1818,7 @@ static cudaError_t launch_o2(const FwdParams& prm, cudaStream_t stream) {
   const int64_t tiles = (prm.row_map ? (prm.H / prm.row_L0) * prm.nrow : prm.H) * nbt;
   int grid = int(tiles < prm.num_sms ? tiles : prm.num_sms);
   if (grid < 1) return cudaSuccess;
-  return launch_pdl(kern, dim3(grid), dim3(F::THREADS), F::SMEM, stream, prm);
+  return launch_pdl(PDL_CONV, kern, dim3(grid), dim3(F::THREADS), F::SMEM, stream, prm);
 }
 
 template <bool CAUSAL, bool GATED, typename T>

@@ -183,7 +183,6 @@ __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) 
   const bool has1 = h0 + 1 < prm.H;
   const int L = int(prm.L), K = int(prm.K);
   float2* tws = sm + L + L / 8;
-  griddep_launch();
   {
     load_padded(tws, prm.twiddle, L);  // plan-owned table
   }
@@ -240,6 +239,9 @@ __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) 
     *reinterpret_cast<float4*>(out0 + off) = make_float4(a0.x, a1.x, a0.y, a1.y);
     if (has1) *reinterpret_cast<float4*>(out1 + off) = make_float4(b0.x, b1.x, b0.y, b1.y);
   }
+  // PDL: the convolution may start its prologue once every CTA is here (an
+  // early trigger let its CTAs take SMs the remaining k_f CTAs needed)
+  griddep_launch();
 }
 
 // Multipass regime, k_f step 2: one CTA per (head, k0) transforms the L'
@@ -439,7 +441,6 @@ __global__ void __launch_bounds__(256) precompute_kf_dit_kernel(const KfParams p
     sincospif(-2.0f * float(e) / float(LF), &sn, &cs);
     tws[pd(e)] = make_float2(cs, sn);
   }
-  griddep_launch();
   griddep_wait();  // PDL: k is read and k_f written only after the previous kernel
   const float* k0row = prm.k + h0 * K;
   const float* k1row = k0row + K;
@@ -469,6 +470,7 @@ __global__ void __launch_bounds__(256) precompute_kf_dit_kernel(const KfParams p
     *reinterpret_cast<float4*>(out0 + off) = make_float4(a0.x, a1.x, a0.y, a1.y);
     if (has1) *reinterpret_cast<float4*>(out1 + off) = make_float4(b0.x, b1.x, b0.y, b1.y);
   }
+  griddep_launch();
 }
 
 cudaError_t launch_precompute_kf_dit(const KfParams& prm, int L0, cudaStream_t s) {
@@ -479,13 +481,13 @@ cudaError_t launch_precompute_kf_dit(const KfParams& prm, int L0, cudaStream_t s
     static int attr[64] = {0};
     if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_dit_kernel<4096>), int(smem), attr))
       return e;
-    return launch_pdl(precompute_kf_dit_kernel<4096>, dim3(grid), dim3(256), smem, s, prm);
+    return launch_pdl(PDL_KF, precompute_kf_dit_kernel<4096>, dim3(grid), dim3(256), smem, s, prm);
   } else if (L0 == 4) {
     const size_t smem = size_t(2 * (8192 + 1024)) * sizeof(float2);
     static int attr[64] = {0};
     if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_dit_kernel<8192>), int(smem), attr))
       return e;
-    return launch_pdl(precompute_kf_dit_kernel<8192>, dim3(grid), dim3(256), smem, s, prm);
+    return launch_pdl(PDL_KF, precompute_kf_dit_kernel<8192>, dim3(grid), dim3(256), smem, s, prm);
   } else {
     return cudaErrorInvalidValue;
   }
@@ -574,7 +576,7 @@ cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s) {
   const size_t smem = fft_smem_bytes(prm.L);
   static int attr[64] = {0};
   if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_kernel), int(smem), attr)) return e;
-  return launch_pdl(precompute_kf_kernel, dim3(unsigned((prm.H + 1) / 2)), dim3(256), smem, s, prm);
+  return launch_pdl(PDL_KF, precompute_kf_kernel, dim3(unsigned((prm.H + 1) / 2)), dim3(256), smem, s, prm);
 }
 
 }  // namespace fc

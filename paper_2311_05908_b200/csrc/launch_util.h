@@ -21,20 +21,26 @@ inline cudaError_t set_smem_attr(const void* kern, int bytes, int* cache /* [64]
 
 // Programmatic dependent launch: kernels that call griddep_wait() before
 // their first read of data an earlier kernel produced (and griddep_launch()
-// once that wait has returned) are launched with the programmatic stream
+// once that wait has returned) may be launched with the programmatic stream
 // serialization attribute, so their prologue (launch, shared-memory tables,
 // barriers, TMEM allocation) overlaps the tail of the previous kernel in the
-// stream.  FFTCONV_PDL=0 launches them normally (A/B switch).
-inline bool pdl_enabled() {
-  static const bool on = [] {
+// stream.  FFTCONV_PDL selects which launches use it (A/B switch):
+// 0 none (default), 1 both, 2 the convolution only, 3 the k_f precompute
+// only.  Measured on B200 (tools/pdl_probe.py, profiles/r02c/pdl_probe.txt):
+// back-to-back convolutions gain 3 % (117.0 -> 113.2 us, cfg2 shape), but
+// the k_f precompute -> convolution chain of a step loses 3-7 us at N = 1024
+// with any of 1-3, so it is off.
+enum PdlKernel { PDL_KF = 0, PDL_CONV = 1 };
+inline bool pdl_enabled(PdlKernel k) {
+  static const int mode = [] {
     const char* e = std::getenv("FFTCONV_PDL");
-    return !(e && e[0] == '0');
+    return e ? std::atoi(e) : 0;
   }();
-  return on;
+  return mode == 1 || (mode == 2 && k == PDL_CONV) || (mode == 3 && k == PDL_KF);
 }
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                              Args&&... args) {
+inline cudaError_t launch_pdl(PdlKernel which, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -44,7 +50,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = pdl_enabled(which) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
