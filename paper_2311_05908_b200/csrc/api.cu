@@ -125,6 +125,23 @@ cudaError_t make_tmap_rows(CUtensorMap* map, void* base, int64_t rows, int64_t h
                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
+// Coupled order-3 tiles (L0 = 8): one row's first N samples n = n0 + 8 (n1 +
+// 32 n2) as a box ordered (n0, n2, n1) -- SMEM offset (n1 * N/256 + n2) * 16
+// + 2 n0 -- so the epilogue-4 threads, which hold consecutive n2, write
+// consecutive 16 B units; one box per row (rows = b * H + h; rows past B*H
+// are zero-filled on load and clipped on store).
+cudaError_t make_tmap_cpl(CUtensorMap* map, const void* base, int64_t B, int64_t H, int64_t N) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return cudaErrorNotSupported;
+  const cuuint64_t dim[4] = {8, cuuint64_t(N / 256), 32, cuuint64_t(B * H)};
+  const cuuint64_t stride[3] = {512, 16, cuuint64_t(N) * 2};
+  const cuuint32_t box[4] = {8, cuuint32_t(N / 256), 32, 1};
+  const cuuint32_t estride[4] = {1, 1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, const_cast<void*>(base), dim, stride, box, estride,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
 cudaError_t make_tmap_sig(CUtensorMap* map, const void* base, int64_t B, int64_t H, int64_t N, int R) {
   EncodeTiledFn enc = encode_tiled();
   if (!enc || N % 256 != 0) return cudaErrorNotSupported;
@@ -240,13 +257,15 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     const bool swz_in = p->dit == 8;
     bool ok = (swz_in ? make_tmap_rows(&prm.tmap_u, const_cast<void*>(u), B, H, p->N, R)
                       : make_tmap_sig(&prm.tmap_u, u, B, H, p->N, R)) == cudaSuccess &&
-              (natural ? make_tmap_sig(&prm.tmap_yo, y, B, H, p->N, R)
-                       : make_tmap_rows(&prm.tmap_yo, y, B, H, p->N, R)) == cudaSuccess;
+              (swz_in  ? make_tmap_cpl(&prm.tmap_yo, y, B, H, p->N)
+               : natural ? make_tmap_sig(&prm.tmap_yo, y, B, H, p->N, R)
+                         : make_tmap_rows(&prm.tmap_yo, y, B, H, p->N, R)) == cudaSuccess;
     if (ok && gated)
       ok = (swz_in ? make_tmap_rows(&prm.tmap_w, const_cast<void*>(w), B, H, p->N, R)
                    : make_tmap_sig(&prm.tmap_w, w, B, H, p->N, R)) == cudaSuccess &&
-           (natural ? make_tmap_sig(&prm.tmap_v, v, B, H, p->N, R)
-                    : make_tmap_rows(&prm.tmap_v, const_cast<void*>(v), B, H, p->N, R)) == cudaSuccess;
+           (swz_in  ? make_tmap_cpl(&prm.tmap_v, v, B, H, p->N)
+            : natural ? make_tmap_sig(&prm.tmap_v, v, B, H, p->N, R)
+                      : make_tmap_rows(&prm.tmap_v, const_cast<void*>(v), B, H, p->N, R)) == cudaSuccess;
     prm.tma_io = ok ? 1 : 0;
     cudaError_t e = launch_fwd_fused(prm, st);
     if (e != cudaSuccess) return cuda_fail(fn, e);

@@ -352,6 +352,9 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
       if (kind == 0) {
         tma_load_4d(sUW, &prm.tmap_u, 0, 0, hc, b0, bar);
         if (GATED) tma_load_4d(sUW + RR * F::ROW_BYTES, &prm.tmap_w, 0, 0, hc, b0, bar);
+      } else if (CPL) {  // (n0, n2, n1)-ordered boxes, one per row (api.cu make_tmap_cpl)
+        tma_load_4d(sV, &prm.tmap_v, 0, 0, 0, int(b0 * H + hc), bar);
+        tma_load_4d(sV + F::ROW_BYTES, &prm.tmap_v, 0, 0, 0, int((b0 + 1) * H + hc), bar);
       } else {
         tma_load_4d(sV, &prm.tmap_v, 0, 0, hc, b0, bar);
       }
@@ -1630,13 +1633,13 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
           st_shared_v4(sstg + swz128(off), st.x, st.y, st.z, st.w);
         };
         // 8 bytes (4 samples) of y at byte offset off: gate, store (coupled tiles)
-        auto put8 = [&](uint32_t off, uint32_t w0, uint32_t w1) {
-          const uint32_t a = sstg + swz128(off);
+        auto put8 = [&](uint32_t off, uint32_t w0, uint32_t w1) {  // (off: final SMEM offset)
+          const uint32_t a = sstg + off;
           if constexpr (!GATED) {
             st_shared_v2(a, w0, w1);
           } else {
             uint2 st = make_uint2(w0, w1);
-            const uint2 vq = ld_shared_u2(sV + swz128(off));
+            const uint2 vq = ld_shared_u2(sV + off);
             if constexpr (std::is_same<T, __half>::value) {
               __half2* a2 = reinterpret_cast<__half2*>(&st);
               const __half2* v2 = reinterpret_cast<const __half2*>(&vq);
@@ -1655,12 +1658,16 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         if constexpr (CPL) {
           // coupled tiles: inner rows n0 = 4 wg + p (items p) at n1 = 8 n1c + e:
           // samples 4 wg + p + 8 (n1 + 32 n2) of real row c' -- 4 consecutive
-          // samples per e, the other warpgroup's 4 beside them
+          // samples per e, the other warpgroup's 4 beside them; the staging
+          // box is ordered (n0, n2, n1) (api.cu make_tmap_cpl), so the lanes'
+          // consecutive n2 are consecutive 16 B units (the natural order put
+          // them 512 B apart: 16-way bank conflicts, 47 M excess wavefronts)
           const int n1c = 2 * o_hh + slice;
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const int n = 4 * wg + 8 * (8 * n1c + e + 32 * o_n2);
-            put8(uint32_t(o_cp * NROW + n) * sizeof(S), IO<S>::pack2(ob[0][e], ob[1][e]), IO<S>::pack2(ob[2][e], ob[3][e]));
+            const uint32_t off = uint32_t(o_cp) * F::ROW_BYTES + uint32_t(8 * n1c + e) * (NROW / 16) +
+                                 uint32_t(o_n2) * 16 + 8 * wg;
+            put8(off, IO<S>::pack2(ob[0][e], ob[1][e]), IO<S>::pack2(ob[2][e], ob[3][e]));
           }
         } else if constexpr (DIT) {
           // items i = inner rows p = q L0I + n0 at 8 n1 of column group n1c:
@@ -1698,7 +1705,12 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
           if (CPL) named_sync(3, kThreads);  // both warpgroups' samples written
           else wg_sync();      // all of y written, all of v read
           if ((!CPL || wg == 0) && filler()) {
-            tma_store_4d(&prm.tmap_yo, CPL ? sV : sY, 0, 0, int(h), int(bt * RR));  // rows past B are clipped
+            if (CPL) {  // one (n0, n2, n1)-ordered box per row
+              tma_store_4d(&prm.tmap_yo, sV, 0, 0, 0, int(bt * RR * H + h));
+              tma_store_4d(&prm.tmap_yo, sV + F::ROW_BYTES, 0, 0, 0, int((bt * RR + 1) * H + h));
+            } else {
+              tma_store_4d(&prm.tmap_yo, sY, 0, 0, int(h), int(bt * RR));  // rows past B are clipped
+            }
             bulk_commit();
             if (CPL) bulk_wait_read0();  // the v slot (y staging) is refilled next
             // v has been read: the output slot goes to tile t + 1 at once
