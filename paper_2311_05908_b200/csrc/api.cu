@@ -187,7 +187,7 @@ static fftconv_status_t run_precompute(fftconv_plan_t p, const float* d_k, const
   prm.L1 = p->L1;
   prm.L2 = p->L2;
   cudaError_t e;
-  if (p->dit > 1 && p->dit < 8) {  // single-pass order 3: L0 blocks of K_f[f' + 2048 k0] per head
+  if (p->dit > 1) {  // single-pass order 3: L0 blocks of K_f[f' + 2048 k0] per head
     e = launch_precompute_kf_dit(prm, p->dit, reinterpret_cast<cudaStream_t>(stream));
     g_launches += H > 0 ? 1 : 0;
   } else if (p->regime == REGIME_MULTIPASS || p->regime == REGIME_PARTIAL) {
@@ -199,10 +199,6 @@ static fftconv_status_t run_precompute(fftconv_plan_t p, const float* d_k, const
     for (int l = 0; l < 4; ++l) prm.lev[l] = p->lev_L0[l];
     e = launch_mp_precompute_kf(prm, p->lev_L0, p->nlev, p->L, block, reinterpret_cast<cudaStream_t>(stream));
     g_launches += H > 0 ? 2 + p->nlev - 1 : 0;
-    if (e == cudaSuccess && p->dit == 8) {  // order 3, L0 = 8: the multipass k_f re-laid out per head
-      e = launch_kf_dif_to_dit(d_kf, H, p->dit, reinterpret_cast<cudaStream_t>(stream));
-      g_launches += H > 0 ? 1 : 0;
-    }
   } else {
     e = launch_precompute_kf(prm, reinterpret_cast<cudaStream_t>(stream));
     g_launches += H > 0 ? 1 : 0;

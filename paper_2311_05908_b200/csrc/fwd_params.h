@@ -102,7 +102,6 @@ cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s);
 cudaError_t launch_precompute_kf_dit(const KfParams& prm, int L0, cudaStream_t s);
 // ... and its multipass (DIF) layout for the backward
 cudaError_t launch_kf_dit_to_dif(const void* src, void* dst, int64_t H, int L0, cudaStream_t s);
-cudaError_t launch_kf_dif_to_dit(void* kf, int64_t H, int L0, cudaStream_t s);
 
 // multipass regime (kernels_mp.cu)
 struct MpParams {

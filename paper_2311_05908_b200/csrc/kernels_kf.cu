@@ -421,7 +421,7 @@ cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Single-pass order-3 plans (fft_size LF = L0 * 2048, L0 in {2, 4}): two
+// Single-pass order-3 plans (fft_size LF = L0 * 2048, L0 in {2, 4}; 8 below): two
 // heads per CTA as above, the LF-point transform in shared memory with
 // twiddles W_LF^e from sincospif of the exact dyadic argument -2e/LF (this
 // precompute is not the hot path), written as L0 blocks per head: block k0
@@ -473,6 +473,102 @@ __global__ void __launch_bounds__(256) precompute_kf_dit_kernel(const KfParams p
   griddep_launch();
 }
 
+// fft_size 16384 (L0 = 8): the data alone fill 147 KB of shared memory, so
+// twiddles are computed per butterfly (sincospif of the exact dyadic
+// argument) instead of read from a table, with 1024 threads (2 radix-8
+// butterflies each per pass; 16384 = 4 * 8^4).
+template <int R, int L, int NS, int TH>
+FC_DEVICE void stockham_pass_otf(float2* x) {
+  constexpr int G = L / R, GPT = G / TH;
+  static_assert(G % TH == 0, "whole butterflies per thread");
+  float2 v[GPT][R];
+#pragma unroll
+  for (int g = 0; g < GPT; ++g) {
+    const int j = threadIdx.x + g * TH;
+    const int jm = j % NS;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[g][r] = x[pd(j + r * G)];
+    if (NS > 1) {
+      constexpr int step = L / (NS * R);  // W_{NS R}^{jm r} = W_L^{jm r step}
+      const int e = jm * step;
+      auto w = [](int ee) {
+        float sn, cs;
+        sincospif(-2.0f * float(ee & (L - 1)) / float(L), &sn, &cs);
+        return make_float2(cs, sn);
+      };
+      const float2 w1 = w(e);
+      if constexpr (R == 2) {
+        v[g][1] = cmulf(v[g][1], w1);
+      } else {
+        const float2 w2 = w(2 * e);
+        v[g][1] = cmulf(v[g][1], w1);
+        v[g][2] = cmulf(v[g][2], w2);
+        v[g][3] = cmulf(v[g][3], cmulf(w1, w2));
+        if constexpr (R == 8) {
+          const float2 w4 = w(4 * e);
+          v[g][4] = cmulf(v[g][4], w4);
+          v[g][5] = cmulf(v[g][5], cmulf(w1, w4));
+          v[g][6] = cmulf(v[g][6], cmulf(w2, w4));
+          v[g][7] = cmulf(v[g][7], cmulf(cmulf(w1, w2), w4));
+        }
+      }
+    }
+    if constexpr (R == 8) dft8(v[g]);
+    else if constexpr (R == 4) dft4(v[g]);
+    else dft2(v[g]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < GPT; ++g) {
+    const int j = threadIdx.x + g * TH;
+    const int jm = j % NS;
+    const int base = (j / NS) * NS * R + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[pd(base + r * NS)] = v[g][r];
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024) precompute_kf_dit16k_kernel(const KfParams prm) {
+  extern __shared__ float2 sm[];  // padded LF data
+  constexpr int LF = 16384, TH = 1024;
+  const int64_t h0 = 2 * int64_t(blockIdx.x);
+  const bool has1 = h0 + 1 < prm.H;
+  const int K = int(prm.K);
+  griddep_wait();  // PDL: k is read and k_f written only after the previous kernel
+  const float* k0row = prm.k + h0 * K;
+  const float* k1row = k0row + K;
+  for (int n = threadIdx.x; n < LF; n += TH)
+    sm[pd(n)] = prm.kb ? make_float2(filter_tap(prm, h0, n), has1 ? filter_tap(prm, h0 + 1, n) : 0.f)
+              : n < K  ? make_float2(k0row[n], has1 ? k1row[n] : 0.f)
+                       : make_float2(0.f, 0.f);
+  __syncthreads();
+  stockham_pass_otf<4, LF, 1, TH>(sm);
+  stockham_pass_otf<8, LF, 4, TH>(sm);
+  stockham_pass_otf<8, LF, 32, TH>(sm);
+  stockham_pass_otf<8, LF, 256, TH>(sm);
+  stockham_pass_otf<8, LF, 2048, TH>(sm);
+  const float2* xs = sm;
+  constexpr int L0 = LF / 2048, CPR = 16;
+  const size_t hbytes = size_t(64) * tab_stride(CPR);
+  uint8_t* out0 = reinterpret_cast<uint8_t*>(prm.kf) + h0 * int64_t(L0 * hbytes);
+  uint8_t* out1 = out0 + L0 * hbytes;
+  for (int q = threadIdx.x; q < L0 * 64 * CPR; q += TH) {  // one destination float4 per step, k2 fastest
+    const int b = q >> 10, d = q & 1023;
+    const int kp = (d >> 8) * 4 + (d & 3), k2 = (d >> 2) & 63;
+    const int f0 = k2 + 64 * (2 * kp) + 2048 * b, f1 = f0 + 64;
+    const float2 z0 = xs[pd(f0)], z1 = xs[pd(f1)], m0 = xs[pd((LF - f0) & (LF - 1))], m1 = xs[pd((LF - f1) & (LF - 1))];
+    const float2 a0 = make_float2(0.5f * (z0.x + m0.x), 0.5f * (z0.y - m0.y));
+    const float2 a1 = make_float2(0.5f * (z1.x + m1.x), 0.5f * (z1.y - m1.y));
+    const float2 b0 = make_float2(0.5f * (z0.y + m0.y), -0.5f * (z0.x - m0.x));
+    const float2 b1 = make_float2(0.5f * (z1.y + m1.y), -0.5f * (z1.x - m1.x));
+    const uint32_t off = uint32_t(b * hbytes) + dit_kf_off(uint32_t(k2), uint32_t(kp));
+    *reinterpret_cast<float4*>(out0 + off) = make_float4(a0.x, a1.x, a0.y, a1.y);
+    if (has1) *reinterpret_cast<float4*>(out1 + off) = make_float4(b0.x, b1.x, b0.y, b1.y);
+  }
+  griddep_launch();
+}
+
 cudaError_t launch_precompute_kf_dit(const KfParams& prm, int L0, cudaStream_t s) {
   if (prm.H <= 0) return cudaSuccess;
   const unsigned grid = unsigned((prm.H + 1) / 2);
@@ -488,6 +584,12 @@ cudaError_t launch_precompute_kf_dit(const KfParams& prm, int L0, cudaStream_t s
     if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_dit_kernel<8192>), int(smem), attr))
       return e;
     return launch_pdl(PDL_KF, precompute_kf_dit_kernel<8192>, dim3(grid), dim3(256), smem, s, prm);
+  } else if (L0 == 8) {
+    const size_t smem = size_t(16384 + 2048) * sizeof(float2);
+    static int attr[64] = {0};
+    if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_dit16k_kernel), int(smem), attr))
+      return e;
+    return launch_pdl(PDL_KF, precompute_kf_dit16k_kernel, dim3(grid), dim3(1024), smem, s, prm);
   } else {
     return cudaErrorInvalidValue;
   }
@@ -519,48 +621,6 @@ __global__ void kf_dit_to_dif_kernel(const uint8_t* __restrict__ src, uint8_t* _
   }
   *reinterpret_cast<float4*>(dst + (h * L0 + k0) * hb + tab_off_rt(CPR, uint32_t(k2), uint32_t(kp))) =
       make_float4(v[0], v[1], v[2], v[3]);
-}
-
-// Order-3 plans with L0 = 8 (fft_size 16384) build k_f with the multipass
-// precompute (block k0 = K_f[k0 + L0 f'], [k2][k1/2] table layout) and
-// re-lay it out in place, one CTA per head (all L0 blocks in shared memory),
-// into the order-3 blocks (block b = K_f[f' + 2048 b], dit_kf_off); each
-// thread writes one destination float4 {re, re', im, im'} (consecutive
-// threads: consecutive 16 B).
-__global__ void __launch_bounds__(512) kf_dif_to_dit_kernel(uint8_t* __restrict__ kf, int L0) {
-  extern __shared__ __align__(16) uint8_t smk[];
-  constexpr int CPR = 16;
-  const uint32_t hb = 64 * tab_stride(CPR);
-  uint8_t* head = kf + int64_t(blockIdx.x) * L0 * hb;
-  const uint32_t sbase = smem_u32(smk);
-  for (uint32_t o = threadIdx.x * 16; o < uint32_t(L0) * hb; o += blockDim.x * 16) cp_async16(sbase + o, head + o, true);
-  cp_async_commit();
-  cp_async_wait_all();
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < L0 * 1024; idx += blockDim.x) {
-    const int b = idx >> 10, d = idx & 1023;
-    const int kp = (d >> 8) * 4 + (d & 3), k2 = (d >> 2) & 63;
-    float v[4];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int f = k2 + 64 * (2 * kp + e) + 2048 * b;
-      const int k0 = f % L0, fp = f / L0;
-      const int k2d = fp % 64, k1d = fp / 64;
-      const float4 q = *reinterpret_cast<const float4*>(smk + k0 * hb + tab_off_rt(CPR, uint32_t(k2d), uint32_t(k1d / 2)));
-      v[e] = (k1d & 1) ? q.y : q.x;
-      v[2 + e] = (k1d & 1) ? q.w : q.z;
-    }
-    *reinterpret_cast<float4*>(head + b * hb + dit_kf_off(uint32_t(k2), uint32_t(kp))) = make_float4(v[0], v[1], v[2], v[3]);
-  }
-}
-
-cudaError_t launch_kf_dif_to_dit(void* kf, int64_t H, int L0, cudaStream_t s) {
-  if (H <= 0) return cudaSuccess;
-  const size_t smem = size_t(L0) * 64 * tab_stride(16);
-  static int attr[64] = {0};
-  if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kf_dif_to_dit_kernel), int(smem), attr)) return e;
-  kf_dif_to_dit_kernel<<<unsigned(H), 512, smem, s>>>(static_cast<uint8_t*>(kf), L0);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_kf_dit_to_dif(const void* src, void* dst, int64_t H, int L0, cudaStream_t s) {

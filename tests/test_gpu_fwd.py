@@ -191,9 +191,7 @@ def test_fwd_order3_single_pass(N, dtype, gated):
     assert plan.info.factors == (N // 1024, 32, 64)
     launch_count_reset()
     got, ref = _run(N, True, dtype, gated, B=37, H=3, seed=31)
-    # precompute_kf + one convolution (L0 = 8: k_f by the multipass column /
-    # row transforms + one in-place re-layout)
-    assert launch_count_reset() == (2 if N < 8192 else 4)
+    assert launch_count_reset() == 2  # precompute_kf + one convolution
     _assert_close(got, ref)
 
 
