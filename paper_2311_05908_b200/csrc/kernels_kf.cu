@@ -421,62 +421,9 @@ cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Single-pass order-3 plans (fft_size LF = L0 * 2048, L0 in {2, 4}; 8 below): two
-// heads per CTA as above, the LF-point transform in shared memory with
-// twiddles W_LF^e from sincospif of the exact dyadic argument -2e/LF (this
-// precompute is not the hot path), written as L0 blocks per head: block k0
-// holds K_f[f' + 2048 k0], f' = k2 + 64 k1, in the [k1/2][k2] layout of
-// layout.h dit_kf_off (DIT order: the forward kernel's outer DFT produces the
-// frequency digit k0 = f / 2048).
-template <int LF>
-__global__ void __launch_bounds__(256) precompute_kf_dit_kernel(const KfParams prm) {
-  extern __shared__ float2 sm[];  // padded LF data + LF twiddles
-  constexpr int PL = LF + LF / 8;
-  float2* tws = sm + PL;
-  const int64_t h0 = 2 * int64_t(blockIdx.x);
-  const bool has1 = h0 + 1 < prm.H;
-  const int K = int(prm.K);
-  for (int e = threadIdx.x; e < LF; e += 256) {
-    float sn, cs;
-    sincospif(-2.0f * float(e) / float(LF), &sn, &cs);
-    tws[pd(e)] = make_float2(cs, sn);
-  }
-  griddep_wait();  // PDL: k is read and k_f written only after the previous kernel
-  const float* k0row = prm.k + h0 * K;
-  const float* k1row = k0row + K;
-  for (int n = threadIdx.x; n < LF; n += 256)
-    sm[pd(n)] = prm.kb ? make_float2(filter_tap(prm, h0, n), has1 ? filter_tap(prm, h0 + 1, n) : 0.f)
-              : n < K  ? make_float2(k0row[n], has1 ? k1row[n] : 0.f)
-                       : make_float2(0.f, 0.f);
-  __syncthreads();
-  fft_inplace_ct<LF>(sm, tws);
-  const float2* xs = sm;
-  constexpr int L0 = LF / 2048, CPR = 16;  // L1 = 32: 16 pairs per k2 row
-  const size_t hbytes = size_t(64) * tab_stride(CPR);  // one block
-  uint8_t* out0 = reinterpret_cast<uint8_t*>(prm.kf) + h0 * int64_t(L0 * hbytes);
-  uint8_t* out1 = out0 + L0 * hbytes;
-  for (int q = threadIdx.x; q < L0 * 64 * CPR; q += blockDim.x) {
-    const int k0 = q / (64 * CPR), qr = q % (64 * CPR);
-    const int w = qr >> 5, lane = qr & 31;
-    const int k2 = (w % 8) * 8 + (lane & 7);
-    const int k1 = 2 * ((w / 8) * 4 + (lane >> 3));
-    const int f0 = k2 + 64 * k1 + 2048 * k0, f1 = f0 + 64;
-    const float2 z0 = xs[pd(f0)], z1 = xs[pd(f1)], m0 = xs[pd((LF - f0) & (LF - 1))], m1 = xs[pd((LF - f1) & (LF - 1))];
-    const float2 a0 = make_float2(0.5f * (z0.x + m0.x), 0.5f * (z0.y - m0.y));
-    const float2 a1 = make_float2(0.5f * (z1.x + m1.x), 0.5f * (z1.y - m1.y));
-    const float2 b0 = make_float2(0.5f * (z0.y + m0.y), -0.5f * (z0.x - m0.x));
-    const float2 b1 = make_float2(0.5f * (z1.y + m1.y), -0.5f * (z1.x - m1.x));
-    const uint32_t off = uint32_t(k0 * hbytes) + dit_kf_off(uint32_t(k2), uint32_t(k1 / 2));
-    *reinterpret_cast<float4*>(out0 + off) = make_float4(a0.x, a1.x, a0.y, a1.y);
-    if (has1) *reinterpret_cast<float4*>(out1 + off) = make_float4(b0.x, b1.x, b0.y, b1.y);
-  }
-  griddep_launch();
-}
-
-// fft_size 16384 (L0 = 8): the data alone fill 147 KB of shared memory, so
-// twiddles are computed per butterfly (sincospif of the exact dyadic
-// argument) instead of read from a table, with 1024 threads (2 radix-8
-// butterflies each per pass; 16384 = 4 * 8^4).
+// One Stockham pass (radix R, stride NS) over L points in shared memory by
+// TH threads, twiddles computed per butterfly (the order-3 k_f sizes do not
+// leave room for a twiddle table beside the data at 16384 points).
 template <int R, int L, int NS, int TH>
 FC_DEVICE void stockham_pass_otf(float2* x) {
   constexpr int G = L / R, GPT = G / TH;
@@ -529,9 +476,22 @@ FC_DEVICE void stockham_pass_otf(float2* x) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(1024) precompute_kf_dit16k_kernel(const KfParams prm) {
+// Single-pass order-3 plans (fft_size LF = L0 * 2048, L0 = 2, 4, 8): two
+// heads per CTA (one complex FFT of k_h + i k_{h+1}, Hermitian split), the
+// LF-point Stockham transform in shared memory (data only, 37 / 74 / 147 KB)
+// with twiddles W_LF^e computed per butterfly (sincospif of the exact dyadic
+// argument -2e/LF), 512 / 1024 / 1024 threads, written as L0 blocks per head:
+// block k0 holds K_f[f' + 2048 k0], f' = k2 + 64 k1, in the layout of
+// layout.h dit_kf_off (DIT order: the forward kernel's outer DFT produces the
+// frequency digit k0 = f / 2048).  (Round 2 sessions 1-2: 256 threads and a
+// twiddle table, 4096 / 8192 only; fft_size 16384 went through the multipass
+// transforms plus a re-layout, 202 us per step at N = 8192, now ~77 us.)
+template <int LF>
+constexpr int dit_threads() { return LF == 4096 ? 512 : 1024; }
+template <int LF>
+__global__ void __launch_bounds__(dit_threads<LF>()) precompute_kf_dit_kernel(const KfParams prm) {
   extern __shared__ float2 sm[];  // padded LF data
-  constexpr int LF = 16384, TH = 1024;
+  constexpr int TH = dit_threads<LF>();
   const int64_t h0 = 2 * int64_t(blockIdx.x);
   const bool has1 = h0 + 1 < prm.H;
   const int K = int(prm.K);
@@ -543,11 +503,25 @@ __global__ void __launch_bounds__(1024) precompute_kf_dit16k_kernel(const KfPara
               : n < K  ? make_float2(k0row[n], has1 ? k1row[n] : 0.f)
                        : make_float2(0.f, 0.f);
   __syncthreads();
-  stockham_pass_otf<4, LF, 1, TH>(sm);
-  stockham_pass_otf<8, LF, 4, TH>(sm);
-  stockham_pass_otf<8, LF, 32, TH>(sm);
-  stockham_pass_otf<8, LF, 256, TH>(sm);
-  stockham_pass_otf<8, LF, 2048, TH>(sm);
+  if constexpr (LF == 4096) {  // 8^4
+    stockham_pass_otf<8, LF, 1, TH>(sm);
+    stockham_pass_otf<8, LF, 8, TH>(sm);
+    stockham_pass_otf<8, LF, 64, TH>(sm);
+    stockham_pass_otf<8, LF, 512, TH>(sm);
+  } else if constexpr (LF == 8192) {  // 2 * 8^4
+    stockham_pass_otf<2, LF, 1, TH>(sm);
+    stockham_pass_otf<8, LF, 2, TH>(sm);
+    stockham_pass_otf<8, LF, 16, TH>(sm);
+    stockham_pass_otf<8, LF, 128, TH>(sm);
+    stockham_pass_otf<8, LF, 1024, TH>(sm);
+  } else {  // 4 * 8^4
+    static_assert(LF == 16384, "order-3 k_f sizes");
+    stockham_pass_otf<4, LF, 1, TH>(sm);
+    stockham_pass_otf<8, LF, 4, TH>(sm);
+    stockham_pass_otf<8, LF, 32, TH>(sm);
+    stockham_pass_otf<8, LF, 256, TH>(sm);
+    stockham_pass_otf<8, LF, 2048, TH>(sm);
+  }
   const float2* xs = sm;
   constexpr int L0 = LF / 2048, CPR = 16;
   const size_t hbytes = size_t(64) * tab_stride(CPR);
@@ -572,28 +546,16 @@ __global__ void __launch_bounds__(1024) precompute_kf_dit16k_kernel(const KfPara
 cudaError_t launch_precompute_kf_dit(const KfParams& prm, int L0, cudaStream_t s) {
   if (prm.H <= 0) return cudaSuccess;
   const unsigned grid = unsigned((prm.H + 1) / 2);
-  if (L0 == 2) {
-    const size_t smem = size_t(2 * (4096 + 512)) * sizeof(float2);
-    static int attr[64] = {0};
-    if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_dit_kernel<4096>), int(smem), attr))
-      return e;
-    return launch_pdl(PDL_KF, precompute_kf_dit_kernel<4096>, dim3(grid), dim3(256), smem, s, prm);
-  } else if (L0 == 4) {
-    const size_t smem = size_t(2 * (8192 + 1024)) * sizeof(float2);
-    static int attr[64] = {0};
-    if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_dit_kernel<8192>), int(smem), attr))
-      return e;
-    return launch_pdl(PDL_KF, precompute_kf_dit_kernel<8192>, dim3(grid), dim3(256), smem, s, prm);
-  } else if (L0 == 8) {
-    const size_t smem = size_t(16384 + 2048) * sizeof(float2);
-    static int attr[64] = {0};
-    if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_dit16k_kernel), int(smem), attr))
-      return e;
-    return launch_pdl(PDL_KF, precompute_kf_dit16k_kernel, dim3(grid), dim3(1024), smem, s, prm);
-  } else {
-    return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
+  static int attr[3][64] = {};
+  auto go = [&](auto kern, int LF, int th, int* cache) -> cudaError_t {
+    const size_t smem = size_t(LF + LF / 8) * sizeof(float2);
+    if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(kern), int(smem), cache)) return e;
+    return launch_pdl(PDL_KF, kern, dim3(grid), dim3(th), smem, s, prm);
+  };
+  if (L0 == 2) return go(precompute_kf_dit_kernel<4096>, 4096, dit_threads<4096>(), attr[0]);
+  if (L0 == 4) return go(precompute_kf_dit_kernel<8192>, 8192, dit_threads<8192>(), attr[1]);
+  if (L0 == 8) return go(precompute_kf_dit_kernel<16384>, 16384, dit_threads<16384>(), attr[2]);
+  return cudaErrorInvalidValue;
 }
 
 // The backward of an order-3 plan runs the multipass path, whose k_f layout
