@@ -151,6 +151,84 @@ FC_DEVICE void fft_inplace_any(float2* xs, const float2* tws, int L) {
   else if (L == 1024) fft_inplace_ct<1024>(xs, tws);
   else fft_inplace_ct<512>(xs, tws);
 }
+// One Stockham pass (radix R, stride NS) over L points in shared memory by
+// TH threads, twiddles computed per butterfly (the order-3 k_f sizes do not
+// leave room for a twiddle table beside the data at 16384 points).
+template <int R, int L, int NS, int TH>
+FC_DEVICE void stockham_pass_otf(float2* x) {
+  constexpr int G = L / R, GPT = (G + TH - 1) / TH;
+  static_assert(G % TH == 0 || G < TH, "whole butterflies per thread");
+  float2 v[GPT][R];
+#pragma unroll
+  for (int g = 0; g < GPT; ++g) {
+    const int j = threadIdx.x + g * TH;
+    if (G < TH && j >= G) break;
+    const int jm = j % NS;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[g][r] = x[pd(j + r * G)];
+    if (NS > 1) {
+      constexpr int step = L / (NS * R);  // W_{NS R}^{jm r} = W_L^{jm r step}
+      const int e = jm * step;
+      auto w = [](int ee) {
+        float sn, cs;
+        sincospif(-2.0f * float(ee & (L - 1)) / float(L), &sn, &cs);
+        return make_float2(cs, sn);
+      };
+      const float2 w1 = w(e);
+      if constexpr (R == 2) {
+        v[g][1] = cmulf(v[g][1], w1);
+      } else {
+        const float2 w2 = w(2 * e);
+        v[g][1] = cmulf(v[g][1], w1);
+        v[g][2] = cmulf(v[g][2], w2);
+        v[g][3] = cmulf(v[g][3], cmulf(w1, w2));
+        if constexpr (R == 8) {
+          const float2 w4 = w(4 * e);
+          v[g][4] = cmulf(v[g][4], w4);
+          v[g][5] = cmulf(v[g][5], cmulf(w1, w4));
+          v[g][6] = cmulf(v[g][6], cmulf(w2, w4));
+          v[g][7] = cmulf(v[g][7], cmulf(cmulf(w1, w2), w4));
+        }
+      }
+    }
+    if constexpr (R == 8) dft8(v[g]);
+    else if constexpr (R == 4) dft4(v[g]);
+    else dft2(v[g]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < GPT; ++g) {
+    const int j = threadIdx.x + g * TH;
+    if (G < TH && j >= G) break;
+    const int jm = j % NS;
+    const int base = (j / NS) * NS * R + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[pd(base + r * NS)] = v[g][r];
+  }
+  __syncthreads();
+}
+
+// The fused plans' k_f transform (L = 512, 1024, 2048; 256 threads), the
+// same passes as fft_inplace_ct with twiddles computed per butterfly: no
+// table load, half the shared memory per CTA.
+FC_DEVICE void fft_otf_any(float2* xs, int L) {
+  if (L == 2048) {  // 4 * 8^3
+    stockham_pass_otf<4, 2048, 1, 256>(xs);
+    stockham_pass_otf<8, 2048, 4, 256>(xs);
+    stockham_pass_otf<8, 2048, 32, 256>(xs);
+    stockham_pass_otf<8, 2048, 256, 256>(xs);
+  } else if (L == 1024) {  // 2 * 8^3
+    stockham_pass_otf<2, 1024, 1, 256>(xs);
+    stockham_pass_otf<8, 1024, 2, 256>(xs);
+    stockham_pass_otf<8, 1024, 16, 256>(xs);
+    stockham_pass_otf<8, 1024, 128, 256>(xs);
+  } else {  // 8^3
+    stockham_pass_otf<8, 512, 1, 256>(xs);
+    stockham_pass_otf<8, 512, 8, 256>(xs);
+    stockham_pass_otf<8, 512, 64, 256>(xs);
+  }
+}
+
 // shared memory of the FFT kernels: padded data + L twiddles
 inline size_t fft_smem_bytes(int64_t L) { return size_t(2 * (L + L / 8)) * sizeof(float2); }
 // L float2 from global (16-byte aligned) into the padded layout
@@ -178,14 +256,10 @@ FC_DEVICE void load_padded(float2* dst, const float2* src, int L) {
 // z = k_h + i k_{h+1} yields both spectra through the Hermitian split
 // K_h[f] = (Z[f] + conj Z[-f]) / 2, K_{h+1}[f] = (Z[f] - conj Z[-f]) / (2i).
 __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) {
-  extern __shared__ float2 sm[];  // padded L data + L twiddles
+  extern __shared__ float2 sm[];  // padded L data (twiddles per butterfly, fft_otf_any)
   const int64_t h0 = 2 * int64_t(blockIdx.x);
   const bool has1 = h0 + 1 < prm.H;
   const int L = int(prm.L), K = int(prm.K);
-  float2* tws = sm + L + L / 8;
-  {
-    load_padded(tws, prm.twiddle, L);  // plan-owned table
-  }
   griddep_wait();  // PDL: k is read and k_f written only after the previous kernel
   const float* k0row = prm.k + h0 * K;
   const float* k1row = k0row + K;
@@ -209,9 +283,8 @@ __global__ void __launch_bounds__(256) precompute_kf_kernel(const KfParams prm) 
       if (n < L) sm[pd(n)] = kv[i];
     }
   }
-  cp_async_wait_all();
   __syncthreads();
-  fft_inplace_any(sm, tws, L);
+  fft_otf_any(sm, L);
   const float2* xs = sm;
   // plan layout: row k2 holds pairs (k1, k1 + 1) as {kr, kr', ki, ki'}
   const int L1 = prm.L1, L2 = prm.L2, cpr = L1 / 2;
@@ -421,61 +494,6 @@ cudaError_t launch_dk_finalize(const DkParams& prm, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// One Stockham pass (radix R, stride NS) over L points in shared memory by
-// TH threads, twiddles computed per butterfly (the order-3 k_f sizes do not
-// leave room for a twiddle table beside the data at 16384 points).
-template <int R, int L, int NS, int TH>
-FC_DEVICE void stockham_pass_otf(float2* x) {
-  constexpr int G = L / R, GPT = G / TH;
-  static_assert(G % TH == 0, "whole butterflies per thread");
-  float2 v[GPT][R];
-#pragma unroll
-  for (int g = 0; g < GPT; ++g) {
-    const int j = threadIdx.x + g * TH;
-    const int jm = j % NS;
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[g][r] = x[pd(j + r * G)];
-    if (NS > 1) {
-      constexpr int step = L / (NS * R);  // W_{NS R}^{jm r} = W_L^{jm r step}
-      const int e = jm * step;
-      auto w = [](int ee) {
-        float sn, cs;
-        sincospif(-2.0f * float(ee & (L - 1)) / float(L), &sn, &cs);
-        return make_float2(cs, sn);
-      };
-      const float2 w1 = w(e);
-      if constexpr (R == 2) {
-        v[g][1] = cmulf(v[g][1], w1);
-      } else {
-        const float2 w2 = w(2 * e);
-        v[g][1] = cmulf(v[g][1], w1);
-        v[g][2] = cmulf(v[g][2], w2);
-        v[g][3] = cmulf(v[g][3], cmulf(w1, w2));
-        if constexpr (R == 8) {
-          const float2 w4 = w(4 * e);
-          v[g][4] = cmulf(v[g][4], w4);
-          v[g][5] = cmulf(v[g][5], cmulf(w1, w4));
-          v[g][6] = cmulf(v[g][6], cmulf(w2, w4));
-          v[g][7] = cmulf(v[g][7], cmulf(cmulf(w1, w2), w4));
-        }
-      }
-    }
-    if constexpr (R == 8) dft8(v[g]);
-    else if constexpr (R == 4) dft4(v[g]);
-    else dft2(v[g]);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int g = 0; g < GPT; ++g) {
-    const int j = threadIdx.x + g * TH;
-    const int jm = j % NS;
-    const int base = (j / NS) * NS * R + jm;
-#pragma unroll
-    for (int r = 0; r < R; ++r) x[pd(base + r * NS)] = v[g][r];
-  }
-  __syncthreads();
-}
-
 // Single-pass order-3 plans (fft_size LF = L0 * 2048, L0 = 2, 4, 8): two
 // heads per CTA (one complex FFT of k_h + i k_{h+1}, Hermitian split), the
 // LF-point Stockham transform in shared memory (data only, 37 / 74 / 147 KB)
@@ -595,7 +613,7 @@ cudaError_t launch_kf_dit_to_dif(const void* src, void* dst, int64_t H, int L0, 
 
 cudaError_t launch_precompute_kf(const KfParams& prm, cudaStream_t s) {
   if (prm.H <= 0) return cudaSuccess;
-  const size_t smem = fft_smem_bytes(prm.L);
+  const size_t smem = size_t(prm.L + prm.L / 8) * sizeof(float2);
   static int attr[64] = {0};
   if (cudaError_t e = set_smem_attr(reinterpret_cast<const void*>(precompute_kf_kernel), int(smem), attr)) return e;
   return launch_pdl(PDL_KF, precompute_kf_kernel, dim3(unsigned((prm.H + 1) / 2)), dim3(256), smem, s, prm);
