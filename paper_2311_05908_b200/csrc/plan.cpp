@@ -22,18 +22,18 @@
 
 // B200 tier cost model coefficients (seconds per feature unit), fitted by
 // tools/cost_model.py on the bench sweep (profiles/r02c/cost_model.md).
-#define COST_B200_0 1.178744e-08
-#define COST_B200_1 1.097990e-08
-#define COST_B200_2 1.577693e-08
-#define COST_B200_3 1.918414e-08
-#define COST_B200_4 3.198669e-12
-#define COST_B200_5 1.063888e-11
-#define COST_B200_6 1.153109e-05
+#define COST_B200_0 1.005051e-08
+#define COST_B200_1 7.413649e-09
+#define COST_B200_2 1.279446e-08
+#define COST_B200_3 1.558044e-08
+#define COST_B200_4 3.572859e-12
+#define COST_B200_5 9.231505e-12
+#define COST_B200_6 1.237435e-05
 #define COST_B200_7 0.000000e+00
-#define COST_B200_8 5.093123e-12
-#define COST_B200_9 5.162027e-11
+#define COST_B200_8 4.945092e-12
+#define COST_B200_9 3.467309e-11
 #define COST_B200_10 0.000000e+00
-#define COST_B200_11 6.556603e-14
+#define COST_B200_11 1.197651e-13
 
 namespace fc {
 
