@@ -46,7 +46,7 @@ struct fftconv_plan_s {
   int32_t nlev = 0;        // multipass: outer levels (L0 = prod lev_L0)
   int32_t lev_L0[4] = {1, 1, 1, 1};
   int32_t Lp = 0;          // multipass: inner (fused) transform length
-  // single-pass order 3 (causal fft_size = dit * 2048, dit in {2, 4}): the
+  // single-pass order 3 (causal fft_size = dit * 2048, dit in {2, 4, 8}): the
   // forward runs one fused kernel (DIT outer DFT in its pointwise step) with
   // the causal 2048-point tables at image offset dit_tab_off, and k_f holds
   // dit blocks per head, block k0 = K_f[f' + 2048 k0]; the backward runs the
