@@ -3,7 +3,7 @@
 # (+ sweep), extra workloads, ncu launch lists + full captures
 cd $(dirname $0)/../..
 O=gpurun_out/final_d; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "rc $?" >> $O/pytest_gpu.log
+[ -z "$SKIP_TESTS" ] && { timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "rc $?" >> $O/pytest_gpu.log; }
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
 ( time python bench.py ) > $O/bench_default.json 2> $O/bench_default.err
 timeout 900 python bench.py --workload cfg2 --steps 50 --warmup 5 --no-cpu-baseline --no-torch-baseline --e2e-steps 0 \
@@ -30,5 +30,6 @@ for r in $d/*.ncu-rep; do
   ncu -i $r --page raw --csv > ${r%.ncu-rep}_raw.csv 2>/dev/null
   ncu -i $r --page source --csv > ${r%.ncu-rep}_source.csv 2>/dev/null
 done
+rm -f $d/*.ncu-rep  # (gpurun copies back <= 64 MiB)
 nvidia-smi > $O/smi.txt
-tail -3 $O/pytest_gpu.log; cat $O/smoke.log | tail -1; tail -c 400 $O/bench_default.json; tail -c 300 $O/reference.json
+cat $O/smoke.log | tail -1; tail -c 400 $O/bench_default.json; tail -c 300 $O/reference.json
