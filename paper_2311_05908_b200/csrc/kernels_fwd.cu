@@ -76,6 +76,9 @@ __device__ long long fc_trace_buf[8][64][24];
 #ifndef FC_DIT_KFS
 #define FC_DIT_KFS 1
 #endif
+#ifndef FC_DIT_SLOT_WG
+#define FC_DIT_SLOT_WG 0
+#endif
 #ifndef FC_O3_FRAG
 #define FC_O3_FRAG 1
 #endif
@@ -150,7 +153,7 @@ struct FwdCfg {
   // (measured: per-warpgroup slots made the order-2 kernels 2 % faster, the
   // gated order-3 kernel 20 % and plain L0 = 4 4 % slower -- register
   // spills --, plain L0 = 2 0.7 % faster; circular tiles have no SMEM for two)
-  static constexpr bool SLOT_WG = !DIT && !CIN;
+  static constexpr bool SLOT_WG = (!DIT || (FC_DIT_SLOT_WG && !CPL)) && !CIN;
   static constexpr uint32_t WG_BYTES = KF_SM + C::al(C::BUFX_BYTES) + (SLOT_WG ? C::al(UW_BYTES) : 0);
   // circular plain tiles (the multipass inner pass): y staging shared by
   // the warpgroups in tile order, leaving by one TMA tensor store each
@@ -982,7 +985,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
 #pragma unroll
         for (int k0 = 0; k0 < 8; ++k0) {  // * k_f[f' + 2048 k0] / 8: kf = {kr_e0, kr_e1, ki_e0, ki_e1}
           const float4 qv = kf[k0];
-          const float2 kr = make_float2(0.125f * qv.x, 0.125f * qv.y), ki = make_float2(0.125f * qv.z, 0.125f * qv.w);
+          const float2 kr = make_float2(qv.x, qv.y), ki = make_float2(qv.z, qv.w);  // (1/8 folded into k_f)
           const float2 zr = fma2(xr[k0], kr, mul2(xi[k0], make_float2(-ki.x, -ki.y)));
           const float2 zi = fma2(xr[k0], ki, mul2(xi[k0], kr));
           xr[k0] = zr; xi[k0] = zi;
@@ -1101,7 +1104,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
 #pragma unroll
             for (int k0 = 0; k0 < 4; ++k0) {
               const float4 qv = kf[c][k0];
-              const float2 kr = make_float2(0.25f * qv.x, 0.25f * qv.y), ki = make_float2(0.25f * qv.z, 0.25f * qv.w);
+              const float2 kr = make_float2(qv.x, qv.y), ki = make_float2(qv.z, qv.w);  // (1/4 folded into k_f)
               const float2 zr = fma2(sr[k0], kr, mul2(si[k0], make_float2(-ki.x, -ki.y)));
               const float2 zi = fma2(sr[k0], ki, mul2(si[k0], kr));
               sr[k0] = zr; si[k0] = zi;
@@ -1148,7 +1151,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
 #pragma unroll
             for (int k0 = 0; k0 < 2; ++k0) {  // * k_f / 2
               const float4 qv = kf[c][k0];
-              const float2 kr = make_float2(0.5f * qv.x, 0.5f * qv.y), ki = make_float2(0.5f * qv.z, 0.5f * qv.w);
+              const float2 kr = make_float2(qv.x, qv.y), ki = make_float2(qv.z, qv.w);  // (1/2 folded into k_f)
               const float2 zr = fma2(sr[k0], kr, mul2(si[k0], make_float2(-ki.x, -ki.y)));
               const float2 zi = fma2(sr[k0], ki, mul2(si[k0], kr));
               sr[k0] = zr; si[k0] = zi;
@@ -1223,7 +1226,6 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
           }
         }
         tmem_ld_wait();
-        constexpr float sc = 1.0f / float(L0I);
 #pragma unroll
         for (int ee = 0; ee < 4; ++ee) {
           const int e = 2 * ee;
@@ -1258,7 +1260,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
 #pragma unroll
           for (int slot = 0; slot < 2; ++slot) {
             const float4 q = kf[slot][ee];
-            const float2 kr = make_float2(sc * q.x, sc * q.y), ki = make_float2(sc * q.z, sc * q.w);
+            const float2 kr = make_float2(q.x, q.y), ki = make_float2(q.z, q.w);  // (1/L0 folded into k_f)
             const float2 nki = make_float2(-ki.x, -ki.y);
             const float2 zr = fma2(si[slot], nki, mul2(sr[slot], kr));
             const float2 zi = fma2(si[slot], kr, mul2(sr[slot], ki));

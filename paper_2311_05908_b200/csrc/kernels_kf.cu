@@ -550,10 +550,13 @@ __global__ void __launch_bounds__(dit_threads<LF>()) precompute_kf_dit_kernel(co
     const int kp = (d >> 8) * 4 + (d & 3), k2 = (d >> 2) & 63;
     const int f0 = k2 + 64 * (2 * kp) + 2048 * b, f1 = f0 + 64;
     const float2 z0 = xs[pd(f0)], z1 = xs[pd(f1)], m0 = xs[pd((LF - f0) & (LF - 1))], m1 = xs[pd((LF - f1) & (LF - 1))];
-    const float2 a0 = make_float2(0.5f * (z0.x + m0.x), 0.5f * (z0.y - m0.y));
-    const float2 a1 = make_float2(0.5f * (z1.x + m1.x), 0.5f * (z1.y - m1.y));
-    const float2 b0 = make_float2(0.5f * (z0.y + m0.y), -0.5f * (z0.x - m0.x));
-    const float2 b1 = make_float2(0.5f * (z1.y + m1.y), -0.5f * (z1.x - m1.x));
+    // Hermitian split (1/2) and the forward kernel's 1/L0 of the outer
+    // inverse DFT, folded here (an exact power of two)
+    constexpr float hs = 0.5f / float(L0);
+    const float2 a0 = make_float2(hs * (z0.x + m0.x), hs * (z0.y - m0.y));
+    const float2 a1 = make_float2(hs * (z1.x + m1.x), hs * (z1.y - m1.y));
+    const float2 b0 = make_float2(hs * (z0.y + m0.y), -hs * (z0.x - m0.x));
+    const float2 b1 = make_float2(hs * (z1.y + m1.y), -hs * (z1.x - m1.x));
     const uint32_t off = uint32_t(b * hbytes) + dit_kf_off(uint32_t(k2), uint32_t(kp));
     *reinterpret_cast<float4*>(out0 + off) = make_float4(a0.x, a1.x, a0.y, a1.y);
     if (has1) *reinterpret_cast<float4*>(out1 + off) = make_float4(b0.x, b1.x, b0.y, b1.y);
@@ -596,8 +599,8 @@ __global__ void kf_dit_to_dif_kernel(const uint8_t* __restrict__ src, uint8_t* _
     const int b = f / 2048, g = f % 2048;
     const int k2s = g % 64, k1s = g / 64;
     const float4 q = *reinterpret_cast<const float4*>(src + (h * L0 + b) * hb + dit_kf_off(uint32_t(k2s), uint32_t(k1s / 2)));
-    v[s] = (k1s & 1) ? q.y : q.x;
-    v[2 + s] = (k1s & 1) ? q.w : q.z;
+    v[s] = float(L0) * ((k1s & 1) ? q.y : q.x);  // (undo the 1/L0 the order-3 layout carries)
+    v[2 + s] = float(L0) * ((k1s & 1) ? q.w : q.z);
   }
   *reinterpret_cast<float4*>(dst + (h * L0 + k0) * hb + tab_off_rt(CPR, uint32_t(k2), uint32_t(kp))) =
       make_float4(v[0], v[1], v[2], v[3]);

@@ -20,8 +20,9 @@ FC_HD uint32_t tab_off_rt(uint32_t cpr, uint32_t row, uint32_t j) { return row *
 template <int CPR>
 FC_HD uint32_t tab_off(uint32_t row, uint32_t j) { return row * (CPR * 16u + 16u) + j * 16u; }
 
-// k_f block of a single-pass order-3 plan (K_f[f' + 2048 k0], f' = k2 + 64 k1,
-// one block per (head, k0)): float4 {kr(k1), kr(k1+1), ki(k1), ki(k1+1)} of
+// k_f block of a single-pass order-3 plan (K_f[f' + 2048 k0] / L0 -- the 1/L0
+// of the outer inverse DFT folded in --, f' = k2 + 64 k1, one block per
+// (head, k0)): float4 {kr(k1), kr(k1+1), ki(k1), ki(k1+1)} of
 // k1 pair kp = k1 / 2 at index ((kp / 4) * 64 + k2) * 4 + kp % 4.  The
 // L0 = 4 epilogue-2 thread (k2 = lane / 4 + ..., kp % 4 = lane % 4, one
 // 16x256b TMEM fragment) reads one float4 per k0 and 4 k1 pairs: 8 lanes

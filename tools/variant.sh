@@ -9,7 +9,7 @@ if [ "$1" = build ]; then
   mkdir -p paper_2311_05908_b200/ablate
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -shared -I include -I $C \
     --expt-relaxed-constexpr $3 -o paper_2311_05908_b200/ablate/libfftconv_$2.so \
-    $C/plan.cpp $C/api.cu $C/kernels_fwd.cu $C/kernels_kf.cu $C/kernels_mp.cu $C/kernels_bwd.cu
+    $C/plan.cpp $C/api.cu $C/kernels_fwd.cu $C/kernels_kf.cu $C/kernels_mp.cu $C/kernels_bwd.cu $C/kernels_f32.cu
 else
   for v in $2; do
     if [ "$v" = main ]; then lib=$PWD/paper_2311_05908_b200/libfftconv.so; else lib=$PWD/paper_2311_05908_b200/ablate/libfftconv_$v.so; fi
