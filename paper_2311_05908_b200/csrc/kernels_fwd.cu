@@ -76,6 +76,9 @@ __device__ long long fc_trace_buf[8][64][24];
 #ifndef FC_DIT_KFS
 #define FC_DIT_KFS 1
 #endif
+#ifndef FC_CPL_UNROLL
+#define FC_CPL_UNROLL 2
+#endif
 #ifndef FC_DIT_SLOT_WG
 #define FC_DIT_SLOT_WG 0
 #endif
@@ -893,7 +896,8 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
       wait_half(0);
       wait_half(1);
       constexpr float R2 = 0.70710678118654752f;
-#pragma unroll 1
+      constexpr int kCplUnroll = FC_CPL_UNROLL;  // both chunks unrolled: no spills, 2 % faster than 1
+#pragma unroll kCplUnroll
       for (int c = 0; c < 2; ++c) {
         const int k1c = 2 * wg + c;
         float yv[2][2][2][4];  // [g][slot][re|im]: {(xb 0, k1), (xb 0, k1 + 1), (xb 1, k1), (xb 1, k1 + 1)}
