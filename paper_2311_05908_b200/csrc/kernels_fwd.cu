@@ -76,6 +76,9 @@ __device__ long long fc_trace_buf[8][64][24];
 #ifndef FC_DIT_KFS
 #define FC_DIT_KFS 1
 #endif
+#ifndef FC_EPI1_UNROLL_DIT  // (experiment: 1 or 2 for every order-3 tile; 0 = the rule below)
+#define FC_EPI1_UNROLL_DIT 0
+#endif
 #ifndef FC_CPL_UNROLL
 #define FC_CPL_UNROLL 2
 #endif
@@ -819,7 +822,11 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
       // causal ones on B200
       // (gated order 3 with L0 = 2: 1 -- with the in-place epilogue 4 below
       // 9 % faster; L0 = 4 keeps 2 and the two-pass epilogue 4: 4-7 % faster)
-      constexpr int kEpi1Unroll = ((GATED && L0I != 2) || !CAUSAL) ? 2 : 1;
+      // (order 3, measured with the fragment epilogue 2: plain L0 = 2 -3.6 %
+      // and L0 = 4 -0.8 % with 2; gated L0 = 8 -1.3 % with 1)
+      constexpr int kEpi1Unroll = (DIT && FC_EPI1_UNROLL_DIT) ? FC_EPI1_UNROLL_DIT
+                                  : DIT ? (GATED ? (L0I == 4 ? 2 : 1) : (L0I <= 4 ? 2 : 1))
+                                        : ((GATED && L0I != 2) || !CAUSAL) ? 2 : 1;
 #pragma unroll kEpi1Unroll
       for (int sub = 0; sub < 2; ++sub) {
         const int k20 = slice * 32 + sub * 16;  // 16 k2 per item
