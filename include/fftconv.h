@@ -89,7 +89,12 @@ typedef struct {
   int64_t fft_size;          /* L                                             */
   int32_t causal;            /* 1 causal (zero-padded), 0 circular            */
   int32_t dtype;             /* fftconv_dtype_t                               */
-  int32_t regime;            /* 1 fused single pass, 2 partial (chunked),
+  int32_t regime;            /* 1 fused single pass (order 2 for fft_size
+                                <= 2048; causal fft_size 4096 / 8192 / 16384
+                                as order 3, the outer L0-point DFT inside the
+                                fused kernel, when the B200 cost model
+                                predicts it faster -- env FFTCONV_DIT=0 / 1
+                                forbids / forces it), 2 partial (chunked),
                                 3 multipass (outer L0-point passes + fused
                                 inner transform, Alg. 4)                     */
   int32_t order;             /* number of transform levels: order-2 Monarch
