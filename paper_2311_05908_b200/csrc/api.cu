@@ -247,7 +247,7 @@ static fftconv_status_t run_fwd(fftconv_plan_t p, const void* u, const void* w, 
     // u, w: natural-order boxes; v, y: 128 B swizzled boxes (epilogue 4
     // gates and stages 16-byte units in place) -- gated L0 = 4 tiles keep
     // natural-order v and y (their epilogue 4 gates in a second pass)
-    const bool natural = gated && p->dit == 4;  // (kernels_fwd.cu: Y_DIRECT)
+    const bool natural = gated && p->dit == 4 && !FC_O3G4_DIRECT;  // (kernels_fwd.cu: Y_DIRECT)
     // (L0 = 8: u, w arrive 128 B swizzled too -- each thread reads one 128 B
     // line of a row, the swizzle spreads 8 lanes' lines over all banks)
     const bool swz_in = p->dit == 8;

@@ -1,5 +1,10 @@
 // fwd_params.h -- launch parameters of the fused forward kernels (internal).
 #pragma once
+// Gated order-3 L0 = 4 tiles: y gated in place in the swizzled v slot (1)
+// or natural-order v / y and a second pass (0).  Kernel and host agree on it.
+#ifndef FC_O3G4_DIRECT
+#define FC_O3G4_DIRECT 0
+#endif
 #include <cstddef>
 #include <cstdint>
 #include <cuda.h>

@@ -1611,7 +1611,7 @@ __global__ void __launch_bounds__(FwdCfg<L1, CAUSAL, GATED, L0I>::THREADS, 1) ff
         // intermediate copy of the conv output, no second pass, one barrier
         // (not for gated order-3 tiles with L0 = 4: the extra registers spill
         // there, 14 % slower; their v / y maps stay natural-order, api.cu)
-        constexpr bool Y_DIRECT = STG && !(GATED && L0I == 4);
+        constexpr bool Y_DIRECT = STG && !(GATED && L0I == 4 && !FC_O3G4_DIRECT);
         const bool direct = Y_DIRECT && prm.tma_io;
         // (coupled tiles: y is staged -- gated: gated in place -- in the v slot)
         const uint32_t sstg = tma_out ? sYS : CPL ? sV : direct ? sY : bufX;
